@@ -1,0 +1,15 @@
+"""Test configuration.
+
+Markers: ``gpu`` = needs a real B200 (run with ``-m gpu``); everything else
+runs on CPU (``-m "not gpu"``) in a few minutes.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
