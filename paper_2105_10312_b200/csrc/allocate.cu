@@ -1,0 +1,361 @@
+// allocate.cu -- A5: the paper's partition-and-allocate heuristics and the 1G
+// baseline, one WARP per task set (gp_allocate).
+//
+// Lane roles: lane i holds task i (its parameters, its Lemma 2 size, its
+// ACT forbidden row); lane s also holds partition SLOT s.  A live slot's index
+// is always the lowest task id of its partition (a merge keeps the lower
+// slot), so the par_list tie-break "lower min task id" (A-17) is the slot
+// index and canonical output labels are popcounts.  The per-partition EDF
+// test is warp-cooperative (lane = task of the partition): conflict flags via
+// popcount on the type mask, U*H via a shuffle sum, the demand walk with a
+// shuffle-min over the next deadlines (gp_edf.cuh explains the exact L_a
+// cut-off).  The ACT prefill runs the n(n-1)/2 pair merges lane-parallel with
+// a per-lane two-task test.
+//
+// Algorithm 1, Lemma 1, Lemma 2 (the minimal m is
+// computed in closed form m = ceil(B / floor((D - f)/c)), exact for the W
+// form), Lemma 3, Algorithm 2 (linear m scan, Def. 3
+// strict bound), Algorithm 3, Def. 4 / Def. 5 orders
+// (P:720-753), forbidden list; conventions C.1.9 / A-17..A-26.
+#include "gp_common.cuh"
+#include "gp_edf.cuh"
+
+namespace gp {
+
+struct AllocArgs {
+  const int32_t *T, *D, *B, *cn, *cc, *fn, *fc;
+  const uint8_t *type;
+  int32_t n_sets, n, M, variant;
+  uint8_t *ok;
+  int8_t *bot;
+  int16_t *bs;
+  int32_t *pi, *k;
+  int64_t *n_tests;
+};
+
+struct TaskLane {
+  int32_t T, D, B, cn, cc, fn, fc, q;
+  uint32_t same;  // mask of tasks with my type
+  bool in;        // lane < n
+};
+
+GP_DEV int32_t task_w(const TaskLane &t, int32_t m, bool x) {
+  return x ? wcet_sat(t.B, t.cc, t.fc, m) : wcet_sat(t.B, t.cn, t.fn, m);
+}
+
+// Warp-cooperative EDF-PDC of partition S at size m (C.1.7).
+GP_DEV bool warp_pdc(const TaskLane &t, uint32_t S, int32_t m, int32_t H) {
+  const int lane = threadIdx.x & 31;
+  const bool in = (S >> lane) & 1u;
+  const bool x = __popc(S & t.same) > 1;  // conflict
+  const int32_t C = in ? task_w(t, m, x) : 0;
+  if (__ballot_sync(GP_FULL, in && C > t.D)) return false;
+  if (__popc(S) == 1) return true;
+  const int32_t UH = warp_sum_i32(in ? C * t.q : 0);
+  if (UH > H) return false;
+  int32_t lcut = H;
+  if (UH < H) {
+    float X = in ? (float)(t.T - t.D) * (float)(C * t.q) : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) X += __shfl_xor_sync(GP_FULL, X, o);
+    const float L = X / (float)(H - UH) * 1.0001f + 2.0f;
+    lcut = L >= (float)H ? H : (int32_t)L;
+  }
+  int32_t nx = in ? t.D : INT32_MAX, dem = 0;
+  for (;;) {
+    const int32_t tt = warp_min_i32(nx);
+    if (tt > lcut) return true;
+    const bool hit = nx == tt;
+    dem += warp_sum_i32(hit ? C : 0);
+    nx += hit ? t.T : 0;
+    if (dem > tt) return false;
+  }
+}
+
+// U(P)*H of partition S at size m (Def. 5 with /T_i, reading A-19).
+GP_DEV int32_t warp_uh(const TaskLane &t, uint32_t S, int32_t m) {
+  const int lane = threadIdx.x & 31;
+  const bool in = (S >> lane) & 1u;
+  const bool x = __popc(S & t.same) > 1;
+  return warp_sum_i32(in ? task_w(t, m, x) * t.q : 0);
+}
+
+// Per-lane two-task EDF-PDC (ACT prefill), same exact shortcuts.
+GP_DEV bool pair_pdc(const int32_t (&C)[2], const int32_t (&D)[2], const int32_t (&T)[2],
+                     const int32_t (&q)[2], int32_t H) {
+  if (C[0] > D[0] || C[1] > D[1]) return false;
+  const int32_t UH = C[0] * q[0] + C[1] * q[1];
+  if (UH > H) return false;
+  const int32_t lcut = pdc_cutoff<2>(C, D, T, q, H, UH);
+  uint32_t ev = 0;
+  return pdc_walk<2>(C, D, T, lcut, ev);
+}
+
+struct WarpScratch {
+  int32_t ord[32];   // ord[r] = slot with par_list rank r
+  int32_t lab[32];   // output label of task i
+  int32_t size[32];  // size of output label j
+  uint32_t forb[32]; // ACT: forbidden task row
+};
+
+__global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
+  __shared__ WarpScratch scr_all[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpScratch &scr = scr_all[wid];
+  const int n = a.n, M = a.M;
+  const uint32_t all = n == 32 ? GP_FULL : ((1u << n) - 1u);
+  for (int64_t set = (int64_t)blockIdx.x * 8 + wid; set < a.n_sets; set += (int64_t)gridDim.x * 8) {
+    const int64_t o = set * n + lane;
+    TaskLane t;
+    t.in = lane < n;
+    const int64_t oo = t.in ? o : set * n;
+    t.T = a.T[oo]; t.D = a.D[oo]; t.B = a.B[oo]; t.cn = a.cn[oo]; t.cc = a.cc[oo];
+    t.fn = a.fn[oo]; t.fc = a.fc[oo];
+    const bool mem = t.in && a.type[oo] == 1;
+    const uint32_t memmask = __ballot_sync(GP_FULL, mem);
+    t.same = mem ? memmask : (all & ~memmask);
+    // input contract and H = lcm of all periods (capped)
+    const bool fields_ok = !t.in || (t.T >= 1 && t.D >= 1 && t.D <= t.T && t.B >= 1 && t.cn >= 1 &&
+                                     t.cc >= t.cn && t.fn >= 0 && t.fc >= t.fn);
+    const int64_t cap = ((int64_t)1 << 31) / (n + 1) - 1;
+    int64_t h = (t.in && fields_ok) ? t.T : (t.in ? -1 : 1);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int64_t other = __shfl_xor_sync(GP_FULL, h, off);
+      h = (h < 0 || other < 0) ? -1 : lcm_capped(h, other, cap);
+    }
+    const bool contract = __all_sync(GP_FULL, fields_ok) && h > 0;
+    const int32_t H = contract ? (int32_t)h : 1;
+    t.q = (contract && t.in) ? H / t.T : 0;
+
+    int64_t tests = 0;
+    bool ok = false;
+    int stage = 0;  // 0: rejected before partitions exist, 1: partitions to report
+    // slot state (lane = slot)
+    uint32_t pm = 0, pex = 0;
+    int32_t psz = 0, puh = 0;
+
+    if (!contract) {
+      tests = -1;
+    } else if (a.variant == GP_1G) {
+      // 1G: the whole GPU as one partition
+      tests = 1;
+      ok = warp_pdc(t, all, M, H);
+      pm = lane == 0 ? all : 0;
+      psz = lane == 0 ? M : 0;
+      stage = 1;
+    } else {
+      const bool act = a.variant == GP_SMS_ACT || a.variant == GP_BF_ACT;
+      const bool sms = a.variant == GP_SMS_ACT || a.variant == GP_SMS_INA;
+      // Lemma 1: sum_i W_i(1,n) * (H/T_i) > M*H  =>  reject
+      const int64_t w1 = t.in ? ((int64_t)t.B * t.cn + t.fn) * (int64_t)t.q : 0;
+      const bool lemma1 = warp_sum_i64(w1) <= (int64_t)M * H;
+      // Lemma 2: m_i = min{m : ceil(B/m) cn + fn <= D}
+      int32_t mi = 0;
+      if (t.in && t.D - t.fn >= t.cn) {
+        const int32_t K = (t.D - t.fn) / t.cn;  // waves allowed: ceil(B/m) <= K
+        const int32_t m0 = (t.B + K - 1) / K;
+        mi = m0 <= M ? (m0 < 1 ? 1 : m0) : 0;
+      }
+      const bool lemma2 = !__ballot_sync(GP_FULL, t.in && mi == 0);
+      if (lemma1 && lemma2) {
+        stage = 1;
+        pm = t.in ? (1u << lane) : 0;
+        psz = mi;
+        puh = t.in ? task_w(t, mi, false) * t.q : 0;
+        int32_t Pi = warp_sum_i32(psz);
+        if (Pi <= M) {
+          ok = true;  // Lemma 3: exit on success at any time (A-24)
+        } else {
+          uint32_t forb_row = 0;
+          if (act) {  // §5.3: test every couple of tasks
+            scr.forb[lane] = 0;
+            __syncwarp();
+            const int np = n * (n - 1) / 2;
+            int64_t my_tests = 0;
+            for (int base = 0; base < np; base += 32) {
+              int idx = base + lane;
+              int i = 0;
+              int rem = idx < np ? idx : 0;
+              while (rem >= n - 1 - i) {
+                rem -= n - 1 - i;
+                ++i;
+              }
+              const int j = i + 1 + rem;
+              const int32_t Ti = __shfl_sync(GP_FULL, t.T, i), Tj = __shfl_sync(GP_FULL, t.T, j);
+              const int32_t Di = __shfl_sync(GP_FULL, t.D, i), Dj = __shfl_sync(GP_FULL, t.D, j);
+              const int32_t Bi = __shfl_sync(GP_FULL, t.B, i), Bj = __shfl_sync(GP_FULL, t.B, j);
+              const int32_t qi = __shfl_sync(GP_FULL, t.q, i), qj = __shfl_sync(GP_FULL, t.q, j);
+              const int32_t mi_ = __shfl_sync(GP_FULL, mi, i), mj_ = __shfl_sync(GP_FULL, mi, j);
+              const uint32_t si = __shfl_sync(GP_FULL, t.same, i);
+              const bool x = (si >> j) & 1u;  // same type -> both in conflict
+              const int32_t cni = __shfl_sync(GP_FULL, t.cn, i), cci = __shfl_sync(GP_FULL, t.cc, i);
+              const int32_t cnj = __shfl_sync(GP_FULL, t.cn, j), ccj = __shfl_sync(GP_FULL, t.cc, j);
+              const int32_t fni = __shfl_sync(GP_FULL, t.fn, i), fci = __shfl_sync(GP_FULL, t.fc, i);
+              const int32_t fnj = __shfl_sync(GP_FULL, t.fn, j), fcj = __shfl_sync(GP_FULL, t.fc, j);
+              const int32_t ci = x ? cci : cni, cj = x ? ccj : cnj;
+              const int32_t fi = x ? fci : fni, fj = x ? fcj : fnj;
+              if (idx < np) {
+                bool merged = false;
+                for (int32_t m = max(mi_, mj_); m < mi_ + mj_ && !merged; ++m) {
+                  ++my_tests;
+                  const int32_t C[2] = {wcet_sat(Bi, ci, fi, m), wcet_sat(Bj, cj, fj, m)};
+                  const int32_t Dv[2] = {Di, Dj}, Tv[2] = {Ti, Tj}, qv[2] = {qi, qj};
+                  merged = pair_pdc(C, Dv, Tv, qv, H);
+                }
+                if (!merged) {
+                  atomicOr(&scr.forb[i], 1u << j);
+                  atomicOr(&scr.forb[j], 1u << i);
+                }
+              }
+            }
+            tests += warp_sum_i64(my_tests);
+            __syncwarp();
+            forb_row = scr.forb[lane];
+          }
+          // Algorithm 1 main loop
+          for (;;) {
+            // par_list order: (U*H desc, slot asc)
+            const bool live = pm != 0;
+            const uint32_t livemask = __ballot_sync(GP_FULL, live);
+            int rank = 0;
+            for (int s2 = 0; s2 < 32; ++s2) {
+              const int32_t u2 = __shfl_sync(GP_FULL, puh, s2);
+              rank += ((livemask >> s2) & 1u) && (u2 > puh || (u2 == puh && s2 < lane));
+            }
+            if (live) scr.ord[rank] = lane;
+            __syncwarp();
+            const int len = __popc(livemask);
+            if (Pi <= M) {
+              ok = true;
+              break;
+            }
+            // Algorithm 3: eligibility of every slot, pick the first in order
+            uint32_t F = 0;  // tasks forbidden with a task of my partition (ACT)
+            if (act)
+              for (int a2 = 0; a2 < n; ++a2) {
+                const uint32_t fr = __shfl_sync(GP_FULL, forb_row, a2);
+                if ((pm >> a2) & 1u) F |= fr;
+              }
+            uint32_t forb_slots = 0;
+            for (int s2 = 0; s2 < 32; ++s2) {
+              const uint32_t m2 = __shfl_sync(GP_FULL, pm, s2);
+              if (m2 & F) forb_slots |= 1u << s2;
+            }
+            const uint32_t elig_mine = live ? (livemask & ~(1u << lane) & ~pex & ~forb_slots) : 0;
+            const int cand_rank = warp_min_i32(elig_mine ? rank : 99);
+            if (cand_rank == 99) break;  // no selectable partition: fail (Alg. 1 l.6-7)
+            const int P = scr.ord[cand_rank];
+            const uint32_t elig = __shfl_sync(GP_FULL, elig_mine, P);
+            const uint32_t pmP = __shfl_sync(GP_FULL, pm, P);
+            const int32_t szP = __shfl_sync(GP_FULL, psz, P);
+            int best = -1;
+            int32_t best_m = 0, best_uh = 0;
+            for (int r = 0; r < len; ++r) {
+              const int Q = scr.ord[r];
+              if (!((elig >> Q) & 1u)) continue;
+              const uint32_t pmQ = __shfl_sync(GP_FULL, pm, Q);
+              const int32_t szQ = __shfl_sync(GP_FULL, psz, Q);
+              const uint32_t S = pmP | pmQ;
+              int32_t got = 0;  // Algorithm 2: linear scan, m < |P1| + |P2| (Def. 3)
+              for (int32_t m = max(szP, szQ); m < szP + szQ; ++m) {
+                ++tests;
+                if (warp_pdc(t, S, m, H)) {
+                  got = m;
+                  break;
+                }
+              }
+              if (!got) {  // add_to_forbidden_moves(P, Q)
+                if (lane == P) pex |= 1u << Q;
+                if (lane == Q) pex |= 1u << P;
+                continue;
+              }
+              const int32_t uh = warp_uh(t, S, got);
+              if (sms) {  // Def. 4 order >>: smallest size, then U*H, then min id
+                if (best < 0 || got < best_m || (got == best_m && (uh < best_uh ||
+                                                                    (uh == best_uh && Q < best)))) {
+                  best = Q;
+                  best_m = got;
+                  best_uh = uh;
+                }
+              } else {  // BF: first success in > order commits
+                best = Q;
+                best_m = got;
+                best_uh = uh;
+                break;
+              }
+            }
+            __syncwarp();
+            if (best >= 0) {  // commit: P u Q replaces P and Q in par_list
+              const int Q = best;
+              const int32_t szQ = __shfl_sync(GP_FULL, psz, Q);
+              const uint32_t pmQ = __shfl_sync(GP_FULL, pm, Q);
+              const int keep = min(P, Q), drop = max(P, Q);
+              Pi -= szP + szQ - best_m;
+              if (lane == keep) {
+                pm = pmP | pmQ;
+                psz = best_m;
+                puh = best_uh;
+                pex = 0;
+              } else if (lane == drop) {
+                pm = 0;
+                psz = 0;
+                puh = 0;
+                pex = 0;
+              }
+              pex &= ~((1u << keep) | (1u << drop));
+            }
+          }
+        }
+      }
+    }
+    // outputs: labels numbered by lowest task id (= slot index)
+    const uint32_t livemask = __ballot_sync(GP_FULL, pm != 0);
+    const int kk = stage ? __popc(livemask) : 0;
+    if (pm) {
+      const int label = __popc(livemask & ((1u << lane) - 1u));
+      scr.size[label] = psz;
+      uint32_t bits = pm;
+      while (bits) {
+        const int tsk = __ffs(bits) - 1;
+        bits &= bits - 1;
+        scr.lab[tsk] = label;
+      }
+    }
+    __syncwarp();
+    const int32_t Pi_out = stage ? warp_sum_i32(psz) : 0;
+    if (t.in) {
+      a.bot[o] = (int8_t)(stage ? scr.lab[lane] : -1);
+      a.bs[o] = (int16_t)((stage && lane < kk) ? scr.size[lane] : 0);
+    }
+    if (lane == 0) {
+      a.ok[set] = ok ? 1 : 0;
+      a.pi[set] = Pi_out;
+      a.k[set] = kk;
+      a.n_tests[set] = tests;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace gp
+
+extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok,
+                                 int8_t *block_of_task, int16_t *block_size, int32_t *pi,
+                                 int32_t *k, int64_t *n_tests, void *stream) {
+  using namespace gp;
+  if (!ts || ts->n_tasks < 1 || ts->n_tasks > kMaxTasks || ts->M < 1 || ts->M > 1024 ||
+      ts->n_sets < 0)
+    return gp_fail(GP_EINVAL, "gp_allocate: bad task sets (n_tasks 1..32, M 1..1024)");
+  if ((int)v < 0 || (int)v > 4) return gp_fail(GP_EINVAL, "gp_allocate: bad variant %d", (int)v);
+  if (ts->n_sets == 0) return gp_cuda_check("gp_allocate");
+  if (!ok || !block_of_task || !block_size || !pi || !k || !n_tests || !ts->T || !ts->D ||
+      !ts->B || !ts->cn || !ts->cc || !ts->fn || !ts->fc || !ts->type)
+    return gp_fail(GP_EINVAL, "gp_allocate: null pointer");
+  AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
+              ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests};
+  int64_t grid = ((int64_t)ts->n_sets + 7) / 8;
+  if (grid > 148 * 64) grid = 148 * 64;
+  k_allocate<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+  return gp_cuda_check("gp_allocate");
+}

@@ -1,0 +1,214 @@
+// generate.cu -- A1: counter-based synthetic task sets (gp_generate).
+// Paper: §7.1 task-set generation.  Definitions C.1.10, readings
+// A-9..A-15 and A-31.
+//
+// Layout of the work: one GROUP of G lanes per task set, G = next power of two
+// >= n_tasks (G = 8 for 6 tasks: 4 sets per warp; G = 32 for 32 tasks).  Lane
+// j of the group owns task j: it draws its own Philox block (counter =
+// (g, attempt, j)), the n-1 spacing points are sorted with a register bitonic
+// network across the group (shuffles, no shared memory), each lane derives
+// its utilisation as the gap to its left neighbour, computes its fields, and
+// a group ballot implements the whole-vector discard.  Writes are coalesced
+// because a set's tasks are contiguous ([set][task] layout).
+#include <cstdarg>
+#include <cstdio>
+
+#include "gp_common.cuh"
+
+namespace gp {
+
+struct GenArgs {
+  int32_t M, n, n_bins, n_prm, sets_per_group, Q, n_periods, b_max;
+  int32_t beta_c, beta_m, beta_den, kc, km, k_den, max_attempts, G;
+  int32_t rep_count, n_sets;
+  uint64_t rep_begin, seed;
+  int32_t menu[kMaxMenu];
+  uint64_t prm_q[kMaxPrm];
+  int32_t *T, *D, *B, *cn, *cc, *fn, *fc, *group;
+  uint8_t *type, *valid;
+};
+
+// Philox4x32-10 (Salmon et al., SC'11).
+GP_DEV void philox4x32_10(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3, uint32_t k0,
+                          uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t lo0 = 0xD2511F53u * x0, hi0 = __umulhi(0xD2511F53u, x0);
+    uint32_t lo1 = 0xCD9E8D57u * x2, hi1 = __umulhi(0xCD9E8D57u, x2);
+    uint32_t y0 = hi1 ^ x1 ^ k0, y2 = hi0 ^ x3 ^ k1;
+    x0 = y0;
+    x1 = lo1;
+    x2 = y2;
+    x3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
+  const int G = a.G;
+  const int lane = threadIdx.x & 31;
+  const int j = lane & (G - 1);  // task slot inside the group
+  const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;  // local set
+  const bool live = l < a.n_sets;
+  const int n = a.n;
+  const unsigned gbase = (unsigned)(lane & ~(G - 1));
+  const unsigned gmask = (G == 32) ? GP_FULL : (((1u << G) - 1u) << gbase);
+
+  int32_t grp = 0, prm_idx = 0, bin = 0;
+  uint64_t g = 0;
+  if (live) {
+    grp = (int32_t)(l / a.rep_count);
+    uint64_t rep = a.rep_begin + (uint64_t)(l % a.rep_count);
+    g = (uint64_t)grp * (uint64_t)a.sets_per_group + rep;  // global set index
+    prm_idx = grp / a.n_bins;
+    bin = grp % a.n_bins;
+  }
+  // U_q = (bin+1) * M * 2^20 / n_bins: total utilisation in Q20 (A-31)
+  const int64_t Uq = ((int64_t)(bin + 1) * a.M << 20) / a.n_bins;
+  const uint64_t pq = a.prm_q[prm_idx];
+  const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+
+  int32_t oT = 0, oD = 0, oB = 0, ocn = 0, occ = 0, ofn = 0, ofc = 0;
+  uint8_t otype = 0;
+  bool done = !live, valid = false;
+  for (int attempt = 0; attempt < a.max_attempts; ++attempt) {
+    if (__ballot_sync(GP_FULL, !done) == 0) break;
+    uint32_t x0 = (uint32_t)g, x1 = (uint32_t)(g >> 32), x2 = (uint32_t)attempt, x3 = (uint32_t)j;
+    philox4x32_10(x0, x1, x2, x3, k0, k1);
+    const uint8_t typ = ((uint64_t)x0 < pq) ? 1 : 0;
+    int32_t pidx = (int32_t)(((uint64_t)x1 * (uint64_t)a.n_periods) >> 32);          // A-11
+    const int32_t Bv = 1 + (int32_t)(((uint64_t)x2 * (uint64_t)a.b_max) >> 32);     // A-13
+    // spacing point; lanes >= n-1 carry the pad U_q so they sort last
+    int64_t pt = (j < n - 1) ? (int64_t)(((uint64_t)x3 * (uint64_t)(Uq + 1)) >> 32) : Uq;
+    // bitonic sort ascending across the G lanes of the group
+    for (int kk = 2; kk <= G; kk <<= 1) {
+      for (int s = kk >> 1; s > 0; s >>= 1) {
+        int64_t o = __shfl_xor_sync(GP_FULL, pt, s);
+        bool asc = (j & kk) == 0, lower = (j & s) == 0;
+        pt = (lower == asc) ? (o < pt ? o : pt) : (o > pt ? o : pt);
+      }
+    }
+    int64_t left = __shfl_up_sync(GP_FULL, pt, 1, G);
+    if (j == 0) left = 0;
+    const int64_t u = pt - left;  // UUniFast via sorted spacings (A-12)
+    // period bump while the baseline execution time is "not reasonable" (A-10)
+    int64_t T = (int64_t)a.menu[pidx] * a.Q;
+    int64_t ab = (u * T) >> 20;
+    const int64_t need = Bv > a.Q ? Bv : a.Q;
+    while (ab < need && pidx < a.n_periods - 1) {
+      ++pidx;
+      T = (int64_t)a.menu[pidx] * a.Q;
+      ab = (u * T) >> 20;
+    }
+    const int64_t D = 3 * T / 4;
+    int64_t cn = ceil_div64(ab, Bv);
+    if (cn < 1) cn = 1;
+    const int64_t fn = ceil_div64(ab * (typ ? a.beta_m : a.beta_c), a.beta_den);
+    const int64_t kf = typ ? a.km : a.kc;
+    const int64_t cc = ceil_div64(cn * kf, a.k_den), fc = ceil_div64(fn * kf, a.k_den);
+    const bool feasible = ((int64_t)((Bv + a.M - 1) / a.M)) * cn + fn <= D;      // A-9
+    const unsigned bad = __ballot_sync(GP_FULL, (j < n) && !feasible) & gmask;
+    if (!done) {
+      oT = (int32_t)T; oD = (int32_t)D; oB = Bv;
+      ocn = (int32_t)cn; occ = (int32_t)cc; ofn = (int32_t)fn; ofc = (int32_t)fc;
+      otype = typ;
+      if (bad == 0) {
+        done = true;
+        valid = true;
+      }
+    }
+  }
+  if (live && j < n) {
+    const int64_t o = l * n + j;
+    a.T[o] = oT; a.D[o] = oD; a.B[o] = oB; a.cn[o] = ocn; a.cc[o] = occ;
+    a.fn[o] = ofn; a.fc[o] = ofc; a.type[o] = otype;
+    if (j == 0) {
+      a.valid[l] = valid ? 1 : 0;
+      a.group[l] = grp;
+    }
+  }
+}
+
+}  // namespace gp
+
+static int64_t host_gcd(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t rep_begin,
+                                 int32_t rep_count, gp_tasksets *out, void *stream) {
+  using namespace gp;
+  if (!p || !out) return gp_fail(GP_EINVAL, "gp_generate: null params or output");
+  if (p->n_tasks < 1 || p->n_tasks > kMaxTasks)
+    return gp_fail(GP_EINVAL, "gp_generate: n_tasks %d not in 1..32", p->n_tasks);
+  if (p->M < 1 || p->M > 1024) return gp_fail(GP_EINVAL, "gp_generate: M %d not in 1..1024", p->M);
+  if (p->n_bins < 1 || p->n_prm < 1 || p->n_prm > kMaxPrm || p->sets_per_group < 1)
+    return gp_fail(GP_EINVAL, "gp_generate: bad n_bins/n_prm/sets_per_group");
+  if (!p->prm_q || !p->period_menu) return gp_fail(GP_EINVAL, "gp_generate: null prm_q/menu");
+  for (int i = 0; i < p->n_prm; ++i)
+    if (p->prm_q[i] > (1ull << 32)) return gp_fail(GP_EINVAL, "gp_generate: prm_q > 2^32");
+  if (p->ticks_per_unit < 1 || p->n_periods < 1 || p->n_periods > kMaxMenu)
+    return gp_fail(GP_EINVAL, "gp_generate: bad Q or n_periods");
+  int64_t Tmax = 0, H = 1;
+  for (int i = 0; i < p->n_periods; ++i) {
+    int64_t t = (int64_t)p->period_menu[i] * p->ticks_per_unit;
+    if (p->period_menu[i] <= 0 || (i > 0 && p->period_menu[i] <= p->period_menu[i - 1]))
+      return gp_fail(GP_EINVAL, "gp_generate: period menu must be positive and ascending");
+    if (t % 4 != 0) return gp_fail(GP_EINVAL, "gp_generate: Q*T must be divisible by 4 (D=3T/4)");
+    if (t > INT32_MAX) return gp_fail(GP_EOVERFLOW, "gp_generate: period overflows int32");
+    Tmax = t > Tmax ? t : Tmax;
+    H = H / host_gcd(H, t) * t;
+    if (H > INT32_MAX) return gp_fail(GP_EOVERFLOW, "gp_generate: menu hyperperiod overflows");
+  }
+  if (p->b_max < 1 || p->beta_den < 1 || p->beta_c_num < 0 || p->beta_m_num < 0 || p->k_den < 1 ||
+      p->kc_num < p->k_den || p->km_num < p->k_den || p->max_attempts < 1)
+    return gp_fail(GP_EINVAL, "gp_generate: bad b_max/beta/k (k >= 1 required)/max_attempts");
+  if (rep_count < 0 || rep_begin + (uint64_t)rep_count > (uint64_t)p->sets_per_group)
+    return gp_fail(GP_EINVAL, "gp_generate: rep range beyond sets_per_group");
+  const int64_t n_groups = (int64_t)p->n_prm * p->n_bins;
+  if (out->n_sets != n_groups * rep_count || out->n_tasks != p->n_tasks)
+    return gp_fail(GP_EINVAL, "gp_generate: out->n_sets must be n_prm*n_bins*rep_count (%lld)",
+                   (long long)(n_groups * rep_count));
+  // field ranges: a <= M*Tmax, cn <= a, fn <= beta*a, cc <= k*cn, fc <= k*fn
+  const int64_t amax = (int64_t)p->M * Tmax;
+  const int64_t bmax = p->beta_c_num > p->beta_m_num ? p->beta_c_num : p->beta_m_num;
+  const int64_t kmax = p->kc_num > p->km_num ? p->kc_num : p->km_num;
+  const int64_t fnmax = (amax * bmax + p->beta_den - 1) / p->beta_den;
+  const int64_t ccmax = (amax * kmax + p->k_den - 1) / p->k_den;
+  const int64_t fcmax = (fnmax * kmax + p->k_den - 1) / p->k_den;
+  if (ccmax > INT32_MAX || fcmax > INT32_MAX || amax > INT32_MAX)
+    return gp_fail(GP_EOVERFLOW, "gp_generate: M*Tmax*k exceeds int32 (fields would overflow)");
+  if (H * (p->n_tasks + 1) >= (1ll << 31))
+    return gp_fail(GP_EOVERFLOW, "gp_generate: menu hyperperiod * (n+1) >= 2^31");
+  if (!out->T || !out->D || !out->B || !out->cn || !out->cc || !out->fn || !out->fc ||
+      !out->type || !out->valid || !out->group)
+    return gp_fail(GP_EINVAL, "gp_generate: null output pointer");
+  out->M = p->M;
+  out->n_groups = (int32_t)n_groups;
+  if (out->n_sets == 0) return GP_OK;
+
+  GenArgs a;
+  a.M = p->M; a.n = p->n_tasks; a.n_bins = p->n_bins; a.n_prm = p->n_prm;
+  a.sets_per_group = p->sets_per_group; a.Q = p->ticks_per_unit; a.n_periods = p->n_periods;
+  a.b_max = p->b_max; a.beta_c = p->beta_c_num; a.beta_m = p->beta_m_num; a.beta_den = p->beta_den;
+  a.kc = p->kc_num; a.km = p->km_num; a.k_den = p->k_den; a.max_attempts = p->max_attempts;
+  int G = 1;
+  while (G < p->n_tasks) G <<= 1;
+  a.G = G;
+  a.rep_count = rep_count; a.n_sets = out->n_sets; a.rep_begin = rep_begin; a.seed = seed;
+  for (int i = 0; i < kMaxMenu; ++i) a.menu[i] = i < p->n_periods ? p->period_menu[i] : 0;
+  for (int i = 0; i < kMaxPrm; ++i) a.prm_q[i] = i < p->n_prm ? p->prm_q[i] : 0;
+  a.T = out->T; a.D = out->D; a.B = out->B; a.cn = out->cn; a.cc = out->cc; a.fn = out->fn;
+  a.fc = out->fc; a.group = out->group; a.type = out->type; a.valid = out->valid;
+  const int64_t threads = (int64_t)out->n_sets * G;
+  const int block = 256;
+  const int64_t grid = (threads + block - 1) / block;
+  k_generate<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a);
+  return gp_cuda_check("gp_generate");
+}

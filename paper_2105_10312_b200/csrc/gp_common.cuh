@@ -1,0 +1,93 @@
+// gp_common.cuh -- device helpers shared by the sm_100a kernels of libgpart.
+// Product code: independent of oracle/ (no shared code, header or table).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gpart.h"
+
+#define GP_DEV __device__ __forceinline__
+#define GP_FULL 0xFFFFFFFFu
+
+namespace gp {
+
+constexpr int kMaxTasks = 32;
+constexpr int kMaxMenu = 16;
+constexpr int kMaxPrm = 16;
+
+// ---- integer helpers -------------------------------------------------------
+GP_DEV int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+GP_DEV int32_t ceil_div32(int32_t a, int32_t b) { return (a + b - 1) / b; }
+
+GP_DEV int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// lcm with saturation: returns -1 when it would exceed `cap`
+GP_DEV int64_t lcm_capped(int64_t a, int64_t b, int64_t cap) {
+  if (a < 0 || b < 0) return -1;
+  int64_t g = gcd64(a, b);
+  int64_t q = a / g;
+  if (q > cap / b) return -1;
+  return q * b;
+}
+
+// W(m) = ceil(B/m)*c + f in 64-bit, saturated to INT32_MAX (C.1.3).
+GP_DEV int32_t wcet_sat(int32_t B, int32_t c, int32_t f, int32_t m) {
+  int64_t w = (int64_t)((B + m - 1) / m) * (int64_t)c + (int64_t)f;
+  return w > INT32_MAX ? INT32_MAX : (int32_t)w;
+}
+
+// ---- warp reductions ---------------------------------------------------------
+GP_DEV int32_t warp_sum_i32(int32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(GP_FULL, v, o);
+  return v;
+}
+GP_DEV int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(GP_FULL, v, o);
+  return v;
+}
+GP_DEV uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(GP_FULL, v, o);
+  return v;
+}
+GP_DEV int32_t warp_min_i32(int32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(GP_FULL, v, o));
+  return v;
+}
+GP_DEV int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t w = __shfl_xor_sync(GP_FULL, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+GP_DEV uint32_t warp_or_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(GP_FULL, v, o);
+  return v;
+}
+
+// ---- SplitMix64 output for state x (order-independent verdict hash) ---------
+GP_DEV uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace gp
+
+// ---- host-side error plumbing (abi.cu) ---------------------------------------
+gp_status gp_fail(gp_status st, const char *fmt, ...);
+gp_status gp_cuda_check(const char *what);

@@ -1,0 +1,85 @@
+// ratio.cu -- A6: segmented reduction to schedulability-rate counts
+// (gp_sched_ratio).  §7.2: "the classical schedulability rate,
+// so that we count the number of schedulable tasksets"; C.1.11.
+// Integer atomics are order-independent, so the counts are deterministic and
+// identical under any sharding (sum over ranks = one all-reduce).
+#include "gp_common.cuh"
+
+gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_slots,
+                               int32_t setting, int64_t *counts, const gp_exhaustive_opts *ex,
+                               cudaStream_t st);
+
+namespace gp {
+
+struct RatioArgs {
+  const uint8_t *verdicts, *valid;
+  const int32_t *group;
+  int32_t n_sets, n_rows, n_groups, slot0, n_slots, setting;
+  int64_t *counts;
+};
+
+// CTA-private histogram in shared memory, then one global atomic per bin.
+__global__ void __launch_bounds__(256) k_ratio(const RatioArgs a) {
+  extern __shared__ unsigned long long hist[];
+  const int bins = a.n_groups * a.n_rows * 3;
+  for (int e = threadIdx.x; e < bins; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int64_t total = (int64_t)a.n_sets * a.n_rows;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(x / a.n_sets);
+    const int64_t set = x - (int64_t)row * a.n_sets;
+    const int32_t g = a.group[set];
+    if (g < 0 || g >= a.n_groups) continue;
+    const bool valid = a.valid[set] != 0;
+    const bool ok = a.verdicts[x] != 0;
+    unsigned long long *h = hist + ((int64_t)g * a.n_rows + row) * 3;
+    if (ok && valid) atomicAdd(h + 0, 1ull);
+    atomicAdd(h + 1, 1ull);
+    if (!valid) atomicAdd(h + 2, 1ull);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < bins; e += blockDim.x) {
+    if (!hist[e]) continue;
+    const int c = e % 3, gr = e / 3, row = gr % a.n_rows, g = gr / a.n_rows;
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(
+        a.counts + (((int64_t)a.setting * a.n_groups + g) * a.n_slots + a.slot0 + row) * 3 + c);
+    atomicAdd(dst, hist[e]);
+  }
+}
+
+}  // namespace gp
+
+extern "C" gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode,
+                                    const uint8_t *verdicts, int32_t n_rows, int32_t slot0,
+                                    int32_t n_slots, int32_t setting, int64_t *counts,
+                                    const gp_exhaustive_opts *ex, void *stream) {
+  using namespace gp;
+  if (!ts || ts->n_sets < 0 || ts->n_groups < 1 || ts->n_tasks < 1 || ts->n_tasks > kMaxTasks)
+    return gp_fail(GP_EINVAL, "gp_sched_ratio: bad task sets");
+  if (n_rows < 1 || slot0 < 0 || slot0 + n_rows > n_slots || setting < 0)
+    return gp_fail(GP_EINVAL, "gp_sched_ratio: need 0 <= slot0, slot0 + n_rows <= n_slots");
+  if (ts->n_sets > 0 && (!ts->valid || !ts->group))
+    return gp_fail(GP_EINVAL, "gp_sched_ratio: null valid/group");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mode == GP_EXHAUSTIVE) {
+    if (verdicts || n_rows != 1) return gp_fail(GP_EINVAL, "EXHAUSTIVE: verdicts must be NULL, n_rows 1");
+    return gp_exhaustive_launch(ts, slot0, n_slots, setting, counts, ex, st);
+  }
+  if (mode != GP_FROM_VERDICTS) return gp_fail(GP_EINVAL, "gp_sched_ratio: bad mode");
+  if (ex) return gp_fail(GP_EINVAL, "FROM_VERDICTS: exhaustive options must be NULL");
+  if (!verdicts || !counts) return gp_fail(GP_EINVAL, "FROM_VERDICTS: null verdicts/counts");
+  if (ts->n_sets == 0) return gp_cuda_check("gp_sched_ratio");
+  const size_t smem = (size_t)ts->n_groups * n_rows * 3 * sizeof(unsigned long long);
+  if (smem > 96 * 1024) return gp_fail(GP_EINVAL, "FROM_VERDICTS: n_groups*n_rows too large");
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_ratio, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  RatioArgs a{verdicts, ts->valid, ts->group, ts->n_sets, n_rows, ts->n_groups, slot0, n_slots,
+              setting, counts};
+  int64_t work = (int64_t)ts->n_sets * n_rows;
+  int64_t grid = (work + 1023) / 1024;
+  if (grid > 148 * 2) grid = 148 * 2;
+  if (grid < 1) grid = 1;
+  k_ratio<<<(unsigned)grid, 256, smem, st>>>(a);
+  return gp_cuda_check("gp_sched_ratio(FROM_VERDICTS)");
+}

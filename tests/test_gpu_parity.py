@@ -1,0 +1,339 @@
+"""GPU parity: every CUDA step through the C ABI vs the CPU oracle, on the same
+seeded inputs, bit-exact (integer path: C.1.x definitions).
+
+Sizes: full per-candidate verdict bitmaps for C1 and 1,000 C2 sets; C3 at its
+parity size (10 bins x 1,000 sets, the bench's launch configuration) with
+per-set outputs sampled and recomputed by the oracle one set at a time;
+heuristics on C2 (2,000 sets), C4 (250 sets, n = 32) and C5 (160 sets);
+random small sets covering n = 1..8, M = 1..12, ragged tails and the edge
+cases (M = 1, single task, D = T, f = 0, contract violations).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import gp_workloads as W
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group")
+
+
+@pytest.fixture(scope="module")
+def G():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2105_10312_b200 import gpart  # raises if libgpart.so is missing
+    return gpart
+
+
+def to_oracle(ts):
+    return oracle.Sets.from_dict(ts.to_host())
+
+
+def gpu_sets(G, d):
+    return G.TaskSets.from_host(d)
+
+
+# ------------------------------------------------------------------ A3 / example
+def test_worked_example_per_sm(G):
+    """5 blocks over (p1, p2) with costs (1, 2) -> (3, 4), WCET 4."""
+    per, w = G.gp_wcet_per_sm(5, [1, 2])
+    assert per.cpu().tolist() == [3, 4] and int(w) == 4
+    per, w = G.gp_wcet_per_sm(5, [1])
+    assert per.cpu().tolist() == [5] and int(w) == 5
+    for B in (0, 1, 7, 33, 1000):
+        for m in (1, 2, 3, 7, 68):
+            costs = list(range(1, m + 1))
+            per, w = G.gp_wcet_per_sm(B, costs, 3)
+            ref_per, ref_w = oracle.wcet_per_sm(B, costs, 3)
+            assert per.cpu().tolist() == ref_per and int(w) == ref_w
+
+
+# ------------------------------------------------------------------ A2
+@pytest.mark.parametrize("M,n", [(1, 1), (4, 3), (5, 4), (8, 6), (3, 5), (12, 4), (6, 7)])
+def test_enumerate_all_ranks(G, M, n):
+    total = G.gp_count_candidates(M, n)
+    bot, bs = G.gp_enumerate(M, n, 0, total)
+    rb, rs = oracle.enumerate_candidates(M, n)
+    assert (bot.cpu().numpy() == rb).all() and (bs.cpu().numpy() == rs).all()
+
+
+def test_enumerate_windows_c3(G):
+    total = G.gp_count_candidates(20, 6)
+    rng = np.random.default_rng(11)
+    for first in [0, 1, 19, 20, total - 1000] + [int(x) for x in rng.integers(0, total - 1000, 6)]:
+        cnt = min(1000, total - first)
+        bot, bs = G.gp_enumerate(20, 6, first, cnt)
+        rb, rs = oracle.enumerate_candidates(20, 6, first, cnt)
+        assert (bot.cpu().numpy() == rb).all() and (bs.cpu().numpy() == rs).all()
+
+
+# ------------------------------------------------------------------ A1
+@pytest.mark.parametrize("key,R,reps", [("c2", 10000, 200), ("c3", 1000, 100), ("c4", 20000, 20),
+                                        ("c5", 10000, 30)])
+def test_generate_bit_exact(G, key, R, reps):
+    gen = W.WORKLOADS[key]["gen"](R=R)
+    n_groups = gen["n_prm"] * gen["n_bins"]
+    ts = G.TaskSets(n_groups * reps, gen["n_tasks"], gen["M"], n_groups)
+    G.gp_generate(gen, W.SEED, 0, reps, ts)
+    ref = oracle.generate(gen, W.SEED, 0, reps)
+    got = ts.to_host()
+    for f in FIELDS:
+        assert (got[f] == getattr(ref, f)).all(), f
+    # a shard from the middle of the repetition range, and a different seed
+    ts2 = G.TaskSets(n_groups * 7, gen["n_tasks"], gen["M"], n_groups)
+    G.gp_generate(gen, W.SEED ^ 0xABCDEF, 13, 7, ts2)
+    ref2 = oracle.generate(gen, W.SEED ^ 0xABCDEF, 13, 7)
+    for f in FIELDS:
+        assert (ts2.to_host()[f] == getattr(ref2, f)).all(), f
+
+
+def test_generate_c5_settings(G):
+    for kc, km in W.C5_SETTINGS[::5]:
+        gen = W.WORKLOADS["c5"]["gen"](R=100, kc=kc, km=km)
+        ts = G.TaskSets(10 * 4, 16, 68, 10)
+        G.gp_generate(gen, W.SEED, 0, 4, ts)
+        ref = oracle.generate(gen, W.SEED, 0, 4)
+        for f in FIELDS:
+            assert (ts.to_host()[f] == getattr(ref, f)).all(), f
+
+
+def test_generate_discard_exhaustion(G):
+    """max_attempts = 1 at the top bin: some sets keep their last draw with
+    valid = 0, identical on both sides (A-9)."""
+    gen = dict(W.WORKLOADS["c2"]["gen"](R=1000), max_attempts=1)
+    ts = G.TaskSets(10 * 100, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 100, ts)
+    ref = oracle.generate(gen, W.SEED, 0, 100)
+    got = ts.to_host()
+    assert (got["valid"] == ref.valid).all() and ref.valid.min() == 0
+    for f in FIELDS:
+        assert (got[f] == getattr(ref, f)).all(), f
+
+
+# ------------------------------------------------------------------ A3
+def test_wcet_batch(G):
+    rng = np.random.default_rng(12)
+    gen = W.WORKLOADS["c2"]["gen"](R=100)
+    ref_sets = oracle.generate(gen, W.SEED, 0, 20)
+    ts = gpu_sets(G, ref_sets.to_dict())
+    bot, bs = oracle.enumerate_candidates(8, 6)
+    pick = rng.integers(0, len(bot), 5000)
+    soc = rng.integers(0, ref_sets.n_sets, 5000).astype(np.int32)
+    w_ref, c_ref = oracle.wcet_batch(ref_sets, soc, bot[pick], bs[pick])
+    w, c = G.gp_wcet(ts, torch.as_tensor(soc).cuda(), torch.as_tensor(bot[pick]).cuda(),
+                     torch.as_tensor(bs[pick]).cuda())
+    assert (w.cpu().numpy() == w_ref).all() and (c.cpu().numpy() == c_ref).all()
+    # malformed candidate (size 0 for a used block) is reported in-band
+    bad_bs = bs[pick[:1]].copy()
+    bad_bs[0, 0] = 0
+    w, c = G.gp_wcet(ts, torch.as_tensor(soc[:1]).cuda(), torch.as_tensor(bot[pick[:1]]).cuda(),
+                     torch.as_tensor(bad_bs).cuda())
+    assert (w.cpu().numpy()[0][bot[pick[0]] == 0] == -1).all()
+
+
+# ------------------------------------------------------------------ A2-A4 fused
+def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1):
+    S = ts.n_sets
+    total = G.gp_count_candidates(ts.M, ts.n_tasks)
+    hi_ = total if hi is None else hi
+    per = torch.empty((S, 4), dtype=torch.int64, device="cuda")
+    words = (hi_ - lo + 31) // 32
+    vb = torch.empty((S, words), dtype=torch.int32, device="cuda") if bits else None
+    work = torch.zeros(1, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, counts, slot0=slot0, n_slots=n_slots, per_set=per,
+                     verdict_bits=vb, words_per_set=words if bits else 0, work_counter=work,
+                     stats=stats, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi)
+    torch.cuda.synchronize()
+    out = per.cpu().numpy()
+    if bits:
+        return out, vb.cpu().numpy().view(np.uint32), stats.cpu().numpy()
+    return out, None, stats.cpu().numpy()
+
+
+def test_exhaustive_c1_table(G):
+    d = W._c1_sets()
+    ts = gpu_sets(G, d)
+    per, vb, st = run_exhaustive(G, ts, bits=True)
+    ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
+    assert (per == ref).all() and (vb == rbits).all()
+    assert per[:, 0].tolist() == [4, 10, 10, 10, 10, 10, 10, 4]
+    assert st[0] == 8 * 26
+
+
+def test_exhaustive_c2_bitmaps(G):
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 100, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 100, ts)
+    per, vb, st = run_exhaustive(G, ts, bits=True)
+    ref, rbits = oracle.exhaustive(to_oracle(ts), bits=True)
+    assert (per == ref).all()
+    assert (vb == rbits).all()
+    assert st[0] == 1000 * 11334
+
+
+def test_exhaustive_c3_parity_config_sampled(G):
+    """C3 at the bench's parity size (10 bins x 1,000 sets, M=20, n=6,
+    694,755 candidates per set) in the launch configuration bench.py times;
+    per-set outputs recomputed by the oracle for a sample of sets."""
+    gen = W.WORKLOADS["c3"]["gen"](R=1000)
+    ts = G.TaskSets(10 * 1000, 6, 20, 10)
+    G.gp_generate(gen, W.SEED, 0, 1000, ts)
+    counts = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
+    per, _, st = run_exhaustive(G, ts, counts=counts)
+    assert st[0] == 10 * 1000 * 694755
+    host = to_oracle(ts)
+    rng = np.random.default_rng(13)
+    sample = sorted(set([0, 999, 5000, 9999] + [int(x) for x in rng.integers(0, 10000, 12)]))
+    ref = oracle.exhaustive(host.subset(sample))
+    assert (per[sample] == ref).all()
+    # properties that hold at any size: counts consistent with per_set
+    c = counts.cpu().numpy()[0, :, 0]
+    exists = per[:, 0] > 0
+    for b in range(10):
+        rows = host.group == b
+        assert c[b, 1] == rows.sum()
+        assert c[b, 0] == (exists & rows & (host.valid == 1)).sum()
+        assert c[b, 2] == ((host.valid == 0) & rows).sum()
+    assert (per[:, 0] >= 0).all() and (per[:, 0] <= 694755).all()
+    assert ((per[:, 0] == 0) == (per[:, 2] == -1)).all()
+
+
+@pytest.mark.parametrize("seed,n,M", [(1, 1, 1), (2, 1, 7), (3, 2, 1), (4, 3, 4), (5, 4, 6),
+                                      (6, 5, 3), (7, 6, 5), (8, 7, 4), (9, 8, 3), (10, 4, 12),
+                                      (11, 3, 12), (12, 6, 9)])
+def test_exhaustive_random_sets(G, seed, n, M):
+    rng = np.random.default_rng(seed)
+    d = W.random_sets(rng, 37, n, M, periods=(4, 6, 8, 12, 24), b_max=2 * M + 3, cost_max=3)
+    ts = gpu_sets(G, d)
+    per, vb, _ = run_exhaustive(G, ts, bits=True)
+    ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
+    assert (per == ref).all() and (vb == rbits).all()
+
+
+def test_exhaustive_rank_windows(G):
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 5, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 3, 5, ts)
+    host = to_oracle(ts)
+    for lo, hi in [(0, 1), (5, 37), (100, 4100), (11000, 11334), (7777, 7778)]:
+        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi)
+        ref, rbits = oracle.exhaustive(host, lo, hi, bits=True)
+        assert (per == ref).all() and (vb == rbits).all(), (lo, hi)
+
+
+def test_exhaustive_contract_violation_reported(G):
+    d = W.random_sets(np.random.default_rng(5), 6, 3, 4)
+    d["D"][2, 1] = d["T"][2, 1] + 1  # D > T violates the contract
+    d["T"][4, :] = [1000003, 1000033, 1000037]  # hyperperiod overflow
+    d["D"][4, :] = d["T"][4, :]
+    ts = gpu_sets(G, d)
+    counts = torch.zeros((1, 1, 1, 3), dtype=torch.int64, device="cuda")
+    per, _, _ = run_exhaustive(G, ts, counts=counts)
+    assert per[2, 0] == -1 and per[4, 0] == -1
+    ok_rows = [0, 1, 3, 5]
+    ref = oracle.exhaustive(oracle.Sets.from_dict(d).subset(ok_rows))
+    assert (per[ok_rows] == ref).all()
+    assert counts.cpu().numpy()[0, 0, 0, 2] == 2  # counted as invalid
+
+
+# ------------------------------------------------------------------ A5
+VARIANTS = ("1G", "SMS_ACT", "SMS_INA", "BF_ACT", "BF_INA")
+
+
+def check_allocate(G, ts, host=None, variants=VARIANTS):
+    host = host or to_oracle(ts)
+    for v in variants:
+        out = G.gp_allocate(ts, v)
+        got = out.to_host()
+        ref = oracle.allocate(host, v)
+        for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
+            if not (got[key] == ref[key]).all():
+                bad = np.nonzero((got[key] != ref[key]).reshape(len(got[key]), -1).any(1))[0]
+                raise AssertionError(f"{v} {key} differs on {len(bad)} sets, first {bad[:5]}")
+
+
+def test_allocate_c1(G):
+    d = W._c1_sets()
+    check_allocate(G, gpu_sets(G, d), oracle.Sets.from_dict(d))
+
+
+def test_allocate_c2(G):
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 200, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 200, ts)
+    check_allocate(G, ts)
+
+
+def test_allocate_c4_subset(G):
+    gen = W.WORKLOADS["c4"]["gen"](R=20000)
+    ts = G.TaskSets(50 * 5, 32, 148, 50)
+    G.gp_generate(gen, W.SEED, 0, 5, ts)
+    check_allocate(G, ts)
+
+
+def test_allocate_c5_subset(G):
+    for kc, km in (W.C5_SETTINGS[0], W.C5_SETTINGS[6], W.C5_SETTINGS[15]):
+        gen = W.WORKLOADS["c5"]["gen"](R=10000, kc=kc, km=km)
+        ts = G.TaskSets(10 * 16, 16, 68, 10)
+        G.gp_generate(gen, W.SEED, 0, 16, ts)
+        check_allocate(G, ts)
+
+
+@pytest.mark.parametrize("seed,n,M", [(21, 1, 1), (22, 2, 1), (23, 5, 3), (24, 8, 4), (25, 12, 6),
+                                      (26, 20, 8), (27, 32, 16), (28, 32, 5), (29, 17, 40)])
+def test_allocate_random_sets(G, seed, n, M):
+    rng = np.random.default_rng(seed)
+    d = W.random_sets(rng, 64, n, M, periods=(20, 40, 50, 100, 200), b_max=3 * M, cost_max=6)
+    check_allocate(G, gpu_sets(G, d), oracle.Sets.from_dict(d))
+
+
+def test_allocate_contract_violation(G):
+    d = W.random_sets(np.random.default_rng(3), 4, 5, 6)
+    d["cc"][1, 0] = d["cn"][1, 0] - 1  # cc < cn
+    out = G.gp_allocate(gpu_sets(G, d), "SMS_INA").to_host()
+    assert out["ok"][1] == 0 and out["n_tests"][1] == -1
+    ref = oracle.allocate(oracle.Sets.from_dict(d).subset([0, 2, 3]), "SMS_INA")
+    for key in ("ok", "pi", "k", "n_tests"):
+        assert (out[key][[0, 2, 3]] == ref[key]).all()
+
+
+# ------------------------------------------------------------------ A6
+def test_sched_ratio_from_verdicts(G):
+    rng = np.random.default_rng(14)
+    S, n_groups, rows = 5000, 50, 5
+    d = W.random_sets(rng, S, 3, 4, n_groups=n_groups)
+    d["valid"] = (rng.random(S) > 0.1).astype(np.uint8)
+    verd = (rng.random((rows, S)) > 0.4).astype(np.uint8)
+    ts = gpu_sets(G, d)
+    counts = torch.zeros((2, n_groups, 7, 3), dtype=torch.int64, device="cuda")
+    G.gp_sched_ratio(ts, G.GP_FROM_VERDICTS, counts, verdicts=torch.as_tensor(verd).cuda(),
+                     slot0=2, n_slots=7, setting=1)
+    G.gp_sched_ratio(ts, G.GP_FROM_VERDICTS, counts, verdicts=torch.as_tensor(verd).cuda(),
+                     slot0=2, n_slots=7, setting=1)  # accumulates
+    ref = np.zeros((2, n_groups, 7, 3), np.int64)
+    h = oracle.Sets.from_dict(d)
+    oracle.sched_ratio(h, verd, 2, 7, 1, ref)
+    oracle.sched_ratio(h, verd, 2, 7, 1, ref)
+    assert (counts.cpu().numpy() == ref).all()
+
+
+def test_pipeline_step_c2_matches_oracle(G):
+    """One whole step (generate -> exhaustive -> 5 variants -> counts) vs the
+    oracle's composition of the same steps."""
+    from paper_2105_10312_b200.pipeline import Pipeline
+    p = Pipeline("c2", reps=30)
+    p.run()
+    torch.cuda.synchronize()
+    host = to_oracle(p.ts)
+    ref = np.zeros((1, 10, 6, 3), np.int64)
+    per = oracle.exhaustive(host)
+    oracle.sched_ratio(host, (per[:, 0] > 0).astype(np.uint8)[None], 0, 6, 0, ref)
+    rows = np.stack([oracle.allocate(host, v)["ok"] for v in VARIANTS])
+    oracle.sched_ratio(host, rows, 1, 6, 0, ref)
+    assert (p.counts.cpu().numpy() == ref).all()
+    assert (p.per_set.cpu().numpy() == per).all()
