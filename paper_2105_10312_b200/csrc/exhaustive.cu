@@ -28,7 +28,7 @@ namespace gp {
 
 constexpr int kWarps = 8;        // warps per CTA
 constexpr int kGrab = 16;        // items per queue grab
-constexpr int kMaxL = 8;         // candidates per lane per item
+constexpr int kMaxL = 64;        // candidates per lane per item
 
 struct ExhArgs {
   const int32_t *T, *D, *B, *cn, *cc, *fn, *fc, *group;
@@ -67,12 +67,15 @@ GP_DEV int64_t set_contract(const ExhArgs &a, int64_t set) {
 }
 
 struct WarpSmem {
-  int32_t set, H, okc, pad;
+  int32_t set, H, okc, n_multi;
   int4 rec[kEnumMaxTasks];   // per task in block order: {W offset, D, T, H/T}
   int32_t T[kEnumMaxTasks], D[kEnumMaxTasks], q[kEnumMaxTasks];
+  int32_t multi[kEnumMaxTasks];  // multi-task blocks: jj | len << 8 | start << 16
   uint32_t memmask, pad2[3];
 };
 
+// EDF-PDC of one block with SZ >= 2 tasks (records in shared memory, block
+// order, starting at `start`), all lanes at their own size s.
 template <int SZ>
 GP_DEV bool eval_block(const WarpSmem &w, const int32_t *__restrict__ Wt, int start, int32_t s,
                        int32_t H, uint32_t &events) {
@@ -87,7 +90,7 @@ GP_DEV bool eval_block(const WarpSmem &w, const int32_t *__restrict__ Wt, int st
     q[a] = r.w;
     bad |= C[a] > D[a];
   }
-  if (SZ == 1 || bad) return !bad;  // single task: schedulable iff C <= D
+  if (bad) return false;
   int32_t UH = 0;
 #pragma unroll
   for (int a = 0; a < SZ; ++a) UH += C[a] * q[a];
@@ -112,8 +115,61 @@ struct BlockDispatch<NT, NT + 1> {
   }
 };
 
+// ---- per-lane accumulation ---------------------------------------------------
+struct LaneAcc {
+  uint32_t n = 0;
+  int32_t pi = INT32_MAX;
+  uint64_t first = ~0ull, hash = 0;
+  uint64_t st_cand = 0, st_blocks = 0, st_tasks = 0;
+  uint32_t st_events = 0;
+};
+
+GP_DEV void record_ok(LaneAcc &acc, uint64_t rank, int32_t sum, uint32_t *bits, uint64_t lo) {
+  ++acc.n;
+  acc.pi = min(acc.pi, sum);
+  acc.first = rank < acc.first ? rank : acc.first;
+  acc.hash += splitmix64(rank);
+  if (bits) {
+    const uint64_t off = rank - lo;
+    atomicOr(bits + (off >> 5), 1u << (off & 31));
+  }
+}
+
+// Lexicographic successor of s, stored REVERSED (sr[0] = last part) so the
+// common step -- grow the last part while sum < M -- touches a fixed register.
+// Otherwise bump the part with the fewest followers jj >= 1 whose followers
+// have slack (sum of sr[0..jj-1] > jj) and reset its followers to 1.
 template <int NT>
-__global__ void __launch_bounds__(kWarps * 32) k_exhaustive(const ExhArgs a) {
+GP_DEV void next_sizes_rev(int M, int k, int32_t (&sr)[NT], int32_t &sum) {
+  if (sum < M) {  // common: grow the last part
+    sr[0] += 1;
+    sum += 1;
+    return;
+  }
+  if (k >= 2 && sr[0] > 1) {  // next: bump the second-to-last part, last := 1
+    sum -= sr[0] - 2;
+    sr[0] = 1;
+    sr[1] += 1;
+    return;
+  }
+  int prefix = 0, pick = -1;
+#pragma unroll
+  for (int jj = 1; jj < NT; ++jj) {
+    prefix += sr[jj - 1];
+    if (pick < 0 && jj < k && prefix > jj) pick = jj;
+  }
+  if (pick < 0) return;  // last candidate of this allocation (never stepped past)
+  int ns = 0;
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    sr[i] = i < pick ? 1 : (i == pick ? sr[i] + 1 : sr[i]);
+    ns += i < k ? sr[i] : 0;
+  }
+  sum = ns;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kWarps * 32, 3) k_exhaustive(const ExhArgs a) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int n = a.n, M = a.M;
   const EnumTables tab = build_enum_tables(smem, M, n);
@@ -123,25 +179,22 @@ __global__ void __launch_bounds__(kWarps * 32) k_exhaustive(const ExhArgs a) {
   const size_t per_warp = ((sizeof(WarpSmem) / 4 + wt_words) + 3) & ~(size_t)3;
   WarpSmem &w = *reinterpret_cast<WarpSmem *>(smem + off + per_warp * warp);
   int32_t *Wt = reinterpret_cast<int32_t *>(&w + 1);
+  const bool stats = a.stats != nullptr;
 
-  // per-lane accumulators for the current set
-  uint32_t acc_n = 0;
-  int32_t acc_pi = INT32_MAX;
-  uint64_t acc_first = ~0ull, acc_hash = 0;
-  uint32_t st_cand = 0, st_blocks = 0, st_events = 0, st_tasks = 0;
+  LaneAcc acc;
   int64_t cur = -1;
 
   auto flush = [&]() {
     if (cur < 0) return;
-    const uint32_t tot = (uint32_t)warp_sum_i32((int32_t)acc_n);
-    const int32_t pi = warp_min_i32(acc_pi);
-    uint64_t first = acc_first;
+    const uint32_t tot = (uint32_t)warp_sum_i32((int32_t)acc.n);
+    const int32_t pi = warp_min_i32(acc.pi);
+    uint64_t first = acc.first;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       uint64_t v = __shfl_xor_sync(GP_FULL, first, o);
       first = v < first ? v : first;
     }
-    const uint64_t h = warp_sum_u64(acc_hash);
+    const uint64_t h = warp_sum_u64(acc.hash);
     if (lane == 0 && tot > 0) {
       long long *ps = reinterpret_cast<long long *>(a.per_set + cur * 4);
       atomicAdd(reinterpret_cast<unsigned long long *>(ps + 0), (unsigned long long)tot);
@@ -149,10 +202,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_exhaustive(const ExhArgs a) {
       atomicMin(ps + 2, (long long)first);
       atomicAdd(reinterpret_cast<unsigned long long *>(ps + 3), h);
     }
-    acc_n = 0;
-    acc_pi = INT32_MAX;
-    acc_first = ~0ull;
-    acc_hash = 0;
+    acc.n = 0;
+    acc.pi = INT32_MAX;
+    acc.first = ~0ull;
+    acc.hash = 0;
   };
 
   for (;;) {
@@ -205,82 +258,126 @@ __global__ void __launch_bounds__(kWarps * 32) k_exhaustive(const ExhArgs a) {
       const uint32_t rho0 = c * 32u * (uint32_t)Lk;
       if (rank_pi + rho0 >= a.hi || rank_pi + min((uint64_t)per_pi, (uint64_t)rho0 + 32u * Lk) <= a.lo)
         continue;
-      // allocation pi: block label of every task, block masks, records
+      // ---- allocation pi (warp-uniform): blocks, conflict flags, records
       const uint64_t labels = unrank_rgs(tab, k, p);
       const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15) : -1;
-      uint32_t bmask[NT];
-      int bstart[NT], blen[NT];
-      int acc = 0;
+      // block j: mask, length, first position in block order; reversed copies
+      // rlen[jj], rpos[jj] describe block k-1-jj (register-static indices)
+      int rlen[NT], rpos[NT];
+      uint32_t mine = 0;
+      int mypos0 = 0, acc_pos = 0;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        bmask[j] = __ballot_sync(GP_FULL, myb == j);
-        blen[j] = __popc(bmask[j]);
-        bstart[j] = acc;
-        acc += blen[j];
-      }
-      if (lane < n) {
-        uint32_t mine = 0;
-        int st = 0;
+        const uint32_t bm = __ballot_sync(GP_FULL, myb == j);
+        const int len = __popc(bm);
+        if (j == myb) {
+          mine = bm;
+          mypos0 = acc_pos;
+        }
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
-          if (j == myb) {
-            mine = bmask[j];
-            st = bstart[j];
+        for (int jj = 0; jj < NT; ++jj)
+          if (jj == k - 1 - j) {
+            rlen[jj] = len;
+            rpos[jj] = acc_pos;
           }
+        acc_pos += len;
+      }
+#pragma unroll
+      for (int jj = 0; jj < NT; ++jj)
+        if (jj >= k) rlen[jj] = 0, rpos[jj] = 0;
+      if (lane < n) {
         const uint32_t same = ((w.memmask >> lane) & 1) ? w.memmask : ~w.memmask;
         const int x = __popc(mine & same) > 1 ? 1 : 0;  // conflict
-        const int pos = st + __popc(mine & ((1u << lane) - 1u));
+        const int pos = mypos0 + __popc(mine & ((1u << lane) - 1u));
         w.rec[pos] = make_int4((lane * 2 + x) * M - 1, w.D[lane], w.T[lane], w.q[lane]);
       }
-      __syncwarp();
-      const int32_t H = w.H;
-      // lanes: candidates rho0 + lane*Lk .. + Lk - 1
-      const uint32_t my0 = rho0 + (uint32_t)lane * (uint32_t)Lk;
-      int32_t s[NT];
-      int32_t sum = 0;
-      bool have = my0 < per_pi;
-      if (have) {
-        unrank_sizes<NT>(tab, k, my0, s);
+      if (lane == 0) {
+        int nm = 0;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) sum += (j < k) ? s[j] : 0;
-      } else {
-#pragma unroll
-        for (int j = 0; j < NT; ++j) s[j] = 1;
+        for (int jj = 0; jj < NT; ++jj)
+          if (rlen[jj] > 1) w.multi[nm++] = jj | (rlen[jj] << 8) | (rpos[jj] << 16);
+        w.n_multi = nm;
       }
-      for (int t = 0; t < Lk; ++t) {
-        const uint64_t rank = rank_pi + my0 + (uint32_t)t;
-        const bool in = have && rank >= a.lo && rank < a.hi;
-        bool ok = in;
-        st_cand += in;
+      __syncwarp();
+      // singleton blocks: W-table offset and deadline in registers
+      int32_t swoff[NT], sdl[NT];
+      int n_single = 0;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          if (j < k && __any_sync(GP_FULL, ok)) {
-            if (ok) {
-              ++st_blocks;
-              st_tasks += blen[j];
-              ok = BlockDispatch<NT, 1>::run(blen[j], w, Wt, bstart[j], s[j], H, st_events);
+      for (int jj = 0; jj < NT; ++jj) {
+        const int4 r = w.rec[rpos[jj]];
+        swoff[jj] = r.x;
+        sdl[jj] = r.y;
+        n_single += rlen[jj] == 1;
+      }
+      const int n_multi = w.n_multi;
+      const int32_t H = w.H;
+      uint32_t *bits = a.bits ? a.bits + cur * a.words : nullptr;
+      // ---- this lane's run of candidates: s-index my0 .. my0 + Lk - 1
+      const uint32_t my0 = rho0 + (uint32_t)lane * (uint32_t)Lk;
+      const uint64_t r0 = rank_pi + my0;
+      int t_hi = Lk;
+      if (a.hi <= r0) t_hi = 0;
+      else if (a.hi - r0 < (uint64_t)t_hi) t_hi = (int)(a.hi - r0);
+      if ((int64_t)t_hi > (int64_t)per_pi - (int64_t)my0) t_hi = (int)max((int64_t)0, (int64_t)per_pi - (int64_t)my0);
+      const int t_lo = a.lo > r0 ? (int)min(a.lo - r0, (uint64_t)Lk) : 0;
+      if (t_lo >= t_hi) t_hi = 0;
+      int32_t sr[NT];
+      int32_t sum = 0;
+      {
+        int32_t s[NT];
+        if (t_hi > 0) {
+          unrank_sizes<NT>(tab, k, my0, s);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) s[j] = 1;
+        }
+#pragma unroll
+        for (int jj = 0; jj < NT; ++jj) {
+          sr[jj] = 1;
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+            if (j == k - 1 - jj) sr[jj] = s[j];
+          sum += jj < k ? sr[jj] : 0;
+        }
+      }
+      if (stats && t_hi > 0) {
+        acc.st_cand += (uint64_t)(t_hi - t_lo);
+        acc.st_blocks += (uint64_t)(t_hi - t_lo) * n_single;
+        acc.st_tasks += (uint64_t)(t_hi - t_lo) * n_single;
+      }
+      const int tmax = (int)__reduce_max_sync(GP_FULL, (unsigned)t_hi);
+      for (int t = 0; t < tmax; ++t) {
+        bool ok = t >= t_lo && t < t_hi;
+        // blocks with one task: schedulable iff C <= D (C.1.7)
+#pragma unroll
+        for (int jj = 0; jj < NT; ++jj)
+          if (rlen[jj] == 1) ok &= Wt[swoff[jj] + sr[jj]] <= sdl[jj];
+        // blocks with >= 2 tasks: the EDF processor-demand test (gp_edf.cuh)
+        for (int mb = 0; mb < n_multi; ++mb) {
+          if (!__any_sync(GP_FULL, ok)) break;
+          const int e = w.multi[mb];
+          const int jj = e & 0xFF, len = (e >> 8) & 0xFF, start = e >> 16;
+          int32_t s = 0;
+#pragma unroll
+          for (int q = 0; q < NT; ++q) s = q == jj ? sr[q] : s;
+          if (ok) {
+            if (stats) {
+              ++acc.st_blocks;
+              acc.st_tasks += len;
             }
+            ok = BlockDispatch<NT, 2>::run(len, w, Wt, start, s, H, acc.st_events);
           }
         }
-        if (ok) {
-          ++acc_n;
-          acc_pi = min(acc_pi, sum);
-          acc_first = rank < acc_first ? rank : acc_first;
-          acc_hash += splitmix64(rank);
-          if (a.bits) {
-            const uint64_t off2 = rank - a.lo;
-            atomicOr(a.bits + cur * a.words + (int64_t)(off2 >> 5), 1u << (off2 & 31));
-          }
-        }
-        if (have && t + 1 < Lk) have = next_sizes<NT>(M, k, s, sum) && (my0 + t + 1 < per_pi);
+        if (ok) record_ok(acc, r0 + (uint32_t)t, sum, bits, a.lo);
+        if (t + 1 < t_hi) next_sizes_rev<NT>(M, k, sr, sum);
       }
       __syncwarp();
     }
   }
   flush();
-  if (a.stats) {
-    const uint64_t c0 = warp_sum_u64(st_cand), c1 = warp_sum_u64(st_blocks);
-    const uint64_t c2 = warp_sum_u64(st_events), c3 = warp_sum_u64(st_tasks);
+  if (stats) {
+    const uint64_t c0 = warp_sum_u64(acc.st_cand), c1 = warp_sum_u64(acc.st_blocks);
+    const uint64_t c2 = warp_sum_u64(acc.st_events), c3 = warp_sum_u64(acc.st_tasks);
     if (lane == 0) {
       atomicAdd(a.stats + 0, c0);
       atomicAdd(a.stats + 1, c1);
@@ -376,12 +473,12 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   a.stats = ex->stats; a.work_counter = ex->work_counter;
   uint64_t items = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
-    uint64_t per = a.L.per_pi[k];
-    int Lk = (int)((per + 31) / 32);
-    if (Lk > kMaxL) Lk = kMaxL;
-    if (Lk < 1) Lk = 1;
+    // balanced chunks of at most 32 * kMaxL size vectors of one allocation
+    const uint64_t per = a.L.per_pi[k];
+    const uint64_t chunks = (per + 32ull * kMaxL - 1) / (32ull * kMaxL);
+    const int Lk = (int)((per + 32ull * chunks - 1) / (32ull * chunks));
     a.lane_L[k] = Lk;
-    a.chunks[k] = (uint32_t)((per + 32ull * Lk - 1) / (32ull * Lk));
+    a.chunks[k] = (uint32_t)chunks;
     a.item_base[k] = items;
     items += a.L.n_pi[k] * a.chunks[k];
   }
@@ -399,14 +496,11 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   if (smem > 227 * 1024) return gp_fail(GP_EINVAL, "EXHAUSTIVE: shared memory need %zu B too large", smem);
   gp_status r;
   switch (n) {
-    case 1: r = launch_exh<1>(a, smem, st); break;
-    case 2: r = launch_exh<2>(a, smem, st); break;
-    case 3: r = launch_exh<3>(a, smem, st); break;
+    case 1: case 2: case 3: r = launch_exh<3>(a, smem, st); break;
     case 4: r = launch_exh<4>(a, smem, st); break;
     case 5: r = launch_exh<5>(a, smem, st); break;
     case 6: r = launch_exh<6>(a, smem, st); break;
-    case 7: r = launch_exh<7>(a, smem, st); break;
-    case 8: r = launch_exh<8>(a, smem, st); break;
+    case 7: case 8: r = launch_exh<8>(a, smem, st); break;
     default: r = launch_exh<12>(a, smem, st); break;
   }
   if (r != GP_OK) return r;

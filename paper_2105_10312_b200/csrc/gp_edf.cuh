@@ -59,7 +59,7 @@ GP_DEV int32_t pdc_cutoff(const int32_t (&C)[SZ], const int32_t (&D)[SZ], const 
   float X = 0.f;
 #pragma unroll
   for (int a = 0; a < SZ; ++a) X += (float)(T[a] - D[a]) * (float)(C[a] * q[a]);
-  const float L = X / (float)(H - UH) * 1.0001f + 2.0f;
+  const float L = __fdividef(X, (float)(H - UH)) * 1.0001f + 2.0f;
   return L >= (float)H ? H : (int32_t)L;
 }
 

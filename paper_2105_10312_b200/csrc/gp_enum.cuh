@@ -155,7 +155,7 @@ GP_DEV void unrank_sizes(const EnumTables &t, int k, uint32_t rho, int32_t (&s)[
     if (j < k) {
       int v = prev + 1;
       for (;;) {
-        uint32_t cnt = t.C(t.M - v, k - 1 - j);
+        uint32_t cnt = t.binom[(t.M - v) * (t.n + 1) + (k - 1 - j)];  // valid ranks keep a >= b >= 0
         if (rho < cnt) break;
         rho -= cnt;
         ++v;
