@@ -8,6 +8,8 @@ GPU per step (weak scaling: every rank adds its own 10,000 sets), all
 whole hot path: gp_generate -> gp_sched_ratio(EXHAUSTIVE) (enumerate + WCET +
 EDF fused) -> gp_allocate x {1G, SMS_ACT, SMS_INA, BF_ACT, BF_INA} ->
 gp_sched_ratio(FROM_VERDICTS) -> NCCL all-reduce of the integer counts.
+Heuristic-only configs (--config c4 / c5) count one candidate eval per
+EDF-PDC test the heuristics run.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--reps R]
   python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
@@ -30,8 +32,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-
 import gp_workloads as W  # noqa: E402
 
 METRIC = "candidate (taskset,partition,alloc) evals/sec at 1/2/4/8 B200; % INT/HBM roofline"
@@ -39,6 +39,7 @@ UNIT = "candidate evals/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 B200_SMS, SMSP_PER_SM, LANES = 148, 4, 32
 FALLBACK_SM_MHZ = 1965.0  # clocks.max.sm of B200 (B200_PROFILING.md)
+DEFAULT_REPS = {"c2": 1000, "c3": 1000, "c4": 2000, "c5": 1000}
 
 
 def parse():
@@ -47,27 +48,34 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c2", "c3"])
-    ap.add_argument("--reps", type=int, default=1000, help="sets per (bin) group per GPU")
+    ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--reps", type=int, default=0, help="sets per (prm, bin) group per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-sets", type=int, default=0, help="0 = auto (~15 s)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.reps = a.reps or DEFAULT_REPS[a.config]
+    return a
 
 
-def workload_config(key, reps, world):
-    wl = W.WORKLOADS[key]
-    n_cand = _count(wl["M"], wl["n"])
-    return wl, n_cand
-
-
-def _count(M, n):
-    from math import comb
+def n_candidates(M, n):
+    from math import comb, factorial
 
     def s2(n_, k):
-        from math import factorial
         return sum((-1) ** j * comb(k, j) * (k - j) ** n_ for j in range(k + 1)) // factorial(k)
     return sum(s2(n, k) * comb(M, k) for k in range(1, min(M, n) + 1))
+
+
+def peak_lane_ops():
+    """Issue ceiling in int32 lane-ops/s: 148 SM x 4 SMSP x 32 lanes x clock."""
+    mhz, src = FALLBACK_SM_MHZ, "B200 clocks.max.sm 1965 MHz (B200_PROFILING.md fallback)"
+    try:
+        with open(PEAKS) as fh:
+            pk = json.load(fh)
+        mhz = float(pk.get("sm_max_mhz", mhz))
+        src = f"MEASURED_PEAKS.json sm_max_mhz {mhz:.0f}"
+    except (OSError, ValueError):
+        pass
+    return B200_SMS * SMSP_PER_SM * LANES * mhz * 1e6, src + " x 148 SM x 4 SMSP x 32 lanes"
 
 
 # --------------------------------------------------------------------------- clocks
@@ -78,7 +86,6 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index = index
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
@@ -114,65 +121,83 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-# --------------------------------------------------------------------------- reference arm
+# --------------------------------------------------------------------------- CPU oracle
+def oracle_step(oracle, wl, gen_list, rep_begin, reps, cores, exhaustive):
+    """One oracle step on a sample: generate + [exhaustive] + 5 heuristics.
+    Returns (candidate evals, seconds)."""
+    t0 = time.perf_counter()
+    evals = 0
+    for gi, gen in enumerate(gen_list):
+        s = oracle.generate(gen, W.SEED, rep_begin, reps)
+        if exhaustive and gi == 0:
+            oracle.exhaustive(s, threads=cores)
+            evals += s.n_sets * n_candidates(wl["M"], wl["n"])
+        for v in W.VARIANT_NAMES:
+            r = oracle.allocate(s, v, threads=cores)
+            if not exhaustive:
+                evals += int(r["n_tests"].clip(min=0).sum())
+    return evals, time.perf_counter() - t0
+
+
+def gens_for(key, R):
+    wl = W.WORKLOADS[key]
+    if key == "c5":
+        return [wl["gen"](R=R, kc=kc, km=km) for kc, km in W.C5_SETTINGS]
+    return [wl["gen"](R=R)]
+
+
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     import oracle
-    wl, n_cand = workload_config(args.config, args.reps, 1)
+    wl = W.WORKLOADS[args.config]
     cores = os.cpu_count() or 1
-    gen = wl["gen"](R=args.reps)
-    sample_reps = 2  # 2 sets per bin = 20 sets per step: ~1-3 s of CPU work per step
-    sets = oracle.generate(gen, W.SEED, 0, sample_reps)
-    times = []
+    sample = {"c2": 20, "c3": 2, "c4": 1, "c5": 2}[args.config]
+    gens = gens_for(args.config, args.reps)
+    if args.config == "c5":
+        gens = gens[:4]  # 4 of the 16 coefficient settings per step
+    evs, secs = [], []
     for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        s = oracle.generate(gen, W.SEED, (it % 50) * sample_reps, sample_reps)
-        oracle.exhaustive(s, threads=cores)
-        for v in W.VARIANT_NAMES:
-            oracle.allocate(s, v, threads=cores)
-        dt = time.perf_counter() - t0
+        e, t = oracle_step(oracle, wl, gens, (it * sample) % max(1, args.reps - sample), sample,
+                           cores, wl["exhaustive"])
         if it >= args.warmup:
-            times.append(dt)
-    per_step = sets.n_sets * n_cand
-    value = per_step * len(times) / sum(times)
+            evs.append(e)
+            secs.append(t)
+    value = sum(evs) / sum(secs)
+    n_groups = gens[0]["n_prm"] * gens[0]["n_bins"]
+    desc = (f"{sample} sets per (prm,bin) group ({sample * n_groups} sets) of {wl['name']} per "
+            f"step x {len(gens)} setting(s): generate + {'exhaustive + ' if wl['exhaustive'] else ''}"
+            f"5 heuristics, C oracle on {cores} threads")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic", "config": {"workload": wl["name"], "M": wl["M"], "n": wl["n"],
-                                        "sets_per_step": sets.n_sets, "candidates_per_set": n_cand},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": wl["name"], "M": wl["M"], "n": wl["n"],
+                   "sets_per_step": sample * n_groups},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"{sets.n_sets} sets ({sample_reps} per bin) of {wl['name']} "
-                                   "per step: generate + exhaustive + 5 heuristics, C oracle, "
-                                   f"{cores} threads"},
+                         "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-# --------------------------------------------------------------------------- cpu baseline
-def cpu_baseline(key, reps, n_cand, target_s=15.0):
+def cpu_baseline(args, target_s=15.0):
     import oracle
-    wl = W.WORKLOADS[key]
-    gen = wl["gen"](R=reps)
+    wl = W.WORKLOADS[args.config]
     cores = os.cpu_count() or 1
-    probe = oracle.generate(gen, W.SEED, 0, 1)  # one set per bin, all bins
-    t0 = time.perf_counter()
-    oracle.exhaustive(probe, threads=cores)
-    dt = time.perf_counter() - t0
-    per_rep = max(dt, 1e-3)
-    k = int(max(1, min(reps, target_s / per_rep)))
-    s = oracle.generate(gen, W.SEED, 0, k)
-    t0 = time.perf_counter()
-    oracle.exhaustive(s, threads=cores)
-    dt = time.perf_counter() - t0
-    return {"value": s.n_sets * n_cand / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"first {k} sets of each of the 10 bins ({s.n_sets} sets, "
-                      f"{s.n_sets * n_cand} candidates) of {wl['name']}, exhaustive verdicts, "
-                      f"{dt:.1f} s on {cores} threads"}
+    gens = gens_for(args.config, args.reps)[:1]
+    e, t = oracle_step(oracle, wl, gens, 0, 1, cores, wl["exhaustive"])  # probe: 1 set/group
+    k = int(max(1, min(args.reps, target_s / max(t, 1e-3))))
+    e, t = oracle_step(oracle, wl, gens, 0, k, cores, wl["exhaustive"])
+    n_groups = gens[0]["n_prm"] * gens[0]["n_bins"]
+    what = "exhaustive candidates" if wl["exhaustive"] else "heuristic EDF tests"
+    return {"value": e / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {k} sets of each of the {n_groups} groups of {wl['name']} "
+                      f"({k * n_groups} sets, {e} {what}): generate + "
+                      f"{'exhaustive + ' if wl['exhaustive'] else ''}5 heuristics, {t:.1f} s "
+                      f"on {cores} threads"}
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -192,44 +217,65 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl, n_cand = workload_config(args.config, args.reps, world)
+    wl = W.WORKLOADS[args.config]
     pipe = Pipeline(args.config, reps=args.reps, rank=rank, world=world)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    exh_ev = []
+    alloc_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    dom_ev = []  # events around the dominant kernel's launches
 
-    def step(i, timed):
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        G.gp_generate(pipe.gens[0], pipe.seed, pipe.rep_begin, pipe.reps, pipe.ts, stream)
-        if timed:
-            e0.record(stream)
-        G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, pipe.counts, slot0=0, n_slots=pipe.n_slots,
-                         setting=0, per_set=pipe.per_set, work_counter=pipe.work,
-                         stats=pipe.stats, stream=stream)
-        if timed:
-            e1.record(stream)
-            exh_ev.append((e0, e1))
-        for vi, v in enumerate(pipe.variants):
-            G.gp_allocate(pipe.ts, v, pipe.alloc[vi], stream)
-        G.gp_sched_ratio(pipe.ts, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts,
-                         slot0=1, n_slots=pipe.n_slots, setting=0, stream=stream)
+    def step(timed, stats=False):
+        """One full step.  The dominant kernel is the exhaustive evaluator
+        when present, else the heuristics (gp_allocate)."""
+        for si, gen in enumerate(pipe.gens):
+            G.gp_generate(gen, pipe.seed, pipe.rep_begin, pipe.reps, pipe.ts, stream)
+            if pipe.exhaustive and si == 0:
+                e0 = e1 = None
+                if timed:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, pipe.counts, slot0=0,
+                                 n_slots=pipe.n_slots, setting=0, per_set=pipe.per_set,
+                                 work_counter=pipe.work, stats=pipe.stats if stats else None,
+                                 stream=stream)
+                if timed:
+                    e1.record(stream)
+                    dom_ev.append((e0, e1))
+            a0 = a1 = None
+            if timed and not pipe.exhaustive:
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+            for vi, v in enumerate(pipe.variants):
+                G.gp_allocate(pipe.ts, v, pipe.alloc[vi], stream,
+                              stats=alloc_stats if stats else None)
+            if a1 is not None:
+                a1.record(stream)
+                dom_ev.append((a0, a1))
+            G.gp_sched_ratio(pipe.ts, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts,
+                             slot0=1 if pipe.exhaustive else 0, n_slots=pipe.n_slots,
+                             setting=si, stream=stream)
         allreduce_counts(pipe.counts)
 
-    for i in range(args.warmup):
-        step(i, False)
+    for _ in range(args.warmup):
+        step(False)
+    # one instrumented, untimed step: per-step work figures (deterministic)
+    pipe.reset_counts()
+    alloc_stats.zero_()
+    step(False, stats=True)
     torch.cuda.synchronize()
+    exh_stats = pipe.stats.cpu().numpy().tolist() if pipe.exhaustive else [0, 0, 0, 0]
+    al_stats = alloc_stats.cpu().numpy().tolist()
     pipe.reset_counts()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     evs = []
-    for i in range(args.steps):
+    for _ in range(args.steps):
         flush.zero_()  # L2 flush between steps, outside the events
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        step(i, True)
+        step(True)
         s1.record(stream)
         evs.append((s0, s1))
     torch.cuda.synchronize()
@@ -237,45 +283,51 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    exh_ms = [a.elapsed_time(b) for a, b in exh_ev]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    dom_ms = [a.elapsed_time(b) for a, b in dom_ev]
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    cand_step_rank = pipe.candidates_per_step()
-    value = cand_step_rank * world * args.steps / (total_ms / 1e3)
-    stats = pipe.stats.cpu().numpy() / args.steps  # per launch (deterministic)
-    tests = pipe.heuristic_tests()
+    if pipe.exhaustive:
+        evals_rank = pipe.candidates_per_step()
+        unit_def = "one canonical candidate's exact verdict (C.1.6-C.1.8)"
+    else:
+        evals_rank = int(al_stats[0])
+        unit_def = "one EDF-PDC test of a (task subset, size) pair run by the heuristics"
+    value = evals_rank * world * args.steps / (total_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (exhaustive evaluator): essential
-    # integer ops per launch: 3 per task of every tested
-    # block (W lookup, C<=D compare, U multiply-add), 4 per deadline examined
-    # (min-select, add, compare, advance), 4 per candidate (successor, verdict).
-    ops = 3 * stats[3] + 4 * stats[2] + 4 * stats[0]
-    exh_avg_s = statistics.mean(exh_ms) / 1e3
-    peak_mhz = FALLBACK_SM_MHZ
-    peak_src = "B200 clocks.max.sm 1965 MHz (B200_PROFILING.md)"
-    try:
-        with open(PEAKS) as fh:
-            pk = json.load(fh)
-        peak_mhz = float(pk.get("sm_max_mhz", peak_mhz))
-        peak_src = f"MEASURED_PEAKS.json sm_max_mhz {peak_mhz:.0f}"
-    except (OSError, ValueError):
-        pass
-    peak_ops = B200_SMS * SMSP_PER_SM * LANES * peak_mhz * 1e6  # 1 warp-inst/clk/SMSP
-    roof = {"bound": "alu", "achieved": ops / exh_avg_s / 1e12, "peak": peak_ops / 1e12,
-            "unit": "Tops/s (int32 lane-ops)", "frac": (ops / exh_avg_s) / peak_ops,
-            "traffic": None, "kernel": "k_exhaustive<6>",
-            "ops_per_launch": float(ops), "ops_per_candidate": float(ops / max(stats[0], 1)),
-            "launch_ms": exh_avg_s * 1e3, "kernel_share_of_step": statistics.mean(exh_ms) /
-            statistics.mean(step_ms), "peak_source": peak_src + " x 148 SM x 4 SMSP x 32 lanes",
-            "events_per_candidate": float(stats[2] / max(stats[0], 1))}
+    # ---- roofline of the dominant kernel: essential int32 lane-ops per launch
+    # (DESIGN.md "Roofline"): 3 per task of every tested block (W lookup,
+    # C<=D compare, U multiply-add) + 4 per deadline examined (min-select, add,
+    # compare, advance) + 4 per candidate (successor, verdict) [exhaustive].
+    peak, peak_src = peak_lane_ops()
+    if pipe.exhaustive:
+        st = exh_stats
+        ops = 3 * st[3] + 4 * st[2] + 4 * st[0]
+        launches = 1
+        kname = f"k_exhaustive<{pipe.n if pipe.n > 3 else 3}>"
+        per_unit = ops / max(st[0], 1)
+        extra = {"candidates_per_launch": st[0], "block_tests_per_launch": st[1],
+                 "deadlines_per_launch": st[2], "events_per_candidate": st[2] / max(st[0], 1)}
+    else:
+        st = al_stats
+        ops = 3 * st[1] + 4 * st[2]
+        launches = len(pipe.variants) * len(pipe.gens)
+        kname = "k_allocate (5 variants)"
+        per_unit = ops / max(st[0], 1)
+        extra = {"edf_tests_per_step": st[0], "tasks_tested_per_step": st[1],
+                 "deadlines_per_step": st[2], "sets_per_step": st[3]}
+    dom_s = sum(dom_ms) / args.steps / 1e3  # per step (sum of the dominant launches)
+    roof = {"bound": "alu", "achieved": ops / dom_s / 1e12, "peak": peak / 1e12,
+            "unit": "T int32 lane-ops/s", "frac": (ops / dom_s) / peak, "traffic": None,
+            "kernel": kname, "launches_per_step": launches, "ops_per_step": float(ops),
+            "ops_per_unit": per_unit, "dominant_ms_per_step": dom_s * 1e3,
+            "kernel_share_of_step": (sum(dom_ms) / args.steps) / (total_ms / args.steps),
+            "peak_source": peak_src, **extra}
 
-    # ---- e2e: the same metric through the C ABI from HOST buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(G, pipe, stream, args, world, n_cand)
+        e2e = run_e2e(G, pipe, stream, args, world, evals_rank)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -283,8 +335,10 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": wl["name"], "M": wl["M"], "n": wl["n"],
                    "sets_per_gpu": pipe.ts.n_sets, "global_sets": pipe.ts.n_sets * world,
-                   "candidates_per_set": n_cand, "candidates_per_step": cand_step_rank * world,
-                   "heuristic_edf_tests_per_step": tests * world,
+                   "coefficient_settings": len(pipe.gens),
+                   "candidates_per_set": pipe.n_cand if pipe.exhaustive else None,
+                   "evals_per_step": evals_rank * world, "eval_unit": unit_def,
+                   "heuristic_edf_tests_per_step": int(al_stats[0]) * world,
                    "variants": list(pipe.variants), "parallelism": f"dp{world}",
                    "l2": "flushed between steps (256 MiB memset outside the events)",
                    "seed": W.SEED},
@@ -295,7 +349,7 @@ def main():
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, args.reps, n_cand)
+        line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -304,38 +358,42 @@ def main():
 
 
 def launches_per_step(pipe):
-    # gp_generate 1 + EXHAUSTIVE (init, main, finalize) 3 + gp_allocate x V + ratio 1
-    return 1 + 3 + len(pipe.variants) + 1
+    # per setting: gp_generate 1 + gp_allocate x V + ratio 1; + EXHAUSTIVE (init, main, finalize)
+    return len(pipe.gens) * (2 + len(pipe.variants)) + (3 if pipe.exhaustive else 0)
 
 
-def run_e2e(G, pipe, stream, args, world, n_cand):
-    """Host task sets (pinned) -> H2D -> exhaustive + allocate + ratio -> D2H."""
+def run_e2e(G, pipe, stream, args, world, evals_rank):
+    """Host task sets (pinned) -> H2D -> evaluation -> D2H, through the C ABI.
+    The host inputs are the first setting's task sets of this rank."""
     import torch
-    host = {f: getattr(pipe.ts, f).cpu().pin_memory() for f in
-            ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group")}
+    fields = ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group")
+    G.gp_generate(pipe.gens[0], pipe.seed, pipe.rep_begin, pipe.reps, pipe.ts, stream)
+    host = {f: getattr(pipe.ts, f).cpu().pin_memory() for f in fields}
     dev = G.TaskSets(pipe.ts.n_sets, pipe.ts.n_tasks, pipe.ts.M, pipe.ts.n_groups)
-    out_per = torch.empty((pipe.ts.n_sets, 4), dtype=torch.int64).pin_memory()
-    out_cnt = torch.empty(tuple(pipe.counts.shape), dtype=torch.int64).pin_memory()
-    out_ver = torch.empty(tuple(pipe.verdicts.shape), dtype=torch.uint8).pin_memory()
+    outs = [pipe.counts, pipe.verdicts] + ([pipe.per_set] if pipe.exhaustive else [])
+    host_out = [torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for t in outs]
     h2d = sum(t.numel() * t.element_size() for t in host.values())
-    d2h = sum(t.numel() * t.element_size() for t in (out_per, out_cnt, out_ver))
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
 
-    def one():
+    def one(with_stats=False):
         for f, t in host.items():
             getattr(dev, f).copy_(t, non_blocking=True)
         pipe.counts.zero_()
-        G.gp_sched_ratio(dev, G.GP_EXHAUSTIVE, pipe.counts, slot0=0, n_slots=pipe.n_slots,
-                         per_set=pipe.per_set, work_counter=pipe.work, stream=stream)
+        if pipe.exhaustive:
+            G.gp_sched_ratio(dev, G.GP_EXHAUSTIVE, pipe.counts, slot0=0, n_slots=pipe.n_slots,
+                             per_set=pipe.per_set, work_counter=pipe.work, stream=stream)
         for vi, v in enumerate(pipe.variants):
-            G.gp_allocate(dev, v, pipe.alloc[vi], stream)
-        G.gp_sched_ratio(dev, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts, slot0=1,
-                         n_slots=pipe.n_slots, stream=stream)
-        out_per.copy_(pipe.per_set, non_blocking=True)
-        out_cnt.copy_(pipe.counts, non_blocking=True)
-        out_ver.copy_(pipe.verdicts, non_blocking=True)
+            G.gp_allocate(dev, v, pipe.alloc[vi], stream, stats=stats if with_stats else None)
+        G.gp_sched_ratio(dev, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts,
+                         slot0=1 if pipe.exhaustive else 0, n_slots=pipe.n_slots, stream=stream)
+        for h, d in zip(host_out, outs):
+            h.copy_(d, non_blocking=True)
 
-    for _ in range(2):
-        one()
+    one(with_stats=True)
+    torch.cuda.synchronize()
+    evals = pipe.candidates_per_step() if pipe.exhaustive else int(stats[0].item())
+    one()
     torch.cuda.synchronize()
     evs = []
     for _ in range(args.steps):
@@ -351,11 +409,10 @@ def run_e2e(G, pipe, stream, args, world, n_cand):
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"value": pipe.ts.n_sets * n_cand * world * args.steps / (ms / 1e3), "unit": UNIT,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms / args.steps,
+    return {"value": evals * world * args.steps / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.steps,
             "path": "pinned host task sets -> H2D -> gp_sched_ratio(EXHAUSTIVE) + gp_allocate x5 "
-                    "+ gp_sched_ratio -> D2H per-set results, verdicts, counts"}
+                    "+ gp_sched_ratio -> D2H counts, verdicts, per-set results (one setting)"}
 
 
 if __name__ == "__main__":

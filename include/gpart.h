@@ -168,11 +168,14 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * of partitions, 0 when rejected by Lemma 1/2), n_tests (EDF-PDC calls; the
  * heuristic-mode "candidate eval" unit).  On a failed Algorithm 1 run the
  * partitions at the moment of failure are reported with ok = 0.
+ * stats: device uint64 [4] or NULL; += {EDF-PDC tests, tasks in tested
+ * partitions, distinct deadlines examined by the demand walks, sets} (the
+ * per-launch work figures of the roofline).
  * Errors: GP_EINVAL (bad struct / variant), GP_ECUDA.
  * ------------------------------------------------------------------------- */
 gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok, int8_t *block_of_task,
                       int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
-                      void *stream);
+                      unsigned long long *stats, void *stream);
 
 /* ---------------------------------------------------------------------------
  * A6 (and A2-A4 fused). gp_sched_ratio -- segmented reduction to the

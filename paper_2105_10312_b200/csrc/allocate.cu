@@ -31,6 +31,7 @@ struct AllocArgs {
   int16_t *bs;
   int32_t *pi, *k;
   int64_t *n_tests;
+  unsigned long long *stats;  // optional: += {EDF tests, tasks tested, deadlines examined, sets}
 };
 
 struct TaskLane {
@@ -44,8 +45,10 @@ GP_DEV int32_t task_w(const TaskLane &t, int32_t m, bool x) {
 }
 
 // Warp-cooperative EDF-PDC of partition S at size m (C.1.7).
-GP_DEV bool warp_pdc(const TaskLane &t, uint32_t S, int32_t m, int32_t H) {
+GP_DEV bool warp_pdc(const TaskLane &t, uint32_t S, int32_t m, int32_t H, uint64_t &st_tasks,
+                     uint64_t &st_events) {
   const int lane = threadIdx.x & 31;
+  st_tasks += __popc(S);
   const bool in = (S >> lane) & 1u;
   const bool x = __popc(S & t.same) > 1;  // conflict
   const int32_t C = in ? task_w(t, m, x) : 0;
@@ -66,6 +69,7 @@ GP_DEV bool warp_pdc(const TaskLane &t, uint32_t S, int32_t m, int32_t H) {
     const int32_t tt = warp_min_i32(nx);
     if (tt > lcut) return true;
     const bool hit = nx == tt;
+    ++st_events;
     dem += warp_sum_i32(hit ? C : 0);
     nx += hit ? t.T : 0;
     if (dem > tt) return false;
@@ -82,21 +86,72 @@ GP_DEV int32_t warp_uh(const TaskLane &t, uint32_t S, int32_t m) {
 
 // Per-lane two-task EDF-PDC (ACT prefill), same exact shortcuts.
 GP_DEV bool pair_pdc(const int32_t (&C)[2], const int32_t (&D)[2], const int32_t (&T)[2],
-                     const int32_t (&q)[2], int32_t H) {
+                     const int32_t (&q)[2], int32_t H, uint32_t &ev) {
   if (C[0] > D[0] || C[1] > D[1]) return false;
   const int32_t UH = C[0] * q[0] + C[1] * q[1];
   if (UH > H) return false;
   const int32_t lcut = pdc_cutoff<2>(C, D, T, q, H, UH);
-  uint32_t ev = 0;
   return pdc_walk<2>(C, D, T, lcut, ev);
 }
 
 struct WarpScratch {
-  int32_t ord[32];   // ord[r] = slot with par_list rank r
-  int32_t lab[32];   // output label of task i
-  int32_t size[32];  // size of output label j
-  uint32_t forb[32]; // ACT: forbidden task row
+  int32_t ord[32];    // ord[r] = slot with par_list rank r
+  int32_t lab[32];    // output label of task i
+  int32_t size[32];   // size of output label j
+  uint32_t forb[32];  // ACT: forbidden task row
+  int32_t plist[32];  // eligible partners of the selected partition, par_list order
+  // the set's tasks, for the lane-serial merge tests
+  int32_t T[32], D[32], B[32], cn[32], cc[32], fn[32], fc[32], q[32];
+  uint32_t same[32];
 };
+
+// Algorithm 2 merge of partition S (<= NS tasks) by ONE lane: sizes
+// m = lo .. hi in order (Def. 3 bound hi = |P1| + |P2| - 1), an EDF-PDC test
+// each.  Returns the first schedulable m (0 if none) and U*H there.
+template <int NS>
+GP_DEV int32_t serial_merge(const WarpScratch &w, uint32_t S, int32_t lo, int32_t hi, int32_t H,
+                            int32_t &uh_out, int64_t &tests, uint64_t &st_tasks,
+                            uint32_t &st_events) {
+  int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS];
+  const int cnt = __popc(S);
+  uint32_t bits = S;
+#pragma unroll
+  for (int a = 0; a < NS; ++a) {
+    const bool v = bits != 0;
+    const int i = v ? __ffs(bits) - 1 : 0;
+    bits &= bits - 1u;
+    const bool x = __popc(S & w.same[i]) > 1;  // conflict
+    T[a] = v ? w.T[i] : INT32_MAX;
+    D[a] = v ? w.D[i] : INT32_MAX;
+    B[a] = v ? w.B[i] : 1;
+    c[a] = v ? (x ? w.cc[i] : w.cn[i]) : 0;
+    f[a] = v ? (x ? w.fc[i] : w.fn[i]) : 0;
+    q[a] = v ? w.q[i] : 0;
+  }
+  for (int32_t m = lo; m <= hi; ++m) {
+    ++tests;
+    st_tasks += cnt;
+    int32_t C[NS];
+    bool bad = false;
+#pragma unroll
+    for (int a = 0; a < NS; ++a) {
+      C[a] = c[a] ? wcet_sat(B[a], c[a], f[a], m) : 0;
+      bad |= C[a] > D[a];
+    }
+    if (bad) continue;
+    int32_t UH = 0;
+#pragma unroll
+    for (int a = 0; a < NS; ++a) UH += C[a] * q[a];
+    if (UH > H) continue;
+    if (cnt > 1) {
+      const int32_t lcut = pdc_cutoff<NS>(C, D, T, q, H, UH);
+      if (!pdc_walk<NS>(C, D, T, lcut, st_events)) continue;
+    }
+    uh_out = UH;
+    return m;
+  }
+  return 0;
+}
 
 __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
   __shared__ WarpScratch scr_all[8];
@@ -104,6 +159,9 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
   WarpScratch &scr = scr_all[wid];
   const int n = a.n, M = a.M;
   const uint32_t all = n == 32 ? GP_FULL : ((1u << n) - 1u);
+  uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // warp-uniform
+  uint64_t st_pair_tasks = 0;                                        // per lane
+  uint32_t st_pair_events = 0;                                       // per lane
   for (int64_t set = (int64_t)blockIdx.x * 8 + wid; set < a.n_sets; set += (int64_t)gridDim.x * 8) {
     const int64_t o = set * n + lane;
     TaskLane t;
@@ -127,6 +185,10 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     const bool contract = __all_sync(GP_FULL, fields_ok) && h > 0;
     const int32_t H = contract ? (int32_t)h : 1;
     t.q = (contract && t.in) ? H / t.T : 0;
+    scr.T[lane] = t.T; scr.D[lane] = t.D; scr.B[lane] = t.B; scr.cn[lane] = t.cn;
+    scr.cc[lane] = t.cc; scr.fn[lane] = t.fn; scr.fc[lane] = t.fc; scr.q[lane] = t.q;
+    scr.same[lane] = t.same;
+    __syncwarp();
 
     int64_t tests = 0;
     bool ok = false;
@@ -140,7 +202,7 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     } else if (a.variant == GP_1G) {
       // 1G: the whole GPU as one partition
       tests = 1;
-      ok = warp_pdc(t, all, M, H);
+      ok = warp_pdc(t, all, M, H, st_tasks, st_events);
       pm = lane == 0 ? all : 0;
       psz = lane == 0 ? M : 0;
       stage = 1;
@@ -201,7 +263,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
                   ++my_tests;
                   const int32_t C[2] = {wcet_sat(Bi, ci, fi, m), wcet_sat(Bj, cj, fj, m)};
                   const int32_t Dv[2] = {Di, Dj}, Tv[2] = {Ti, Tj}, qv[2] = {qi, qj};
-                  merged = pair_pdc(C, Dv, Tv, qv, H);
+                  st_pair_tasks += 2;
+                  merged = pair_pdc(C, Dv, Tv, qv, H, st_pair_events);
                 }
                 if (!merged) {
                   atomicOr(&scr.forb[i], 1u << j);
@@ -251,7 +314,61 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
             const int32_t szP = __shfl_sync(GP_FULL, psz, P);
             int best = -1;
             int32_t best_m = 0, best_uh = 0;
-            for (int r = 0; r < len; ++r) {
+            // eligible partners in par_list order -> lane e holds partner plist[e]
+            const int Qr = lane < len ? scr.ord[lane] : 0;
+            const bool el = lane < len && ((elig >> Qr) & 1u);
+            const uint32_t elb = __ballot_sync(GP_FULL, el);
+            if (el) scr.plist[__popc(elb & ((1u << lane) - 1u))] = Qr;
+            __syncwarp();
+            const int E = __popc(elb);
+            const int Qe = lane < E ? scr.plist[lane] : 0;
+            const uint32_t pmQe = __shfl_sync(GP_FULL, pm, Qe);
+            const int32_t szQe = __shfl_sync(GP_FULL, psz, Qe);
+            const uint32_t Se = pmP | pmQe;
+            const int maxcnt = __reduce_max_sync(GP_FULL, lane < E ? (unsigned)__popc(Se) : 0u);
+            bool done_round = false;
+            if (maxcnt <= 8) {
+              // every partner's merge scan runs on its own lane (exact: the scans
+              // of one round are independent; only failures feed later rounds)
+              int64_t my_tests = 0;
+              int32_t got = 0, uh = 0;
+              if (lane < E) {
+                const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
+                got = maxcnt <= 4
+                          ? serial_merge<4>(scr, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events)
+                          : serial_merge<8>(scr, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+              }
+              const uint32_t succ = __ballot_sync(GP_FULL, lane < E && got > 0);
+              int cut = E;  // partners whose tests the sequential order performs
+              if (sms) {
+                uint64_t key = (lane < E && got > 0)
+                                   ? ((uint64_t)got << 40) | ((uint64_t)(uint32_t)uh << 8) | (uint64_t)Qe
+                                   : ~0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  const uint64_t k2 = __shfl_xor_sync(GP_FULL, key, o);
+                  key = k2 < key ? k2 : key;
+                }
+                if (key != ~0ull) {
+                  best = (int)(key & 0xFF);
+                  best_m = (int32_t)(key >> 40);
+                  best_uh = (int32_t)((key >> 8) & 0xFFFFFFFFu);
+                }
+              } else if (succ) {  // BF: the first success in par_list order commits
+                cut = __ffs(succ);  // partners 0 .. cut-1 were tried
+                const int e0 = cut - 1;
+                best = __shfl_sync(GP_FULL, Qe, e0);
+                best_m = __shfl_sync(GP_FULL, got, e0);
+                best_uh = __shfl_sync(GP_FULL, uh, e0);
+              }
+              tests += warp_sum_i64(lane < cut ? my_tests : 0);
+              const bool failed = lane < cut && lane < E && got == 0;
+              const uint32_t failQ = warp_or_u32(failed ? (1u << Qe) : 0u);
+              if (lane == P) pex |= failQ;                 // add_to_forbidden_moves(P, Q)
+              if ((failQ >> lane) & 1u) pex |= 1u << P;
+              done_round = true;
+            }
+            for (int r = 0; r < len && !done_round; ++r) {
               const int Q = scr.ord[r];
               if (!((elig >> Q) & 1u)) continue;
               const uint32_t pmQ = __shfl_sync(GP_FULL, pm, Q);
@@ -260,7 +377,7 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
               int32_t got = 0;  // Algorithm 2: linear scan, m < |P1| + |P2| (Def. 3)
               for (int32_t m = max(szP, szQ); m < szP + szQ; ++m) {
                 ++tests;
-                if (warp_pdc(t, S, m, H)) {
+                if (warp_pdc(t, S, m, H, st_tasks, st_events)) {
                   got = m;
                   break;
                 }
@@ -328,6 +445,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
       a.bot[o] = (int8_t)(stage ? scr.lab[lane] : -1);
       a.bs[o] = (int16_t)((stage && lane < kk) ? scr.size[lane] : 0);
     }
+    st_sets += 1;
+    st_tests += tests > 0 ? (uint64_t)tests : 0;
     if (lane == 0) {
       a.ok[set] = ok ? 1 : 0;
       a.pi[set] = Pi_out;
@@ -336,13 +455,23 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     }
     __syncwarp();
   }
+  if (a.stats) {
+    const uint64_t pt = warp_sum_u64(st_pair_tasks), pe = warp_sum_u64(st_pair_events);
+    if (lane == 0) {
+      atomicAdd(a.stats + 0, (unsigned long long)st_tests);
+      atomicAdd(a.stats + 1, (unsigned long long)(st_tasks + pt));
+      atomicAdd(a.stats + 2, (unsigned long long)(st_events + pe));
+      atomicAdd(a.stats + 3, (unsigned long long)st_sets);
+    }
+  }
 }
 
 }  // namespace gp
 
 extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok,
                                  int8_t *block_of_task, int16_t *block_size, int32_t *pi,
-                                 int32_t *k, int64_t *n_tests, void *stream) {
+                                 int32_t *k, int64_t *n_tests, unsigned long long *stats,
+                                 void *stream) {
   using namespace gp;
   if (!ts || ts->n_tasks < 1 || ts->n_tasks > kMaxTasks || ts->M < 1 || ts->M > 1024 ||
       ts->n_sets < 0)
@@ -353,7 +482,8 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *o
       !ts->B || !ts->cn || !ts->cc || !ts->fn || !ts->fc || !ts->type)
     return gp_fail(GP_EINVAL, "gp_allocate: null pointer");
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
-              ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests};
+              ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
+              stats};
   int64_t grid = ((int64_t)ts->n_sets + 7) / 8;
   if (grid > 148 * 64) grid = 148 * 64;
   k_allocate<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);

@@ -37,9 +37,24 @@ GP_DEV int64_t lcm_capped(int64_t a, int64_t b, int64_t cap) {
   return q * b;
 }
 
+// ceil(B/m) for 0 <= B, 1 <= m <= 1024 without an integer division when B is
+// small (< 2^22: every generated set, b_max <= 4096): a float reciprocal
+// estimate is within 1 of the quotient and one correction each way makes it
+// exact.
+GP_DEV int32_t ceil_div_pos(int32_t B, int32_t m) {
+  const int32_t num = B + m - 1;
+  if (B < (1 << 22)) {
+    int32_t q = (int32_t)((float)num * __frcp_rn((float)m));
+    q += (q + 1) * m <= num;
+    q -= q * m > num;
+    return q;
+  }
+  return num / m;
+}
+
 // W(m) = ceil(B/m)*c + f in 64-bit, saturated to INT32_MAX (C.1.3).
 GP_DEV int32_t wcet_sat(int32_t B, int32_t c, int32_t f, int32_t m) {
-  int64_t w = (int64_t)((B + m - 1) / m) * (int64_t)c + (int64_t)f;
+  int64_t w = (int64_t)ceil_div_pos(B, m) * (int64_t)c + (int64_t)f;
   return w > INT32_MAX ? INT32_MAX : (int32_t)w;
 }
 

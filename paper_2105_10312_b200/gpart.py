@@ -66,7 +66,7 @@ _lib.gp_count_candidates.argtypes = [C.c_int32, C.c_int32, _P]
 _lib.gp_enumerate.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _P, _P, _P]
 _lib.gp_wcet.argtypes = [_P, _P, _P, _P, C.c_int64, _P, _P, _P]
 _lib.gp_wcet_per_sm.argtypes = [C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P]
-_lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P]
+_lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.gp_sched_ratio.argtypes = [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 _P, _P, _P]
 for _f in ("gp_generate", "gp_count_candidates", "gp_enumerate", "gp_wcet", "gp_wcet_per_sm",
@@ -206,14 +206,14 @@ class AllocOut:
                 for k in ("ok", "block_of_task", "block_size", "pi", "k", "n_tests")}
 
 
-def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None):
+def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=None):
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     if out is None:
         out = AllocOut(ts.n_sets, ts.n_tasks, ts.T.device)
     s = ts.struct()
     _check(_lib.gp_allocate(C.byref(s), v, _ptr(out.ok), _ptr(out.block_of_task),
                             _ptr(out.block_size), _ptr(out.pi), _ptr(out.k), _ptr(out.n_tests),
-                            _stream(stream)))
+                            _ptr(stats), _stream(stream)))
     return out
 
 

@@ -68,7 +68,7 @@ class Pipeline:
 
     @property
     def rep_begin(self):
-        return self.rank * self.reps
+        return shard_plan(self.rank, self.world, self.reps)[0]
 
     def run(self, stream=None):
         """Enqueue one full step (no host synchronisation)."""
@@ -101,6 +101,17 @@ class Pipeline:
         self.counts.zero_()
         if self.exhaustive and self.stats is not None:
             self.stats.zero_()
+
+
+def shard_plan(rank: int, world: int, reps_per_rank: int):
+    """Weak-scaling shard of the repetition axis: every rank
+    takes the same number of repetitions of EVERY (prm, bin) group, so all
+    ranks see the same utilisation mix.  Returns (rep_begin, rep_count,
+    sets_per_group) for gp_generate; the union over ranks is every set of the
+    world-size job exactly once, and integer counts sum exactly."""
+    if not (0 <= rank < world) or reps_per_rank < 1:
+        raise ValueError("bad shard")
+    return rank * reps_per_rank, reps_per_rank, reps_per_rank * world
 
 
 def allreduce_counts(counts: torch.Tensor):
