@@ -32,16 +32,35 @@ struct AllocArgs {
   int32_t *pi, *k;
   int64_t *n_tests;
   unsigned long long *stats;  // optional: += {EDF tests, tasks tested, deadlines examined, sets}
+  int32_t use_tab;            // per-warp table of ceil(B_i/m) in dynamic shared memory
 };
+
+// ceil(B_i / m) from the warp's per-set table (uint16, built once per set)
+// or computed directly when the table is off or B does not fit 16 bits.
+struct Waves {
+  const uint16_t *tab;  // [n][M] or null
+  int32_t M;
+  GP_DEV int32_t operator()(int i, int32_t B, int32_t m) const {
+    // merged sizes may exceed M (Alg. 2 scans up to |P1|+|P2|-1): compute those
+    return (tab && m <= M) ? (int32_t)tab[i * M + m - 1] : ceil_div_pos(B, m);
+  }
+};
+
+GP_DEV int32_t w_from_waves(int32_t waves, int32_t c, int32_t f) {
+  const int64_t w = (int64_t)waves * (int64_t)c + (int64_t)f;
+  return w > INT32_MAX ? INT32_MAX : (int32_t)w;
+}
 
 struct TaskLane {
   int32_t T, D, B, cn, cc, fn, fc, q;
   uint32_t same;  // mask of tasks with my type
   bool in;        // lane < n
+  Waves wv;
 };
 
 GP_DEV int32_t task_w(const TaskLane &t, int32_t m, bool x) {
-  return x ? wcet_sat(t.B, t.cc, t.fc, m) : wcet_sat(t.B, t.cn, t.fn, m);
+  const int32_t wv = t.wv(threadIdx.x & 31, t.B, m);
+  return x ? w_from_waves(wv, t.cc, t.fc) : w_from_waves(wv, t.cn, t.fn);
 }
 
 // Warp-cooperative EDF-PDC of partition S at size m (C.1.7).
@@ -109,10 +128,10 @@ struct WarpScratch {
 // m = lo .. hi in order (Def. 3 bound hi = |P1| + |P2| - 1), an EDF-PDC test
 // each.  Returns the first schedulable m (0 if none) and U*H there.
 template <int NS>
-GP_DEV int32_t serial_merge(const WarpScratch &w, uint32_t S, int32_t lo, int32_t hi, int32_t H,
-                            int32_t &uh_out, int64_t &tests, uint64_t &st_tasks,
-                            uint32_t &st_events) {
-  int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS];
+GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, uint32_t S, int32_t lo,
+                            int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
+                            uint64_t &st_tasks, uint32_t &st_events) {
+  int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   const int cnt = __popc(S);
   uint32_t bits = S;
 #pragma unroll
@@ -124,6 +143,7 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, uint32_t S, int32_t lo, int32_
     T[a] = v ? w.T[i] : INT32_MAX;
     D[a] = v ? w.D[i] : INT32_MAX;
     B[a] = v ? w.B[i] : 1;
+    id[a] = i;
     c[a] = v ? (x ? w.cc[i] : w.cn[i]) : 0;
     f[a] = v ? (x ? w.fc[i] : w.fn[i]) : 0;
     q[a] = v ? w.q[i] : 0;
@@ -135,7 +155,7 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, uint32_t S, int32_t lo, int32_
     bool bad = false;
 #pragma unroll
     for (int a = 0; a < NS; ++a) {
-      C[a] = c[a] ? wcet_sat(B[a], c[a], f[a], m) : 0;
+      C[a] = c[a] ? w_from_waves(wv(id[a], B[a], m), c[a], f[a]) : 0;
       bad |= C[a] > D[a];
     }
     if (bad) continue;
@@ -155,9 +175,11 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, uint32_t S, int32_t lo, int32_
 
 __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
   __shared__ WarpScratch scr_all[8];
+  extern __shared__ uint16_t wtab_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpScratch &scr = scr_all[wid];
   const int n = a.n, M = a.M;
+  uint16_t *wtab = a.use_tab ? wtab_all + (size_t)wid * n * M : nullptr;
   const uint32_t all = n == 32 ? GP_FULL : ((1u << n) - 1u);
   uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // warp-uniform
   uint64_t st_pair_tasks = 0;                                        // per lane
@@ -188,6 +210,17 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     scr.T[lane] = t.T; scr.D[lane] = t.D; scr.B[lane] = t.B; scr.cn[lane] = t.cn;
     scr.cc[lane] = t.cc; scr.fn[lane] = t.fn; scr.fc[lane] = t.fc; scr.q[lane] = t.q;
     scr.same[lane] = t.same;
+    // per-set table of ceil(B_i/m) (the wave counts of C.1.3), if B fits 16 bits
+    const bool tab_ok = wtab && __all_sync(GP_FULL, !t.in || t.B <= 65535);
+    __syncwarp();
+    if (tab_ok) {
+      for (int e = lane; e < n * M; e += 32) {
+        const int i = e / M, m = e - i * M + 1;
+        wtab[e] = (uint16_t)ceil_div_pos(scr.B[i], m);
+      }
+    }
+    t.wv.tab = tab_ok ? wtab : nullptr;
+    t.wv.M = M;
     __syncwarp();
 
     int64_t tests = 0;
@@ -261,7 +294,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
                 bool merged = false;
                 for (int32_t m = max(mi_, mj_); m < mi_ + mj_ && !merged; ++m) {
                   ++my_tests;
-                  const int32_t C[2] = {wcet_sat(Bi, ci, fi, m), wcet_sat(Bj, cj, fj, m)};
+                  const int32_t C[2] = {w_from_waves(t.wv(i, Bi, m), ci, fi),
+                                        w_from_waves(t.wv(j, Bj, m), cj, fj)};
                   const int32_t Dv[2] = {Di, Dj}, Tv[2] = {Ti, Tj}, qv[2] = {qi, qj};
                   st_pair_tasks += 2;
                   merged = pair_pdc(C, Dv, Tv, qv, H, st_pair_events);
@@ -276,35 +310,44 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
             __syncwarp();
             forb_row = scr.forb[lane];
           }
-          // Algorithm 1 main loop
+          // Algorithm 1 main loop.  par_list order and the ACT exclusions depend
+          // only on the partitions, so they are recomputed after commits only.
+          bool dirty = true;
+          int rank = 0, len = 0;
+          bool live = false;
+          uint32_t livemask = 0, forb_slots = 0;
           for (;;) {
-            // par_list order: (U*H desc, slot asc)
-            const bool live = pm != 0;
-            const uint32_t livemask = __ballot_sync(GP_FULL, live);
-            int rank = 0;
-            for (int s2 = 0; s2 < 32; ++s2) {
-              const int32_t u2 = __shfl_sync(GP_FULL, puh, s2);
-              rank += ((livemask >> s2) & 1u) && (u2 > puh || (u2 == puh && s2 < lane));
+            if (dirty) {
+              // par_list order: (U*H desc, slot asc)
+              live = pm != 0;
+              livemask = __ballot_sync(GP_FULL, live);
+              rank = 0;
+              for (int s2 = 0; s2 < 32; ++s2) {
+                const int32_t u2 = __shfl_sync(GP_FULL, puh, s2);
+                rank += ((livemask >> s2) & 1u) && (u2 > puh || (u2 == puh && s2 < lane));
+              }
+              if (live) scr.ord[rank] = lane;
+              __syncwarp();
+              len = __popc(livemask);
+              uint32_t F = 0;  // tasks forbidden with a task of my partition (ACT)
+              if (act)
+                for (int a2 = 0; a2 < n; ++a2) {
+                  const uint32_t fr = __shfl_sync(GP_FULL, forb_row, a2);
+                  if ((pm >> a2) & 1u) F |= fr;
+                }
+              forb_slots = 0;
+              if (act)
+                for (int s2 = 0; s2 < 32; ++s2) {
+                  const uint32_t m2 = __shfl_sync(GP_FULL, pm, s2);
+                  if (m2 & F) forb_slots |= 1u << s2;
+                }
+              dirty = false;
             }
-            if (live) scr.ord[rank] = lane;
-            __syncwarp();
-            const int len = __popc(livemask);
             if (Pi <= M) {
               ok = true;
               break;
             }
             // Algorithm 3: eligibility of every slot, pick the first in order
-            uint32_t F = 0;  // tasks forbidden with a task of my partition (ACT)
-            if (act)
-              for (int a2 = 0; a2 < n; ++a2) {
-                const uint32_t fr = __shfl_sync(GP_FULL, forb_row, a2);
-                if ((pm >> a2) & 1u) F |= fr;
-              }
-            uint32_t forb_slots = 0;
-            for (int s2 = 0; s2 < 32; ++s2) {
-              const uint32_t m2 = __shfl_sync(GP_FULL, pm, s2);
-              if (m2 & F) forb_slots |= 1u << s2;
-            }
             const uint32_t elig_mine = live ? (livemask & ~(1u << lane) & ~pex & ~forb_slots) : 0;
             const int cand_rank = warp_min_i32(elig_mine ? rank : 99);
             if (cand_rank == 99) break;  // no selectable partition: fail (Alg. 1 l.6-7)
@@ -335,8 +378,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
               if (lane < E) {
                 const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
                 got = maxcnt <= 4
-                          ? serial_merge<4>(scr, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events)
-                          : serial_merge<8>(scr, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                          ? serial_merge<4>(scr, t.wv, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events)
+                          : serial_merge<8>(scr, t.wv, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
               }
               const uint32_t succ = __ballot_sync(GP_FULL, lane < E && got > 0);
               int cut = E;  // partners whose tests the sequential order performs
@@ -421,6 +464,7 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
                 pex = 0;
               }
               pex &= ~((1u << keep) | (1u << drop));
+              dirty = true;
             }
           }
         }
@@ -481,11 +525,17 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *o
   if (!ok || !block_of_task || !block_size || !pi || !k || !n_tests || !ts->T || !ts->D ||
       !ts->B || !ts->cn || !ts->cc || !ts->fn || !ts->fc || !ts->type)
     return gp_fail(GP_EINVAL, "gp_allocate: null pointer");
+  // per-warp ceil(B/m) table: 8 warps x n x M x 2 bytes when it fits (C4: 76 KB)
+  size_t tab = (size_t)8 * ts->n_tasks * ts->M * sizeof(uint16_t);
+  const bool use_tab = tab <= 100 * 1024;
+  if (!use_tab) tab = 0;
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-              stats};
+              stats, use_tab ? 1 : 0};
+  if (tab > 48 * 1024)
+    cudaFuncSetAttribute(k_allocate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
   int64_t grid = ((int64_t)ts->n_sets + 7) / 8;
   if (grid > 148 * 64) grid = 148 * 64;
-  k_allocate<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+  k_allocate<<<(unsigned)grid, 256, tab, (cudaStream_t)stream>>>(a);
   return gp_cuda_check("gp_allocate");
 }
