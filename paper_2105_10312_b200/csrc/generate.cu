@@ -79,45 +79,55 @@ __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
     const uint8_t typ = ((uint64_t)x0 < pq) ? 1 : 0;
     int32_t pidx = (int32_t)(((uint64_t)x1 * (uint64_t)a.n_periods) >> 32);          // A-11
     const int32_t Bv = 1 + (int32_t)(((uint64_t)x2 * (uint64_t)a.b_max) >> 32);     // A-13
-    // spacing point; lanes >= n-1 carry the pad U_q so they sort last
-    int64_t pt = (j < n - 1) ? (int64_t)(((uint64_t)x3 * (uint64_t)(Uq + 1)) >> 32) : Uq;
+    // spacing point; lanes >= n-1 carry the pad U_q so they sort last (U_q < 2^31)
+    uint32_t pt = (j < n - 1) ? (uint32_t)(((uint64_t)x3 * (uint64_t)(Uq + 1)) >> 32) : (uint32_t)Uq;
     // bitonic sort ascending across the G lanes of the group
     for (int kk = 2; kk <= G; kk <<= 1) {
       for (int s = kk >> 1; s > 0; s >>= 1) {
-        int64_t o = __shfl_xor_sync(GP_FULL, pt, s);
-        bool asc = (j & kk) == 0, lower = (j & s) == 0;
-        pt = (lower == asc) ? (o < pt ? o : pt) : (o > pt ? o : pt);
+        const uint32_t o = __shfl_xor_sync(GP_FULL, pt, s);
+        const bool asc = (j & kk) == 0, lower = (j & s) == 0;
+        pt = (lower == asc) ? min(o, pt) : max(o, pt);
       }
     }
-    int64_t left = __shfl_up_sync(GP_FULL, pt, 1, G);
+    uint32_t left = __shfl_up_sync(GP_FULL, pt, 1, G);
     if (j == 0) left = 0;
-    const int64_t u = pt - left;  // UUniFast via sorted spacings (A-12)
+    const uint64_t u = pt - left;  // UUniFast via sorted spacings (A-12)
     // period bump while the baseline execution time is "not reasonable" (A-10)
     int64_t T = (int64_t)a.menu[pidx] * a.Q;
-    int64_t ab = (u * T) >> 20;
+    int64_t ab = (int64_t)((u * (uint64_t)T) >> 20);
     const int64_t need = Bv > a.Q ? Bv : a.Q;
     while (ab < need && pidx < a.n_periods - 1) {
       ++pidx;
       T = (int64_t)a.menu[pidx] * a.Q;
-      ab = (u * T) >> 20;
+      ab = (int64_t)((u * (uint64_t)T) >> 20);
     }
-    const int64_t D = 3 * T / 4;
-    int64_t cn = ceil_div64(ab, Bv);
-    if (cn < 1) cn = 1;
-    const int64_t fn = ceil_div64(ab * (typ ? a.beta_m : a.beta_c), a.beta_den);
-    const int64_t kf = typ ? a.km : a.kc;
-    const int64_t cc = ceil_div64(cn * kf, a.k_den), fc = ceil_div64(fn * kf, a.k_den);
-    const bool feasible = ((int64_t)((Bv + a.M - 1) / a.M)) * cn + fn <= D;      // A-9
+    // host validation bounds a <= M * Tmax < 2^31, so 32-bit arithmetic is exact below
+    const uint32_t a32 = (uint32_t)ab, T32 = (uint32_t)T;
+    const uint32_t D = 3u * (T32 / 4u);                                            // P:944 (4 | T)
+    uint32_t cn = (a32 + (uint32_t)Bv - 1u) / (uint32_t)Bv;
+    if (cn < 1u) cn = 1u;
+    // fn = ceil(a * beta_num / beta_den) without 64-bit division: a = qd*den + r
+    const uint32_t bnum = typ ? (uint32_t)a.beta_m : (uint32_t)a.beta_c, bden = (uint32_t)a.beta_den;
+    const uint32_t qd = a32 / bden, rd = a32 - qd * bden;
+    const uint32_t fn = qd * bnum + (rd * bnum + bden - 1u) / bden;
+    const uint32_t waves = (uint32_t)ceil_div_pos(Bv, a.M);
+    const bool feasible = (uint64_t)waves * cn + fn <= (uint64_t)D;                // A-9
     const unsigned bad = __ballot_sync(GP_FULL, (j < n) && !feasible) & gmask;
     if (!done) {
-      oT = (int32_t)T; oD = (int32_t)D; oB = Bv;
-      ocn = (int32_t)cn; occ = (int32_t)cc; ofn = (int32_t)fn; ofc = (int32_t)fc;
+      oT = (int32_t)T32; oD = (int32_t)D; oB = Bv;
+      ocn = (int32_t)cn; ofn = (int32_t)fn;
       otype = typ;
       if (bad == 0) {
         done = true;
         valid = true;
       }
     }
+  }
+  // conflict costs of the committed draw (A-14): c^c = ceil(k cn), f^c = ceil(k fn)
+  {
+    const int64_t kf = otype ? a.km : a.kc;
+    occ = (int32_t)ceil_div64((int64_t)ocn * kf, a.k_den);
+    ofc = (int32_t)ceil_div64((int64_t)ofn * kf, a.k_den);
   }
   if (live && j < n) {
     const int64_t o = l * n + j;
@@ -169,6 +179,9 @@ extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t
   if (p->b_max < 1 || p->beta_den < 1 || p->beta_c_num < 0 || p->beta_m_num < 0 || p->k_den < 1 ||
       p->kc_num < p->k_den || p->km_num < p->k_den || p->max_attempts < 1)
     return gp_fail(GP_EINVAL, "gp_generate: bad b_max/beta/k (k >= 1 required)/max_attempts");
+  if ((int64_t)p->beta_den * (p->beta_c_num > p->beta_m_num ? p->beta_c_num : p->beta_m_num) >=
+      (1ll << 31))
+    return gp_fail(GP_EOVERFLOW, "gp_generate: beta_den * beta_num must stay below 2^31");
   if (rep_count < 0 || rep_begin + (uint64_t)rep_count > (uint64_t)p->sets_per_group)
     return gp_fail(GP_EINVAL, "gp_generate: rep range beyond sets_per_group");
   const int64_t n_groups = (int64_t)p->n_prm * p->n_bins;
