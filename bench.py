@@ -52,6 +52,12 @@ def parse():
     ap.add_argument("--reps", type=int, default=0, help="sets per (prm, bin) group per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--f3", action="store_true",
+                    help="use the subset-threshold evaluator (SURVEY §8(f) f3, a different work "
+                         "unit, reported separately) instead of the direct per-candidate path")
+    ap.add_argument("--f3-hash", action="store_true",
+                    help="with --f3, also enumerate the schedulable candidates for the verdict "
+                         "hash (parity check; counts and ratios do not need it)")
     a = ap.parse_args()
     a.reps = a.reps or DEFAULT_REPS[a.config]
     return a
@@ -63,6 +69,23 @@ def n_candidates(M, n):
     def s2(n_, k):
         return sum((-1) ** j * comb(k, j) * (k - j) ** n_ for j in range(k + 1)) // factorial(k)
     return sum(s2(n, k) * comb(M, k) for k in range(1, min(M, n) + 1))
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the latest committed
+    ncu --set full capture (profiles/rNN/ncu_metrics.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_metrics.json")),
+                       reverse=True):
+        try:
+            with open(path) as fh:
+                m = json.load(fh)
+        except (OSError, ValueError):
+            continue
+        e = m.get(workload)
+        if isinstance(e, dict) and e.get("dram_bytes") is not None:
+            return e["dram_bytes"], os.path.relpath(path, ROOT)
+    return None, None
 
 
 def peak_lane_ops():
@@ -222,6 +245,10 @@ def main():
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     alloc_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    exh_mode = G.GP_THRESHOLD if args.f3 else G.GP_EXHAUSTIVE
+    exh_flags = G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0
+    if args.f3 and not pipe.exhaustive:
+        raise SystemExit("--f3 needs an exhaustive config (c2, c3)")
     dom_ev = []  # events around the dominant kernel's launches
 
     def step(timed, stats=False):
@@ -234,10 +261,10 @@ def main():
                 if timed:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, pipe.counts, slot0=0,
+                G.gp_sched_ratio(pipe.ts, exh_mode, pipe.counts, slot0=0,
                                  n_slots=pipe.n_slots, setting=0, per_set=pipe.per_set,
                                  work_counter=pipe.work, stats=pipe.stats if stats else None,
-                                 stream=stream)
+                                 stream=stream, flags=exh_flags)
                 if timed:
                     e1.record(stream)
                     dom_ev.append((e0, e1))
@@ -291,6 +318,10 @@ def main():
     if pipe.exhaustive:
         evals_rank = pipe.candidates_per_step()
         unit_def = "one canonical candidate's exact verdict (C.1.6-C.1.8)"
+        if args.f3:
+            unit_def = ("one canonical candidate's exact verdict, resolved by the subset-threshold "
+                        "evaluator (f3: per-subset thresholds + closed-form counts; NOT one "
+                        "EDF test per candidate -- reported separately from the direct path)")
     else:
         evals_rank = int(al_stats[0])
         unit_def = "one EDF-PDC test of a (task subset, size) pair run by the heuristics"
@@ -301,7 +332,16 @@ def main():
     # C<=D compare, U multiply-add) + 4 per deadline examined (min-select, add,
     # compare, advance) + 4 per candidate (successor, verdict) [exhaustive].
     peak, peak_src = peak_lane_ops()
-    if pipe.exhaustive:
+    if pipe.exhaustive and args.f3:
+        st = exh_stats  # {sets, threshold tests, deadlines, schedulable enumerated}
+        ops = 3 * (pipe.n / 2) * st[1] + 4 * st[2] + 4 * st[3]
+        launches = 1
+        kname = "k_threshold"
+        per_unit = ops / max(st[0], 1)
+        extra = {"sets_per_launch": st[0], "threshold_tests_per_launch": st[1],
+                 "deadlines_per_launch": st[2], "schedulable_enumerated_per_launch": st[3],
+                 "ops_per_unit_is": "per set"}
+    elif pipe.exhaustive:
         st = exh_stats
         ops = 3 * st[3] + 4 * st[2] + 4 * st[0]
         launches = 1
@@ -318,8 +358,11 @@ def main():
         extra = {"edf_tests_per_step": st[0], "tasks_tested_per_step": st[1],
                  "deadlines_per_step": st[2], "sets_per_step": st[3]}
     dom_s = sum(dom_ms) / args.steps / 1e3  # per step (sum of the dominant launches)
+    traffic, traffic_src = (ncu_traffic(wl["name"]) if pipe.exhaustive and not args.f3
+                            else (None, None))
     roof = {"bound": "alu", "achieved": ops / dom_s / 1e12, "peak": peak / 1e12,
-            "unit": "T int32 lane-ops/s", "frac": (ops / dom_s) / peak, "traffic": None,
+            "unit": "T int32 lane-ops/s", "frac": (ops / dom_s) / peak, "traffic": traffic,
+            "traffic_source": traffic_src,
             "kernel": kname, "launches_per_step": launches, "ops_per_step": float(ops),
             "ops_per_unit": per_unit, "dominant_ms_per_step": dom_s * 1e3,
             "kernel_share_of_step": (sum(dom_ms) / args.steps) / (total_ms / args.steps),
@@ -333,7 +376,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": wl["name"], "M": wl["M"], "n": wl["n"],
+        "config": {"workload": wl["name"] + ("+f3_threshold" if args.f3 else "")
+                   + ("_hash" if args.f3 and args.f3_hash else ""),
+                   "M": wl["M"], "n": wl["n"],
                    "sets_per_gpu": pipe.ts.n_sets, "global_sets": pipe.ts.n_sets * world,
                    "coefficient_settings": len(pipe.gens),
                    "candidates_per_set": pipe.n_cand if pipe.exhaustive else None,
@@ -381,7 +426,9 @@ def run_e2e(G, pipe, stream, args, world, evals_rank):
             getattr(dev, f).copy_(t, non_blocking=True)
         pipe.counts.zero_()
         if pipe.exhaustive:
-            G.gp_sched_ratio(dev, G.GP_EXHAUSTIVE, pipe.counts, slot0=0, n_slots=pipe.n_slots,
+            G.gp_sched_ratio(dev, G.GP_THRESHOLD if args.f3 else G.GP_EXHAUSTIVE, pipe.counts,
+                             flags=G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0,
+                             slot0=0, n_slots=pipe.n_slots,
                              per_set=pipe.per_set, work_counter=pipe.work, stream=stream)
         for vi, v in enumerate(pipe.variants):
             G.gp_allocate(dev, v, pipe.alloc[vi], stream, stats=stats if with_stats else None)

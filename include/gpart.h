@@ -82,7 +82,7 @@ typedef struct {
 } gp_gen_params;
 
 typedef enum { GP_1G = 0, GP_SMS_ACT = 1, GP_SMS_INA = 2, GP_BF_ACT = 3, GP_BF_INA = 4 } gp_variant;
-typedef enum { GP_FROM_VERDICTS = 0, GP_EXHAUSTIVE = 1 } gp_ratio_mode;
+typedef enum { GP_FROM_VERDICTS = 0, GP_EXHAUSTIVE = 1, GP_THRESHOLD = 2 } gp_ratio_mode;
 
 /* ---------------------------------------------------------------------------
  * A1. gp_generate -- counter-based synthetic task sets (§7.1; C.1.10).
@@ -168,6 +168,11 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * of partitions, 0 when rejected by Lemma 1/2), n_tests (EDF-PDC calls; the
  * heuristic-mode "candidate eval" unit).  On a failed Algorithm 1 run the
  * partitions at the moment of failure are reported with ok = 0.
+ * efficiency: device int64 [n_sets][4] or NULL (P:965-966,
+ * P:1009-1014): the scheduled workload as work per period scaled by
+ * the set's hyperperiod H -- {lower = sum cn_i B_i H/T_i (no conflict),
+ * upper = sum cc_i B_i H/T_i (all in conflict), achieved = sum c_i^x B_i H/T_i
+ * for the reported partitions (0 when rejected by Lemma 1/2), H}.
  * stats: device uint64 [4] or NULL; += {EDF-PDC tests, tasks in tested
  * partitions, distinct deadlines examined by the demand walks, sets} (the
  * per-launch work figures of the roofline).
@@ -175,7 +180,7 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * ------------------------------------------------------------------------- */
 gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok, int8_t *block_of_task,
                       int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
-                      unsigned long long *stats, void *stream);
+                      int64_t *efficiency, unsigned long long *stats, void *stream);
 
 /* ---------------------------------------------------------------------------
  * A6 (and A2-A4 fused). gp_sched_ratio -- segmented reduction to the
@@ -201,6 +206,15 @@ gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok, int8_t *
  *   per-window per_set rows merge by sum / min / min / sum).
  *   Limits: n_tasks <= 12, M <= 256, C(M,k) < 2^32; else GP_EINVAL; N_c >=
  *   2^63 -> GP_EOVERFLOW.
+ * mode GP_THRESHOLD (a different work unit, reported
+ *   separately): the same per_set outputs and counts as GP_EXHAUSTIVE, exact by
+ *   resource monotonicity: per set, m*(S) = min{s : EDF-PDC(S,s)}
+ *   for each of the 2^n - 1 task subsets (binary search), then per allocation
+ *   pi the schedulable size vectors are exactly s >= m* (componentwise), so
+ *   n_sched = sum_pi C(M - sum(m* - 1), k), pi_star = min sum(m*), first_rank =
+ *   rank(pi, m*); the hash enumerates the schedulable vectors only (skipped with
+ *   GP_EX_NO_HASH).  Full rank window only; verdict_bits must be NULL;
+ *   work_counter unused.
  * ------------------------------------------------------------------------- */
 typedef struct {
   uint64_t rank_lo, rank_hi;  /* window [lo, hi) of candidate ranks; hi = UINT64_MAX -> N_c  */
@@ -209,8 +223,12 @@ typedef struct {
   int64_t words_per_set;      /* >= ceil((hi - lo) / 32) when verdict_bits != NULL            */
   unsigned long long *work_counter; /* device scratch, >= 1 u64 (work queue), required     */
   unsigned long long *stats;  /* device [4] or NULL: += {candidates, block tests,
-                                 deadline points examined, tasks in tested blocks}            */
+                                 deadline points examined, tasks in tested blocks}
+                                 (THRESHOLD: {sets, threshold tests, deadline points,
+                                 schedulable candidates enumerated for the hash})              */
+  uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0)        */
 } gp_exhaustive_opts;
+#define GP_EX_NO_HASH 1u
 
 gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode, const uint8_t *verdicts,
                          int32_t n_rows, int32_t slot0, int32_t n_slots, int32_t setting,

@@ -87,6 +87,7 @@ def _declare(L):
     L.gpref_sched_ratio.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P]
     L.gpref_uunisort.argtypes = [C.c_int32, C.c_int64, P, P]
     L.gpref_task_fields.argtypes = [P, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P]
+    L.gpref_efficiency.argtypes = [P, P, P]
     L.gpref_splitmix64.argtypes = [C.c_uint64]
     L.gpref_splitmix64.restype = C.c_uint64
 
@@ -320,6 +321,15 @@ def allocate(sets: Sets, variant, threads=None):
     _check(lib().gpref_allocate(C.byref(cs), v, _p(ok), _p(bot), _p(bs), _p(pi), _p(k), _p(nt), th),
            "allocate")
     return dict(ok=ok, block_of_task=bot, block_size=bs, pi=pi, k=k, n_tests=nt)
+
+
+def efficiency(sets: Sets, block_of_task):
+    """[n_sets][4] = (lower, upper, achieved, H): work-based utilisations x H."""
+    bot = np.ascontiguousarray(block_of_task, dtype=np.int8)
+    eff = np.zeros((sets.n_sets, 4), np.int64)
+    cs = sets._c()
+    _check(lib().gpref_efficiency(C.byref(cs), _p(bot), _p(eff)), "efficiency")
+    return eff
 
 
 def sched_ratio(sets: Sets, verdict_rows, slot0, n_slots, setting, counts):

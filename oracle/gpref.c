@@ -882,6 +882,45 @@ int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int8_t *bl
   return 0;
 }
 
+/* §8(f) f2: scheduled workload ("efficiency") of an allocation (P:965-966,
+ * P:1009-1014), in the integer W form: the work of task i is
+ * its blocks times its per-block cost, c_i^x * B_i (the a of C = k(a/m + b),
+ * reading A-1/A-14), as a utilisation scaled by the set's hyperperiod H:
+ *   lower    = sum_i cn_i * B_i * (H/T_i)      (no task in conflict)
+ *   upper    = sum_i cc_i * B_i * (H/T_i)      (every task in conflict)
+ *   achieved = sum_i c_i^{x_i} * B_i * (H/T_i) (x_i from the allocation)
+ * eff[set] = {lower, upper, achieved (0 without an allocation), H}.        */
+int gpref_efficiency(const gpref_sets *s, const int8_t *block_of_task, int64_t *eff) {
+  int32_t n = s->n_tasks;
+  for (int32_t set = 0; set < s->n_sets; ++set) {
+    int64_t T[32], H;
+    for (int32_t i = 0; i < n; ++i) T[i] = s->T[(int64_t)set * n + i];
+    if (gpref_hyperperiod(n, T, &H) != 0) return 2;
+    const int8_t *lab = block_of_task + (int64_t)set * n;
+    const uint8_t *type = s->type + (int64_t)set * n;
+    int has_alloc = lab[0] >= 0;
+    i128 lo = 0, up = 0, ach = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      int64_t b = (int64_t)set * n + i;
+      int64_t q = H / T[i];
+      lo += (i128)s->cn[b] * s->B[b] * q;
+      up += (i128)s->cc[b] * s->B[b] * q;
+      if (has_alloc) {
+        uint32_t mask = 0;
+        for (int32_t j = 0; j < n; ++j)
+          if (lab[j] == lab[i]) mask |= 1u << j;
+        int x = gpref_conflict(n, type, mask, i);
+        ach += (i128)(x ? s->cc[b] : s->cn[b]) * s->B[b] * q;
+      }
+    }
+    eff[set * 4 + 0] = (int64_t)lo;
+    eff[set * 4 + 1] = (int64_t)up;
+    eff[set * 4 + 2] = (int64_t)ach;
+    eff[set * 4 + 3] = H;
+  }
+  return 0;
+}
+
 /* ======================================================================= */
 /* A1: generator (§7.1; §8(c) C.1.10, readings A-9..A-15)          */
 /* ======================================================================= */

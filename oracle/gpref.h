@@ -88,6 +88,9 @@ int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int8_t *bl
                    int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                    int32_t n_threads);
 
+/* ---- f2: scheduled workload of an allocation ---- */
+int gpref_efficiency(const gpref_sets *s, const int8_t *block_of_task, int64_t *eff);
+
 /* ---- A6: segmented ratio reduction (§7.2; §8(c) C.1.11) ---- */
 int gpref_sched_ratio(const gpref_sets *s, const uint8_t *verdicts, int32_t n_rows,
                       int32_t slot0, int32_t n_slots, int32_t setting, int64_t *counts);

@@ -31,6 +31,7 @@ struct AllocArgs {
   int16_t *bs;
   int32_t *pi, *k;
   int64_t *n_tests;
+  int64_t *eff;               // optional [n_sets][4]: scheduled workload (f2)
   unsigned long long *stats;  // optional: += {EDF tests, tasks tested, deadlines examined, sets}
   int32_t use_tab;            // per-warp table of ceil(B_i/m) in dynamic shared memory
 };
@@ -119,6 +120,7 @@ struct WarpScratch {
   int32_t size[32];   // size of output label j
   uint32_t forb[32];  // ACT: forbidden task row
   int32_t plist[32];  // eligible partners of the selected partition, par_list order
+  uint32_t pmask[32]; // task mask of output label j
   // the set's tasks, for the lane-serial merge tests
   int32_t T[32], D[32], B[32], cn[32], cc[32], fn[32], fc[32], q[32];
   uint32_t same[32];
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     if (pm) {
       const int label = __popc(livemask & ((1u << lane) - 1u));
       scr.size[label] = psz;
+      scr.pmask[label] = pm;
       uint32_t bits = pm;
       while (bits) {
         const int tsk = __ffs(bits) - 1;
@@ -491,6 +494,23 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     }
     st_sets += 1;
     st_tests += tests > 0 ? (uint64_t)tests : 0;
+    if (a.eff) {
+      // f2: work c^x * B per period, x H
+      const int64_t w = t.in ? (int64_t)t.B * t.q : 0;
+      const int64_t lo = warp_sum_i64(w * t.cn), up = warp_sum_i64(w * t.cc);
+      int64_t mine = 0;
+      if (stage && t.in) {
+        const bool x = __popc(scr.pmask[scr.lab[lane]] & t.same) > 1;  // conflict
+        mine = w * (x ? t.cc : t.cn);
+      }
+      const int64_t ach = warp_sum_i64(mine);
+      if (lane == 0) {
+        a.eff[set * 4 + 0] = lo;
+        a.eff[set * 4 + 1] = up;
+        a.eff[set * 4 + 2] = ach;
+        a.eff[set * 4 + 3] = contract ? H : 0;
+      }
+    }
     if (lane == 0) {
       a.ok[set] = ok ? 1 : 0;
       a.pi[set] = Pi_out;
@@ -514,8 +534,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
 
 extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok,
                                  int8_t *block_of_task, int16_t *block_size, int32_t *pi,
-                                 int32_t *k, int64_t *n_tests, unsigned long long *stats,
-                                 void *stream) {
+                                 int32_t *k, int64_t *n_tests, int64_t *efficiency,
+                                 unsigned long long *stats, void *stream) {
   using namespace gp;
   if (!ts || ts->n_tasks < 1 || ts->n_tasks > kMaxTasks || ts->M < 1 || ts->M > 1024 ||
       ts->n_sets < 0)
@@ -531,7 +551,7 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *o
   if (!use_tab) tab = 0;
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-              stats, use_tab ? 1 : 0};
+              efficiency, stats, use_tab ? 1 : 0};
   if (tab > 48 * 1024)
     cudaFuncSetAttribute(k_allocate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
   int64_t grid = ((int64_t)ts->n_sets + 7) / 8;

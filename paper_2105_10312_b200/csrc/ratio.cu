@@ -8,6 +8,9 @@
 gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_slots,
                                int32_t setting, int64_t *counts, const gp_exhaustive_opts *ex,
                                cudaStream_t st);
+gp_status gp_threshold_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_slots,
+                              int32_t setting, int64_t *counts, const gp_exhaustive_opts *ex,
+                              cudaStream_t st);
 
 namespace gp {
 
@@ -62,8 +65,9 @@ extern "C" gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode,
   if (ts->n_sets > 0 && (!ts->valid || !ts->group))
     return gp_fail(GP_EINVAL, "gp_sched_ratio: null valid/group");
   cudaStream_t st = (cudaStream_t)stream;
-  if (mode == GP_EXHAUSTIVE) {
+  if (mode == GP_EXHAUSTIVE || mode == GP_THRESHOLD) {
     if (verdicts || n_rows != 1) return gp_fail(GP_EINVAL, "EXHAUSTIVE: verdicts must be NULL, n_rows 1");
+    if (mode == GP_THRESHOLD) return gp_threshold_launch(ts, slot0, n_slots, setting, counts, ex, st);
     return gp_exhaustive_launch(ts, slot0, n_slots, setting, counts, ex, st);
   }
   if (mode != GP_FROM_VERDICTS) return gp_fail(GP_EINVAL, "gp_sched_ratio: bad mode");

@@ -20,7 +20,8 @@ GP_OK, GP_EINVAL, GP_EOVERFLOW, GP_ECUDA = 0, 1, 2, 3
 GP_1G, GP_SMS_ACT, GP_SMS_INA, GP_BF_ACT, GP_BF_INA = range(5)
 VARIANTS = {"1G": GP_1G, "SMS_ACT": GP_SMS_ACT, "SMS_INA": GP_SMS_INA, "BF_ACT": GP_BF_ACT,
             "BF_INA": GP_BF_INA}
-GP_FROM_VERDICTS, GP_EXHAUSTIVE = 0, 1
+GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD = 0, 1, 2
+GP_EX_NO_HASH = 1
 UINT64_MAX = 2**64 - 1
 
 FIELDS_I32 = ("T", "D", "B", "cn", "cc", "fn", "fc")
@@ -56,7 +57,7 @@ class _GenC(C.Structure):
 class _ExOptsC(C.Structure):
     _fields_ = [("rank_lo", C.c_uint64), ("rank_hi", C.c_uint64), ("per_set", C.c_void_p),
                 ("verdict_bits", C.c_void_p), ("words_per_set", C.c_int64),
-                ("work_counter", C.c_void_p), ("stats", C.c_void_p)]
+                ("work_counter", C.c_void_p), ("stats", C.c_void_p), ("flags", C.c_uint32)]
 
 
 _P = C.c_void_p
@@ -66,7 +67,7 @@ _lib.gp_count_candidates.argtypes = [C.c_int32, C.c_int32, _P]
 _lib.gp_enumerate.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _P, _P, _P]
 _lib.gp_wcet.argtypes = [_P, _P, _P, _P, C.c_int64, _P, _P, _P]
 _lib.gp_wcet_per_sm.argtypes = [C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P]
-_lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]
+_lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.gp_sched_ratio.argtypes = [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 _P, _P, _P]
 for _f in ("gp_generate", "gp_count_candidates", "gp_enumerate", "gp_wcet", "gp_wcet_per_sm",
@@ -200,10 +201,19 @@ class AllocOut:
         self.pi = torch.empty(n_sets, dtype=torch.int32, device=device)
         self.k = torch.empty(n_sets, dtype=torch.int32, device=device)
         self.n_tests = torch.empty(n_sets, dtype=torch.int64, device=device)
+        self.efficiency = None  # optional [n_sets][4] (f2), allocate with want_efficiency()
+
+    def want_efficiency(self):
+        self.efficiency = torch.empty((self.ok.shape[0], 4), dtype=torch.int64,
+                                      device=self.ok.device)
+        return self
 
     def to_host(self):
-        return {k: getattr(self, k).cpu().numpy()
-                for k in ("ok", "block_of_task", "block_size", "pi", "k", "n_tests")}
+        d = {k: getattr(self, k).cpu().numpy()
+             for k in ("ok", "block_of_task", "block_size", "pi", "k", "n_tests")}
+        if self.efficiency is not None:
+            d["efficiency"] = self.efficiency.cpu().numpy()
+        return d
 
 
 def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=None):
@@ -213,21 +223,21 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
     s = ts.struct()
     _check(_lib.gp_allocate(C.byref(s), v, _ptr(out.ok), _ptr(out.block_of_task),
                             _ptr(out.block_size), _ptr(out.pi), _ptr(out.k), _ptr(out.n_tests),
-                            _ptr(stats), _stream(stream)))
+                            _ptr(out.efficiency), _ptr(stats), _stream(stream)))
     return out
 
 
 def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=None, setting=0,
                    per_set=None, verdict_bits=None, words_per_set=0, work_counter=None,
-                   stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None):
+                   stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None, flags=0):
     """FROM_VERDICTS: verdicts uint8 [n_rows][n_sets]; EXHAUSTIVE: per_set int64 [n_sets][4]
     (+ work_counter int64 [>=1], optional verdict_bits int32/uint32 [n_sets][words], stats
     int64 [4]).  counts int64 [n_settings][n_groups][n_slots][3] is accumulated."""
     s = ts.struct()
-    if mode == GP_EXHAUSTIVE:
+    if mode in (GP_EXHAUSTIVE, GP_THRESHOLD):
         n_rows = 1
         ex = _ExOptsC(rank_lo, rank_hi, _ptr(per_set), _ptr(verdict_bits), words_per_set,
-                      _ptr(work_counter), _ptr(stats))
+                      _ptr(work_counter), _ptr(stats), flags)
         exp = C.byref(ex)
         vp = None
     else:

@@ -71,7 +71,7 @@ def test_host_validation_before_any_cuda(G):
     assert lib.gp_enumerate(4, 13, 0, 1, None, None, None) == G.GP_EINVAL
     assert lib.gp_enumerate(4, 3, 20, 10, None, None, None) == G.GP_EINVAL  # beyond N_c = 26
     assert lib.gp_wcet_per_sm(5, 0, None, 0, None, None, None) == G.GP_EINVAL  # m = 0
-    assert lib.gp_allocate(None, 0, None, None, None, None, None, None, None, None) == G.GP_EINVAL
+    assert lib.gp_allocate(None, 0, None, None, None, None, None, None, None, None, None) == G.GP_EINVAL
     import gp_workloads as W
     gen = W.WORKLOADS["c2"]["gen"](R=10)
     ts = G._TaskSetsC(100, 6, 8, 10)

@@ -248,9 +248,13 @@ VARIANTS = ("1G", "SMS_ACT", "SMS_INA", "BF_ACT", "BF_INA")
 def check_allocate(G, ts, host=None, variants=VARIANTS):
     host = host or to_oracle(ts)
     for v in variants:
-        out = G.gp_allocate(ts, v)
+        out = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks).want_efficiency())
         got = out.to_host()
         ref = oracle.allocate(host, v)
+        # f2: scheduled workload of the reported allocation (contract-respecting sets)
+        eff = oracle.efficiency(host, ref["block_of_task"])
+        okc = got["n_tests"] >= 0
+        assert (got["efficiency"][okc] == eff[okc]).all(), f"{v} efficiency"
         for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
             if not (got[key] == ref[key]).all():
                 bad = np.nonzero((got[key] != ref[key]).reshape(len(got[key]), -1).any(1))[0]
@@ -337,3 +341,60 @@ def test_pipeline_step_c2_matches_oracle(G):
     oracle.sched_ratio(host, rows, 1, 6, 0, ref)
     assert (p.counts.cpu().numpy() == ref).all()
     assert (p.per_set.cpu().numpy() == per).all()
+
+
+# ------------------------------------------------------------------ f3: subset thresholds
+def run_threshold(G, ts, counts=None, n_slots=1, no_hash=False):
+    per = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    G.gp_sched_ratio(ts, G.GP_THRESHOLD, counts, slot0=0, n_slots=n_slots, per_set=per,
+                     stats=stats, flags=G.GP_EX_NO_HASH if no_hash else 0)
+    torch.cuda.synchronize()
+    return per.cpu().numpy(), stats.cpu().numpy()
+
+
+def test_threshold_c1_and_c2_match_oracle(G):
+    """f3: the subset-threshold evaluator gives the same per-set
+    outputs as the definition (the oracle's direct enumeration), hash included."""
+    d = W._c1_sets()
+    per, _ = run_threshold(G, gpu_sets(G, d))
+    assert (per == oracle.exhaustive(oracle.Sets.from_dict(d))).all()
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 100, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 100, ts)
+    per, st = run_threshold(G, ts)
+    ref = oracle.exhaustive(to_oracle(ts))
+    assert (per == ref).all()
+    assert st[0] == 1000 and st[3] == ref[:, 0].sum()
+    per2, _ = run_threshold(G, ts, no_hash=True)
+    assert (per2[:, :3] == ref[:, :3]).all() and (per2[:, 3] == 0).all()
+
+
+def test_threshold_matches_direct_path_c3_full(G):
+    """At the C3 parity size every set's f3 output equals the direct evaluator's
+    (which the sampled oracle check above pins), counts included."""
+    gen = W.WORKLOADS["c3"]["gen"](R=1000)
+    ts = G.TaskSets(10 * 1000, 6, 20, 10)
+    G.gp_generate(gen, W.SEED, 0, 1000, ts)
+    c1 = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
+    c2 = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
+    direct, _, _ = run_exhaustive(G, ts, counts=c1)
+    thr, _ = run_threshold(G, ts, counts=c2)
+    assert (direct == thr).all()
+    assert (c1.cpu().numpy() == c2.cpu().numpy()).all()
+    sample = [3, 4321, 9998]
+    assert (thr[sample] == oracle.exhaustive(to_oracle(ts).subset(sample))).all()
+
+
+@pytest.mark.parametrize("seed,n,M", [(31, 1, 1), (32, 2, 5), (33, 4, 3), (34, 5, 7), (35, 7, 4),
+                                      (36, 8, 3), (37, 3, 12), (38, 6, 9)])
+def test_threshold_random_sets(G, seed, n, M):
+    rng = np.random.default_rng(seed)
+    d = W.random_sets(rng, 29, n, M, periods=(4, 6, 8, 12, 24), b_max=2 * M + 3, cost_max=3)
+    d["D"][5, 0] = d["T"][5, 0] + 1  # one contract violation: reported, counted invalid
+    counts = torch.zeros((1, 1, 1, 3), dtype=torch.int64, device="cuda")
+    per, _ = run_threshold(G, gpu_sets(G, d), counts=counts)
+    ok_rows = [g for g in range(29) if g != 5]
+    ref = oracle.exhaustive(oracle.Sets.from_dict(d).subset(ok_rows))
+    assert (per[ok_rows] == ref).all()
+    assert per[5, 0] == -1 and counts.cpu().numpy()[0, 0, 0, 2] == 1

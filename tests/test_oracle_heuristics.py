@@ -182,3 +182,43 @@ def test_heuristics_find_solutions_on_c4(c4_small):
     one_g = oracle.allocate(s, "1G")["ok"].mean()
     for v in VARIANTS:
         assert oracle.allocate(s, v)["ok"].mean() >= one_g
+
+
+# ---------------------------------------------------------------- f2 efficiency
+def _eff_sets(types, cn=10, cc=23, B=2, T=100):
+    n = len(types)
+    return make_sets(8, [dict(T=T, D=T, B=B, cn=cn, cc=cc, fn=0, fc=0, type=t) for t in types])
+
+
+def test_efficiency_spec_examples():
+    """SPEC S:420-422 in the work form (work = c * B per period):
+    one memory + one compute per partition -> achieved = lower;
+    one partition holding >= 2 of each type (1G) -> achieved = upper;
+    one conflicting memory task among conflict-free ones -> lower + its (cc-cn)B."""
+    s = _eff_sets([0, 1, 0, 1])
+    e = oracle.efficiency(s, np.array([[0, 0, 1, 1]], np.int8))[0]
+    assert e[3] == 100 and e[0] == 4 * 10 * 2 and e[1] == 4 * 23 * 2
+    assert e[2] == e[0]
+    e = oracle.efficiency(s, np.array([[0, 0, 0, 0]], np.int8))[0]
+    assert e[2] == e[1]
+    # tasks 1 and 3 (memory) share partition 1 with nobody else of their type? no:
+    # labels [0, 1, 2, 1]: tasks 1,3 memory together -> both conflict; 0 and 2 alone
+    e = oracle.efficiency(s, np.array([[0, 1, 2, 1]], np.int8))[0]
+    assert e[2] == 2 * 10 * 2 + 2 * 23 * 2
+    # rejected (no allocation): achieved 0, bounds still reported
+    e = oracle.efficiency(s, np.array([[-1, -1, -1, -1]], np.int8))[0]
+    assert e[2] == 0 and e[0] == 80
+
+
+def test_efficiency_bounds_on_heuristic_solutions(c4_small):
+    s = c4_small
+    for v in ("1G",) + VARIANTS:
+        r = oracle.allocate(s, v)
+        e = oracle.efficiency(s, r["block_of_task"])
+        assert (e[:, 0] <= e[:, 1]).all()
+        has = r["k"] > 0
+        assert ((e[has, 0] <= e[has, 2]) & (e[has, 2] <= e[has, 1])).all()
+        assert (e[~has, 2] == 0).all()
+        if v == "1G":  # P:1011-1012: 1G always schedules the worst load
+            mixed = [(s.type[g].sum() >= 2) and ((1 - s.type[g]).sum() >= 2) for g in range(s.n_sets)]
+            assert all(e[g, 2] == e[g, 1] for g in range(s.n_sets) if mixed[g])
