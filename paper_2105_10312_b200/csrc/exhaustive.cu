@@ -19,6 +19,7 @@
 //   Per set: n_sched / pi* / first rank / verdict hash are reduced in
 //   registers and flushed with one set of atomics per item run.
 #include <cstdio>
+#include <cstdlib>
 
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
@@ -132,6 +133,71 @@ GP_DEV void record_ok(LaneAcc &acc, uint64_t rank, int32_t sum, uint32_t *bits, 
   if (bits) {
     const uint64_t off = rank - lo;
     atomicOr(bits + (off >> 5), 1u << (off & 31));
+  }
+}
+
+// ---- per-warp helpers shared by both evaluation paths -----------------------
+GP_DEV void exh_flush(const ExhArgs &a, LaneAcc &acc, int64_t cur, int lane) {
+  if (cur < 0) return;
+  const uint32_t tot = (uint32_t)warp_sum_i32((int32_t)acc.n);
+  const int32_t pi = warp_min_i32(acc.pi);
+  uint64_t first = acc.first;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t v = __shfl_xor_sync(GP_FULL, first, o);
+    first = v < first ? v : first;
+  }
+  const uint64_t h = warp_sum_u64(acc.hash);
+  if (lane == 0 && tot > 0) {
+    long long *ps = reinterpret_cast<long long *>(a.per_set + cur * 4);
+    atomicAdd(reinterpret_cast<unsigned long long *>(ps + 0), (unsigned long long)tot);
+    atomicMin(ps + 1, (long long)pi);
+    atomicMin(ps + 2, (long long)first);
+    atomicAdd(reinterpret_cast<unsigned long long *>(ps + 3), h);
+  }
+  acc.n = 0;
+  acc.pi = INT32_MAX;
+  acc.first = ~0ull;
+  acc.hash = 0;
+}
+
+// load one set into the warp's shared memory: contract, H, H/T_i, types and
+// the W table W[i][x][s] = ceil(B_i/s) c_i^x + f_i^x (C.1.3)
+GP_DEV void exh_load_set(const ExhArgs &a, WarpSmem &w, int32_t *Wt, int64_t set, int lane) {
+  const int n = a.n, M = a.M;
+  const int64_t H = set_contract(a, set);
+  __syncwarp();
+  if (lane < n) {
+    const int64_t o = set * n + lane;
+    w.T[lane] = a.T[o];
+    w.D[lane] = a.D[o];
+    w.q[lane] = H > 0 ? (int32_t)(H / a.T[o]) : 0;
+  }
+  const uint32_t mm = __ballot_sync(GP_FULL, lane < n && a.type[set * n + min(lane, n - 1)] == 1);
+  if (lane == 0) {
+    w.H = (int32_t)(H > 0 ? H : 0);
+    w.okc = H > 0;
+    w.memmask = mm;
+  }
+  if (H > 0) {
+    for (int e = lane; e < 2 * n * M; e += 32) {
+      const int i = e / (2 * M), x = (e / M) & 1, s = e % M + 1;
+      const int64_t o = set * n + i;
+      Wt[e] = x ? wcet_sat(a.B[o], a.cc[o], a.fc[o], s) : wcet_sat(a.B[o], a.cn[o], a.fn[o], s);
+    }
+  }
+  __syncwarp();
+}
+
+GP_DEV void exh_stats_flush(const ExhArgs &a, LaneAcc &acc, int lane) {
+  if (!a.stats) return;
+  const uint64_t c0 = warp_sum_u64(acc.st_cand), c1 = warp_sum_u64(acc.st_blocks);
+  const uint64_t c2 = warp_sum_u64(acc.st_events), c3 = warp_sum_u64(acc.st_tasks);
+  if (lane == 0) {
+    atomicAdd(a.stats + 0, c0);
+    atomicAdd(a.stats + 1, c1);
+    atomicAdd(a.stats + 2, c2);
+    atomicAdd(a.stats + 3, c3);
   }
 }
 
@@ -387,6 +453,297 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_exhaustive(const ExhArgs a) 
   }
 }
 
+// ============================================================================
+// Shape-specialised path (n <= 6), items in SHAPE-MAJOR order.
+//
+// The shape of an allocation pi is the sequence of its block sizes in label
+// order (a composition of n; CUTS has bit p set when a block ends after task
+// position p).  With the shape a template parameter, k, every block's task
+// count and position are compile-time constants: the task records live in
+// registers, the size vector is a fixed-length register array, the successor
+// has no runtime bounds and the multi-task blocks need no dispatch.  Work
+// items are ordered shape-major (all sets' items of shape 0, then shape 1,
+// ...) so that, at any moment, the warps of the GPU execute the same shape's
+// code: the instruction working set stays that of ONE instantiation.
+// ============================================================================
+constexpr int kMaxShapeN = 6;
+constexpr int kMaxShapes = 1 << (kMaxShapeN - 1);  // compositions of n
+constexpr int kMaxRgs = 203;                        // Bell(6)
+
+struct ShapeTable {
+  int32_t n_shapes;
+  uint32_t cuts[kMaxShapes];
+  int32_t k[kMaxShapes];
+  int32_t first[kMaxShapes + 1];        // into entry[]
+  uint32_t entry[kMaxRgs];              // labels (4 bits/task) | p << 24 (index among k-RGS)
+  uint64_t item_base[kMaxShapes + 1];   // cumulative items over shapes
+  uint32_t items_per_set[kMaxShapes];   // entries * chunks(k)
+  int32_t n_single[kMaxShapes];         // blocks with one task
+};
+
+constexpr int cpopc(unsigned x) { return x ? (int)(x & 1u) + cpopc(x >> 1) : 0; }
+constexpr int shape_start(int N, unsigned cuts, int j) {
+  int b = 0;
+  if (j == 0) return 0;
+  for (int p = 0; p < N - 1; ++p)
+    if ((cuts >> p) & 1u) {
+      ++b;
+      if (b == j) return p + 1;
+    }
+  return N;
+}
+constexpr int shape_len(int N, unsigned cuts, int j) {
+  return shape_start(N, cuts, j + 1) - shape_start(N, cuts, j);
+}
+
+template <int N>
+struct TaskRegs {
+  int32_t woff[N], D[N], T[N], q[N];
+};
+
+template <int N, int S0, int L>
+GP_DEV bool eval_multi(const int32_t *__restrict__ Wt, const TaskRegs<N> &r, int32_t s,
+                       int32_t H, uint32_t &ev) {
+  int32_t C[L], D[L], T[L], q[L];
+  bool bad = false;
+#pragma unroll
+  for (int a = 0; a < L; ++a) {
+    C[a] = Wt[r.woff[S0 + a] + s];
+    D[a] = r.D[S0 + a];
+    T[a] = r.T[S0 + a];
+    q[a] = r.q[S0 + a];
+    bad |= C[a] > D[a];
+  }
+  if (bad) return false;
+  int32_t UH = 0;
+#pragma unroll
+  for (int a = 0; a < L; ++a) UH += C[a] * q[a];
+  if (UH > H) return false;
+  const int32_t lcut = pdc_cutoff<L>(C, D, T, q, H, UH);
+  return pdc_walk<L>(C, D, T, lcut, ev);
+}
+
+// sizes are stored reversed: sr[jj] is the size of block K-1-jj
+template <int N, unsigned CUTS, int JJ, int K>
+GP_DEV void shape_singles(const int32_t *__restrict__ Wt, const TaskRegs<N> &r,
+                          const int32_t (&sr)[K], bool &ok) {
+  if constexpr (JJ < K) {
+    constexpr int J = K - 1 - JJ;
+    constexpr int S0 = shape_start(N, CUTS, J), L = shape_len(N, CUTS, J);
+    if constexpr (L == 1) ok &= Wt[r.woff[S0] + sr[JJ]] <= r.D[S0];
+    shape_singles<N, CUTS, JJ + 1, K>(Wt, r, sr, ok);
+  }
+}
+
+template <int N, unsigned CUTS, int JJ, int K>
+GP_DEV void shape_multis(const int32_t *__restrict__ Wt, const TaskRegs<N> &r,
+                         const int32_t (&sr)[K], int32_t H, bool &ok, LaneAcc &acc, bool stats) {
+  if constexpr (JJ < K) {
+    constexpr int J = K - 1 - JJ;
+    constexpr int S0 = shape_start(N, CUTS, J), L = shape_len(N, CUTS, J);
+    if constexpr (L > 1) {
+      if (__any_sync(GP_FULL, ok)) {
+        if (ok) {
+          if (stats) {
+            ++acc.st_blocks;
+            acc.st_tasks += L;
+          }
+          ok = eval_multi<N, S0, L>(Wt, r, sr[JJ], H, acc.st_events);
+        }
+      }
+    }
+    shape_multis<N, CUTS, JJ + 1, K>(Wt, r, sr, H, ok, acc, stats);
+  }
+}
+
+template <int K>
+GP_DEV void next_sizes_rev_static(int M, int32_t (&sr)[K], int32_t &sum) {
+  if (sum < M) {  // common: grow the last part
+    sr[0] += 1;
+    sum += 1;
+    return;
+  }
+  if constexpr (K >= 2) {
+    if (sr[0] > 1) {  // bump the second-to-last part, last := 1
+      sum -= sr[0] - 2;
+      sr[0] = 1;
+      sr[1] += 1;
+      return;
+    }
+    int prefix = 0, pick = -1;
+#pragma unroll
+    for (int jj = 1; jj < K; ++jj) {
+      prefix += sr[jj - 1];
+      if (pick < 0 && prefix > jj) pick = jj;
+    }
+    if (pick < 0) return;
+    int ns = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      sr[i] = i < pick ? 1 : (i == pick ? sr[i] + 1 : sr[i]);
+      ns += sr[i];
+    }
+    sum = ns;
+  }
+}
+
+struct ShapeItem {
+  const int32_t *Wt;
+  const WarpSmem *w;
+  const EnumTables *tab;
+  uint32_t *bits;
+  uint64_t r0, lo;  // rank of this lane's first candidate; rank window start
+  int32_t M, H, t_lo, t_hi;
+  uint32_t my0;
+  bool stats;
+};
+
+template <int N, unsigned CUTS>
+GP_DEV void run_shape(const ShapeItem &c, LaneAcc &acc) {
+  constexpr int K = cpopc(CUTS) + 1;
+  TaskRegs<N> r;
+#pragma unroll
+  for (int p = 0; p < N; ++p) {
+    const int4 v = c.w->rec[p];
+    r.woff[p] = v.x;
+    r.D[p] = v.y;
+    r.T[p] = v.z;
+    r.q[p] = v.w;
+  }
+  int32_t sr[K];
+  int32_t sum = 0;
+  {
+    int32_t s[K];
+    if (c.t_hi > 0) {
+      unrank_sizes<K>(*c.tab, K, c.my0, s);
+    } else {
+#pragma unroll
+      for (int j = 0; j < K; ++j) s[j] = 1;
+    }
+#pragma unroll
+    for (int jj = 0; jj < K; ++jj) {
+      sr[jj] = s[K - 1 - jj];
+      sum += sr[jj];
+    }
+  }
+  const int tmax = (int)__reduce_max_sync(GP_FULL, (unsigned)c.t_hi);
+  for (int t = 0; t < tmax; ++t) {
+    bool ok = t >= c.t_lo && t < c.t_hi;
+    shape_singles<N, CUTS, 0, K>(c.Wt, r, sr, ok);
+    shape_multis<N, CUTS, 0, K>(c.Wt, r, sr, c.H, ok, acc, c.stats);
+    if (ok) record_ok(acc, c.r0 + (uint32_t)t, sum, c.bits, c.lo);
+    if (t + 1 < c.t_hi) next_sizes_rev_static<K>(c.M, sr, sum);
+  }
+}
+
+template <int N, unsigned C>
+GP_DEV void shape_dispatch(unsigned cuts, const ShapeItem &c, LaneAcc &acc) {
+  if constexpr (C < (1u << (N - 1))) {
+    if (cuts == C) run_shape<N, C>(c, acc);
+    else shape_dispatch<N, C + 1>(cuts, c, acc);
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kWarps * 32, 3)
+    k_exhaustive_shaped(const ExhArgs a, const ShapeTable sh) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int n = a.n, M = a.M;
+  const EnumTables tab = build_enum_tables(smem, M, n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t off = (enum_table_words(M, n) + 3) & ~(size_t)3;
+  const size_t per_warp = ((sizeof(WarpSmem) / 4 + (size_t)2 * n * M) + 3) & ~(size_t)3;
+  WarpSmem &w = *reinterpret_cast<WarpSmem *>(smem + off + per_warp * warp);
+  int32_t *Wt = reinterpret_cast<int32_t *>(&w + 1);
+  const bool stats = a.stats != nullptr;
+  LaneAcc acc;
+  int64_t cur = -1;
+  int shape = 0;
+  for (;;) {
+    uint64_t base = 0;
+    if (lane == 0) base = atomicAdd(a.work_counter, (unsigned long long)kGrab);
+    base = __shfl_sync(GP_FULL, base, 0);
+    if (base >= a.total_items) break;
+    const uint64_t end = min(base + (uint64_t)kGrab, a.total_items);
+    for (uint64_t it = base; it < end; ++it) {
+      while (shape + 1 < sh.n_shapes && it >= sh.item_base[shape + 1]) ++shape;
+      while (it < sh.item_base[shape]) --shape;
+      const int k = sh.k[shape];
+      const uint32_t chunks = a.chunks[k];
+      const uint64_t local = it - sh.item_base[shape];
+      const int64_t set = (int64_t)(local / sh.items_per_set[shape]);
+      const uint32_t rem = (uint32_t)(local - (uint64_t)set * sh.items_per_set[shape]);
+      const uint32_t e = rem / chunks, c = rem - e * chunks;
+      if (set != cur) {
+        exh_flush(a, acc, cur, lane);
+        cur = set;
+        exh_load_set(a, w, Wt, set, lane);
+      }
+      if (!w.okc) continue;
+      const uint32_t ent = sh.entry[sh.first[shape] + e];
+      const uint32_t p = ent >> 24;
+      const int Lk = a.lane_L[k];
+      const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
+      const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
+      const uint32_t rho0 = c * 32u * (uint32_t)Lk;
+      if (rank_pi + rho0 >= a.hi || rank_pi + min((uint64_t)per_pi, (uint64_t)rho0 + 32u * Lk) <= a.lo)
+        continue;
+      // records in block order (block = label; labels ascend with first appearance)
+      const int myb = lane < n ? (int)((ent >> (4 * lane)) & 15) : -1;
+      uint32_t mine = 0;
+      int mypos0 = 0, acc_pos = 0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const uint32_t bm = __ballot_sync(GP_FULL, myb == j);
+        if (j == myb) {
+          mine = bm;
+          mypos0 = acc_pos;
+        }
+        acc_pos += __popc(bm);
+      }
+      if (lane < n) {
+        const uint32_t same = ((w.memmask >> lane) & 1) ? w.memmask : ~w.memmask;
+        const int x = __popc(mine & same) > 1 ? 1 : 0;  // conflict
+        const int pos = mypos0 + __popc(mine & ((1u << lane) - 1u));
+        w.rec[pos] = make_int4((lane * 2 + x) * M - 1, w.D[lane], w.T[lane], w.q[lane]);
+      }
+      __syncwarp();
+      ShapeItem ctx;
+      ctx.Wt = Wt;
+      ctx.w = &w;
+      ctx.tab = &tab;
+      ctx.bits = a.bits ? a.bits + cur * a.words : nullptr;
+      ctx.lo = a.lo;
+      ctx.M = M;
+      ctx.H = w.H;
+      ctx.stats = stats;
+      ctx.my0 = rho0 + (uint32_t)lane * (uint32_t)Lk;
+      ctx.r0 = rank_pi + ctx.my0;
+      {
+        int t_hi = Lk;
+        if (a.hi <= ctx.r0) t_hi = 0;
+        else if (a.hi - ctx.r0 < (uint64_t)t_hi) t_hi = (int)(a.hi - ctx.r0);
+        if ((int64_t)t_hi > (int64_t)per_pi - (int64_t)ctx.my0)
+          t_hi = (int)max((int64_t)0, (int64_t)per_pi - (int64_t)ctx.my0);
+        const int t_lo = a.lo > ctx.r0 ? (int)min(a.lo - ctx.r0, (uint64_t)Lk) : 0;
+        ctx.t_lo = t_lo;
+        ctx.t_hi = t_lo < t_hi ? t_hi : 0;
+        if (stats && ctx.t_hi > 0) {
+          // every candidate tests all of its single-task blocks (one task each)
+          const int n_single = sh.n_single[shape];
+          acc.st_cand += (uint64_t)(ctx.t_hi - ctx.t_lo);
+          acc.st_blocks += (uint64_t)(ctx.t_hi - ctx.t_lo) * n_single;
+          acc.st_tasks += (uint64_t)(ctx.t_hi - ctx.t_lo) * n_single;
+        }
+      }
+      shape_dispatch<N, 0>(sh.cuts[shape], ctx, acc);
+      __syncwarp();
+    }
+  }
+  exh_flush(a, acc, cur, lane);
+  exh_stats_flush(a, acc, lane);
+}
+
 __global__ void k_exh_init(int64_t *per_set, int32_t n_sets) {
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_sets;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -443,6 +800,92 @@ static gp_status launch_exh(ExhArgs &a, size_t smem, cudaStream_t st) {
   return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) main kernel");
 }
 
+// Host: every RGS of length n in lexicographic order, grouped by shape.
+static void build_shape_table(int n, const ExhArgs &a, ShapeTable &sh) {
+  struct E {
+    uint32_t cuts;
+    int k;
+    uint32_t entry;
+    int n_single;
+  };
+  E list[kMaxRgs];
+  int cnt = 0, lab[kMaxShapeN] = {0}, pcount[kMaxShapeN + 2] = {0};
+  for (;;) {
+    int k = 0, size[kMaxShapeN] = {0};
+    uint32_t packed = 0;
+    for (int i = 0; i < n; ++i) {
+      k = lab[i] + 1 > k ? lab[i] + 1 : k;
+      size[lab[i]] += 1;
+      packed |= (uint32_t)lab[i] << (4 * i);
+    }
+    uint32_t cuts = 0;
+    int acc = 0, singles = 0;
+    for (int j = 0; j < k; ++j) {
+      acc += size[j];
+      singles += size[j] == 1;
+      if (j < k - 1) cuts |= 1u << (acc - 1);
+    }
+    if (k <= a.L.kmax)  // k blocks need k <= M SMs
+      list[cnt++] = E{cuts, k, packed | ((uint32_t)pcount[k]++ << 24), singles};
+    int i = n - 1;  // lexicographic RGS successor
+    for (; i >= 1; --i) {
+      int mx = 0;
+      for (int j = 0; j < i; ++j) mx = lab[j] > mx ? lab[j] : mx;
+      if (lab[i] <= mx) break;
+    }
+    if (i < 1) break;
+    lab[i] += 1;
+    for (int j = i + 1; j < n; ++j) lab[j] = 0;
+  }
+  // stable grouping by shape (cuts ascending), lexicographic order kept inside
+  sh.n_shapes = 0;
+  int e = 0;
+  uint64_t items = 0;
+  for (uint32_t c = 0; c < (1u << (n - 1)); ++c) {
+    const int first = e;
+    int k = 0, singles = 0;
+    for (int x = 0; x < cnt; ++x)
+      if (list[x].cuts == c) {
+        sh.entry[e++] = list[x].entry;
+        k = list[x].k;
+        singles = list[x].n_single;
+      }
+    if (e == first) continue;
+    const int sidx = sh.n_shapes++;
+    sh.cuts[sidx] = c;
+    sh.k[sidx] = k;
+    sh.first[sidx] = first;
+    sh.n_single[sidx] = singles;
+    sh.items_per_set[sidx] = (uint32_t)(e - first) * a.chunks[k];
+    sh.item_base[sidx] = items;
+    items += (uint64_t)sh.items_per_set[sidx] * (uint64_t)a.n_sets;
+  }
+  sh.first[sh.n_shapes] = e;
+  sh.item_base[sh.n_shapes] = items;
+}
+
+template <int N>
+static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
+  static ShapeTable sh;  // host staging, copied into the kernel parameters
+  build_shape_table(N, a, sh);
+  if (sh.item_base[sh.n_shapes] != a.total_items)
+    return gp_fail(GP_EINVAL, "EXHAUSTIVE: shape table does not cover the candidate space");
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_exhaustive_shaped<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exhaustive_shaped<N>, kWarps * 32, smem);
+  if (occ < 1) occ = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t want = (a.total_items + kGrab * kWarps - 1) / (kGrab * kWarps);
+  uint64_t grid = (uint64_t)sms * occ;
+  if (want < grid) grid = want > 0 ? want : 1;
+  k_exhaustive_shaped<N><<<(unsigned)grid, kWarps * 32, smem, st>>>(a, sh);
+  return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) shaped kernel");
+}
+
 }  // namespace gp
 
 // Called by gp_sched_ratio (ratio.cu) for GP_EXHAUSTIVE.
@@ -495,6 +938,20 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   const size_t smem = (((enum_table_words(M, n) + 3) & ~(size_t)3) + per_warp * kWarps) * 4;
   if (smem > 227 * 1024) return gp_fail(GP_EINVAL, "EXHAUSTIVE: shared memory need %zu B too large", smem);
   gp_status r;
+  static const bool generic_only = getenv("GP_EXH_GENERIC") != nullptr;  // A/B switch
+  if (n <= kMaxShapeN && !generic_only) {
+    switch (n) {
+      case 1: r = launch_shaped<1>(a, smem, st); break;
+      case 2: r = launch_shaped<2>(a, smem, st); break;
+      case 3: r = launch_shaped<3>(a, smem, st); break;
+      case 4: r = launch_shaped<4>(a, smem, st); break;
+      case 5: r = launch_shaped<5>(a, smem, st); break;
+      default: r = launch_shaped<6>(a, smem, st); break;
+    }
+    if (r != GP_OK) return r;
+    k_exh_finalize<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(a);
+    return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) finalize");
+  }
   switch (n) {
     case 1: case 2: case 3: r = launch_exh<3>(a, smem, st); break;
     case 4: r = launch_exh<4>(a, smem, st); break;
