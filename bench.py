@@ -71,9 +71,9 @@ def n_candidates(M, n):
     return sum(s2(n, k) * comb(M, k) for k in range(1, min(M, n) + 1))
 
 
-def ncu_traffic(workload):
-    """DRAM bytes per launch of the dominant kernel from the latest committed
-    ncu --set full capture (profiles/rNN/ncu_metrics.json), or None."""
+def ncu_entry(workload):
+    """The latest committed ncu --set full capture of the dominant kernel
+    (profiles/rNN/ncu_metrics.json): (entry dict, source path) or (None, None)."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_metrics.json")),
                        reverse=True):
@@ -84,7 +84,7 @@ def ncu_traffic(workload):
             continue
         e = m.get(workload)
         if isinstance(e, dict) and e.get("dram_bytes") is not None:
-            return e["dram_bytes"], os.path.relpath(path, ROOT)
+            return e, os.path.relpath(path, ROOT)
     return None, None
 
 
@@ -358,11 +358,16 @@ def main():
         extra = {"edf_tests_per_step": st[0], "tasks_tested_per_step": st[1],
                  "deadlines_per_step": st[2], "sets_per_step": st[3]}
     dom_s = sum(dom_ms) / args.steps / 1e3  # per step (sum of the dominant launches)
-    traffic, traffic_src = (ncu_traffic(wl["name"]) if pipe.exhaustive and not args.f3
-                            else (None, None))
+    prof, prof_src = (ncu_entry(wl["name"]) if pipe.exhaustive and not args.f3
+                      else (None, None))
+    traffic = prof["dram_bytes"] if prof else None
     roof = {"bound": "alu", "achieved": ops / dom_s / 1e12, "peak": peak / 1e12,
             "unit": "T int32 lane-ops/s", "frac": (ops / dom_s) / peak, "traffic": traffic,
-            "traffic_source": traffic_src,
+            "traffic_source": prof_src,
+            "ncu_issue": ({k: prof.get(k) for k in ("inst_issued_pct", "alu_pipe_pct",
+                                                    "fma_pipe_pct", "warp_inst_per_candidate",
+                                                    "active_threads_per_inst")} | {"source": prof_src})
+            if prof else None,
             "kernel": kname, "launches_per_step": launches, "ops_per_step": float(ops),
             "ops_per_unit": per_unit, "dominant_ms_per_step": dom_s * 1e3,
             "kernel_share_of_step": (sum(dom_ms) / args.steps) / (total_ms / args.steps),
