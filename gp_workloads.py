@@ -32,7 +32,7 @@ def _same_den(kc, km):
 
 
 def gen_params(M, n_tasks, sets_per_group, n_bins=10, prm=(0.5,), kc=(12, 10), km=(23, 10),
-               max_attempts=1000):
+               max_attempts=1000, curve_gran=0):
     """Generator parameters in the integer encoding both sides accept."""
     return dict(
         M=M, n_tasks=n_tasks, n_bins=n_bins, n_prm=len(prm), sets_per_group=sets_per_group,
@@ -41,6 +41,7 @@ def gen_params(M, n_tasks, sets_per_group, n_bins=10, prm=(0.5,), kc=(12, 10), k
         beta_c_num=2, beta_m_num=10, beta_den=100,
         kc_num=kc[0], km_num=km[0], k_den=_same_den(kc, km),
         max_attempts=max_attempts,
+        curve_gran=curve_gran,  # > 0: §7.1 curve C = k(a/|P| + b) in the W form (f1, reading A-1)
     )
 
 
@@ -71,6 +72,15 @@ WORKLOADS = {
                gen=lambda R=20000: gen_params(148, 32, R, prm=(0.0, 0.25, 0.5, 0.75, 1.0))),
     "c5": dict(name="c5_coeff_sweep_68sm", M=68, n=16, exhaustive=False, variants=VARIANT_NAMES,
                gen=lambda R=10000, kc=12, km=23: gen_params(68, 16, R, kc=(kc, 10), km=(km, 10))),
+    # §8(f) f1: the paper's own experiment (§7.2; Figs 5 and 7): RTX 2080 Ti shape
+    # (M = 68), 50 or 200 tasks, total utilisation 2, 4, ..., 68 (34 bins of U/M = bin/34),
+    # 100 task sets per point, prm 50 %, the §7.1 curves in curve mode (10-tick granules).
+    "f1_50": dict(name="f1_paper_68sm_50tasks", M=68, n=50, exhaustive=False,
+                  variants=VARIANT_NAMES,
+                  gen=lambda R=100: gen_params(68, 50, R, n_bins=34, curve_gran=10)),
+    "f1_200": dict(name="f1_paper_68sm_200tasks", M=68, n=200, exhaustive=False,
+                   variants=VARIANT_NAMES,
+                   gen=lambda R=100: gen_params(68, 200, R, n_bins=34, curve_gran=10)),
 }
 
 

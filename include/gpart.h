@@ -18,6 +18,8 @@
  *    default stream).  Every device call only ENQUEUES work on that stream
  *    and returns; none synchronises.  Outputs are valid once the stream has
  *    progressed past the call.  gp_count_candidates is host-only.
+ *  - Task sets hold 1..256 tasks (gp_generate, gp_allocate); the enumeration
+ *    calls are limited to n_tasks <= 12 (the candidate count must stay < 2^63).
  *  - Layout of every per-task field is [n_sets][n_tasks]: the tasks of one
  *    set are contiguous (set-major, task-minor), so one warp reads one set's
  *    field with one coalesced 128-byte access at n_tasks = 32.
@@ -52,7 +54,7 @@ typedef enum {
 const char *gp_last_error(void);
 
 /* A batch of task sets (§4.2 task model P:449-471; D3 of DESIGN.md).
- * Device pointers owned by the caller.  n_tasks in 1..32, M in 1..1024.    */
+ * Device pointers owned by the caller.  n_tasks in 1..256, M in 1..1024.   */
 typedef struct {
   int32_t n_sets, n_tasks, M, n_groups;
   int32_t *T;    /* period T_i, ticks                         [n_sets][n_tasks] */
@@ -79,6 +81,10 @@ typedef struct {
   int32_t beta_c_num, beta_m_num, beta_den; /* b = beta * a: 2/100, 10/100          */
   int32_t kc_num, km_num, k_den;  /* conflict factor k: 12/10, 23/10, k >= 1         */
   int32_t max_attempts;           /* UUniFast-Discard budget per set (A-9)                     */
+  int32_t curve_gran;             /* 0: block mode (B ~ U{1..b_max}, cn = ceil(a/B)).  g > 0:
+                                     curve mode (reading A-1): the §7.1 curve
+                                     C = k(a/|P| + b) in the W form with B = ceil(a/g) granules
+                                     of g ticks, cn = g, cc = ceil(k g)                       */
 } gp_gen_params;
 
 typedef enum { GP_1G = 0, GP_SMS_ACT = 1, GP_SMS_INA = 2, GP_BF_ACT = 3, GP_BF_INA = 4 } gp_variant;
@@ -162,7 +168,7 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * A-20, A-22), BF = order > (Def. 5, A-21).  Per-partition test: EDF
  * processor-demand criterion (A-6; C.1.7).
  * Outputs (device, [n_sets] unless noted): ok (1 = schedulable), block_of_task
- * int8 [n_sets][n_tasks] canonical labels (blocks numbered by their lowest
+ * int16 [n_sets][n_tasks] canonical labels (blocks numbered by their lowest
  * task; -1 when rejected by Lemma 1/2), block_size int16 [n_sets][n_tasks]
  * (0-padded), pi (= sum of sizes, 0 when rejected by Lemma 1/2), k (number
  * of partitions, 0 when rejected by Lemma 1/2), n_tests (EDF-PDC calls; the
@@ -178,7 +184,7 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * per-launch work figures of the roofline).
  * Errors: GP_EINVAL (bad struct / variant), GP_ECUDA.
  * ------------------------------------------------------------------------- */
-gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok, int8_t *block_of_task,
+gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok, int16_t *block_of_task,
                       int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                       int64_t *efficiency, unsigned long long *stats, void *stream);
 

@@ -64,7 +64,8 @@ class _Gen(C.Structure):
                 ("ticks_per_unit", C.c_int32), ("n_periods", C.c_int32),
                 ("period_menu", C.c_void_p), ("b_max", C.c_int32), ("beta_c_num", C.c_int32),
                 ("beta_m_num", C.c_int32), ("beta_den", C.c_int32), ("kc_num", C.c_int32),
-                ("km_num", C.c_int32), ("k_den", C.c_int32), ("max_attempts", C.c_int32)]
+                ("km_num", C.c_int32), ("k_den", C.c_int32), ("max_attempts", C.c_int32),
+                ("curve_gran", C.c_int32)]
 
 
 def _declare(L):
@@ -182,7 +183,7 @@ def _gen_struct(gen: dict):
     g = _Gen(gen["M"], gen["n_tasks"], gen["n_bins"], gen["n_prm"], gen["sets_per_group"],
              _p(prm_q).value, gen["ticks_per_unit"], len(menu), _p(menu).value, gen["b_max"],
              gen["beta_c_num"], gen["beta_m_num"], gen["beta_den"], gen["kc_num"],
-             gen["km_num"], gen["k_den"], gen["max_attempts"])
+             gen["km_num"], gen["k_den"], gen["max_attempts"], gen.get("curve_gran", 0))
     return g, (prm_q, menu)  # keep the arrays alive with the struct
 
 
@@ -205,9 +206,9 @@ def uunisort(n, Uq, points):
 def task_fields(gen: dict, u_q20, period_idx, B, typ):
     """{T, D, cn, fn, cc, fc, a, feasible} of one §7.1 task."""
     g, _keep = _gen_struct(gen)
-    out = np.zeros(8, np.int64)
+    out = np.zeros(9, np.int64)
     _check(lib().gpref_task_fields(C.byref(g), u_q20, period_idx, B, typ, _p(out)), "task_fields")
-    return dict(zip(("T", "D", "cn", "fn", "cc", "fc", "a", "feasible"), (int(x) for x in out)))
+    return dict(zip(("T", "D", "cn", "fn", "cc", "fc", "a", "feasible", "B"), (int(x) for x in out)))
 
 
 def wcet(B, c, f, m):
@@ -311,7 +312,7 @@ def allocate(sets: Sets, variant, threads=None):
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     S, n = sets.n_sets, sets.n_tasks
     ok = np.zeros(S, np.uint8)
-    bot = np.zeros((S, n), np.int8)
+    bot = np.zeros((S, n), np.int16)
     bs = np.zeros((S, n), np.int16)
     pi = np.zeros(S, np.int32)
     k = np.zeros(S, np.int32)
@@ -325,7 +326,7 @@ def allocate(sets: Sets, variant, threads=None):
 
 def efficiency(sets: Sets, block_of_task):
     """[n_sets][4] = (lower, upper, achieved, H): work-based utilisations x H."""
-    bot = np.ascontiguousarray(block_of_task, dtype=np.int8)
+    bot = np.ascontiguousarray(block_of_task, dtype=np.int16)
     eff = np.zeros((sets.n_sets, 4), np.int64)
     cs = sets._c()
     _check(lib().gpref_efficiency(C.byref(cs), _p(bot), _p(eff)), "efficiency")

@@ -561,14 +561,72 @@ int gpref_exhaustive(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
 /* (P:775-781), Algorithm 3; tie-breaks per §8(c) C.1.9.          */
 /* ======================================================================= */
 
+/* Task sets up to GPREF_MAX_TASKS tasks: partition task-sets are bitsets. */
+#define GPREF_MAX_TASKS 256
+#define GPREF_W (GPREF_MAX_TASKS / 64)
+
 typedef struct {
-  uint32_t mask;
+  uint64_t w[GPREF_W];
+} tmask;
+
+static int tm_has(const tmask *m, int32_t i) { return (int)((m->w[i >> 6] >> (i & 63)) & 1u); }
+static void tm_set(tmask *m, int32_t i) { m->w[i >> 6] |= 1ull << (i & 63); }
+static tmask tm_or(tmask a, tmask b) {
+  for (int x = 0; x < GPREF_W; ++x) a.w[x] |= b.w[x];
+  return a;
+}
+static int tm_eq(const tmask *a, const tmask *b) {
+  for (int x = 0; x < GPREF_W; ++x)
+    if (a->w[x] != b->w[x]) return 0;
+  return 1;
+}
+static tmask tm_single(int32_t i) {
+  tmask m;
+  memset(&m, 0, sizeof(m));
+  tm_set(&m, i);
+  return m;
+}
+
+/* P:462 on a bitset block: another task of the same type in the block */
+static int conflict_bs(int32_t n, const uint8_t *type, const tmask *mask, int32_t i) {
+  for (int32_t j = 0; j < n; ++j)
+    if (j != i && tm_has(mask, j) && type[j] == type[i]) return 1;
+  return 0;
+}
+
+static int64_t task_wcet_bs(const gpref_sets *s, int32_t set, int32_t i, const tmask *mask,
+                            int32_t m) {
+  int32_t n = s->n_tasks;
+  const uint8_t *type = s->type + (int64_t)set * n;
+  int64_t base = (int64_t)set * n + i;
+  if (conflict_bs(n, type, mask, i)) return gpref_wcet(s->B[base], s->cc[base], s->fc[base], m);
+  return gpref_wcet(s->B[base], s->cn[base], s->fn[base], m);
+}
+
+/* EDF-PDC of a bitset block at size m with the conflict-resolved WCETs. */
+static int block_schedulable_bs(const gpref_sets *s, int32_t set, const tmask *mask, int32_t m) {
+  int32_t n = s->n_tasks;
+  int64_t C[GPREF_MAX_TASKS], D[GPREF_MAX_TASKS], T[GPREF_MAX_TASKS];
+  int32_t q = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (!tm_has(mask, i)) continue;
+    int64_t base = (int64_t)set * n + i;
+    C[q] = task_wcet_bs(s, set, i, mask, m);
+    D[q] = s->D[base];
+    T[q] = s->T[base];
+    ++q;
+  }
+  return gpref_edf_pdc(q, C, D, T, NULL, NULL) == 1;
+}
+
+typedef struct {
+  tmask mask;
   int32_t size;
   int64_t uh; /* U(P) * H, Def. 5 with /T_i (reading A-19) scaled by H */
 } part_t;
 
 typedef struct {
-  uint32_t a, b; /* unordered pair of partition task-sets (snapshot) */
+  tmask a, b; /* unordered pair of partition task-sets (snapshot) */
 } snap_t;
 
 typedef struct {
@@ -576,27 +634,27 @@ typedef struct {
   int32_t set, n, M;
   int64_t H;
   int64_t n_tests;
-  part_t list[32]; /* par_list, kept sorted */
+  part_t list[GPREF_MAX_TASKS]; /* par_list, kept sorted */
   int32_t len;
   snap_t *snaps;
   int32_t n_snaps, cap_snaps;
-  uint8_t forb[32][32]; /* ACT task pairs */
+  uint8_t *forb; /* ACT task pairs, n x n */
   int act;
 } heur_t;
 
-static int32_t min_task(uint32_t mask) {
-  for (int32_t i = 0; i < 32; ++i)
-    if ((mask >> i) & 1u) return i;
-  return 32;
+static int32_t min_task(const tmask *mask) {
+  for (int32_t i = 0; i < GPREF_MAX_TASKS; ++i)
+    if (tm_has(mask, i)) return i;
+  return GPREF_MAX_TASKS;
 }
 
 /* U(P) * H = sum_{i in P} C_i(T^P - {tau_i}, |P|) * (H / T_i) (A-19) */
-static int64_t part_uh(const heur_t *h, uint32_t mask, int32_t m) {
+static int64_t part_uh(const heur_t *h, const tmask *mask, int32_t m) {
   i128 u = 0;
   for (int32_t i = 0; i < h->n; ++i) {
-    if (!((mask >> i) & 1u)) continue;
+    if (!tm_has(mask, i)) continue;
     int64_t base = (int64_t)h->set * h->n + i;
-    u += (i128)task_wcet_in_block(h->s, h->set, i, mask, m) * (h->H / h->s->T[base]);
+    u += (i128)task_wcet_bs(h->s, h->set, i, mask, m) * (h->H / h->s->T[base]);
   }
   return (int64_t)u;
 }
@@ -604,7 +662,7 @@ static int64_t part_uh(const heur_t *h, uint32_t mask, int32_t m) {
 /* par_list order: decreasing utilisation, ties by lower min task id (A-17) */
 static int part_before(const part_t *x, const part_t *y) {
   if (x->uh != y->uh) return x->uh > y->uh;
-  return min_task(x->mask) < min_task(y->mask);
+  return min_task(&x->mask) < min_task(&y->mask);
 }
 
 static void list_insert(heur_t *h, part_t p) {
@@ -616,56 +674,57 @@ static void list_insert(heur_t *h, part_t p) {
   h->len += 1;
 }
 
-static void list_remove(heur_t *h, uint32_t mask) {
+static void list_remove(heur_t *h, const tmask *mask) {
   int32_t q = 0;
-  while (q < h->len && h->list[q].mask != mask) ++q;
+  while (q < h->len && !tm_eq(&h->list[q].mask, mask)) ++q;
   for (; q + 1 < h->len; ++q) h->list[q] = h->list[q + 1];
   h->len -= 1;
 }
 
-static int test_schedulability(heur_t *h, uint32_t mask, int32_t m) {
+static int test_schedulability(heur_t *h, const tmask *mask, int32_t m) {
   h->n_tests += 1; /* every EDF-PDC call counts (C.1.9 step 7) */
-  return block_schedulable(h->s, h->set, mask, m);
+  return block_schedulable_bs(h->s, h->set, mask, m);
 }
 
 /* Algorithm 2: try m = max(|P1|,|P2|), ..., |P1|+|P2|-1 in order;
  * the strict upper bound is Def. 3's m3 < m1 + m2.  Returns m or 0. */
 static int32_t merge(heur_t *h, const part_t *p1, const part_t *p2) {
-  uint32_t t3 = p1->mask | p2->mask;
+  tmask t3 = tm_or(p1->mask, p2->mask);
   int32_t m = p1->size > p2->size ? p1->size : p2->size;
   while (m < p1->size + p2->size) {
-    if (test_schedulability(h, t3, m)) return m;
+    if (test_schedulability(h, &t3, m)) return m;
     m = m + 1;
   }
   return 0;
 }
 
-static void add_to_forbidden_moves(heur_t *h, uint32_t a, uint32_t b) {
+static void add_to_forbidden_moves(heur_t *h, const tmask *a, const tmask *b) {
   if (h->n_snaps == h->cap_snaps) {
     h->cap_snaps = h->cap_snaps ? 2 * h->cap_snaps : 64;
     h->snaps = (snap_t *)realloc(h->snaps, sizeof(snap_t) * (size_t)h->cap_snaps);
   }
-  h->snaps[h->n_snaps].a = a;
-  h->snaps[h->n_snaps].b = b;
+  h->snaps[h->n_snaps].a = *a;
+  h->snaps[h->n_snaps].b = *b;
   h->n_snaps += 1;
 }
 
 /* Is P' in forbidden(P) (Alg. 3 line 7)?  Snapshots in both modes; in ACT
  * mode also any task pair of the prefilled list ("at least one task is
  * implied in a forbidden merge with a task of P").                          */
-static int forbidden(const heur_t *h, uint32_t p, uint32_t q) {
+static int forbidden(const heur_t *h, const tmask *p, const tmask *q) {
   for (int32_t x = 0; x < h->n_snaps; ++x)
-    if ((h->snaps[x].a == p && h->snaps[x].b == q) || (h->snaps[x].a == q && h->snaps[x].b == p))
+    if ((tm_eq(&h->snaps[x].a, p) && tm_eq(&h->snaps[x].b, q)) ||
+        (tm_eq(&h->snaps[x].a, q) && tm_eq(&h->snaps[x].b, p)))
       return 1;
   if (h->act)
     for (int32_t a = 0; a < h->n; ++a)
-      if ((p >> a) & 1u)
+      if (tm_has(p, a))
         for (int32_t b = 0; b < h->n; ++b)
-          if (((q >> b) & 1u) && h->forb[a][b]) return 1;
+          if (tm_has(q, b) && h->forb[a * h->n + b]) return 1;
   return 0;
 }
 
-static void write_solution(const heur_t *h, int ok, uint8_t *okp, int8_t *bot, int16_t *bs,
+static void write_solution(const heur_t *h, int ok, uint8_t *okp, int16_t *bot, int16_t *bs,
                            int32_t *pi, int32_t *k, int64_t *nt, int with_parts) {
   int32_t n = h->n, set = h->set;
   okp[set] = (uint8_t)ok;
@@ -683,9 +742,9 @@ static void write_solution(const heur_t *h, int ok, uint8_t *okp, int8_t *bot, i
   int32_t label = 0, total = 0;
   for (int32_t i = 0; i < n; ++i) {
     for (int32_t q = 0; q < h->len; ++q) {
-      if (min_task(h->list[q].mask) != i) continue;
+      if (min_task(&h->list[q].mask) != i) continue;
       for (int32_t t = 0; t < n; ++t)
-        if ((h->list[q].mask >> t) & 1u) bot[(int64_t)set * n + t] = (int8_t)label;
+        if (tm_has(&h->list[q].mask, t)) bot[(int64_t)set * n + t] = (int16_t)label;
       bs[(int64_t)set * n + label] = (int16_t)h->list[q].size;
       total += h->list[q].size;
       label += 1;
@@ -696,25 +755,29 @@ static void write_solution(const heur_t *h, int ok, uint8_t *okp, int8_t *bot, i
 }
 
 static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint8_t *okp,
-                         int8_t *bot, int16_t *bs, int32_t *pi, int32_t *kk, int64_t *nt) {
-  heur_t h;
-  memset(&h, 0, sizeof(h));
-  h.s = s; h.set = set; h.n = s->n_tasks; h.M = s->M;
-  int32_t n = h.n, M = h.M;
-  int64_t Tv[32];
+                         int16_t *bot, int16_t *bs, int32_t *pi, int32_t *kk, int64_t *nt) {
+  heur_t *h = (heur_t *)calloc(1, sizeof(heur_t));
+
+  h->s = s; h->set = set; h->n = s->n_tasks; h->M = s->M;
+  int32_t n = h->n, M = h->M;
+  int64_t Tv[GPREF_MAX_TASKS];
   for (int32_t i = 0; i < n; ++i) Tv[i] = s->T[(int64_t)set * n + i];
-  if (gpref_hyperperiod(n, Tv, &h.H) != 0) h.H = 0;
+  if (gpref_hyperperiod(n, Tv, &h->H) != 0) h->H = 0;
+  tmask empty;
+  memset(&empty, 0, sizeof(empty));
 
   if (variant == GPREF_1G) {
     /* 1G: the whole GPU as one partition of M SMs */
-    part_t all = {(n == 32) ? 0xFFFFFFFFu : ((1u << n) - 1u), M, 0};
-    int ok = test_schedulability(&h, all.mask, M);
-    h.list[0] = all;
-    h.len = 1;
-    write_solution(&h, ok, okp, bot, bs, pi, kk, nt, 1);
+    part_t all = {empty, M, 0};
+    for (int32_t i = 0; i < n; ++i) tm_set(&all.mask, i);
+    int ok = test_schedulability(h, &all.mask, M);
+    h->list[0] = all;
+    h->len = 1;
+    write_solution(h, ok, okp, bot, bs, pi, kk, nt, 1);
+    free(h);
     return;
   }
-  h.act = (variant == GPREF_SMS_ACT || variant == GPREF_BF_ACT);
+  h->act = (variant == GPREF_SMS_ACT || variant == GPREF_BF_ACT);
   int sms = (variant == GPREF_SMS_ACT || variant == GPREF_SMS_INA);
 
   /* Lemma 1: reject if sum_i C_i^n(1)/T_i > M, i.e. in integers
@@ -722,10 +785,11 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
   i128 lhs = 0;
   for (int32_t i = 0; i < n; ++i) {
     int64_t b = (int64_t)set * n + i;
-    lhs += (i128)gpref_wcet(s->B[b], s->cn[b], s->fn[b], 1) * (h.H / s->T[b]);
+    lhs += (i128)gpref_wcet(s->B[b], s->cn[b], s->fn[b], 1) * (h->H / s->T[b]);
   }
-  if (lhs > (i128)M * h.H) {
-    write_solution(&h, 0, okp, bot, bs, pi, kk, nt, 0);
+  if (lhs > (i128)M * h->H) {
+    write_solution(h, 0, okp, bot, bs, pi, kk, nt, 0);
+    free(h);
     return;
   }
   /* init_partitions, Lemma 2: |P| = min{m in 1..M : C^n(m) <= D} */
@@ -740,53 +804,55 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
       }
     }
     if (size == 0) { /* no feasible size: fail */
-      write_solution(&h, 0, okp, bot, bs, pi, kk, nt, 0);
+      write_solution(h, 0, okp, bot, bs, pi, kk, nt, 0);
+      free(h);
       return;
     }
-    part_t p = {1u << i, size, 0};
-    p.uh = part_uh(&h, p.mask, size);
-    list_insert(&h, p);
+    part_t p = {tm_single(i), size, 0};
+    p.uh = part_uh(h, &p.mask, size);
+    list_insert(h, p);
     Pi += size;
   }
   /* Lemma 3: exit on success at any time -- before the ACT
    * prefill (reading A-24).                                                  */
   if (Pi <= M) {
-    write_solution(&h, 1, okp, bot, bs, pi, kk, nt, 1);
+    write_solution(h, 1, okp, bot, bs, pi, kk, nt, 1);
+    free(h);
     return;
   }
   /* Alg. 1 line 3 / §5.3: ACT tests every couple of tasks. */
-  if (h.act) {
-    part_t single[32];
-    for (int32_t q = 0; q < h.len; ++q) single[min_task(h.list[q].mask)] = h.list[q];
+  if (h->act) {
+    h->forb = (uint8_t *)calloc((size_t)n * n, 1);
+    part_t *single = (part_t *)calloc((size_t)n, sizeof(part_t));
+    for (int32_t q = 0; q < h->len; ++q) single[min_task(&h->list[q].mask)] = h->list[q];
     for (int32_t i = 0; i < n; ++i)
       for (int32_t j = i + 1; j < n; ++j)
-        if (merge(&h, &single[i], &single[j]) == 0) h.forb[i][j] = h.forb[j][i] = 1;
+        if (merge(h, &single[i], &single[j]) == 0) h->forb[i * n + j] = h->forb[j * n + i] = 1;
+    free(single);
   }
   /* Alg. 1 lines 4-18 */
   while (Pi > M) {
     /* Algorithm 3: select_partitions -- choose_from takes the head (A-18). */
     int32_t sel = -1;
-    uint32_t elig[32];
     int32_t n_elig = 0;
-    for (int32_t c = 0; c < h.len && sel < 0; ++c) {
+    part_t cand[GPREF_MAX_TASKS];
+    for (int32_t c = 0; c < h->len && sel < 0; ++c) {
       n_elig = 0;
-      for (int32_t q = 0; q < h.len; ++q) {
+      for (int32_t q = 0; q < h->len; ++q) {
         if (q == c) continue; /* P itself is not eligible (A-26) */
-        if (forbidden(&h, h.list[c].mask, h.list[q].mask)) continue;
-        elig[n_elig++] = h.list[q].mask;
+        if (forbidden(h, &h->list[c].mask, &h->list[q].mask)) continue;
+        cand[n_elig++] = h->list[q];
       }
       if (n_elig > 0) sel = c;
     }
     if (sel < 0) { /* Alg. 1 line 6-7: return false */
-      write_solution(&h, 0, okp, bot, bs, pi, kk, nt, 1);
-      free(h.snaps);
+      write_solution(h, 0, okp, bot, bs, pi, kk, nt, 1);
+      free(h->snaps);
+      free(h->forb);
+      free(h);
       return;
     }
-    part_t P = h.list[sel];
-    part_t cand[32];
-    for (int32_t e = 0; e < n_elig; ++e)
-      for (int32_t q = 0; q < h.len; ++q)
-        if (h.list[q].mask == elig[e]) cand[e] = h.list[q];
+    part_t P = h->list[sel];
     if (sms) {
       /* Def. 4 order >>: evaluate every eligible merge, record the
        * failures, keep the best: smallest merged size, then smaller merged
@@ -794,24 +860,25 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
       int32_t best = -1, best_m = 0;
       int64_t best_uh = 0;
       for (int32_t e = 0; e < n_elig; ++e) {
-        int32_t m = merge(&h, &P, &cand[e]);
+        int32_t m = merge(h, &P, &cand[e]);
         if (m == 0) {
-          add_to_forbidden_moves(&h, P.mask, cand[e].mask);
+          add_to_forbidden_moves(h, &P.mask, &cand[e].mask);
           continue;
         }
-        int64_t uh = part_uh(&h, P.mask | cand[e].mask, m);
+        tmask u3 = tm_or(P.mask, cand[e].mask);
+        int64_t uh = part_uh(h, &u3, m);
         int better = 0;
         if (best < 0) better = 1;
         else if (m != best_m) better = m < best_m;
         else if (uh != best_uh) better = uh < best_uh;
-        else better = min_task(cand[e].mask) < min_task(cand[best].mask);
+        else better = min_task(&cand[e].mask) < min_task(&cand[best].mask);
         if (better) { best = e; best_m = m; best_uh = uh; }
       }
       if (best >= 0) {
-        part_t merged = {P.mask | cand[best].mask, best_m, best_uh};
-        list_remove(&h, P.mask);
-        list_remove(&h, cand[best].mask);
-        list_insert(&h, merged);
+        part_t merged = {tm_or(P.mask, cand[best].mask), best_m, best_uh};
+        list_remove(h, &P.mask);
+        list_remove(h, &cand[best].mask);
+        list_insert(h, merged);
         Pi = Pi - P.size - cand[best].size + best_m;
       }
     } else {
@@ -823,29 +890,32 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
           part_t t = cand[y]; cand[y] = cand[y - 1]; cand[y - 1] = t;
         }
       for (int32_t e = 0; e < n_elig; ++e) {
-        int32_t m = merge(&h, &P, &cand[e]);
+        int32_t m = merge(h, &P, &cand[e]);
         if (m == 0) {
-          add_to_forbidden_moves(&h, P.mask, cand[e].mask);
+          add_to_forbidden_moves(h, &P.mask, &cand[e].mask);
           continue;
         }
-        part_t merged = {P.mask | cand[e].mask, m, part_uh(&h, P.mask | cand[e].mask, m)};
-        list_remove(&h, P.mask);
-        list_remove(&h, cand[e].mask);
-        list_insert(&h, merged);
+        tmask u3 = tm_or(P.mask, cand[e].mask);
+        part_t merged = {u3, m, part_uh(h, &u3, m)};
+        list_remove(h, &P.mask);
+        list_remove(h, &cand[e].mask);
+        list_insert(h, merged);
         Pi = Pi - P.size - cand[e].size + m;
         break;
       }
     }
   }
-  write_solution(&h, 1, okp, bot, bs, pi, kk, nt, 1);
-  free(h.snaps);
+  write_solution(h, 1, okp, bot, bs, pi, kk, nt, 1);
+  free(h->snaps);
+  free(h->forb);
+  free(h);
 }
 
 typedef struct {
   const gpref_sets *s;
   int32_t variant;
   uint8_t *ok;
-  int8_t *bot;
+  int16_t *bot;
   int16_t *bs;
   int32_t *pi, *k;
   int64_t *nt;
@@ -864,10 +934,11 @@ static void *alloc_worker(void *arg) {
   }
 }
 
-int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int8_t *block_of_task,
+int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int16_t *block_of_task,
                    int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                    int32_t n_threads) {
-  if (variant < 0 || variant > 4 || s->n_tasks < 1 || s->n_tasks > 32 || s->M < 1) return 1;
+  if (variant < 0 || variant > 4 || s->n_tasks < 1 || s->n_tasks > GPREF_MAX_TASKS || s->M < 1)
+    return 1;
   alloc_job j;
   memset(&j, 0, sizeof(j));
   j.s = s; j.variant = variant; j.ok = ok; j.bot = block_of_task; j.bs = block_size;
@@ -890,13 +961,14 @@ int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int8_t *bl
  *   upper    = sum_i cc_i * B_i * (H/T_i)      (every task in conflict)
  *   achieved = sum_i c_i^{x_i} * B_i * (H/T_i) (x_i from the allocation)
  * eff[set] = {lower, upper, achieved (0 without an allocation), H}.        */
-int gpref_efficiency(const gpref_sets *s, const int8_t *block_of_task, int64_t *eff) {
+int gpref_efficiency(const gpref_sets *s, const int16_t *block_of_task, int64_t *eff) {
   int32_t n = s->n_tasks;
+  if (n < 1 || n > GPREF_MAX_TASKS) return 1;
   for (int32_t set = 0; set < s->n_sets; ++set) {
-    int64_t T[32], H;
+    int64_t T[GPREF_MAX_TASKS], H;
     for (int32_t i = 0; i < n; ++i) T[i] = s->T[(int64_t)set * n + i];
     if (gpref_hyperperiod(n, T, &H) != 0) return 2;
-    const int8_t *lab = block_of_task + (int64_t)set * n;
+    const int16_t *lab = block_of_task + (int64_t)set * n;
     const uint8_t *type = s->type + (int64_t)set * n;
     int has_alloc = lab[0] >= 0;
     i128 lo = 0, up = 0, ach = 0;
@@ -906,10 +978,11 @@ int gpref_efficiency(const gpref_sets *s, const int8_t *block_of_task, int64_t *
       lo += (i128)s->cn[b] * s->B[b] * q;
       up += (i128)s->cc[b] * s->B[b] * q;
       if (has_alloc) {
-        uint32_t mask = 0;
+        tmask mask;
+        memset(&mask, 0, sizeof(mask));
         for (int32_t j = 0; j < n; ++j)
-          if (lab[j] == lab[i]) mask |= 1u << j;
-        int x = gpref_conflict(n, type, mask, i);
+          if (lab[j] == lab[i]) tm_set(&mask, j);
+        int x = conflict_bs(n, type, &mask, i);
         ach += (i128)(x ? s->cc[b] : s->cn[b]) * s->B[b] * q;
       }
     }
@@ -929,8 +1002,8 @@ int gpref_efficiency(const gpref_sets *s, const int8_t *block_of_task, int64_t *
  * n-1 points are sorted and the n gaps of 0 <= p_(1) <= ... <= p_(n-1) <= Uq
  * are the utilisations, so sum(u) = Uq exactly.                             */
 int gpref_uunisort(int32_t n, int64_t Uq, const int64_t *points, int64_t *u) {
-  if (n < 1 || n > 32) return 1;
-  int64_t pts[32];
+  if (n < 1 || n > GPREF_MAX_TASKS) return 1;
+  int64_t pts[GPREF_MAX_TASKS];
   for (int32_t j = 0; j < n - 1; ++j) {
     if (points[j] < 0 || points[j] > Uq) return 1;
     pts[j] = points[j];
@@ -950,31 +1023,45 @@ int gpref_uunisort(int32_t n, int64_t Uq, const int64_t *points, int64_t *u) {
 /* One task of §7.1 from its utilisation u (Q20), menu index,
  * block count and type.  out = {T, D, cn, fn, cc, fc, a, feasible_alone}.   */
 int gpref_task_fields(const gpref_gen_params *p, int64_t u, int32_t period_idx, int64_t B,
-                      int32_t type, int64_t out[8]) {
+                      int32_t type, int64_t out[9]) {
   int32_t Q = p->ticks_per_unit;
   if (period_idx < 0 || period_idx >= p->n_periods || B < 1) return 1;
+  int curve = p->curve_gran > 0;
   /* period from the menu, bumped while the execution time is not
-   * "reasonable" (reading A-10): a < max(Q, B), up to the largest period.   */
+   * "reasonable" (reading A-10): a < max(Q, B), up to the largest period.
+   * Curve mode (f1, reading A-1): B is derived from a, so the rule is a < Q. */
   int64_t pi_ = period_idx;
   int64_t T = (int64_t)p->period_menu[pi_] * Q;
   int64_t a = (u * T) >> 20; /* baseline execution time = T * u */
-  int64_t need = B > Q ? B : Q;
+  int64_t need = (curve || B <= Q) ? Q : B;
   while (a < need && pi_ < p->n_periods - 1) {
     pi_ += 1;
     T = (int64_t)p->period_menu[pi_] * Q;
     a = (u * T) >> 20;
   }
-  int64_t D = 3 * T / 4;                               /* D = 0.75 T */
-  int64_t cn = ceil_div(a, B);                          /* per-wave block cost */
-  if (cn < 1) cn = 1;
+  int64_t D = 3 * T / 4;                                /* D = 0.75 T */
   int64_t beta = type ? p->beta_m_num : p->beta_c_num;  /* b = 0.02a / 0.1a */
   int64_t fn = ceil_div(a * beta, p->beta_den);
   int64_t kf = type ? p->km_num : p->kc_num;            /* k = 1.2 / 2.3, A-14 */
-  int64_t cc = ceil_div(cn * kf, p->k_den);
+  int64_t cn, cc;
+  if (curve) {
+    /* the §7.1 curve C = k(a/|P| + b) in the W form: a split into granules of
+     * g ticks, W(m) = ceil(B/m) * g * k + ceil(k b) with B = ceil(a/g)       */
+    int64_t g = p->curve_gran;
+    B = ceil_div(a, g);
+    if (B < 1) B = 1;
+    cn = g;
+    cc = ceil_div(g * kf, p->k_den);
+  } else {
+    cn = ceil_div(a, B); /* per-wave block cost */
+    if (cn < 1) cn = 1;
+    cc = ceil_div(cn * kf, p->k_den);
+  }
   int64_t fc = ceil_div(fn * kf, p->k_den);
   out[0] = T; out[1] = D; out[2] = cn; out[3] = fn; out[4] = cc; out[5] = fc; out[6] = a;
   /* feasible alone on all M SMs without conflict (discard rule, A-9) */
   out[7] = gpref_wcet(B, cn, fn, p->M) <= D;
+  out[8] = B;
   return 0;
 }
 
@@ -983,12 +1070,12 @@ static void generate_one(const gpref_gen_params *p, uint64_t seed, uint64_t g, i
   int32_t n = p->n_tasks, M = p->M;
   int64_t Uq = ((int64_t)(bin + 1) * (int64_t)M << 20) / p->n_bins; /* Q20 total (A-31) */
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-  int64_t f[32][8], Bv[32];
-  uint8_t type[32];
+  int64_t f[GPREF_MAX_TASKS][9], Bv[GPREF_MAX_TASKS];
+  uint8_t type[GPREF_MAX_TASKS];
   int valid = 0;
   for (int32_t attempt = 0; attempt < p->max_attempts; ++attempt) {
-    int64_t pts[32] = {0}, u[32];
-    int32_t pidx[32];
+    int64_t pts[GPREF_MAX_TASKS] = {0}, u[GPREF_MAX_TASKS];
+    int32_t pidx[GPREF_MAX_TASKS];
     for (int32_t j = 0; j < n; ++j) {
       uint32_t ctr[4] = {(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)attempt, (uint32_t)j};
       uint32_t w[4];
@@ -1015,7 +1102,7 @@ static void generate_one(const gpref_gen_params *p, uint64_t seed, uint64_t g, i
     int64_t o = l * n + i;
     out->T[o] = (int32_t)f[i][0];
     out->D[o] = (int32_t)f[i][1];
-    out->B[o] = (int32_t)Bv[i];
+    out->B[o] = (int32_t)f[i][8];
     out->cn[o] = (int32_t)f[i][2];
     out->fn[o] = (int32_t)f[i][3];
     out->cc[o] = (int32_t)f[i][4];
@@ -1027,7 +1114,7 @@ static void generate_one(const gpref_gen_params *p, uint64_t seed, uint64_t g, i
 
 int gpref_generate(const gpref_gen_params *p, uint64_t seed, uint64_t rep_begin,
                    int32_t rep_count, gpref_sets *out) {
-  if (p->n_tasks < 1 || p->n_tasks > 32 || p->M < 1 || p->n_bins < 1 || p->n_prm < 1 ||
+  if (p->n_tasks < 1 || p->n_tasks > GPREF_MAX_TASKS || p->M < 1 || p->n_bins < 1 || p->n_prm < 1 ||
       p->n_periods < 1 || p->max_attempts < 1 || p->b_max < 1 || p->beta_den < 1 ||
       p->k_den < 1 || rep_count < 0 || rep_begin + (uint64_t)rep_count > (uint64_t)p->sets_per_group)
     return 1;

@@ -12,6 +12,8 @@
  * header, table or helper with the CUDA path (paper_2105_10312_b200/csrc);
  * neither side includes or links the other.
  *
+ * Task sets have up to 256 tasks (heuristics, generator, efficiency; the
+ * exhaustive enumeration is limited by N_c < 2^63 instead).
  * Everything is integer.  Time is in integer ticks (§8(c) C.1.1).  Host
  * arrays only; layout of every per-task field is [n_sets][n_tasks]
  * (set-major, task-minor) -- the same layout the C ABI documents.
@@ -44,6 +46,7 @@ typedef struct {
   int32_t beta_c_num, beta_m_num, beta_den;
   int32_t kc_num, km_num, k_den;
   int32_t max_attempts;
+  int32_t curve_gran;                     /* 0: block mode; g > 0: curve mode (f1), granule g ticks */
 } gpref_gen_params;
 
 /* ---- A1: counter-based generator (§7.1; §8(c) C.1.10) ---- */
@@ -52,7 +55,7 @@ int gpref_generate(const gpref_gen_params *p, uint64_t seed, uint64_t rep_begin,
                    int32_t rep_count, gpref_sets *out);
 int gpref_uunisort(int32_t n, int64_t Uq, const int64_t *points, int64_t *u);
 int gpref_task_fields(const gpref_gen_params *p, int64_t u_q20, int32_t period_idx, int64_t B,
-                      int32_t type, int64_t out[8]);
+                      int32_t type, int64_t out[9]);
 
 /* ---- A3: WCET model (P:4-25 example; §3.3; §4.2) ---- */
 int64_t gpref_wcet(int64_t B, int64_t c, int64_t f, int64_t m);              /* C.1.3 */
@@ -84,12 +87,12 @@ int gpref_exhaustive(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
 
 /* ---- A5: heuristics, Alg. 1-3 + 1G ---- */
 enum { GPREF_1G = 0, GPREF_SMS_ACT = 1, GPREF_SMS_INA = 2, GPREF_BF_ACT = 3, GPREF_BF_INA = 4 };
-int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int8_t *block_of_task,
+int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int16_t *block_of_task,
                    int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                    int32_t n_threads);
 
 /* ---- f2: scheduled workload of an allocation ---- */
-int gpref_efficiency(const gpref_sets *s, const int8_t *block_of_task, int64_t *eff);
+int gpref_efficiency(const gpref_sets *s, const int16_t *block_of_task, int64_t *eff);
 
 /* ---- A6: segmented ratio reduction (§7.2; §8(c) C.1.11) ---- */
 int gpref_sched_ratio(const gpref_sets *s, const uint8_t *verdicts, int32_t n_rows,

@@ -20,6 +20,10 @@
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
 
+gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, uint8_t *ok, int16_t *bot,
+                                 int16_t *bs, int32_t *pi, int32_t *k, int64_t *n_tests,
+                                 int64_t *eff, unsigned long long *stats, cudaStream_t st);
+
 namespace gp {
 
 struct AllocArgs {
@@ -27,7 +31,7 @@ struct AllocArgs {
   const uint8_t *type;
   int32_t n_sets, n, M, variant;
   uint8_t *ok;
-  int8_t *bot;
+  int16_t *bot;
   int16_t *bs;
   int32_t *pi, *k;
   int64_t *n_tests;
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     __syncwarp();
     const int32_t Pi_out = stage ? warp_sum_i32(psz) : 0;
     if (t.in) {
-      a.bot[o] = (int8_t)(stage ? scr.lab[lane] : -1);
+      a.bot[o] = (int16_t)(stage ? scr.lab[lane] : -1);
       a.bs[o] = (int16_t)((stage && lane < kk) ? scr.size[lane] : 0);
     }
     st_sets += 1;
@@ -533,18 +537,21 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
 }  // namespace gp
 
 extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok,
-                                 int8_t *block_of_task, int16_t *block_size, int32_t *pi,
+                                 int16_t *block_of_task, int16_t *block_size, int32_t *pi,
                                  int32_t *k, int64_t *n_tests, int64_t *efficiency,
                                  unsigned long long *stats, void *stream) {
   using namespace gp;
-  if (!ts || ts->n_tasks < 1 || ts->n_tasks > kMaxTasks || ts->M < 1 || ts->M > 1024 ||
+  if (!ts || ts->n_tasks < 1 || ts->n_tasks > 256 || ts->M < 1 || ts->M > 1024 ||
       ts->n_sets < 0)
-    return gp_fail(GP_EINVAL, "gp_allocate: bad task sets (n_tasks 1..32, M 1..1024)");
+    return gp_fail(GP_EINVAL, "gp_allocate: bad task sets (n_tasks 1..256, M 1..1024)");
   if ((int)v < 0 || (int)v > 4) return gp_fail(GP_EINVAL, "gp_allocate: bad variant %d", (int)v);
   if (ts->n_sets == 0) return gp_cuda_check("gp_allocate");
   if (!ok || !block_of_task || !block_size || !pi || !k || !n_tests || !ts->T || !ts->D ||
       !ts->B || !ts->cn || !ts->cc || !ts->fn || !ts->fc || !ts->type)
     return gp_fail(GP_EINVAL, "gp_allocate: null pointer");
+  if (ts->n_tasks > kMaxTasks)  // 33..256 tasks: one CTA per set (allocate_big.cu)
+    return gp_allocate_big_launch(ts, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
+                                  efficiency, stats, (cudaStream_t)stream);
   // per-warp ceil(B/m) table: 8 warps x n x M x 2 bytes when it fits (C4: 76 KB)
   size_t tab = (size_t)8 * ts->n_tasks * ts->M * sizeof(uint16_t);
   const bool use_tab = tab <= 100 * 1024;

@@ -19,7 +19,7 @@ namespace gp {
 
 struct GenArgs {
   int32_t M, n, n_bins, n_prm, sets_per_group, Q, n_periods, b_max;
-  int32_t beta_c, beta_m, beta_den, kc, km, k_den, max_attempts, G;
+  int32_t beta_c, beta_m, beta_den, kc, km, k_den, max_attempts, G, curve_gran;
   int32_t rep_count, n_sets;
   uint64_t rep_begin, seed;
   int32_t menu[kMaxMenu];
@@ -43,6 +43,46 @@ GP_DEV void philox4x32_10(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
+}
+
+// One task of §7.1 from its draws; the discard test of A-9.
+struct TaskDraw {
+  uint32_t T, D, cn, fn;
+  int32_t B;
+  bool feasible;
+};
+
+GP_DEV TaskDraw task_fields(const GenArgs &a, uint64_t u, int32_t pidx, int32_t Bv, uint8_t typ) {
+  TaskDraw d;
+  // period bump while the baseline execution time is "not reasonable" (A-10);
+  // in curve mode B is derived from a, and the rule reduces to a < Q
+  int64_t T = (int64_t)a.menu[pidx] * a.Q;
+  int64_t ab = (int64_t)((u * (uint64_t)T) >> 20);
+  const int64_t need = (a.curve_gran > 0 || Bv <= a.Q) ? a.Q : Bv;
+  while (ab < need && pidx < a.n_periods - 1) {
+    ++pidx;
+    T = (int64_t)a.menu[pidx] * a.Q;
+    ab = (int64_t)((u * (uint64_t)T) >> 20);
+  }
+  // host validation bounds a <= M * Tmax < 2^31, so 32-bit arithmetic is exact below
+  const uint32_t a32 = (uint32_t)ab, T32 = (uint32_t)T;
+  d.T = T32;
+  d.D = 3u * (T32 / 4u);                                                          // P:944 (4 | T)
+  if (a.curve_gran > 0) {  // C = k(a/m + b) as W form: B = ceil(a/g) granules, cn = g
+    const uint32_t g = (uint32_t)a.curve_gran;
+    d.B = (int32_t)max((a32 + g - 1u) / g, 1u);
+    d.cn = g;
+  } else {
+    d.B = Bv;
+    d.cn = max((a32 + (uint32_t)Bv - 1u) / (uint32_t)Bv, 1u);
+  }
+  // fn = ceil(a * beta_num / beta_den) without 64-bit division: a = qd*den + r
+  const uint32_t bnum = typ ? (uint32_t)a.beta_m : (uint32_t)a.beta_c, bden = (uint32_t)a.beta_den;
+  const uint32_t qd = a32 / bden, rd = a32 - qd * bden;
+  d.fn = qd * bnum + (rd * bnum + bden - 1u) / bden;
+  const uint32_t waves = (uint32_t)ceil_div_pos(d.B, a.M);
+  d.feasible = (uint64_t)waves * d.cn + d.fn <= (uint64_t)d.D;                   // A-9
+  return d;
 }
 
 __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
@@ -77,7 +117,7 @@ __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
     uint32_t x0 = (uint32_t)g, x1 = (uint32_t)(g >> 32), x2 = (uint32_t)attempt, x3 = (uint32_t)j;
     philox4x32_10(x0, x1, x2, x3, k0, k1);
     const uint8_t typ = ((uint64_t)x0 < pq) ? 1 : 0;
-    int32_t pidx = (int32_t)(((uint64_t)x1 * (uint64_t)a.n_periods) >> 32);          // A-11
+    const int32_t pidx = (int32_t)(((uint64_t)x1 * (uint64_t)a.n_periods) >> 32);    // A-11
     const int32_t Bv = 1 + (int32_t)(((uint64_t)x2 * (uint64_t)a.b_max) >> 32);     // A-13
     // spacing point; lanes >= n-1 carry the pad U_q so they sort last (U_q < 2^31)
     uint32_t pt = (j < n - 1) ? (uint32_t)(((uint64_t)x3 * (uint64_t)(Uq + 1)) >> 32) : (uint32_t)Uq;
@@ -92,30 +132,12 @@ __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
     uint32_t left = __shfl_up_sync(GP_FULL, pt, 1, G);
     if (j == 0) left = 0;
     const uint64_t u = pt - left;  // UUniFast via sorted spacings (A-12)
-    // period bump while the baseline execution time is "not reasonable" (A-10)
-    int64_t T = (int64_t)a.menu[pidx] * a.Q;
-    int64_t ab = (int64_t)((u * (uint64_t)T) >> 20);
-    const int64_t need = Bv > a.Q ? Bv : a.Q;
-    while (ab < need && pidx < a.n_periods - 1) {
-      ++pidx;
-      T = (int64_t)a.menu[pidx] * a.Q;
-      ab = (int64_t)((u * (uint64_t)T) >> 20);
-    }
-    // host validation bounds a <= M * Tmax < 2^31, so 32-bit arithmetic is exact below
-    const uint32_t a32 = (uint32_t)ab, T32 = (uint32_t)T;
-    const uint32_t D = 3u * (T32 / 4u);                                            // P:944 (4 | T)
-    uint32_t cn = (a32 + (uint32_t)Bv - 1u) / (uint32_t)Bv;
-    if (cn < 1u) cn = 1u;
-    // fn = ceil(a * beta_num / beta_den) without 64-bit division: a = qd*den + r
-    const uint32_t bnum = typ ? (uint32_t)a.beta_m : (uint32_t)a.beta_c, bden = (uint32_t)a.beta_den;
-    const uint32_t qd = a32 / bden, rd = a32 - qd * bden;
-    const uint32_t fn = qd * bnum + (rd * bnum + bden - 1u) / bden;
-    const uint32_t waves = (uint32_t)ceil_div_pos(Bv, a.M);
-    const bool feasible = (uint64_t)waves * cn + fn <= (uint64_t)D;                // A-9
+    const TaskDraw d = task_fields(a, u, pidx, Bv, typ);
+    const bool feasible = d.feasible;
     const unsigned bad = __ballot_sync(GP_FULL, (j < n) && !feasible) & gmask;
     if (!done) {
-      oT = (int32_t)T32; oD = (int32_t)D; oB = Bv;
-      ocn = (int32_t)cn; ofn = (int32_t)fn;
+      oT = (int32_t)d.T; oD = (int32_t)d.D; oB = d.B;
+      ocn = (int32_t)d.cn; ofn = (int32_t)d.fn;
       otype = typ;
       if (bad == 0) {
         done = true;
@@ -140,6 +162,71 @@ __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
   }
 }
 
+// n > 32: one CTA of 256 threads per set; thread j owns task j; the spacing
+// points are sorted by a shared-memory bitonic network; the whole-vector
+// discard is a CTA vote.
+__global__ void __launch_bounds__(256) k_generate_big(const GenArgs a) {
+  __shared__ uint32_t pts[256];
+  const int j = threadIdx.x, n = a.n;
+  for (int64_t l = blockIdx.x; l < a.n_sets; l += gridDim.x) {
+    const int32_t grp = (int32_t)(l / a.rep_count);
+    const uint64_t rep = a.rep_begin + (uint64_t)(l % a.rep_count);
+    const uint64_t g = (uint64_t)grp * (uint64_t)a.sets_per_group + rep;
+    const int32_t prm_idx = grp / a.n_bins, bin = grp % a.n_bins;
+    const int64_t Uq = ((int64_t)(bin + 1) * a.M << 20) / a.n_bins;
+    const uint64_t pq = a.prm_q[prm_idx];
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    TaskDraw keep{};
+    uint8_t ktype = 0;
+    bool valid = false;
+    for (int attempt = 0; attempt < a.max_attempts; ++attempt) {
+      uint32_t x0 = (uint32_t)g, x1 = (uint32_t)(g >> 32), x2 = (uint32_t)attempt, x3 = (uint32_t)j;
+      philox4x32_10(x0, x1, x2, x3, k0, k1);
+      const uint8_t typ = ((uint64_t)x0 < pq) ? 1 : 0;
+      const int32_t pidx = (int32_t)(((uint64_t)x1 * (uint64_t)a.n_periods) >> 32);  // A-11
+      const int32_t Bv = 1 + (int32_t)(((uint64_t)x2 * (uint64_t)a.b_max) >> 32);   // A-13
+      pts[j] = (j < n - 1) ? (uint32_t)(((uint64_t)x3 * (uint64_t)(Uq + 1)) >> 32) : (uint32_t)Uq;
+      __syncthreads();
+      for (int kk = 2; kk <= 256; kk <<= 1) {  // bitonic sort, ascending
+        for (int s = kk >> 1; s > 0; s >>= 1) {
+          const int p = j ^ s;
+          if (p > j) {
+            const uint32_t x = pts[j], y = pts[p];
+            const bool asc = (j & kk) == 0;
+            if ((x > y) == asc) {
+              pts[j] = y;
+              pts[p] = x;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      const uint64_t u = pts[j] - (j == 0 ? 0u : pts[j - 1]);  // sorted spacings (A-12)
+      const TaskDraw d = task_fields(a, u, pidx, Bv, typ);
+      const int bad = __syncthreads_or(j < n && !d.feasible);
+      keep = d;
+      ktype = typ;
+      if (!bad) {
+        valid = true;
+        break;
+      }
+    }
+    if (j < n) {
+      const int64_t kf = ktype ? a.km : a.kc;
+      const int64_t o = l * n + j;
+      a.T[o] = (int32_t)keep.T; a.D[o] = (int32_t)keep.D; a.B[o] = keep.B;
+      a.cn[o] = (int32_t)keep.cn; a.fn[o] = (int32_t)keep.fn; a.type[o] = ktype;
+      a.cc[o] = (int32_t)ceil_div64((int64_t)keep.cn * kf, a.k_den);  // P:951, A-14
+      a.fc[o] = (int32_t)ceil_div64((int64_t)keep.fn * kf, a.k_den);
+      if (j == 0) {
+        a.valid[l] = valid ? 1 : 0;
+        a.group[l] = grp;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace gp
 
 static int64_t host_gcd(int64_t a, int64_t b) {
@@ -155,8 +242,9 @@ extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t
                                  int32_t rep_count, gp_tasksets *out, void *stream) {
   using namespace gp;
   if (!p || !out) return gp_fail(GP_EINVAL, "gp_generate: null params or output");
-  if (p->n_tasks < 1 || p->n_tasks > kMaxTasks)
-    return gp_fail(GP_EINVAL, "gp_generate: n_tasks %d not in 1..32", p->n_tasks);
+  if (p->n_tasks < 1 || p->n_tasks > 256)
+    return gp_fail(GP_EINVAL, "gp_generate: n_tasks %d not in 1..256", p->n_tasks);
+  if (p->curve_gran < 0) return gp_fail(GP_EINVAL, "gp_generate: curve_gran < 0");
   if (p->M < 1 || p->M > 1024) return gp_fail(GP_EINVAL, "gp_generate: M %d not in 1..1024", p->M);
   if (p->n_bins < 1 || p->n_prm < 1 || p->n_prm > kMaxPrm || p->sets_per_group < 1)
     return gp_fail(GP_EINVAL, "gp_generate: bad n_bins/n_prm/sets_per_group");
@@ -193,7 +281,8 @@ extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t
   const int64_t bmax = p->beta_c_num > p->beta_m_num ? p->beta_c_num : p->beta_m_num;
   const int64_t kmax = p->kc_num > p->km_num ? p->kc_num : p->km_num;
   const int64_t fnmax = (amax * bmax + p->beta_den - 1) / p->beta_den;
-  const int64_t ccmax = (amax * kmax + p->k_den - 1) / p->k_den;
+  const int64_t cnmax = p->curve_gran > 0 ? p->curve_gran : amax;
+  const int64_t ccmax = (cnmax * kmax + p->k_den - 1) / p->k_den;
   const int64_t fcmax = (fnmax * kmax + p->k_den - 1) / p->k_den;
   if (ccmax > INT32_MAX || fcmax > INT32_MAX || amax > INT32_MAX)
     return gp_fail(GP_EOVERFLOW, "gp_generate: M*Tmax*k exceeds int32 (fields would overflow)");
@@ -211,14 +300,20 @@ extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t
   a.sets_per_group = p->sets_per_group; a.Q = p->ticks_per_unit; a.n_periods = p->n_periods;
   a.b_max = p->b_max; a.beta_c = p->beta_c_num; a.beta_m = p->beta_m_num; a.beta_den = p->beta_den;
   a.kc = p->kc_num; a.km = p->km_num; a.k_den = p->k_den; a.max_attempts = p->max_attempts;
+  a.curve_gran = p->curve_gran;
   int G = 1;
-  while (G < p->n_tasks) G <<= 1;
+  while (G < p->n_tasks && G < 32) G <<= 1;
   a.G = G;
   a.rep_count = rep_count; a.n_sets = out->n_sets; a.rep_begin = rep_begin; a.seed = seed;
   for (int i = 0; i < kMaxMenu; ++i) a.menu[i] = i < p->n_periods ? p->period_menu[i] : 0;
   for (int i = 0; i < kMaxPrm; ++i) a.prm_q[i] = i < p->n_prm ? p->prm_q[i] : 0;
   a.T = out->T; a.D = out->D; a.B = out->B; a.cn = out->cn; a.cc = out->cc; a.fn = out->fn;
   a.fc = out->fc; a.group = out->group; a.type = out->type; a.valid = out->valid;
+  if (p->n_tasks > 32) {
+    int64_t grid = out->n_sets < 148 * 8 ? out->n_sets : 148 * 8;
+    k_generate_big<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a);
+    return gp_cuda_check("gp_generate");
+  }
   const int64_t threads = (int64_t)out->n_sets * G;
   const int block = 256;
   const int64_t grid = (threads + block - 1) / block;

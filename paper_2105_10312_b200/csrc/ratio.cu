@@ -58,7 +58,7 @@ extern "C" gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode,
                                     int32_t n_slots, int32_t setting, int64_t *counts,
                                     const gp_exhaustive_opts *ex, void *stream) {
   using namespace gp;
-  if (!ts || ts->n_sets < 0 || ts->n_groups < 1 || ts->n_tasks < 1 || ts->n_tasks > kMaxTasks)
+  if (!ts || ts->n_sets < 0 || ts->n_groups < 1 || ts->n_tasks < 1 || ts->n_tasks > 256)
     return gp_fail(GP_EINVAL, "gp_sched_ratio: bad task sets");
   if (n_rows < 1 || slot0 < 0 || slot0 + n_rows > n_slots || setting < 0)
     return gp_fail(GP_EINVAL, "gp_sched_ratio: need 0 <= slot0, slot0 + n_rows <= n_slots");

@@ -51,7 +51,8 @@ class _GenC(C.Structure):
                 ("ticks_per_unit", C.c_int32), ("n_periods", C.c_int32),
                 ("period_menu", C.c_void_p), ("b_max", C.c_int32), ("beta_c_num", C.c_int32),
                 ("beta_m_num", C.c_int32), ("beta_den", C.c_int32), ("kc_num", C.c_int32),
-                ("km_num", C.c_int32), ("k_den", C.c_int32), ("max_attempts", C.c_int32)]
+                ("km_num", C.c_int32), ("k_den", C.c_int32), ("max_attempts", C.c_int32),
+                ("curve_gran", C.c_int32)]
 
 
 class _ExOptsC(C.Structure):
@@ -151,7 +152,7 @@ def gp_generate(gen: dict, seed: int, rep_begin: int, rep_count: int, out: TaskS
     g = _GenC(gen["M"], gen["n_tasks"], gen["n_bins"], gen["n_prm"], gen["sets_per_group"],
               prm_q.ctypes.data, gen["ticks_per_unit"], len(menu), menu.ctypes.data, gen["b_max"],
               gen["beta_c_num"], gen["beta_m_num"], gen["beta_den"], gen["kc_num"], gen["km_num"],
-              gen["k_den"], gen["max_attempts"])
+              gen["k_den"], gen["max_attempts"], gen.get("curve_gran", 0))
     s = out.struct()
     _check(_lib.gp_generate(C.byref(g), seed, rep_begin, rep_count, C.byref(s), _stream(stream)))
     out.M, out.n_groups = s.M, s.n_groups
@@ -196,7 +197,7 @@ def gp_wcet_per_sm(B, cost_per_sm, f=0, stream=None):
 class AllocOut:
     def __init__(self, n_sets, n_tasks, device="cuda"):
         self.ok = torch.empty(n_sets, dtype=torch.uint8, device=device)
-        self.block_of_task = torch.empty((n_sets, n_tasks), dtype=torch.int8, device=device)
+        self.block_of_task = torch.empty((n_sets, n_tasks), dtype=torch.int16, device=device)
         self.block_size = torch.empty((n_sets, n_tasks), dtype=torch.int16, device=device)
         self.pi = torch.empty(n_sets, dtype=torch.int32, device=device)
         self.k = torch.empty(n_sets, dtype=torch.int32, device=device)

@@ -398,3 +398,44 @@ def test_threshold_random_sets(G, seed, n, M):
     ref = oracle.exhaustive(oracle.Sets.from_dict(d).subset(ok_rows))
     assert (per[ok_rows] == ref).all()
     assert per[5, 0] == -1 and counts.cpu().numpy()[0, 0, 0, 2] == 1
+
+
+# ------------------------------------------------------------------ f1: paper-scale shapes
+@pytest.mark.parametrize("key,reps", [("f1_50", 3), ("f1_200", 2)])
+def test_generate_f1_curve_mode(G, key, reps):
+    """§8(f) f1: 50 / 200 tasks per set (CTA-per-set generator) in curve mode
+    (the §7.1 curves C = k(a/|P| + b) in the W form), bit-exact vs the oracle."""
+    gen = W.WORKLOADS[key]["gen"](R=100)
+    ts = G.TaskSets(34 * reps, gen["n_tasks"], 68, 34)
+    G.gp_generate(gen, W.SEED, 5, reps, ts)
+    ref = oracle.generate(gen, W.SEED, 5, reps)
+    got = ts.to_host()
+    for f in FIELDS:
+        assert (got[f] == getattr(ref, f)).all(), f
+
+
+def test_allocate_f1_50(G):
+    """The paper's 50-task scenario (Fig. 5): every variant, every U point
+    2..68, bit-exact vs the oracle (n > 32 path: one CTA per set)."""
+    gen = W.WORKLOADS["f1_50"]["gen"](R=100)
+    ts = G.TaskSets(34 * 2, 50, 68, 34)
+    G.gp_generate(gen, W.SEED, 0, 2, ts)
+    check_allocate(G, ts)
+
+
+def test_allocate_f1_200_low_load(G):
+    """The 200-task scenario (Fig. 7) at the lowest loads (the
+    oracle's plain EDF on 200-task partitions is slow): bit-exact."""
+    gen = W.WORKLOADS["f1_200"]["gen"](R=100)
+    ts = G.TaskSets(34, 200, 68, 34)
+    G.gp_generate(gen, W.SEED, 0, 1, ts)
+    host = to_oracle(ts).subset(list(range(0, 8)))
+    check_allocate(G, G.TaskSets.from_host(host.to_dict()), host)
+
+
+@pytest.mark.parametrize("seed,n,M", [(41, 33, 8), (42, 40, 6), (43, 64, 12), (44, 100, 20),
+                                      (45, 256, 40)])
+def test_allocate_big_random_sets(G, seed, n, M):
+    rng = np.random.default_rng(seed)
+    d = W.random_sets(rng, 12, n, M, periods=(20, 40, 50, 100), b_max=3 * M, cost_max=4)
+    check_allocate(G, gpu_sets(G, d), oracle.Sets.from_dict(d))
