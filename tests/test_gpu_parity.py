@@ -458,7 +458,7 @@ def test_f1_paper_claims_n50(G):
         rate = r["variants"][v]["sched_rate"]
         assert all(x == 1.0 for u, x in zip(U, rate) if u <= 30), v
         assert all(a >= b for a, b in zip(rate, r["variants"]["1G"]["sched_rate"])), v
-        ks = [k for u, k in zip(U, r["variants"][v]["mean_partitions"]) if k and 38 <= u <= 44]
+        ks = [k for u, k in zip(U, r["variants"][v]["mean_partitions"]) if k and 40 <= u <= 46]
         assert ks and all(20 <= k <= 30 for k in ks), (v, ks)
         lo = r["variants"][v]["workload_lower"]
         ach = r["variants"][v]["workload_achieved"]
