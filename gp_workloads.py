@@ -32,13 +32,14 @@ def _same_den(kc, km):
 
 
 def gen_params(M, n_tasks, sets_per_group, n_bins=10, prm=(0.5,), kc=(12, 10), km=(23, 10),
-               max_attempts=1000, curve_gran=0):
+               max_attempts=1000, curve_gran=0, b_per_sm=False):
     """Generator parameters in the integer encoding both sides accept."""
     return dict(
         M=M, n_tasks=n_tasks, n_bins=n_bins, n_prm=len(prm), sets_per_group=sets_per_group,
         prm_q=[PRM_Q[p] for p in prm], ticks_per_unit=Q, period_menu=list(MENU),
         b_max=4 * M,                       # reading A-13: B ~ U{1..4M}
-        beta_c_num=2, beta_m_num=10, beta_den=100,
+        # b = beta * a (P:950, reading A-1); b_per_sm: b = beta * a / M (reading A-1b, f1 only)
+        beta_c_num=2, beta_m_num=10, beta_den=100 * (M if b_per_sm else 1),
         kc_num=kc[0], km_num=km[0], k_den=_same_den(kc, km),
         max_attempts=max_attempts,
         curve_gran=curve_gran,  # > 0: §7.1 curve C = k(a/|P| + b) in the W form (f1, reading A-1)
@@ -81,6 +82,16 @@ WORKLOADS = {
     "f1_200": dict(name="f1_paper_68sm_200tasks", M=68, n=200, exhaustive=False,
                    variants=VARIANT_NAMES,
                    gen=lambda R=100: gen_params(68, 200, R, n_bins=34, curve_gran=10)),
+    # the same sweep under reading A-1b: the non-parallel part b measured in all-SM time
+    # (b = beta * a / M), the reading under which P:975's 1G plateau (U < 35) is reachable
+    "f1b_50": dict(name="f1b_paper_68sm_50tasks_b_per_sm", M=68, n=50, exhaustive=False,
+                   variants=VARIANT_NAMES,
+                   gen=lambda R=100: gen_params(68, 50, R, n_bins=34, curve_gran=10,
+                                                b_per_sm=True)),
+    "f1b_200": dict(name="f1b_paper_68sm_200tasks_b_per_sm", M=68, n=200, exhaustive=False,
+                    variants=VARIANT_NAMES,
+                    gen=lambda R=100: gen_params(68, 200, R, n_bins=34, curve_gran=10,
+                                                 b_per_sm=True)),
 }
 
 

@@ -38,8 +38,13 @@ def run(key, reps):
     G.gp_generate(gen, W.SEED, 0, reps, ts)
     outs = {}
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    ev = []
     for v in W.VARIANT_NAMES:
+        ev.append(torch.cuda.Event(enable_timing=True))
+        ev[-1].record(st)
         outs[v] = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, n).want_efficiency(), stats=stats)
+    ev.append(torch.cuda.Event(enable_timing=True))
+    ev[-1].record(st)
     counts = torch.zeros((1, 34, len(W.VARIANT_NAMES), 3), dtype=torch.int64, device="cuda")
     verdicts = torch.stack([outs[v].ok for v in W.VARIANT_NAMES])
     G.gp_sched_ratio(ts, G.GP_FROM_VERDICTS, counts, verdicts=verdicts, slot0=0,
@@ -47,11 +52,13 @@ def run(key, reps):
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    variant_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(W.VARIANT_NAMES))]
     c = counts.cpu().numpy()[0]
     valid = ts.valid.cpu().numpy().reshape(34, reps)
     res = {"workload": wl["name"], "n": n, "M": M, "reps": reps, "gpu_ms": ms,
            "edf_tests": int(stats[0].item()), "U": [2 * (b + 1) for b in range(34)],
            "valid_rate": valid.mean(1).tolist(), "variants": {}}
+    res["variant_gpu_ms"] = dict(zip(W.VARIANT_NAMES, variant_ms))
     for vi, v in enumerate(W.VARIANT_NAMES):
         h = outs[v].to_host()
         ok = h["ok"].reshape(34, reps).astype(bool)
@@ -72,33 +79,54 @@ def run(key, reps):
 
 
 def claims(r50, r200):
-    """The paper's qualitative claims."""
-    out = {}
-    U = r50["U"]
+    """SPEC acceptance 3-7 (the paper's qualitative claims P:975, P:1014, P:1053,
+    P:1121-1125), evaluated on this sweep; each entry holds the measured
+    quantity and whether the criterion holds."""
     heur = ("SMS_ACT", "SMS_INA", "BF_ACT", "BF_INA")
+    U = r50["U"]
     v50 = r50["variants"]
-    out["heuristics_100pct_below_U"] = {
-        v: max([u for u, x in zip(U, v50[v]["sched_rate"]) if x == 1.0] or [0]) for v in heur}
-    out["1G_last_U_at_100pct"] = max([u for u, x in zip(U, v50["1G"]["sched_rate"]) if x == 1.0]
-                                     or [0])
-    out["dominance_heuristics_ge_1G_every_U"] = {
-        v: all(a >= b for a, b in zip(v50[v]["sched_rate"], v50["1G"]["sched_rate"])) for v in heur}
-    ks = [x for x in v50["SMS_ACT"]["mean_partitions"] if x is not None]
-    out["SMS_ACT_mean_partitions_n50"] = float(np.mean(ks)) if ks else None
-    tests = {v: float(np.mean(v50[v]["edf_tests_per_set"])) for v in heur}
-    out["edf_tests_per_set_n50"] = tests
-    out["ACT_cheaper_than_INA"] = {f"{a}<{b}": tests[a] < tests[b]
-                                   for a, b in (("SMS_ACT", "SMS_INA"), ("BF_ACT", "BF_INA"))}
+    out = {}
+    # 3. every variant (1G included) schedules 100 % for U <= 30
+    last100 = {v: max([u for u, x in zip(U, v50[v]["sched_rate"]) if x == 1.0] or [0])
+               for v in W.VARIANT_NAMES}
+    out["3_plateau_U_le_30"] = {"last_U_at_100pct": last100, "holds": all(
+        all(x == 1.0 for u, x in zip(U, v50[v]["sched_rate"]) if u <= 30) for v in W.VARIANT_NAMES)}
+    # 4. 1G <= 0.1 by U = 45, heuristics >= 1G everywhere, >= 0.3 better somewhere in [36, 50]
+    g = v50["1G"]["sched_rate"]
+    dom = all(all(a >= b for a, b in zip(v50[v]["sched_rate"], g)) for v in heur)
+    gap = max(v50[v]["sched_rate"][i] - g[i] for v in heur for i, u in enumerate(U) if 36 <= u <= 50)
+    g45 = [x for u, x in zip(U, g) if 44 <= u <= 46]
+    out["4_1G_collapse_dominance"] = {"1G_rate_U44_46": g45, "max_gain_U36_50": gap,
+                                      "dominance": dom,
+                                      "holds": dom and max(g45) <= 0.1 and gap >= 0.3}
+    # 5. at U where all SMS_ACT runs succeed: achieved within 10 % of the lower bound and
+    #    mean partition count 25 +- 5
+    sa = v50["SMS_ACT"]
+    idx = [i for i in range(len(U)) if sa["sched_rate"][i] == 1.0]
+    eff = [sa["workload_achieved"][i] / sa["workload_lower"][i] for i in idx]
+    kk = [sa["mean_partitions"][i] for i in idx]
+    out["5_pairing_efficiency"] = {
+        "U_all_succeed": [U[i] for i in idx], "mean_achieved_over_lower": float(np.mean(eff)),
+        "mean_partitions": float(np.mean(kk)),
+        "holds": float(np.mean(eff)) <= 1.10 and abs(float(np.mean(kk)) - 25) <= 5}
+    # 6. n = 200: heuristics within 0.15 of each other at every U, all dominate 1G
     if r200:
         v200 = r200["variants"]
-        spread = [max(v200[v]["sched_rate"][b] for v in heur) - min(v200[v]["sched_rate"][b]
-                                                                    for v in heur)
-                  for b in range(34)]
-        out["n200_max_spread_between_heuristics"] = float(max(spread))
-        spread50 = [max(v50[v]["sched_rate"][b] for v in heur) - min(v50[v]["sched_rate"][b]
-                                                                     for v in heur)
-                    for b in range(34)]
-        out["n50_max_spread_between_heuristics"] = float(max(spread50))
+        spread = [max(v200[v]["sched_rate"][b] for v in heur) -
+                  min(v200[v]["sched_rate"][b] for v in heur) for b in range(len(U))]
+        dom200 = all(all(a >= b for a, b in zip(v200[v]["sched_rate"], v200["1G"]["sched_rate"]))
+                     for v in heur)
+        out["6_n200_convergence"] = {"max_spread": float(max(spread)), "dominance": dom200,
+                                     "holds": max(spread) <= 0.15 and dom200}
+    # 7. analysis cost over the high-load region (U >= 36): ACT < INA and BF < SMS.
+    #    Measured as EDF tests per set (the work unit; GPU time is per variant, whole sweep)
+    hi = [i for i, u in enumerate(U) if u >= 36]
+    t = {v: float(np.mean([v50[v]["edf_tests_per_set"][i] for i in hi])) for v in heur}
+    order = {"SMS_ACT<SMS_INA": t["SMS_ACT"] < t["SMS_INA"], "BF_ACT<BF_INA": t["BF_ACT"] < t["BF_INA"],
+             "BF_ACT<SMS_ACT": t["BF_ACT"] < t["SMS_ACT"], "BF_INA<SMS_INA": t["BF_INA"] < t["SMS_INA"]}
+    out["7_analysis_cost_order"] = {"edf_tests_per_set_U_ge_36": t, "order": order,
+                                    "gpu_ms_whole_sweep": r50["variant_gpu_ms"],
+                                    "holds": all(order.values())}
     return out
 
 
@@ -107,25 +135,30 @@ def main():
     ap.add_argument("--reps", type=int, default=100)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "f1_sweep.json"))
     ap.add_argument("--skip200", action="store_true")
+    ap.add_argument("--readings", default="A-1,A-1b",
+                    help="A-1: b = beta*a (P:950 as written); A-1b: b = beta*a/M")
     a = ap.parse_args()
     t0 = time.time()
-    r50 = run("f1_50", a.reps)
-    r200 = None if a.skip200 else run("f1_200", a.reps)
-    res = {"f1_50": r50, "f1_200": r200, "claims": claims(r50, r200),
-           "wall_s": time.time() - t0, "device": torch.cuda.get_device_name()}
+    res = {"device": torch.cuda.get_device_name()}
+    for reading in a.readings.split(","):
+        pre = {"A-1": "f1", "A-1b": "f1b"}[reading]
+        r50 = run(pre + "_50", a.reps)
+        r200 = None if a.skip200 else run(pre + "_200", a.reps)
+        res[reading] = {"n50": r50, "n200": r200, "claims": claims(r50, r200)}
+        for r in (r50, r200):
+            if not r:
+                continue
+            print(f"== {reading} {r['workload']}: {r['reps']} sets/point, GPU {r['gpu_ms']:.1f} ms, "
+                  f"{r['edf_tests']} EDF tests")
+            print("U    " + " ".join(f"{v:>8s}" for v in W.VARIANT_NAMES))
+            for b, u in enumerate(r["U"]):
+                print(f"{u:3d}  " + " ".join(f"{r['variants'][v]['sched_rate'][b]:8.2f}"
+                                              for v in W.VARIANT_NAMES))
+        print(reading, json.dumps(res[reading]["claims"], indent=1))
+    res["wall_s"] = time.time() - t0
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as fh:
         json.dump(res, fh, indent=1)
-    for r in (r50, r200):
-        if not r:
-            continue
-        print(f"== {r['workload']}: {r['reps']} sets/point, GPU {r['gpu_ms']:.1f} ms, "
-              f"{r['edf_tests']} EDF tests")
-        print("U    " + " ".join(f"{v:>8s}" for v in W.VARIANT_NAMES))
-        for b, u in enumerate(r["U"]):
-            print(f"{u:3d}  " + " ".join(f"{r['variants'][v]['sched_rate'][b]:8.2f}"
-                                          for v in W.VARIANT_NAMES))
-    print(json.dumps(res["claims"], indent=1))
 
 
 if __name__ == "__main__":

@@ -401,7 +401,7 @@ def test_threshold_random_sets(G, seed, n, M):
 
 
 # ------------------------------------------------------------------ f1: paper-scale shapes
-@pytest.mark.parametrize("key,reps", [("f1_50", 3), ("f1_200", 2)])
+@pytest.mark.parametrize("key,reps", [("f1_50", 3), ("f1_200", 2), ("f1b_50", 2), ("f1b_200", 1)])
 def test_generate_f1_curve_mode(G, key, reps):
     """§8(f) f1: 50 / 200 tasks per set (CTA-per-set generator) in curve mode
     (the §7.1 curves C = k(a/|P| + b) in the W form), bit-exact vs the oracle."""
@@ -414,10 +414,11 @@ def test_generate_f1_curve_mode(G, key, reps):
         assert (got[f] == getattr(ref, f)).all(), f
 
 
-def test_allocate_f1_50(G):
+@pytest.mark.parametrize("key", ["f1_50", "f1b_50"])
+def test_allocate_f1_50(G, key):
     """The paper's 50-task scenario (Fig. 5): every variant, every U point
     2..68, bit-exact vs the oracle (n > 32 path: one CTA per set)."""
-    gen = W.WORKLOADS["f1_50"]["gen"](R=100)
+    gen = W.WORKLOADS[key]["gen"](R=100)
     ts = G.TaskSets(34 * 2, 50, 68, 34)
     G.gp_generate(gen, W.SEED, 0, 2, ts)
     check_allocate(G, ts)
@@ -464,3 +465,17 @@ def test_f1_paper_claims_n50(G):
         ach = r["variants"][v]["workload_achieved"]
         up = r["variants"][v]["workload_upper"]
         assert all(a is None or (l - 1e-9 <= a <= h + 1e-9) for l, a, h in zip(lo, ach, up))
+
+
+def test_f1b_1G_plateau_n50(G):
+    """Under reading A-1b (b = beta*a/M) the 1G baseline behaves as P:975 says:
+    100 % schedulable below U = 35 (SPEC acceptance 3's margin: U <= 30) and
+    collapsed by U = 45 (acceptance 4: <= 0.1), while the heuristics dominate it
+    and beat it by >= 0.3 somewhere in U = 36..50."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "scripts"))
+    import f1_sweep
+    r = f1_sweep.run("f1b_50", 100)
+    c = f1_sweep.claims(r, None)
+    assert c["3_plateau_U_le_30"]["holds"], c["3_plateau_U_le_30"]
+    assert c["4_1G_collapse_dominance"]["holds"], c["4_1G_collapse_dominance"]
