@@ -85,6 +85,7 @@ def _declare(L):
     L.gpref_unrank.argtypes = [C.c_int32, C.c_int32, C.c_uint64, P, P]
     L.gpref_exhaustive.argtypes = [P, C.c_uint64, C.c_uint64, P, P, C.c_int64, C.c_int32]
     L.gpref_allocate.argtypes = [P, C.c_int32, P, P, P, P, P, P, C.c_int32]
+    L.gpref_allocate_ex.argtypes = [P, C.c_int32, P, P, P, P, P, P, P, C.c_int32]
     L.gpref_sched_ratio.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P]
     L.gpref_uunisort.argtypes = [C.c_int32, C.c_int64, P, P]
     L.gpref_task_fields.argtypes = [P, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P]
@@ -308,7 +309,18 @@ def exhaustive(sets: Sets, rank_lo=0, rank_hi=None, bits=False, threads=None):
     return (per, vb) if bits else per
 
 
-def allocate(sets: Sets, variant, threads=None):
+class _AllocOpts(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("admissible", C.c_void_p)]
+
+
+AL_BINARY_MERGE = 1   # f4: Algorithm 2 by binary search
+AL_INCREASING = 2     # f4: par_list in increasing utilisation
+
+
+def allocate(sets: Sets, variant, threads=None, flags=0, sizes=None):
+    """Heuristics (Alg. 1-3) / 1G.  f4 variants: ``flags`` (AL_BINARY_MERGE,
+    AL_INCREASING) and ``sizes`` = the admissible partition sizes (MIG-style
+    slices; None = every size)."""
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     S, n = sets.n_sets, sets.n_tasks
     ok = np.zeros(S, np.uint8)
@@ -319,8 +331,15 @@ def allocate(sets: Sets, variant, threads=None):
     nt = np.zeros(S, np.int64)
     cs = sets._c()
     th = threads or os.cpu_count() or 1
-    _check(lib().gpref_allocate(C.byref(cs), v, _p(ok), _p(bot), _p(bs), _p(pi), _p(k), _p(nt), th),
-           "allocate")
+    adm = None
+    if sizes is not None:
+        adm = np.zeros(sets.M + 1, np.uint8)
+        for m in sizes:
+            assert 1 <= m <= sets.M, "admissible sizes lie in 1..M"
+            adm[m] = 1
+    opts = _AllocOpts(int(flags), None if adm is None else adm.ctypes.data)
+    _check(lib().gpref_allocate_ex(C.byref(cs), v, C.byref(opts), _p(ok), _p(bot), _p(bs), _p(pi),
+                                   _p(k), _p(nt), th), "allocate")
     return dict(ok=ok, block_of_task=bot, block_size=bs, pi=pi, k=k, n_tests=nt)
 
 

@@ -640,6 +640,10 @@ typedef struct {
   int32_t n_snaps, cap_snaps;
   uint8_t *forb; /* ACT task pairs, n x n */
   int act;
+  /* f4 variants (gpref_alloc_opts) */
+  int binary;                /* Algorithm 2 by binary search      */
+  int increasing;            /* par_list in increasing utilisation */
+  const uint8_t *admissible; /* [M+1]: admissible partition sizes, or NULL */
 } heur_t;
 
 static int32_t min_task(const tmask *mask) {
@@ -659,16 +663,32 @@ static int64_t part_uh(const heur_t *h, const tmask *mask, int32_t m) {
   return (int64_t)u;
 }
 
-/* par_list order: decreasing utilisation, ties by lower min task id (A-17) */
+/* Best-fit order (A-21): decreasing utilisation, ties by lower min task id.
+ * It is also the par_list order (A-17) unless the f4 increasing variant is on. */
 static int part_before(const part_t *x, const part_t *y) {
   if (x->uh != y->uh) return x->uh > y->uh;
   return min_task(&x->mask) < min_task(&y->mask);
 }
 
+/* par_list order: decreasing utilisation (A-17), or increasing
+ * (f4: "decreasing/increasing utilization order"); ties by lower min task id. */
+static int list_before(const heur_t *h, const part_t *x, const part_t *y) {
+  if (x->uh != y->uh) return h->increasing ? x->uh < y->uh : x->uh > y->uh;
+  return min_task(&x->mask) < min_task(&y->mask);
+}
+
+/* Is m an admissible partition size?  Without a mask every m >= 1 is (the
+ * paper's Algorithm 2 may even exceed M); with a mask (f4, MIG-style slices,
+ * P:1139) only the listed sizes 1..M are.                                    */
+static int size_ok(const heur_t *h, int32_t m) {
+  if (!h->admissible) return m >= 1;
+  return m >= 1 && m <= h->M && h->admissible[m];
+}
+
 static void list_insert(heur_t *h, part_t p) {
   int32_t pos = h->len;
   for (int32_t q = 0; q < h->len; ++q)
-    if (part_before(&p, &h->list[q])) { pos = q; break; }
+    if (list_before(h, &p, &h->list[q])) { pos = q; break; }
   for (int32_t q = h->len; q > pos; --q) h->list[q] = h->list[q - 1];
   h->list[pos] = p;
   h->len += 1;
@@ -687,15 +707,36 @@ static int test_schedulability(heur_t *h, const tmask *mask, int32_t m) {
 }
 
 /* Algorithm 2: try m = max(|P1|,|P2|), ..., |P1|+|P2|-1 in order;
- * the strict upper bound is Def. 3's m3 < m1 + m2.  Returns m or 0. */
+ * the strict upper bound is Def. 3's m3 < m1 + m2.  Returns m or 0.
+ * f4 variants: only admissible sizes are tried, and the binary search
+ * "between max{|P1|,|P2|} and |P1|+|P2|" replaces the scan: over
+ * the ascending list L of candidate sizes, lo = 0, hi = |L|; while lo < hi:
+ * mid = floor((lo+hi)/2), schedulable at L[mid] ? hi = mid : lo = mid + 1;
+ * the answer is L[lo] if lo < |L|.  Schedulability is monotone in m (W_i is
+ * non-increasing in m, C.1.3; the demand test is monotone in the C_i), so both
+ * searches return the same m; only the number of tests differs.            */
 static int32_t merge(heur_t *h, const part_t *p1, const part_t *p2) {
   tmask t3 = tm_or(p1->mask, p2->mask);
-  int32_t m = p1->size > p2->size ? p1->size : p2->size;
-  while (m < p1->size + p2->size) {
-    if (test_schedulability(h, &t3, m)) return m;
-    m = m + 1;
+  int32_t first = p1->size > p2->size ? p1->size : p2->size;
+  int32_t *L = (int32_t *)malloc(sizeof(int32_t) * (size_t)(p1->size + p2->size));
+  int32_t len = 0;
+  for (int32_t m = first; m < p1->size + p2->size; ++m)
+    if (size_ok(h, m)) L[len++] = m;
+  int32_t found = 0;
+  if (!h->binary) {
+    for (int32_t x = 0; x < len && !found; ++x)
+      if (test_schedulability(h, &t3, L[x])) found = L[x];
+  } else {
+    int32_t lo = 0, hi = len;
+    while (lo < hi) {
+      int32_t mid = (lo + hi) / 2;
+      if (test_schedulability(h, &t3, L[mid])) hi = mid;
+      else lo = mid + 1;
+    }
+    if (lo < len) found = L[lo];
   }
-  return 0;
+  free(L);
+  return found;
 }
 
 static void add_to_forbidden_moves(heur_t *h, const tmask *a, const tmask *b) {
@@ -754,11 +795,17 @@ static void write_solution(const heur_t *h, int ok, uint8_t *okp, int16_t *bot, 
   k[set] = label;
 }
 
-static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint8_t *okp,
-                         int16_t *bot, int16_t *bs, int32_t *pi, int32_t *kk, int64_t *nt) {
+static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant,
+                         const gpref_alloc_opts *opts, uint8_t *okp, int16_t *bot, int16_t *bs,
+                         int32_t *pi, int32_t *kk, int64_t *nt) {
   heur_t *h = (heur_t *)calloc(1, sizeof(heur_t));
 
   h->s = s; h->set = set; h->n = s->n_tasks; h->M = s->M;
+  if (opts) {
+    h->binary = (opts->flags & GPREF_AL_BINARY_MERGE) != 0;
+    h->increasing = (opts->flags & GPREF_AL_INCREASING) != 0;
+    h->admissible = opts->admissible;
+  }
   int32_t n = h->n, M = h->M;
   int64_t Tv[GPREF_MAX_TASKS];
   for (int32_t i = 0; i < n; ++i) Tv[i] = s->T[(int64_t)set * n + i];
@@ -767,10 +814,13 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
   memset(&empty, 0, sizeof(empty));
 
   if (variant == GPREF_1G) {
-    /* 1G: the whole GPU as one partition of M SMs */
-    part_t all = {empty, M, 0};
+    /* 1G: the whole GPU as one partition of M SMs; with a
+     * size mask, the largest admissible size (f4)                           */
+    int32_t size = M;
+    while (!size_ok(h, size)) size -= 1;
+    part_t all = {empty, size, 0};
     for (int32_t i = 0; i < n; ++i) tm_set(&all.mask, i);
-    int ok = test_schedulability(h, &all.mask, M);
+    int ok = test_schedulability(h, &all.mask, size);
     h->list[0] = all;
     h->len = 1;
     write_solution(h, ok, okp, bot, bs, pi, kk, nt, 1);
@@ -792,13 +842,14 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
     free(h);
     return;
   }
-  /* init_partitions, Lemma 2: |P| = min{m in 1..M : C^n(m) <= D} */
+  /* init_partitions, Lemma 2: |P| = min{m in 1..M : C^n(m) <= D}
+   * (f4: m admissible)                                                       */
   int32_t Pi = 0;
   for (int32_t i = 0; i < n; ++i) {
     int64_t b = (int64_t)set * n + i;
     int32_t size = 0;
     for (int32_t m = 1; m <= M; ++m) {
-      if (gpref_wcet(s->B[b], s->cn[b], s->fn[b], m) - s->D[b] <= 0) {
+      if (size_ok(h, m) && gpref_wcet(s->B[b], s->cn[b], s->fn[b], m) - s->D[b] <= 0) {
         size = m;
         break;
       }
@@ -914,6 +965,7 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant, uint
 typedef struct {
   const gpref_sets *s;
   int32_t variant;
+  const gpref_alloc_opts *opts;
   uint8_t *ok;
   int16_t *bot;
   int16_t *bs;
@@ -930,18 +982,30 @@ static void *alloc_worker(void *arg) {
     int32_t set = j->next++;
     pthread_mutex_unlock(&j->mu);
     if (set >= j->s->n_sets) return NULL;
-    allocate_one(j->s, set, j->variant, j->ok, j->bot, j->bs, j->pi, j->k, j->nt);
+    allocate_one(j->s, set, j->variant, j->opts, j->ok, j->bot, j->bs, j->pi, j->k, j->nt);
   }
 }
 
 int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int16_t *block_of_task,
                    int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                    int32_t n_threads) {
+  return gpref_allocate_ex(s, variant, NULL, ok, block_of_task, block_size, pi, k, n_tests,
+                           n_threads);
+}
+
+int gpref_allocate_ex(const gpref_sets *s, int32_t variant, const gpref_alloc_opts *opts,
+                      uint8_t *ok, int16_t *block_of_task, int16_t *block_size, int32_t *pi,
+                      int32_t *k, int64_t *n_tests, int32_t n_threads) {
   if (variant < 0 || variant > 4 || s->n_tasks < 1 || s->n_tasks > GPREF_MAX_TASKS || s->M < 1)
     return 1;
+  if (opts && opts->admissible) { /* at least one admissible size in 1..M */
+    int any = 0;
+    for (int32_t m = 1; m <= s->M; ++m) any |= opts->admissible[m] != 0;
+    if (!any) return 1;
+  }
   alloc_job j;
   memset(&j, 0, sizeof(j));
-  j.s = s; j.variant = variant; j.ok = ok; j.bot = block_of_task; j.bs = block_size;
+  j.s = s; j.variant = variant; j.opts = opts; j.ok = ok; j.bot = block_of_task; j.bs = block_size;
   j.pi = pi; j.k = k; j.nt = n_tests;
   pthread_mutex_init(&j.mu, NULL);
   if (n_threads < 1) n_threads = 1;

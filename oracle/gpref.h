@@ -91,6 +91,18 @@ int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int16_t *b
                    int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                    int32_t n_threads);
 
+/* ---- f4: the variants the paper names ---- */
+enum { GPREF_AL_BINARY_MERGE = 1, /* Algorithm 2 by binary search */
+       GPREF_AL_INCREASING = 2 }; /* par_list in increasing utilisation */
+typedef struct {
+  uint32_t flags;
+  const uint8_t *admissible; /* [M+1]; admissible[m] != 0: partitions of m SMs allowed
+                                (MIG-style slices); NULL: every size */
+} gpref_alloc_opts;
+int gpref_allocate_ex(const gpref_sets *s, int32_t variant, const gpref_alloc_opts *opts,
+                      uint8_t *ok, int16_t *block_of_task, int16_t *block_size, int32_t *pi,
+                      int32_t *k, int64_t *n_tests, int32_t n_threads);
+
 /* ---- f2: scheduled workload of an allocation ---- */
 int gpref_efficiency(const gpref_sets *s, const int16_t *block_of_task, int64_t *eff);
 
