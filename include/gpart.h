@@ -182,11 +182,38 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * stats: device uint64 [4] or NULL; += {EDF-PDC tests, tasks in tested
  * partitions, distinct deadlines examined by the demand walks, sets} (the
  * per-launch work figures of the roofline).
- * Errors: GP_EINVAL (bad struct / variant), GP_ECUDA.
+ * opts: NULL or the f4 variants below.
+ * Errors: GP_EINVAL (bad struct / variant / options), GP_ECUDA.
  * ------------------------------------------------------------------------- */
-gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok, int16_t *block_of_task,
-                      int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
-                      int64_t *efficiency, unsigned long long *stats, void *stream);
+typedef enum {
+  GP_AL_BINARY_MERGE = 1, /* Algorithm 2 by binary search "between max{|P1|,|P2|} and
+                             |P1|+|P2|": lower-bound search over the ascending
+                             candidate sizes (lo = 0, hi = |L|, mid = (lo+hi)/2).  Same
+                             partitions as the linear scan (schedulability is monotone in m),
+                             fewer EDF tests; only n_tests changes.                         */
+  GP_AL_INCREASING = 2    /* par_list in increasing utilisation order; ties by
+                             lower min task id.  Best-fit partner order stays U*H desc (A-21). */
+} gp_alloc_flag;
+
+/* f4 options of gp_allocate.  Host memory; NULL = the paper's
+ * defaults (linear scan, decreasing order, every partition size).
+ * size_mask: NULL, or ceil(M/32) host words; bit (m-1) % 32 of word (m-1) / 32
+ *   set = partitions of m SMs are admissible (MIG-style slices).  Bits
+ *   above M are ignored; at least one size in 1..M must be admissible
+ *   (GP_EINVAL).  With a mask, Lemma 2 sizes round up to the next admissible
+ *   size, Algorithm 2 tries admissible sizes only (all <= M), and 1G uses the
+ *   largest admissible size.  Without a mask merged sizes follow the paper
+ *   (Algorithm 2 may try sizes above M).  Placement of slices on the GPU (GPC
+ *   boundaries) is not modelled: only the sizes are restricted.              */
+typedef struct {
+  uint32_t flags;            /* gp_alloc_flag bits; unknown bits -> GP_EINVAL */
+  const uint32_t *size_mask; /* see above */
+} gp_alloc_opts;
+
+gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *opts,
+                      uint8_t *ok, int16_t *block_of_task, int16_t *block_size, int32_t *pi,
+                      int32_t *k, int64_t *n_tests, int64_t *efficiency,
+                      unsigned long long *stats, void *stream);
 
 /* ---------------------------------------------------------------------------
  * A6 (and A2-A4 fused). gp_sched_ratio -- segmented reduction to the

@@ -17,12 +17,18 @@
 // form), Lemma 3, Algorithm 2 (linear m scan, Def. 3
 // strict bound), Algorithm 3, Def. 4 / Def. 5 orders
 // (P:720-753), forbidden list; conventions C.1.9 / A-17..A-26.
+// f4 variants (gp_alloc_opts): binary-search merge
+// (P:704-706), increasing par_list order, admissible partition
+// sizes -- compiled into a second instantiation (kGen) so that the
+// paper's default path keeps its plain linear scan.
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
+#include "gp_sizes.cuh"
 
-gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, uint8_t *ok, int16_t *bot,
-                                 int16_t *bs, int32_t *pi, int32_t *k, int64_t *n_tests,
-                                 int64_t *eff, unsigned long long *stats, cudaStream_t st);
+gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, const gp::AllocVariantOpts &vo,
+                                 uint8_t *ok, int16_t *bot, int16_t *bs, int32_t *pi, int32_t *k,
+                                 int64_t *n_tests, int64_t *eff, unsigned long long *stats,
+                                 cudaStream_t st);
 
 namespace gp {
 
@@ -38,6 +44,7 @@ struct AllocArgs {
   int64_t *eff;               // optional [n_sets][4]: scheduled workload (f2)
   unsigned long long *stats;  // optional: += {EDF tests, tasks tested, deadlines examined, sets}
   int32_t use_tab;            // per-warp table of ceil(B_i/m) in dynamic shared memory
+  AllocVariantOpts vo;        // f4
 };
 
 // ceil(B_i / m) from the warp's per-set table (uint16, built once per set)
@@ -120,6 +127,7 @@ GP_DEV bool pair_pdc(const int32_t (&C)[2], const int32_t (&D)[2], const int32_t
 
 struct WarpScratch {
   int32_t ord[32];    // ord[r] = slot with par_list rank r
+  int32_t bord[32];   // bord[r] = slot with best-fit rank r (U*H desc, A-21)
   int32_t lab[32];    // output label of task i
   int32_t size[32];   // size of output label j
   uint32_t forb[32];  // ACT: forbidden task row
@@ -133,9 +141,9 @@ struct WarpScratch {
 // Algorithm 2 merge of partition S (<= NS tasks) by ONE lane: sizes
 // m = lo .. hi in order (Def. 3 bound hi = |P1| + |P2| - 1), an EDF-PDC test
 // each.  Returns the first schedulable m (0 if none) and U*H there.
-template <int NS>
-GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, uint32_t S, int32_t lo,
-                            int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
+template <int NS, bool kGen>
+GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, const SizeSpace &z, uint32_t S,
+                            int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
                             uint64_t &st_tasks, uint32_t &st_events) {
   int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   const int cnt = __popc(S);
@@ -154,7 +162,9 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, uint32_t S, i
     f[a] = v ? (x ? w.fc[i] : w.fn[i]) : 0;
     q[a] = v ? w.q[i] : 0;
   }
-  for (int32_t m = lo; m <= hi; ++m) {
+  // one EDF-PDC test at size m; on success U*H is recorded (the last success
+  // of a search is its answer)
+  auto test = [&](int32_t m) -> bool {
     ++tests;
     st_tasks += cnt;
     int32_t C[NS];
@@ -164,28 +174,43 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, uint32_t S, i
       C[a] = c[a] ? w_from_waves(wv(id[a], B[a], m), c[a], f[a]) : 0;
       bad |= C[a] > D[a];
     }
-    if (bad) continue;
+    if (bad) return false;
     int32_t UH = 0;
 #pragma unroll
     for (int a = 0; a < NS; ++a) UH += C[a] * q[a];
-    if (UH > H) continue;
+    if (UH > H) return false;
     if (cnt > 1) {
       const int32_t lcut = pdc_cutoff<NS>(C, D, T, q, H, UH);
-      if (!pdc_walk<NS>(C, D, T, lcut, st_events)) continue;
+      if (!pdc_walk<NS>(C, D, T, lcut, st_events)) return false;
     }
     uh_out = UH;
-    return m;
-  }
-  return 0;
+    return true;
+  };
+  return search_sizes<kGen>(z, lo, hi, test);
 }
 
+template <bool kGen>
 __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
   __shared__ WarpScratch scr_all[8];
-  extern __shared__ uint16_t wtab_all[];
+  extern __shared__ __align__(16) uint16_t wtab_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpScratch &scr = scr_all[wid];
   const int n = a.n, M = a.M;
   uint16_t *wtab = a.use_tab ? wtab_all + (size_t)wid * n * M : nullptr;
+  // f4: admissible-size tables after the ceil(B/m) tables
+  SizeSpace z{nullptr, M, 0, false};
+  bool incr = false;
+  if constexpr (kGen) {
+    z.binary = (a.vo.flags & GP_AL_BINARY_MERGE) != 0;
+    incr = (a.vo.flags & GP_AL_INCREASING) != 0;
+    if (a.vo.masked) {
+      const size_t off = a.use_tab ? (size_t)8 * n * M : 0;
+      SizeTables *tb = reinterpret_cast<SizeTables *>(wtab_all + ((off + 7) & ~(size_t)7));
+      build_size_tables(*tb, a.vo.mask, M);
+      z.tab = tb;
+      z.A = tb->ge[M + 1];
+    }
+  }
   const uint32_t all = n == 32 ? GP_FULL : ((1u << n) - 1u);
   uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // warp-uniform
   uint64_t st_pair_tasks = 0;                                        // per lane
@@ -241,9 +266,10 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     } else if (a.variant == GP_1G) {
       // 1G: the whole GPU as one partition
       tests = 1;
-      ok = warp_pdc(t, all, M, H, st_tasks, st_events);
+      const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
+      ok = warp_pdc(t, all, m1, H, st_tasks, st_events);
       pm = lane == 0 ? all : 0;
-      psz = lane == 0 ? M : 0;
+      psz = lane == 0 ? m1 : 0;
       stage = 1;
     } else {
       const bool act = a.variant == GP_SMS_ACT || a.variant == GP_BF_ACT;
@@ -257,6 +283,7 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
         const int32_t K = (t.D - t.fn) / t.cn;  // waves allowed: ceil(B/m) <= K
         const int32_t m0 = (t.B + K - 1) / K;
         mi = m0 <= M ? (m0 < 1 ? 1 : m0) : 0;
+        if (kGen && mi) mi = z.round_up(mi);  // f4: smallest admissible size >= m0
       }
       const bool lemma2 = !__ballot_sync(GP_FULL, t.in && mi == 0);
       if (lemma1 && lemma2) {
@@ -297,15 +324,16 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
               const int32_t ci = x ? cci : cni, cj = x ? ccj : cnj;
               const int32_t fi = x ? fci : fni, fj = x ? fcj : fnj;
               if (idx < np) {
-                bool merged = false;
-                for (int32_t m = max(mi_, mj_); m < mi_ + mj_ && !merged; ++m) {
+                auto pair_test = [&](int32_t m) -> bool {
                   ++my_tests;
                   const int32_t C[2] = {w_from_waves(t.wv(i, Bi, m), ci, fi),
                                         w_from_waves(t.wv(j, Bj, m), cj, fj)};
                   const int32_t Dv[2] = {Di, Dj}, Tv[2] = {Ti, Tj}, qv[2] = {qi, qj};
                   st_pair_tasks += 2;
-                  merged = pair_pdc(C, Dv, Tv, qv, H, st_pair_events);
-                }
+                  return pair_pdc(C, Dv, Tv, qv, H, st_pair_events);
+                };
+                const bool merged =
+                    search_sizes<kGen>(z, max(mi_, mj_), mi_ + mj_ - 1, pair_test) != 0;
                 if (!merged) {
                   atomicOr(&scr.forb[i], 1u << j);
                   atomicOr(&scr.forb[j], 1u << i);
@@ -324,15 +352,23 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
           uint32_t livemask = 0, forb_slots = 0;
           for (;;) {
             if (dirty) {
-              // par_list order: (U*H desc, slot asc)
+              // par_list order: (U*H desc, slot asc), or U*H asc (f4 increasing);
+              // best-fit partner order: always U*H desc (A-21)
               live = pm != 0;
               livemask = __ballot_sync(GP_FULL, live);
               rank = 0;
+              int brank = 0;
               for (int s2 = 0; s2 < 32; ++s2) {
                 const int32_t u2 = __shfl_sync(GP_FULL, puh, s2);
-                rank += ((livemask >> s2) & 1u) && (u2 > puh || (u2 == puh && s2 < lane));
+                const bool lv = (livemask >> s2) & 1u;
+                brank += lv && (u2 > puh || (u2 == puh && s2 < lane));
+                if (kGen && incr) rank += lv && (u2 < puh || (u2 == puh && s2 < lane));
               }
-              if (live) scr.ord[rank] = lane;
+              if (!(kGen && incr)) rank = brank;
+              if (live) {
+                scr.ord[rank] = lane;
+                scr.bord[brank] = lane;
+              }
               __syncwarp();
               len = __popc(livemask);
               uint32_t F = 0;  // tasks forbidden with a task of my partition (ACT)
@@ -363,8 +399,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
             const int32_t szP = __shfl_sync(GP_FULL, psz, P);
             int best = -1;
             int32_t best_m = 0, best_uh = 0;
-            // eligible partners in par_list order -> lane e holds partner plist[e]
-            const int Qr = lane < len ? scr.ord[lane] : 0;
+            // eligible partners in best-fit order -> lane e holds partner plist[e]
+            const int Qr = lane < len ? scr.bord[lane] : 0;
             const bool el = lane < len && ((elig >> Qr) & 1u);
             const uint32_t elb = __ballot_sync(GP_FULL, el);
             if (el) scr.plist[__popc(elb & ((1u << lane) - 1u))] = Qr;
@@ -384,8 +420,8 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
               if (lane < E) {
                 const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
                 got = maxcnt <= 4
-                          ? serial_merge<4>(scr, t.wv, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events)
-                          : serial_merge<8>(scr, t.wv, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                          ? serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events)
+                          : serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
               }
               const uint32_t succ = __ballot_sync(GP_FULL, lane < E && got > 0);
               int cut = E;  // partners whose tests the sequential order performs
@@ -418,19 +454,17 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
               done_round = true;
             }
             for (int r = 0; r < len && !done_round; ++r) {
-              const int Q = scr.ord[r];
+              const int Q = scr.bord[r];
               if (!((elig >> Q) & 1u)) continue;
               const uint32_t pmQ = __shfl_sync(GP_FULL, pm, Q);
               const int32_t szQ = __shfl_sync(GP_FULL, psz, Q);
               const uint32_t S = pmP | pmQ;
-              int32_t got = 0;  // Algorithm 2: linear scan, m < |P1| + |P2| (Def. 3)
-              for (int32_t m = max(szP, szQ); m < szP + szQ; ++m) {
+              // Algorithm 2: m < |P1| + |P2| (Def. 3), warp-cooperative tests
+              auto wtest = [&](int32_t m) -> bool {
                 ++tests;
-                if (warp_pdc(t, S, m, H, st_tasks, st_events)) {
-                  got = m;
-                  break;
-                }
-              }
+                return warp_pdc(t, S, m, H, st_tasks, st_events);
+              };
+              const int32_t got = search_sizes<kGen>(z, max(szP, szQ), szP + szQ - 1, wtest);
               if (!got) {  // add_to_forbidden_moves(P, Q)
                 if (lane == P) pex |= 1u << Q;
                 if (lane == Q) pex |= 1u << P;
@@ -536,33 +570,55 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
 
 }  // namespace gp
 
-extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, uint8_t *ok,
-                                 int16_t *block_of_task, int16_t *block_size, int32_t *pi,
-                                 int32_t *k, int64_t *n_tests, int64_t *efficiency,
+extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *opts,
+                                 uint8_t *ok, int16_t *block_of_task, int16_t *block_size,
+                                 int32_t *pi, int32_t *k, int64_t *n_tests, int64_t *efficiency,
                                  unsigned long long *stats, void *stream) {
   using namespace gp;
   if (!ts || ts->n_tasks < 1 || ts->n_tasks > 256 || ts->M < 1 || ts->M > 1024 ||
       ts->n_sets < 0)
     return gp_fail(GP_EINVAL, "gp_allocate: bad task sets (n_tasks 1..256, M 1..1024)");
   if ((int)v < 0 || (int)v > 4) return gp_fail(GP_EINVAL, "gp_allocate: bad variant %d", (int)v);
+  AllocVariantOpts vo{};
+  if (opts) {
+    if (opts->flags & ~(uint32_t)(GP_AL_BINARY_MERGE | GP_AL_INCREASING))
+      return gp_fail(GP_EINVAL, "gp_allocate: unknown option flags 0x%x", opts->flags);
+    vo.flags = opts->flags;
+    if (opts->size_mask) {
+      const int words = (ts->M + 31) / 32;
+      int any = 0;
+      for (int w = 0; w < words; ++w) {
+        uint32_t m = opts->size_mask[w];
+        if (w == words - 1 && (ts->M & 31)) m &= (1u << (ts->M & 31)) - 1u;  // sizes <= M only
+        vo.mask[w] = m;
+        any |= m != 0;
+      }
+      if (!any) return gp_fail(GP_EINVAL, "gp_allocate: size_mask admits no size in 1..M");
+      vo.masked = 1;
+    }
+  }
   if (ts->n_sets == 0) return gp_cuda_check("gp_allocate");
   if (!ok || !block_of_task || !block_size || !pi || !k || !n_tests || !ts->T || !ts->D ||
       !ts->B || !ts->cn || !ts->cc || !ts->fn || !ts->fc || !ts->type)
     return gp_fail(GP_EINVAL, "gp_allocate: null pointer");
   if (ts->n_tasks > kMaxTasks)  // 33..256 tasks: one CTA per set (allocate_big.cu)
-    return gp_allocate_big_launch(ts, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-                                  efficiency, stats, (cudaStream_t)stream);
+    return gp_allocate_big_launch(ts, (int32_t)v, vo, ok, block_of_task, block_size, pi, k,
+                                  n_tests, efficiency, stats, (cudaStream_t)stream);
   // per-warp ceil(B/m) table: 8 warps x n x M x 2 bytes when it fits (C4: 76 KB)
   size_t tab = (size_t)8 * ts->n_tasks * ts->M * sizeof(uint16_t);
   const bool use_tab = tab <= 100 * 1024;
   if (!use_tab) tab = 0;
+  const bool gen = vo.flags != 0 || vo.masked;
+  size_t smem = tab;
+  if (gen && vo.masked) smem = ((tab + 15) & ~(size_t)15) + sizeof(SizeTables);
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-              efficiency, stats, use_tab ? 1 : 0};
-  if (tab > 48 * 1024)
-    cudaFuncSetAttribute(k_allocate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
+              efficiency, stats, use_tab ? 1 : 0, vo};
+  auto kern = gen ? k_allocate<true> : k_allocate<false>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t grid = ((int64_t)ts->n_sets + 7) / 8;
   if (grid > 148 * 64) grid = 148 * 64;
-  k_allocate<<<(unsigned)grid, 256, tab, (cudaStream_t)stream>>>(a);
+  kern<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(a);
   return gp_cuda_check("gp_allocate");
 }

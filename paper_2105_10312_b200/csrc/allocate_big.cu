@@ -10,8 +10,10 @@
 // the scans are independent, only failures feed later rounds) with a
 // thread-serial EDF test for merged partitions of <= 16 tasks; larger merges
 // and 1G use a CTA-cooperative EDF test (thread = task).
+// f4 variants as in allocate.cu (kGen instantiation).
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
+#include "gp_sizes.cuh"
 
 namespace gp {
 
@@ -30,6 +32,7 @@ struct BigArgs {
   int64_t *n_tests;
   int64_t *eff;
   unsigned long long *stats;
+  AllocVariantOpts vo;  // f4
 };
 
 struct BigSmem {
@@ -39,7 +42,7 @@ struct BigSmem {
   uint32_t pex[kBigN][kBW];       // slot -> slots whose merge failed (snapshots)
   uint32_t forb[kBigN][kBW];      // task -> forbidden tasks (ACT)
   uint32_t fslots[kBigN][kBW];    // slot -> slots excluded by ACT task pairs
-  int32_t psz[kBigN], puh[kBigN], ord[kBigN], plist[kBigN], lab[kBigN], lsize[kBigN];
+  int32_t psz[kBigN], puh[kBigN], ord[kBigN], bord[kBigN], plist[kBigN], lab[kBigN], lsize[kBigN];
   uint32_t live[kBW];
   uint32_t scratch[kBW];          // broadcast of a merged task set
   int64_t red64[8];
@@ -126,9 +129,10 @@ GP_DEV bool cta_pdc(BigSmem &s, const uint32_t *S, int32_t m, int32_t H, int n,
 }
 
 // Algorithm 2 merge by ONE thread for a merged partition of <= kSerialMax tasks.
-GP_DEV int32_t big_serial_merge(const BigSmem &s, const uint32_t (&S)[kBW], int32_t lo, int32_t hi,
-                                int32_t H, int32_t &uh_out, int64_t &tests, uint64_t &st_tasks,
-                                uint32_t &st_events) {
+template <bool kGen>
+GP_DEV int32_t big_serial_merge(const BigSmem &s, const SizeSpace &z, const uint32_t (&S)[kBW],
+                                int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
+                                uint64_t &st_tasks, uint32_t &st_events) {
   int32_t T[kSerialMax], D[kSerialMax], Bv[kSerialMax], c[kSerialMax], f[kSerialMax],
       q[kSerialMax];
   int cnt = 0;
@@ -149,7 +153,7 @@ GP_DEV int32_t big_serial_merge(const BigSmem &s, const uint32_t (&S)[kBW], int3
     q[a] = v ? s.q[i] : 0;
     cnt += v;
   }
-  for (int32_t m = lo; m <= hi; ++m) {
+  auto test = [&](int32_t m) -> bool {
     ++tests;
     st_tasks += cnt;
     int32_t C[kSerialMax];
@@ -159,25 +163,38 @@ GP_DEV int32_t big_serial_merge(const BigSmem &s, const uint32_t (&S)[kBW], int3
       C[a] = c[a] ? wcet_sat(Bv[a], c[a], f[a], m) : 0;
       bad |= C[a] > D[a];
     }
-    if (bad) continue;
+    if (bad) return false;
     int32_t UH = 0;
 #pragma unroll
     for (int a = 0; a < kSerialMax; ++a) UH += C[a] * q[a];
-    if (UH > H) continue;
+    if (UH > H) return false;
     if (cnt > 1) {
       const int32_t lcut = pdc_cutoff<kSerialMax>(C, D, T, q, H, UH);
-      if (!pdc_walk<kSerialMax>(C, D, T, lcut, st_events)) continue;
+      if (!pdc_walk<kSerialMax>(C, D, T, lcut, st_events)) return false;
     }
     uh_out = UH;
-    return m;
-  }
-  return 0;
+    return true;
+  };
+  return search_sizes<kGen>(z, lo, hi, test);
 }
 
+template <bool kGen>
 __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BigSmem &s = *reinterpret_cast<BigSmem *>(smem_raw);
   const int t = threadIdx.x, n = a.n, M = a.M;
+  SizeSpace z{nullptr, M, 0, false};
+  bool incr = false;
+  if constexpr (kGen) {
+    z.binary = (a.vo.flags & GP_AL_BINARY_MERGE) != 0;
+    incr = (a.vo.flags & GP_AL_INCREASING) != 0;
+    if (a.vo.masked) {
+      SizeTables *tb = reinterpret_cast<SizeTables *>(smem_raw + ((sizeof(BigSmem) + 15) & ~(size_t)15));
+      build_size_tables(*tb, a.vo.mask, M);
+      z.tab = tb;
+      z.A = tb->ge[M + 1];
+    }
+  }
   const bool act = a.variant == GP_SMS_ACT || a.variant == GP_BF_ACT;
   const bool sms = a.variant == GP_SMS_ACT || a.variant == GP_SMS_INA;
   uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // thread 0's copies
@@ -238,9 +255,10 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
       if (in) atomicOr(&s.pm[0][t >> 5], 1u << (t & 31));
       __syncthreads();
       tests = 1;
-      ok = cta_pdc(s, s.pm[0], M, H32, n, st_tasks, st_events);
+      const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
+      ok = cta_pdc(s, s.pm[0], m1, H32, n, st_tasks, st_events);
       if (t == 0) {
-        s.psz[0] = M;
+        s.psz[0] = m1;
         s.live[0] = 1u;
       }
       stage = 1;
@@ -254,6 +272,7 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
         const int32_t K = (s.D[t] - s.fn[t]) / s.cn[t];
         const int32_t m0 = (s.B[t] + K - 1) / K;
         mi = m0 <= M ? max(m0, 1) : 0;
+        if (kGen && mi) mi = z.round_up(mi);  // f4: smallest admissible size >= m0
       }
       const bool lemma2 = !__syncthreads_or(in && mi == 0);
       if (lemma1 && lemma2) {
@@ -285,8 +304,8 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
               S[j >> 5] |= 1u << (j & 31);
               int32_t uh;
               const int32_t mi_ = s.psz[i], mj_ = s.psz[j];
-              const int32_t got = big_serial_merge(s, S, max(mi_, mj_), mi_ + mj_ - 1, H32, uh,
-                                                   my_tests, my_tasks, my_events);
+              const int32_t got = big_serial_merge<kGen>(s, z, S, max(mi_, mj_), mi_ + mj_ - 1,
+                                                         H32, uh, my_tests, my_tasks, my_events);
               if (!got) {
                 atomicOr(&s.forb[i][j >> 5], 1u << (j & 31));
                 atomicOr(&s.forb[j][i >> 5], 1u << (i & 31));
@@ -298,13 +317,23 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
           int rank = 0, len = 0;
           for (;;) {
             if (dirty) {
-              // par_list order (U*H desc, slot asc) and the ACT exclusions
+              // par_list order (U*H desc, slot asc; f4: U*H asc), best-fit partner
+              // order (U*H desc, A-21) and the ACT exclusions
               const bool live = bs_has(s.live, t);
               rank = 0;
+              int brank = 0;
               if (live)
-                for (int u = 0; u < n; ++u)
-                  rank += bs_has(s.live, u) && (s.puh[u] > s.puh[t] || (s.puh[u] == s.puh[t] && u < t));
-              if (live) s.ord[rank] = t;
+                for (int u = 0; u < n; ++u) {
+                  const bool lv = bs_has(s.live, u);
+                  brank += lv && (s.puh[u] > s.puh[t] || (s.puh[u] == s.puh[t] && u < t));
+                  if (kGen && incr)
+                    rank += lv && (s.puh[u] < s.puh[t] || (s.puh[u] == s.puh[t] && u < t));
+                }
+              if (!(kGen && incr)) rank = brank;
+              if (live) {
+                s.ord[rank] = t;
+                s.bord[brank] = t;
+              }
               len = 0;
 #pragma unroll
               for (int w = 0; w < kBW; ++w) len += __popc(s.live[w]);
@@ -342,10 +371,10 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
             const int cand = cta_min32(s, nonempty ? rank : INT32_MAX);
             if (cand == INT32_MAX) break;  // no selectable partition: fail
             const int P = s.ord[cand];
-            // partners in par_list order -> plist
+            // partners in best-fit order -> plist
             bool el = false;
             if (t < len) {
-              const int Q = s.ord[t];
+              const int Q = s.bord[t];
               el = Q != P && !bs_has(s.pex[P], Q) && !(act && bs_has(s.fslots[P], Q));
             }
             // block prefix of el over t (8 warps)
@@ -359,7 +388,7 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
               before += w < (t >> 5) ? s.red32[w] : 0;
               E += s.red32[w];
             }
-            if (el) s.plist[before + __popc(bal & ((1u << (t & 31)) - 1u))] = s.ord[t];
+            if (el) s.plist[before + __popc(bal & ((1u << (t & 31)) - 1u))] = s.bord[t];
             __syncthreads();
             // merged sizes
             const int Qe = t < E ? s.plist[t] : 0;
@@ -382,8 +411,8 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
               int32_t got = 0, uh = 0;
               if (t < E) {
                 const int32_t szQ = s.psz[Qe];
-                got = big_serial_merge(s, Se, max(szP, szQ), szP + szQ - 1, H32, uh, my_tests,
-                                       my_tasks, my_events);
+                got = big_serial_merge<kGen>(s, z, Se, max(szP, szQ), szP + szQ - 1, H32, uh,
+                                             my_tests, my_tasks, my_events);
               }
               // first success (BF) / best (SMS), tests counted in sequential order
               const int first_ok = cta_min32(s, (t < E && got > 0) ? t : INT32_MAX);
@@ -439,14 +468,11 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
                 uint32_t S2[kBW];
 #pragma unroll
                 for (int w = 0; w < kBW; ++w) S2[w] = s.scratch[w];
-                int32_t got = 0;
-                for (int32_t m = max(szP, szQ); m < szP + szQ; ++m) {
+                auto ctest = [&](int32_t m) -> bool {
                   ++tests;
-                  if (cta_pdc(s, S2, m, H32, n, st_tasks, st_events)) {
-                    got = m;
-                    break;
-                  }
-                }
+                  return cta_pdc(s, S2, m, H32, n, st_tasks, st_events);
+                };
+                const int32_t got = search_sizes<kGen>(z, max(szP, szQ), szP + szQ - 1, ctest);
                 if (!got) {
                   if (t == 0) {
                     s.pex[P][Q >> 5] |= 1u << (Q & 31);
@@ -566,19 +592,23 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
 
 }  // namespace gp
 
-gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, uint8_t *ok, int16_t *bot,
-                                 int16_t *bs, int32_t *pi, int32_t *k, int64_t *n_tests,
-                                 int64_t *eff, unsigned long long *stats, cudaStream_t st) {
+gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, const gp::AllocVariantOpts &vo,
+                                 uint8_t *ok, int16_t *bot, int16_t *bs, int32_t *pi, int32_t *k,
+                                 int64_t *n_tests, int64_t *eff, unsigned long long *stats,
+                                 cudaStream_t st) {
   using namespace gp;
   BigArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
-            ts->n_tasks, ts->M, v, ok, bot, bs, pi, k, n_tests, eff, stats};
-  const size_t smem = sizeof(BigSmem);
-  cudaFuncSetAttribute(k_allocate_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            ts->n_tasks, ts->M, v, ok, bot, bs, pi, k, n_tests, eff, stats, vo};
+  const bool gen = vo.flags != 0 || vo.masked;
+  size_t smem = sizeof(BigSmem);
+  if (gen && vo.masked) smem = ((smem + 15) & ~(size_t)15) + sizeof(SizeTables);
+  auto kern = gen ? k_allocate_big<true> : k_allocate_big<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_allocate_big, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)148 * occ;
   if (grid > ts->n_sets) grid = ts->n_sets;
-  k_allocate_big<<<(unsigned)grid, 256, smem, st>>>(a);
+  kern<<<(unsigned)grid, 256, smem, st>>>(a);
   return gp_cuda_check("gp_allocate (n > 32)");
 }

@@ -1,0 +1,89 @@
+// gp_sizes.cuh -- the partition sizes Algorithm 2 may try, and how it tries them
+// (SURVEY §8(f) f4).
+//
+// Paper default (Def. 3): every m in max(|P1|,|P2|) ..
+// |P1|+|P2|-1, in increasing order, first schedulable wins.  f4 variants:
+//   * admissible sizes only (MIG-style slices): m in the caller's
+//     mask, which lies in 1..M;
+//   * binary search "between max{|P1|,|P2|} and |P1|+|P2|", as a
+//     lower-bound search over the ascending candidate list: lo = 0, hi = |L|;
+//     mid = (lo+hi)/2; schedulable(L[mid]) ? hi = mid : lo = mid + 1.
+// Schedulability is monotone in m (W is non-increasing in m and the demand
+// test is monotone in the C_i), so both searches return the same size.
+#pragma once
+#include "gp_common.cuh"
+
+namespace gp {
+
+constexpr int kMaxMaskWords = 32;  // M <= 1024
+
+// gp_alloc_opts as the kernels receive it (by value: no device allocation)
+struct AllocVariantOpts {
+  uint32_t flags;
+  int32_t masked;
+  uint32_t mask[kMaxMaskWords];  // bits above M cleared by the launcher
+};
+
+// Shared-memory tables of an admissible-size mask (built once per CTA).
+struct SizeTables {
+  int16_t adm[1024];  // admissible sizes, ascending
+  int16_t ge[1026];   // ge[m] = index in adm of the first admissible size >= m (m = 0..M+1)
+};
+
+struct SizeSpace {
+  const SizeTables *tab;  // null: every size (the paper's default)
+  int32_t M, A;           // A = number of admissible sizes
+  bool binary;
+  GP_DEV int32_t idx_ge(int32_t m) const { return tab ? tab->ge[min(max(m, 0), M + 1)] : m; }
+  GP_DEV int32_t val(int32_t x) const { return tab ? tab->adm[x] : x; }
+  // smallest admissible size >= m (0 if none); identity without a mask
+  GP_DEV int32_t round_up(int32_t m) const {
+    if (!tab) return m;
+    const int32_t x = idx_ge(m);
+    return x < A ? val(x) : 0;
+  }
+  GP_DEV int32_t largest() const { return tab ? tab->adm[A - 1] : M; }
+};
+
+// Build the tables from the mask (bit m-1 of word (m-1)/32 = size m admissible)
+// with all threads of the CTA; ends with __syncthreads().
+GP_DEV void build_size_tables(SizeTables &t, const uint32_t (&mask)[kMaxMaskWords], int32_t M) {
+  for (int32_t m = threadIdx.x; m <= M + 1; m += blockDim.x) {
+    // number of admissible sizes in 1..m-1
+    int32_t below = 0;
+    const int32_t bits = m - 1 < M ? max(m - 1, 0) : M;
+    for (int w = 0; w < (bits >> 5); ++w) below += __popc(mask[w]);
+    if (bits & 31) below += __popc(mask[bits >> 5] & ((1u << (bits & 31)) - 1u));
+    t.ge[m] = (int16_t)below;
+    if (m >= 1 && m <= M && ((mask[(m - 1) >> 5] >> ((m - 1) & 31)) & 1u)) t.adm[below] = (int16_t)m;
+  }
+  __syncthreads();
+}
+
+// Algorithm 2's size search: the smallest candidate m in [lo, hi] with test(m),
+// 0 if none.  kGen = false compiles to the paper's plain linear scan.
+template <bool kGen, class F>
+GP_DEV int32_t search_sizes(const SizeSpace &z, int32_t lo, int32_t hi, F &&test) {
+  if constexpr (!kGen) {
+    for (int32_t m = lo; m <= hi; ++m)
+      if (test(m)) return m;
+    return 0;
+  } else {
+    if (hi < lo) return 0;
+    int32_t l = z.idx_ge(lo), r = z.idx_ge(hi + 1);  // candidates [l, r)
+    if (!z.binary) {
+      for (int32_t x = l; x < r; ++x)
+        if (test(z.val(x))) return z.val(x);
+      return 0;
+    }
+    const int32_t R = r;
+    while (l < r) {
+      const int32_t mid = (l + r) >> 1;
+      if (test(z.val(mid))) r = mid;
+      else l = mid + 1;
+    }
+    return l < R ? z.val(l) : 0;
+  }
+}
+
+}  // namespace gp

@@ -68,7 +68,7 @@ _lib.gp_count_candidates.argtypes = [C.c_int32, C.c_int32, _P]
 _lib.gp_enumerate.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _P, _P, _P]
 _lib.gp_wcet.argtypes = [_P, _P, _P, _P, C.c_int64, _P, _P, _P]
 _lib.gp_wcet_per_sm.argtypes = [C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P]
-_lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+_lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.gp_sched_ratio.argtypes = [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 _P, _P, _P]
 for _f in ("gp_generate", "gp_count_candidates", "gp_enumerate", "gp_wcet", "gp_wcet_per_sm",
@@ -217,12 +217,34 @@ class AllocOut:
         return d
 
 
-def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=None):
+class _AllocOptsC(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("size_mask", C.c_void_p)]
+
+
+GP_AL_BINARY_MERGE = 1  # f4: Algorithm 2 by binary search
+GP_AL_INCREASING = 2    # f4: par_list in increasing utilisation
+
+
+def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=None, flags=0,
+                sizes=None):
+    """A5 heuristics / 1G.  f4: ``flags`` (GP_AL_*) and ``sizes`` = admissible
+    partition sizes (iterable of ints; None = every size)."""
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     if out is None:
         out = AllocOut(ts.n_sets, ts.n_tasks, ts.T.device)
     s = ts.struct()
-    _check(_lib.gp_allocate(C.byref(s), v, _ptr(out.ok), _ptr(out.block_of_task),
+    opts = None
+    if flags or sizes is not None:
+        mask = (C.c_uint32 * ((ts.M + 31) // 32))()
+        if sizes is not None:
+            for m in sizes:
+                if not 1 <= int(m) <= ts.M:
+                    raise GpError(GP_EINVAL, f"admissible size {m} outside 1..M")
+                mask[(int(m) - 1) // 32] |= 1 << ((int(m) - 1) % 32)
+        opts = _AllocOptsC(int(flags), C.cast(mask, C.c_void_p) if sizes is not None else None)
+        opts._keep = mask
+    _check(_lib.gp_allocate(C.byref(s), v, C.byref(opts) if opts is not None else None,
+                            _ptr(out.ok), _ptr(out.block_of_task),
                             _ptr(out.block_size), _ptr(out.pi), _ptr(out.k), _ptr(out.n_tests),
                             _ptr(out.efficiency), _ptr(stats), _stream(stream)))
     return out

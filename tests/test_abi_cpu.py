@@ -71,7 +71,7 @@ def test_host_validation_before_any_cuda(G):
     assert lib.gp_enumerate(4, 13, 0, 1, None, None, None) == G.GP_EINVAL
     assert lib.gp_enumerate(4, 3, 20, 10, None, None, None) == G.GP_EINVAL  # beyond N_c = 26
     assert lib.gp_wcet_per_sm(5, 0, None, 0, None, None, None) == G.GP_EINVAL  # m = 0
-    assert lib.gp_allocate(None, 0, None, None, None, None, None, None, None, None, None) == G.GP_EINVAL
+    assert lib.gp_allocate(None, 0, None, None, None, None, None, None, None, None, None, None) == G.GP_EINVAL
     import gp_workloads as W
     gen = W.WORKLOADS["c2"]["gen"](R=10)
     ts = G._TaskSetsC(100, 6, 8, 10)
@@ -83,6 +83,27 @@ def test_host_validation_before_any_cuda(G):
     with pytest.raises(G.GpError) as e:
         G.gp_generate(big, 1, 0, 10, _Fake(ts))
     assert e.value.status == G.GP_EOVERFLOW
+
+
+def test_allocate_options_validated_on_host(G):
+    """f4 options (gp_alloc_opts): unknown flag bits and a size mask with no
+    admissible size in 1..M are GP_EINVAL before any launch (n_sets = 0)."""
+    import ctypes as C
+    ts = G._TaskSetsC(0, 6, 8, 1)
+    lib = G._lib
+    bad_flags = G._AllocOptsC(8, None)
+    assert lib.gp_allocate(C.byref(ts), 1, C.byref(bad_flags), None, None, None, None, None,
+                           None, None, None, None) == G.GP_EINVAL
+    mask = (C.c_uint32 * 1)(0xFFFFFF00)  # only sizes 9..32, all above M = 8
+    empty = G._AllocOptsC(0, C.cast(mask, C.c_void_p))
+    assert lib.gp_allocate(C.byref(ts), 1, C.byref(empty), None, None, None, None, None,
+                           None, None, None, None) == G.GP_EINVAL
+    assert "admits no size" in G.gp_last_error()
+    ok_mask = (C.c_uint32 * 1)(0x80)  # size 8 only
+    good = G._AllocOptsC(G.GP_AL_BINARY_MERGE | G.GP_AL_INCREASING, C.cast(ok_mask, C.c_void_p))
+    # valid options pass validation (GP_ECUDA here only because there is no device)
+    assert lib.gp_allocate(C.byref(ts), 1, C.byref(good), None, None, None, None, None,
+                           None, None, None, None) in (G.GP_OK, G.GP_ECUDA)
 
 
 class _Fake:

@@ -245,12 +245,13 @@ def test_exhaustive_contract_violation_reported(G):
 VARIANTS = ("1G", "SMS_ACT", "SMS_INA", "BF_ACT", "BF_INA")
 
 
-def check_allocate(G, ts, host=None, variants=VARIANTS):
+def check_allocate(G, ts, host=None, variants=VARIANTS, flags=0, sizes=None):
     host = host or to_oracle(ts)
     for v in variants:
-        out = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks).want_efficiency())
+        out = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks).want_efficiency(),
+                            flags=flags, sizes=sizes)
         got = out.to_host()
-        ref = oracle.allocate(host, v)
+        ref = oracle.allocate(host, v, flags=flags, sizes=sizes)
         # f2: scheduled workload of the reported allocation (contract-respecting sets)
         eff = oracle.efficiency(host, ref["block_of_task"])
         okc = got["n_tests"] >= 0
@@ -258,7 +259,8 @@ def check_allocate(G, ts, host=None, variants=VARIANTS):
         for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
             if not (got[key] == ref[key]).all():
                 bad = np.nonzero((got[key] != ref[key]).reshape(len(got[key]), -1).any(1))[0]
-                raise AssertionError(f"{v} {key} differs on {len(bad)} sets, first {bad[:5]}")
+                raise AssertionError(f"{v} {key} differs on {len(bad)} sets, first {bad[:5]} "
+                                     f"(flags {flags}, sizes {sizes})")
 
 
 def test_allocate_c1(G):
@@ -483,3 +485,76 @@ def test_f1b_1G_plateau_n50(G):
     g = r["variants"]["1G"]["sched_rate"]
     assert last["1G"] >= 28 and all(x >= 0.95 for u, x in zip(r["U"], g) if u <= 30), g
     assert c["4_1G_collapse_dominance"]["holds"], c["4_1G_collapse_dominance"]
+
+
+# ------------------------------------------------------------------ f4: variants
+F4_CASES = [(1, None), (2, None), (3, None), (0, "mig"), (1, "mig"), (3, "mig"), (0, "sparse")]
+
+
+def _f4_sizes(kind, M):
+    if kind is None:
+        return None
+    if kind == "mig":  # MIG-style slices: 1/7, 2/7, 3/7, 4/7, 7/7 of the GPU
+        return sorted({max(1, (M * g) // 7) for g in (1, 2, 3, 4, 7)})
+    rng = np.random.default_rng(M)
+    return sorted({M} | {int(x) for x in rng.choice(np.arange(1, M), min(M - 1, 9), replace=False)})
+
+
+@pytest.mark.parametrize("flags,kind", F4_CASES)
+def test_allocate_f4_c4(G, flags, kind):
+    """§8(f) f4: every variant with binary merge,
+    increasing order and admissible-size masks, bit-exact vs the oracle."""
+    gen = W.WORKLOADS["c4"]["gen"](R=20000)
+    ts = G.TaskSets(50 * 3, 32, 148, 50)
+    G.gp_generate(gen, W.SEED, 11, 3, ts)
+    check_allocate(G, ts, flags=flags, sizes=_f4_sizes(kind, 148))
+
+
+@pytest.mark.parametrize("flags,kind", F4_CASES)
+def test_allocate_f4_c5(G, flags, kind):
+    gen = W.WORKLOADS["c5"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 20, 16, 68, 10)
+    G.gp_generate(gen, W.SEED, 3, 20, ts)
+    check_allocate(G, ts, flags=flags, sizes=_f4_sizes(kind, 68))
+
+
+@pytest.mark.parametrize("flags,kind", [(3, None), (1, "mig"), (2, "sparse")])
+def test_allocate_f4_big(G, flags, kind):
+    """The CTA-per-set kernel (50 tasks, f1 shape) with the f4 variants."""
+    gen = W.WORKLOADS["f1_50"]["gen"](R=100)
+    ts = G.TaskSets(34, 50, 68, 34)
+    G.gp_generate(gen, W.SEED, 1, 1, ts)
+    check_allocate(G, ts, flags=flags, sizes=_f4_sizes(kind, 68))
+
+
+@pytest.mark.parametrize("seed,n,M", [(51, 5, 4), (52, 12, 10), (53, 32, 24), (54, 40, 16)])
+def test_allocate_f4_random(G, seed, n, M):
+    rng = np.random.default_rng(seed)
+    d = W.random_sets(rng, 24, n, M, periods=(20, 40, 50, 100), b_max=3 * M, cost_max=4)
+    for flags, kind in ((3, "sparse"), (1, "mig"), (2, None)):
+        check_allocate(G, gpu_sets(G, d), oracle.Sets.from_dict(d), flags=flags,
+                       sizes=_f4_sizes(kind, M))
+
+
+def test_allocate_f4_hand_traces(G):
+    """The oracle's hand-traced f4 examples (tests/test_oracle_f4.py) on the GPU:
+    binary merge 2 tests vs linear 4; increasing order changes the partners."""
+    def sets(M, tasks):
+        n = len(tasks)
+        d = {k: np.array([[t[k] for t in tasks]], np.int32) for k in ("T", "D", "B", "cn", "cc", "fn", "fc")}
+        d["type"] = np.array([[t["type"] for t in tasks]], np.uint8)
+        d.update(M=M, n_groups=1, valid=np.ones(1, np.uint8), group=np.zeros(1, np.int32))
+        return d
+    def task(c, T, typ, B=1):
+        return dict(T=T, D=T, B=B, cn=c, cc=c, fn=0, fc=0, type=typ)
+    pair = sets(10, [task(1, 100, 1, B=310), task(1, 100, 0, B=610)])
+    for flags, tests in ((0, 4), (G.GP_AL_BINARY_MERGE, 2)):
+        r = G.gp_allocate(gpu_sets(G, pair), "SMS_INA", flags=flags).to_host()
+        assert r["ok"][0] == 1 and r["block_size"][0][0] == 10 and r["n_tests"][0] == tests
+    order = sets(2, [task(6, 10, 0), task(4, 10, 0), task(3, 10, 0)])
+    r = G.gp_allocate(gpu_sets(G, order), "SMS_INA", flags=G.GP_AL_INCREASING).to_host()
+    assert list(r["block_of_task"][0]) == [0, 1, 1]
+    r = G.gp_allocate(gpu_sets(G, order), "BF_INA", flags=G.GP_AL_INCREASING).to_host()
+    assert list(r["block_of_task"][0]) == [0, 1, 0]
+    r = G.gp_allocate(gpu_sets(G, pair), "SMS_ACT", sizes=[2, 4, 8, 10]).to_host()
+    assert r["ok"][0] == 1 and r["block_size"][0][0] == 10
