@@ -27,7 +27,7 @@ import gp_workloads as W  # noqa: E402
 from paper_2105_10312_b200 import gpart as G  # noqa: E402
 
 
-def run(key, reps):
+def run(key, reps, flags=0, sizes=None):
     wl = W.WORKLOADS[key]
     gen = wl["gen"](R=reps)
     n, M = wl["n"], wl["M"]
@@ -42,7 +42,8 @@ def run(key, reps):
     for v in W.VARIANT_NAMES:
         ev.append(torch.cuda.Event(enable_timing=True))
         ev[-1].record(st)
-        outs[v] = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, n).want_efficiency(), stats=stats)
+        outs[v] = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, n).want_efficiency(), stats=stats,
+                                flags=flags, sizes=sizes)
     ev.append(torch.cuda.Event(enable_timing=True))
     ev[-1].record(st)
     counts = torch.zeros((1, 34, len(W.VARIANT_NAMES), 3), dtype=torch.int64, device="cuda")
@@ -55,7 +56,8 @@ def run(key, reps):
     variant_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(W.VARIANT_NAMES))]
     c = counts.cpu().numpy()[0]
     valid = ts.valid.cpu().numpy().reshape(34, reps)
-    res = {"workload": wl["name"], "n": n, "M": M, "reps": reps, "gpu_ms": ms,
+    res = {"workload": wl["name"], "n": n, "M": M, "reps": reps, "gpu_ms": ms, "flags": flags,
+           "sizes": sizes,
            "edf_tests": int(stats[0].item()), "U": [2 * (b + 1) for b in range(34)],
            "valid_rate": valid.mean(1).tolist(), "variants": {}}
     res["variant_gpu_ms"] = dict(zip(W.VARIANT_NAMES, variant_ms))
@@ -135,6 +137,7 @@ def main():
     ap.add_argument("--reps", type=int, default=100)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01", "f1_sweep.json"))
     ap.add_argument("--skip200", action="store_true")
+    ap.add_argument("--f4", action="store_true", help="also run the f4 variants (n = 50)")
     ap.add_argument("--readings", default="A-1,A-1b",
                     help="A-1: b = beta*a (P:950 as written); A-1b: b = beta*a/M")
     a = ap.parse_args()
@@ -155,6 +158,22 @@ def main():
                 print(f"{u:3d}  " + " ".join(f"{r['variants'][v]['sched_rate'][b]:8.2f}"
                                               for v in W.VARIANT_NAMES))
         print(reading, json.dumps(res[reading]["claims"], indent=1))
+    if a.f4:
+        # f4 variants at paper scale (reading A-1): binary merge, increasing order,
+        # MIG-style slices (1/7, 2/7, 3/7, 4/7, 7/7 of the 68 SMs)
+        mig = sorted({max(1, (68 * g) // 7) for g in (1, 2, 3, 4, 7)})
+        f4 = {}
+        for name, fl, sz in (("binary", G.GP_AL_BINARY_MERGE, None),
+                             ("increasing", G.GP_AL_INCREASING, None),
+                             ("mig_slices", 0, mig), ("mig_slices_binary", G.GP_AL_BINARY_MERGE, mig)):
+            r = run("f1_50", a.reps, fl, sz)
+            f4[name] = {"gpu_ms": r["gpu_ms"], "edf_tests": r["edf_tests"],
+                        "variant_gpu_ms": r["variant_gpu_ms"], "sizes": sz,
+                        "sched_rate": {v: r["variants"][v]["sched_rate"] for v in W.VARIANT_NAMES},
+                        "mean_tests_per_set": {v: float(np.mean(r["variants"][v]["edf_tests_per_set"]))
+                                               for v in W.VARIANT_NAMES}}
+            print(f"f4 {name}: GPU {r['gpu_ms']:.1f} ms, {r['edf_tests']} EDF tests")
+        res["f4_n50"] = f4
     res["wall_s"] = time.time() - t0
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as fh:
