@@ -230,7 +230,13 @@ gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *
  * mode GP_EXHAUSTIVE: evaluates every candidate of every set directly --
  *   rank -> (k, pi, s) unranking, conflict flags and W per task (A3), and
  *   the EDF processor-demand test of every block (A4); candidate verdict =
- *   AND over its blocks (C.1.8).  Per set it writes ex->per_set[set][4] =
+ *   AND over its blocks (C.1.8).  For n_tasks <= 8 and M <= 32 the block
+ *   verdicts are memoised per (task subset, size) -- 2^n - 1 subsets x M
+ *   sizes, every one tested -- and each candidate's verdict is the AND of its
+ *   blocks' memoised verdicts, evaluated 32 candidates per word along runs of
+ *   the last part (a stream-ordered workspace of n_sets * 2^n * 4 bytes is
+ *   allocated and freed on `stream`); GP_EX_PER_CANDIDATE forces the
+ *   per-candidate EDF tests.  Both give identical outputs.  Per set it writes ex->per_set[set][4] =
  *   {n_sched, pi_star = min sum(s) over schedulable candidates (0 if none),
  *   first_rank (-1 if none), hash = sum of splitmix64(rank) mod 2^64 over
  *   schedulable ranks}, optional per-candidate verdict bits, and adds the
@@ -259,9 +265,12 @@ typedef struct {
                                  deadline points examined, tasks in tested blocks}
                                  (THRESHOLD: {sets, threshold tests, deadline points,
                                  schedulable candidates enumerated for the hash})              */
-  uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0)        */
+  uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0);
+                                 GP_EX_PER_CANDIDATE (EXHAUSTIVE): force the per-candidate
+                                 evaluator; unknown bits -> GP_EINVAL                          */
 } gp_exhaustive_opts;
 #define GP_EX_NO_HASH 1u
+#define GP_EX_PER_CANDIDATE 2u
 
 gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode, const uint8_t *verdicts,
                          int32_t n_rows, int32_t slot0, int32_t n_slots, int32_t setting,

@@ -18,7 +18,7 @@ OUT = os.path.join(PKG, "libgpart.so")
 BUILD = os.path.join(PKG, "build")
 
 SOURCES = ["abi.cu", "generate.cu", "enumerate.cu", "wcet.cu", "exhaustive.cu", "allocate.cu",
-           "ratio.cu", "threshold.cu", "allocate_big.cu"]
+           "ratio.cu", "threshold.cu", "allocate_big.cu", "exhaustive_bp.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", INCLUDE, "-I", CSRC]

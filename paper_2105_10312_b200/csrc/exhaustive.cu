@@ -24,48 +24,9 @@
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
 #include "gp_enum.cuh"
+#include "gp_exh.cuh"
 
 namespace gp {
-
-constexpr int kWarps = 8;        // warps per CTA
-constexpr int kGrab = 16;        // items per queue grab
-constexpr int kMaxL = 64;        // candidates per lane per item
-
-struct ExhArgs {
-  const int32_t *T, *D, *B, *cn, *cc, *fn, *fc, *group;
-  const uint8_t *type, *valid;
-  int32_t n_sets, n, M, n_groups;
-  RankLayout L;
-  uint64_t lo, hi;
-  int64_t *per_set;
-  uint32_t *bits;
-  int64_t words;
-  int64_t *counts;
-  int32_t slot0, n_slots, setting;
-  unsigned long long *stats;
-  unsigned long long *work_counter;
-  uint64_t items_per_set, total_items;
-  uint64_t item_base[kEnumMaxTasks + 2];
-  uint32_t chunks[kEnumMaxTasks + 2];
-  int32_t lane_L[kEnumMaxTasks + 2];
-};
-
-// Per-set input contract (gpart.h): returns H = lcm(T) or -1.
-GP_DEV int64_t set_contract(const ExhArgs &a, int64_t set) {
-  const int n = a.n;
-  int64_t H = 1;
-  const int64_t cap = ((int64_t)1 << 31) / (n + 1);
-  for (int i = 0; i < n; ++i) {
-    const int64_t o = set * n + i;
-    const int32_t T = a.T[o], D = a.D[o];
-    if (T < 1 || D < 1 || D > T || a.B[o] < 1 || a.cn[o] < 1 || a.cc[o] < a.cn[o] ||
-        a.fn[o] < 0 || a.fc[o] < a.fn[o])
-      return -1;
-    H = lcm_capped(H, T, cap - 1);
-    if (H < 0) return -1;
-  }
-  return H;
-}
 
 struct WarpSmem {
   int32_t set, H, okc, n_multi;
@@ -116,51 +77,6 @@ struct BlockDispatch<NT, NT + 1> {
   }
 };
 
-// ---- per-lane accumulation ---------------------------------------------------
-struct LaneAcc {
-  uint32_t n = 0;
-  int32_t pi = INT32_MAX;
-  uint64_t first = ~0ull, hash = 0;
-  uint64_t st_cand = 0, st_blocks = 0, st_tasks = 0;
-  uint32_t st_events = 0;
-};
-
-GP_DEV void record_ok(LaneAcc &acc, uint64_t rank, int32_t sum, uint32_t *bits, uint64_t lo) {
-  ++acc.n;
-  acc.pi = min(acc.pi, sum);
-  acc.first = rank < acc.first ? rank : acc.first;
-  acc.hash += splitmix64(rank);
-  if (bits) {
-    const uint64_t off = rank - lo;
-    atomicOr(bits + (off >> 5), 1u << (off & 31));
-  }
-}
-
-// ---- per-warp helpers shared by both evaluation paths -----------------------
-GP_DEV void exh_flush(const ExhArgs &a, LaneAcc &acc, int64_t cur, int lane) {
-  if (cur < 0) return;
-  const uint32_t tot = (uint32_t)warp_sum_i32((int32_t)acc.n);
-  const int32_t pi = warp_min_i32(acc.pi);
-  uint64_t first = acc.first;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint64_t v = __shfl_xor_sync(GP_FULL, first, o);
-    first = v < first ? v : first;
-  }
-  const uint64_t h = warp_sum_u64(acc.hash);
-  if (lane == 0 && tot > 0) {
-    long long *ps = reinterpret_cast<long long *>(a.per_set + cur * 4);
-    atomicAdd(reinterpret_cast<unsigned long long *>(ps + 0), (unsigned long long)tot);
-    atomicMin(ps + 1, (long long)pi);
-    atomicMin(ps + 2, (long long)first);
-    atomicAdd(reinterpret_cast<unsigned long long *>(ps + 3), h);
-  }
-  acc.n = 0;
-  acc.pi = INT32_MAX;
-  acc.first = ~0ull;
-  acc.hash = 0;
-}
-
 // load one set into the warp's shared memory: contract, H, H/T_i, types and
 // the W table W[i][x][s] = ceil(B_i/s) c_i^x + f_i^x (C.1.3)
 GP_DEV void exh_load_set(const ExhArgs &a, WarpSmem &w, int32_t *Wt, int64_t set, int lane) {
@@ -187,51 +103,6 @@ GP_DEV void exh_load_set(const ExhArgs &a, WarpSmem &w, int32_t *Wt, int64_t set
     }
   }
   __syncwarp();
-}
-
-GP_DEV void exh_stats_flush(const ExhArgs &a, LaneAcc &acc, int lane) {
-  if (!a.stats) return;
-  const uint64_t c0 = warp_sum_u64(acc.st_cand), c1 = warp_sum_u64(acc.st_blocks);
-  const uint64_t c2 = warp_sum_u64(acc.st_events), c3 = warp_sum_u64(acc.st_tasks);
-  if (lane == 0) {
-    atomicAdd(a.stats + 0, c0);
-    atomicAdd(a.stats + 1, c1);
-    atomicAdd(a.stats + 2, c2);
-    atomicAdd(a.stats + 3, c3);
-  }
-}
-
-// Lexicographic successor of s, stored REVERSED (sr[0] = last part) so the
-// common step -- grow the last part while sum < M -- touches a fixed register.
-// Otherwise bump the part with the fewest followers jj >= 1 whose followers
-// have slack (sum of sr[0..jj-1] > jj) and reset its followers to 1.
-template <int NT>
-GP_DEV void next_sizes_rev(int M, int k, int32_t (&sr)[NT], int32_t &sum) {
-  if (sum < M) {  // common: grow the last part
-    sr[0] += 1;
-    sum += 1;
-    return;
-  }
-  if (k >= 2 && sr[0] > 1) {  // next: bump the second-to-last part, last := 1
-    sum -= sr[0] - 2;
-    sr[0] = 1;
-    sr[1] += 1;
-    return;
-  }
-  int prefix = 0, pick = -1;
-#pragma unroll
-  for (int jj = 1; jj < NT; ++jj) {
-    prefix += sr[jj - 1];
-    if (pick < 0 && jj < k && prefix > jj) pick = jj;
-  }
-  if (pick < 0) return;  // last candidate of this allocation (never stepped past)
-  int ns = 0;
-#pragma unroll
-  for (int i = 0; i < NT; ++i) {
-    sr[i] = i < pick ? 1 : (i == pick ? sr[i] + 1 : sr[i]);
-    ns += i < k ? sr[i] : 0;
-  }
-  sum = ns;
 }
 
 template <int NT>
@@ -888,6 +759,8 @@ static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
 
 }  // namespace gp
 
+gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a, cudaStream_t st);
+
 // Called by gp_sched_ratio (ratio.cu) for GP_EXHAUSTIVE.
 gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_slots,
                                int32_t setting, int64_t *counts, const gp_exhaustive_opts *ex,
@@ -914,6 +787,9 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   a.per_set = ex->per_set; a.bits = ex->verdict_bits; a.words = ex->words_per_set;
   a.counts = counts; a.slot0 = slot0; a.n_slots = n_slots; a.setting = setting;
   a.stats = ex->stats; a.work_counter = ex->work_counter;
+  if (ex->flags & ~(uint32_t)(GP_EX_NO_HASH | GP_EX_PER_CANDIDATE))
+    return gp_fail(GP_EINVAL, "EXHAUSTIVE: unknown flags 0x%x", ex->flags);
+  a.flags = ex->flags;
   uint64_t items = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
     // balanced chunks of at most 32 * kMaxL size vectors of one allocation
@@ -933,6 +809,15 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   cudaMemsetAsync(ex->work_counter, 0, 8, st);
   int64_t g1 = (ts->n_sets + 255) / 256;
   k_exh_init<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(ex->per_set, ts->n_sets);
+  // default for n <= 8, M <= 32: bit-sliced verdicts over memoised block
+  // verdicts (exhaustive_bp.cu); otherwise, or on request, per candidate
+  static const bool percand_env = getenv("GP_EXH_PERCAND") != nullptr;  // A/B switch
+  if (n <= 8 && M <= 32 && !(ex->flags & GP_EX_PER_CANDIDATE) && !percand_env) {
+    gp_status r = gp_exhaustive_bp_launch(a, st);
+    if (r != GP_OK) return r;
+    k_exh_finalize<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(a);
+    return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) finalize");
+  }
   const size_t wt_words = (size_t)2 * n * M;
   const size_t per_warp = ((sizeof(WarpSmem) / 4 + wt_words) + 3) & ~(size_t)3;
   const size_t smem = (((enum_table_words(M, n) + 3) & ~(size_t)3) + per_warp * kWarps) * 4;

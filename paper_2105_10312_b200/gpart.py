@@ -22,6 +22,7 @@ VARIANTS = {"1G": GP_1G, "SMS_ACT": GP_SMS_ACT, "SMS_INA": GP_SMS_INA, "BF_ACT":
             "BF_INA": GP_BF_INA}
 GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD = 0, 1, 2
 GP_EX_NO_HASH = 1
+GP_EX_PER_CANDIDATE = 2  # force the per-candidate EXHAUSTIVE evaluator
 UINT64_MAX = 2**64 - 1
 
 FIELDS_I32 = ("T", "D", "B", "cn", "cc", "fn", "fc")

@@ -136,7 +136,10 @@ def test_wcet_batch(G):
 
 
 # ------------------------------------------------------------------ A2-A4 fused
-def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1):
+EVALUATORS = pytest.mark.parametrize("ev", [0, 2], ids=["bitsliced", "per_candidate"])
+
+
+def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1, flags=0):
     S = ts.n_sets
     total = G.gp_count_candidates(ts.M, ts.n_tasks)
     hi_ = total if hi is None else hi
@@ -147,7 +150,8 @@ def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slo
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, counts, slot0=slot0, n_slots=n_slots, per_set=per,
                      verdict_bits=vb, words_per_set=words if bits else 0, work_counter=work,
-                     stats=stats, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi)
+                     stats=stats, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi,
+                     flags=flags)
     torch.cuda.synchronize()
     out = per.cpu().numpy()
     if bits:
@@ -155,28 +159,31 @@ def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slo
     return out, None, stats.cpu().numpy()
 
 
-def test_exhaustive_c1_table(G):
+@EVALUATORS
+def test_exhaustive_c1_table(G, ev):
     d = W._c1_sets()
     ts = gpu_sets(G, d)
-    per, vb, st = run_exhaustive(G, ts, bits=True)
+    per, vb, st = run_exhaustive(G, ts, bits=True, flags=ev)
     ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
     assert (per == ref).all() and (vb == rbits).all()
     assert per[:, 0].tolist() == [4, 10, 10, 10, 10, 10, 10, 4]
     assert st[0] == 8 * 26
 
 
-def test_exhaustive_c2_bitmaps(G):
+@EVALUATORS
+def test_exhaustive_c2_bitmaps(G, ev):
     gen = W.WORKLOADS["c2"]["gen"](R=10000)
     ts = G.TaskSets(10 * 100, 6, 8, 10)
     G.gp_generate(gen, W.SEED, 0, 100, ts)
-    per, vb, st = run_exhaustive(G, ts, bits=True)
+    per, vb, st = run_exhaustive(G, ts, bits=True, flags=ev)
     ref, rbits = oracle.exhaustive(to_oracle(ts), bits=True)
     assert (per == ref).all()
     assert (vb == rbits).all()
     assert st[0] == 1000 * 11334
 
 
-def test_exhaustive_c3_parity_config_sampled(G):
+@EVALUATORS
+def test_exhaustive_c3_parity_config_sampled(G, ev):
     """C3 at the bench's parity size (10 bins x 1,000 sets, M=20, n=6,
     694,755 candidates per set) in the launch configuration bench.py times;
     per-set outputs recomputed by the oracle for a sample of sets."""
@@ -184,7 +191,7 @@ def test_exhaustive_c3_parity_config_sampled(G):
     ts = G.TaskSets(10 * 1000, 6, 20, 10)
     G.gp_generate(gen, W.SEED, 0, 1000, ts)
     counts = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
-    per, _, st = run_exhaustive(G, ts, counts=counts)
+    per, _, st = run_exhaustive(G, ts, counts=counts, flags=ev)
     assert st[0] == 10 * 1000 * 694755
     host = to_oracle(ts)
     rng = np.random.default_rng(13)
@@ -205,40 +212,56 @@ def test_exhaustive_c3_parity_config_sampled(G):
 
 @pytest.mark.parametrize("seed,n,M", [(1, 1, 1), (2, 1, 7), (3, 2, 1), (4, 3, 4), (5, 4, 6),
                                       (6, 5, 3), (7, 6, 5), (8, 7, 4), (9, 8, 3), (10, 4, 12),
-                                      (11, 3, 12), (12, 6, 9)])
-def test_exhaustive_random_sets(G, seed, n, M):
+                                      (11, 3, 12), (12, 6, 9), (13, 3, 40), (14, 8, 32),
+                                      (15, 2, 31)])
+@EVALUATORS
+def test_exhaustive_random_sets(G, seed, n, M, ev):
     rng = np.random.default_rng(seed)
     d = W.random_sets(rng, 37, n, M, periods=(4, 6, 8, 12, 24), b_max=2 * M + 3, cost_max=3)
     ts = gpu_sets(G, d)
-    per, vb, _ = run_exhaustive(G, ts, bits=True)
+    per, vb, _ = run_exhaustive(G, ts, bits=True, flags=ev)
     ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
     assert (per == ref).all() and (vb == rbits).all()
 
 
-def test_exhaustive_rank_windows(G):
+@EVALUATORS
+def test_exhaustive_rank_windows(G, ev):
     gen = W.WORKLOADS["c2"]["gen"](R=10000)
     ts = G.TaskSets(10 * 5, 6, 8, 10)
     G.gp_generate(gen, W.SEED, 3, 5, ts)
     host = to_oracle(ts)
-    for lo, hi in [(0, 1), (5, 37), (100, 4100), (11000, 11334), (7777, 7778)]:
-        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi)
+    for lo, hi in [(0, 1), (5, 37), (100, 4100), (11000, 11334), (7777, 7778), (33, 34), (31, 65)]:
+        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi, flags=ev)
         ref, rbits = oracle.exhaustive(host, lo, hi, bits=True)
         assert (per == ref).all() and (vb == rbits).all(), (lo, hi)
 
 
-def test_exhaustive_contract_violation_reported(G):
+@EVALUATORS
+def test_exhaustive_contract_violation_reported(G, ev):
     d = W.random_sets(np.random.default_rng(5), 6, 3, 4)
     d["D"][2, 1] = d["T"][2, 1] + 1  # D > T violates the contract
     d["T"][4, :] = [1000003, 1000033, 1000037]  # hyperperiod overflow
     d["D"][4, :] = d["T"][4, :]
     ts = gpu_sets(G, d)
     counts = torch.zeros((1, 1, 1, 3), dtype=torch.int64, device="cuda")
-    per, _, _ = run_exhaustive(G, ts, counts=counts)
+    per, _, _ = run_exhaustive(G, ts, counts=counts, flags=ev)
     assert per[2, 0] == -1 and per[4, 0] == -1
     ok_rows = [0, 1, 3, 5]
     ref = oracle.exhaustive(oracle.Sets.from_dict(d).subset(ok_rows))
     assert (per[ok_rows] == ref).all()
     assert counts.cpu().numpy()[0, 0, 0, 2] == 2  # counted as invalid
+
+
+def test_exhaustive_no_hash_and_flag_validation(G):
+    """GP_EX_NO_HASH zeroes only the hash; unknown flag bits are GP_EINVAL."""
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 20, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 20, ts)
+    full, _, _ = run_exhaustive(G, ts)
+    nh, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NO_HASH)
+    assert (nh[:, :3] == full[:, :3]).all() and (nh[:, 3] == 0).all()
+    with pytest.raises(G.GpError):
+        run_exhaustive(G, ts, flags=8)
 
 
 # ------------------------------------------------------------------ A5
