@@ -110,8 +110,73 @@ __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *mem
   }
 }
 
-// ---- main pass: bit-sliced verdicts over runs ---------------------------------
-__global__ void __launch_bounds__(kWarps * 32, 4) k_exh_bp(const ExhArgs a, const uint32_t *memo) {
+// ---- RGS table: labels of every allocation, in rank order (k, then lex) -------
+__global__ void k_exh_rgs_table(const ExhArgs a, uint32_t *rgs) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const EnumTables tab = build_enum_tables(smem, a.M, a.n);
+  uint32_t total = 0;
+  for (int k = 1; k <= a.L.kmax; ++k) total += (uint32_t)a.L.n_pi[k];
+  for (uint32_t g = threadIdx.x; g < total; g += blockDim.x) {
+    int k = 1;
+    uint32_t base = 0;
+    while (g >= base + (uint32_t)a.L.n_pi[k]) base += (uint32_t)a.L.n_pi[k++];
+    rgs[g] = (uint32_t)unrank_rgs(tab, k, g - base);  // 4 bits per task, n <= 8
+  }
+}
+
+// Prefix index -> prefix (p_0..p_{kp-1}), parts >= 1, sum <= Mx, lexicographic;
+// stored reversed (pr[0] = p_{kp-1}).  C(Mx - c, r) counts the completions.
+GP_DEV void unrank_prefix_rev(const EnumTables &t, int kp, int Mx, uint32_t rho,
+                              int32_t (&pr)[kBpMaxN], int32_t &psum) {
+  int prev = 0;
+#pragma unroll
+  for (int j = 0; j < kBpMaxN; ++j) {
+    if (j < kp) {
+      int v = prev + 1;
+      for (;;) {
+        const uint32_t cnt = t.binom[(Mx - v) * (t.n + 1) + (kp - 1 - j)];
+        if (rho < cnt) break;
+        rho -= cnt;
+        ++v;
+      }
+#pragma unroll
+      for (int jj = 0; jj < kBpMaxN; ++jj)
+        if (jj == kp - 1 - j) pr[jj] = v - prev;
+      prev = v;
+    }
+  }
+  psum = prev;
+}
+
+// s-index (lexicographic rank among k-part size vectors, sum <= M) of the
+// vector (prefix, 1): sum over parts j of the vectors that differ first at j
+// with a smaller part, by the hockey-stick identity
+//   sum_{v=c_{j-1}+1}^{c_j - 1} C(M - v, k-1-j) = C(M - c_{j-1}, k-j) - C(M - c_j + 1, k-j)
+// (c_j = prefix sums).
+GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t (&pr)[kBpMaxN]) {
+  uint32_t r = 0;
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < kBpMaxN - 1; ++j) {
+    if (j < k - 1) {
+      int part = 0;
+#pragma unroll
+      for (int jj = 0; jj < kBpMaxN; ++jj)
+        if (jj == k - 2 - j) part = pr[jj];
+      const int cn = c + part;
+      r += t.C(M - c, k - j) - t.C(M - cn + 1, k - j);
+      c = cn;
+    }
+  }
+  return r;
+}
+
+// ---- main pass: bit-sliced verdicts over runs -----------------------------------
+// item = (set, allocation pi); its runs (one per prefix, C(M-1, k-1) of them)
+// are split evenly over the 32 lanes, so every lane iterates the same number
+// of times.
+__global__ void __launch_bounds__(kWarps * 32, 4)
+    k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int n = a.n, M = a.M;
   const EnumTables tab = build_enum_tables(smem, M, n);
@@ -129,7 +194,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exh_bp(const ExhArgs a, cons
     const uint64_t end = min(base + (uint64_t)kGrab, a.total_items);
     for (uint64_t it = base; it < end; ++it) {
       const int64_t set = (int64_t)(it / a.items_per_set);
-      uint64_t local = it - (uint64_t)set * a.items_per_set;
+      const uint32_t g = (uint32_t)(it - (uint64_t)set * a.items_per_set);  // RGS index
       if (set != cur) {
         exh_flush(a, acc, cur, lane);
         cur = set;
@@ -137,21 +202,14 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exh_bp(const ExhArgs a, cons
       }
       if (!okc) continue;  // contract violation: finalize reports it
       int k = 1;
-      while (k < a.L.kmax && local >= a.item_base[k + 1]) ++k;
-      local -= a.item_base[k];
-      const uint32_t chunks = a.chunks[k];
-      const uint32_t p = (uint32_t)(local / chunks);
-      const uint32_t c = (uint32_t)(local % chunks);
-      const int Lk = a.lane_L[k];
+      while (k < a.L.kmax && g >= (uint32_t)a.item_base[k + 1]) ++k;
+      const uint32_t p = g - (uint32_t)a.item_base[k];
       const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
       const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
-      const uint32_t rho0 = c * 32u * (uint32_t)Lk;
-      if (rank_pi + rho0 >= a.hi || rank_pi + min((uint64_t)per_pi, (uint64_t)rho0 + 32u * Lk) <= a.lo)
-        continue;
-      // allocation pi: block j's task mask -> its verdict word V[S_j]; reversed
-      // into Vr[jj] = word of block k-1-jj to match the reversed sizes
-      const uint64_t labels = unrank_rgs(tab, k, p);
-      const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15) : -1;
+      if (rank_pi >= a.hi || rank_pi + per_pi <= a.lo) continue;
+      // blocks of pi -> verdict words, reversed: Vr[jj] = V[S_{k-1-jj}]
+      const uint32_t labels = rgs[g];
+      const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
       uint32_t bmask = 0;
 #pragma unroll
       for (int j = 0; j < kBpMaxN; ++j) {
@@ -162,50 +220,42 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exh_bp(const ExhArgs a, cons
       uint32_t Vr[kBpMaxN];
 #pragma unroll
       for (int jj = 0; jj < kBpMaxN; ++jj) Vr[jj] = __shfl_sync(GP_FULL, vw, max(k - 1 - jj, 0));
-      // this lane's candidates: s-index my0 + t, t in [t_lo, t_hi)
-      const uint32_t my0 = rho0 + (uint32_t)lane * (uint32_t)Lk;
-      const uint64_t r0 = rank_pi + my0;
-      int t_hi = Lk;
-      if (a.hi <= r0) t_hi = 0;
-      else if (a.hi - r0 < (uint64_t)t_hi) t_hi = (int)(a.hi - r0);
-      if ((int64_t)t_hi > (int64_t)per_pi - (int64_t)my0)
-        t_hi = (int)max((int64_t)0, (int64_t)per_pi - (int64_t)my0);
-      const int t_lo = a.lo > r0 ? (int)min(a.lo - r0, (uint64_t)Lk) : 0;
-      if (t_lo < t_hi) {  // no warp collective inside
-        int32_t sr[kBpMaxN];
-        int32_t sum = 0;
-        {
-          int32_t s[kBpMaxN];
-          unrank_sizes<kBpMaxN>(tab, k, my0 + (uint32_t)t_lo, s);
+      // this lane's runs [r_lo, r_hi) among C(M-1, k-1)
+      const uint32_t n_runs = tab.C(M - 1, k - 1);
+      const uint32_t per_lane = (n_runs + 31u) >> 5;
+      const uint32_t r_lo = min(n_runs, (uint32_t)lane * per_lane);
+      const uint32_t r_hi = min(n_runs, r_lo + per_lane);
+      if (r_lo < r_hi) {  // no warp collective inside
+        const int kp = k - 1;
+        int32_t pr[kBpMaxN];
 #pragma unroll
-          for (int jj = 0; jj < kBpMaxN; ++jj) {
-            sr[jj] = 1;
-#pragma unroll
-            for (int j = 0; j < kBpMaxN; ++j)
-              if (j == k - 1 - jj) sr[jj] = s[j];
-            sum += jj < k ? sr[jj] : 0;
-          }
-        }
-        acc.st_cand += (uint64_t)(t_hi - t_lo);
+        for (int jj = 0; jj < kBpMaxN; ++jj) pr[jj] = 1;
+        int32_t psum = 0;
+        unrank_prefix_rev(tab, kp, M - 1, r_lo, pr, psum);
+        uint64_t rk = rank_pi + run_start_sidx(tab, k, M, pr);  // rank of (prefix, 1)
         uint32_t *bits = a.bits ? a.bits + cur * a.words : nullptr;
-        int t = t_lo;
-        for (;;) {
-          // the run segment: last part sr[0] .. sr[0] + seg - 1
-          const int seg = min(M - sum + 1, t_hi - t);
-          uint32_t pre = 1u;
+        uint64_t cands = 0;
+        for (uint32_t r = r_lo; r < r_hi; ++r) {
+          const int len = M - psum;  // last part 1 .. len
+          uint32_t pre = 1u;  // prefix blocks: block kp-1-jj has size pr[jj], word Vr[jj+1]
 #pragma unroll
-          for (int jj = 1; jj < kBpMaxN; ++jj)
-            if (jj < k) pre &= Vr[jj] >> (sr[jj] - 1);
-          uint32_t okb = 0;
-          if (pre & 1u) {
-            okb = Vr[0] >> (sr[0] - 1);
-            if (seg < 32) okb &= (1u << seg) - 1u;
+          for (int jj = 0; jj < kBpMaxN - 1; ++jj)
+            if (jj < kp) pre &= Vr[jj + 1] >> (pr[jj] - 1);
+          uint32_t okb = (pre & 1u) ? Vr[0] : 0u;
+          if (len < 32) okb &= (1u << len) - 1u;
+          // rank window [lo, hi): candidate b has rank rk + b
+          if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
+          if (rk + (uint64_t)len > a.hi)
+            okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
+          {  // candidates of this run inside the window
+            const uint64_t in_lo = rk < a.lo ? min(a.lo - rk, (uint64_t)len) : 0;
+            const uint64_t in_hi = rk + (uint64_t)len > a.hi ? (a.hi > rk ? a.hi - rk : 0) : (uint64_t)len;
+            cands += in_hi > in_lo ? in_hi - in_lo : 0;
           }
           if (okb) {
             const int fb = __ffs(okb) - 1;
-            const uint64_t rk = r0 + (uint32_t)t;
             acc.n += __popc(okb);
-            acc.pi = min(acc.pi, sum + fb);
+            acc.pi = min(acc.pi, psum + fb + 1);
             acc.first = min(acc.first, rk + (uint64_t)fb);
             if (want_hash) {
               uint32_t w = okb;
@@ -215,19 +265,18 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exh_bp(const ExhArgs a, cons
                 acc.hash += splitmix64(rk + (uint64_t)b);
               }
             }
-            if (bits) {  // verdict bits of the segment, word-level
-              const uint64_t off = rk - a.lo;
+            if (bits) {  // verdict bits of the run, word-level
+              const uint64_t off = rk - a.lo + (uint64_t)fb;
+              const uint32_t w2 = okb >> fb;
               const uint32_t sh = (uint32_t)(off & 31u);
-              atomicOr(bits + (off >> 5), okb << sh);
-              if (sh && (okb >> (32u - sh))) atomicOr(bits + (off >> 5) + 1, okb >> (32u - sh));
+              atomicOr(bits + (off >> 5), w2 << sh);
+              if (sh && (w2 >> (32u - sh))) atomicOr(bits + (off >> 5) + 1, w2 >> (32u - sh));
             }
           }
-          t += seg;
-          if (t >= t_hi) break;
-          sr[0] += seg - 1;  // end of this run (sum == M), then the lexicographic successor
-          sum += seg - 1;
-          next_sizes_rev<kBpMaxN>(M, k, sr, sum);
+          rk += (uint64_t)len;
+          if (kp > 0 && r + 1 < r_hi) next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
         }
+        acc.st_cand += cands;
       }
     }
   }
@@ -243,17 +292,31 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_exh_bp(const ExhArgs a, cons
 // Called by gp_exhaustive_launch (exhaustive.cu) when n <= 8, M <= 32 and the
 // caller did not ask for the per-candidate evaluator.  `a` is fully set up
 // (items, rank window, per_set initialised); finalize runs after.
-gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a, cudaStream_t st) {
+gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   using namespace gp;
-  const int n = a.n, M = a.M;
+  const int n = a0.n, M = a0.M;
   if (n > kBpMaxN || M > kBpMaxM) return gp_fail(GP_EINVAL, "EXHAUSTIVE(bp): n <= 8, M <= 32");
-  uint32_t *memo = nullptr;
-  const size_t bytes = (size_t)a.n_sets * ((size_t)1 << n) * sizeof(uint32_t);
-  if (cudaMallocAsync(reinterpret_cast<void **>(&memo), bytes, st) != cudaSuccess)
+  // items = (set, allocation): item_base[k] = first RGS index with k blocks
+  ExhArgs a = a0;
+  uint64_t n_rgs = 0;
+  for (int k = 1; k <= a.L.kmax; ++k) {
+    a.item_base[k] = n_rgs;
+    n_rgs += a.L.n_pi[k];
+  }
+  a.item_base[a.L.kmax + 1] = n_rgs;
+  a.items_per_set = n_rgs;
+  a.total_items = n_rgs * (uint64_t)a.n_sets;
+  const size_t memo_words = (size_t)a.n_sets * ((size_t)1 << n);
+  uint32_t *ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void **>(&ws), (memo_words + n_rgs) * sizeof(uint32_t), st) !=
+      cudaSuccess)
     return gp_cuda_check("EXHAUSTIVE(bp): workspace allocation");
+  uint32_t *memo = ws, *rgs = ws + memo_words;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = ((enum_table_words(M, n) + 3) & ~(size_t)3) * 4;
+  k_exh_rgs_table<<<1, 256, smem, st>>>(a, rgs);
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
@@ -261,16 +324,15 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a, cudaStream_t st) {
   }
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
   if (r == GP_OK) {
-    const size_t smem = ((enum_table_words(M, n) + 3) & ~(size_t)3) * 4;
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_bp, kWarps * 32, smem);
     if (occ < 1) occ = 1;
     uint64_t want = (a.total_items + kGrab * kWarps - 1) / (kGrab * kWarps);
     uint64_t grid = (uint64_t)sms * occ;
     if (want < grid) grid = want > 0 ? want : 1;
-    k_exh_bp<<<(unsigned)grid, kWarps * 32, smem, st>>>(a, memo);
+    k_exh_bp<<<(unsigned)grid, kWarps * 32, smem, st>>>(a, memo, rgs);
     r = gp_cuda_check("EXHAUSTIVE(bp) main kernel");
   }
-  cudaFreeAsync(memo, st);
+  cudaFreeAsync(ws, st);
   return r;
 }
