@@ -171,11 +171,57 @@ GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t 
   return r;
 }
 
+// j-th (0-based) set bit of x, j < popc(x)
+GP_DEV int select_bit(uint32_t x, int j) {
+  int pos = 0;
+  int c = __popc(x & 0xFFFFu);
+  if (j >= c) { j -= c; pos += 16; x >>= 16; }
+  c = __popc(x & 0xFFu);
+  if (j >= c) { j -= c; pos += 8; x >>= 8; }
+  c = __popc(x & 0xFu);
+  if (j >= c) { j -= c; pos += 4; x >>= 4; }
+  c = __popc(x & 0x3u);
+  if (j >= c) { j -= c; pos += 2; x >>= 2; }
+  return pos + (j >= (int)(x & 1u) ? 1 : 0);
+}
+
+// Verdict hash of the warp's schedulable candidates of one iteration: lane l
+// holds okb (bit b = rank rk + b).  The ranks are spread over the 32 lanes
+// in rounds (owner lane by a binary search over the exclusive prefix counts),
+// so splitmix64 runs on full warps whatever the distribution of the bits.
+GP_DEV uint64_t warp_hash_bits(uint32_t okb, uint64_t rk, int lane) {
+  const int cnt = __popc(okb);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(GP_FULL, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(GP_FULL, incl, 31);
+  const int excl = incl - cnt;
+  uint64_t h = 0;
+  for (int base = 0; base < total; base += 32) {
+    const int e = base + lane;
+    int L = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int x = __shfl_sync(GP_FULL, excl, L + step);
+      if (x <= e) L += step;
+    }
+    const uint32_t wL = __shfl_sync(GP_FULL, okb, L);
+    const uint64_t rL = __shfl_sync(GP_FULL, rk, L);
+    const int xL = __shfl_sync(GP_FULL, excl, L);
+    if (e < total) h += splitmix64(rL + (uint64_t)select_bit(wL, e - xL));
+  }
+  return h;
+}
+
 // ---- main pass: bit-sliced verdicts over runs -----------------------------------
-// item = (set, allocation pi); its runs (one per prefix, C(M-1, k-1) of them)
-// are split evenly over the 32 lanes, so every lane iterates the same number
-// of times.
-__global__ void __launch_bounds__(kWarps * 32, 4)
+// item = (set, allocation pi), in k-DESCENDING groups (the largest allocations
+// are handed out first, the small ones fill the tail); a pi's runs (one per
+// prefix, C(M-1, k-1) of them) are split evenly over the 32 lanes, so every
+// lane iterates the same number of times.
+__global__ void __launch_bounds__(kWarps * 32, 3)
     k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int n = a.n, M = a.M;
@@ -193,22 +239,24 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
     if (base >= a.total_items) break;
     const uint64_t end = min(base + (uint64_t)kGrab, a.total_items);
     for (uint64_t it = base; it < end; ++it) {
-      const int64_t set = (int64_t)(it / a.items_per_set);
-      const uint32_t g = (uint32_t)(it - (uint64_t)set * a.items_per_set);  // RGS index
+      int k = a.L.kmax;  // groups k = kmax, kmax-1, ..., 1; item_base[k] = end of group k
+      while (k > 1 && it >= a.item_base[k]) --k;
+      const uint64_t local = it - (k == a.L.kmax ? 0 : a.item_base[k + 1]);
+      const uint32_t npi = (uint32_t)a.L.n_pi[k];
+      const int64_t set = (int64_t)(local / npi);
+      const uint32_t p = (uint32_t)(local - (uint64_t)set * npi);
       if (set != cur) {
         exh_flush(a, acc, cur, lane);
         cur = set;
         okc = memo[set * nsub] != 0;
       }
       if (!okc) continue;  // contract violation: finalize reports it
-      int k = 1;
-      while (k < a.L.kmax && g >= (uint32_t)a.item_base[k + 1]) ++k;
-      const uint32_t p = g - (uint32_t)a.item_base[k];
       const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
       const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
       if (rank_pi >= a.hi || rank_pi + per_pi <= a.lo) continue;
+      const bool full = rank_pi >= a.lo && rank_pi + per_pi <= a.hi;  // no window clipping
       // blocks of pi -> verdict words, reversed: Vr[jj] = V[S_{k-1-jj}]
-      const uint32_t labels = rgs[g];
+      const uint32_t labels = rgs[a.rgs_base[k] + p];
       const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
       uint32_t bmask = 0;
 #pragma unroll
@@ -220,34 +268,48 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
       uint32_t Vr[kBpMaxN];
 #pragma unroll
       for (int jj = 0; jj < kBpMaxN; ++jj) Vr[jj] = __shfl_sync(GP_FULL, vw, max(k - 1 - jj, 0));
-      // this lane's runs [r_lo, r_hi) among C(M-1, k-1)
+      // this lane's runs [r_lo, r_hi) among C(M-1, k-1); all lanes iterate
+      // `iters` times (idle lanes with an empty word) so the hash can run on
+      // the whole warp
       const uint32_t n_runs = tab.C(M - 1, k - 1);
-      const uint32_t per_lane = (n_runs + 31u) >> 5;
-      const uint32_t r_lo = min(n_runs, (uint32_t)lane * per_lane);
-      const uint32_t r_hi = min(n_runs, r_lo + per_lane);
-      if (r_lo < r_hi) {  // no warp collective inside
-        const int kp = k - 1;
-        int32_t pr[kBpMaxN];
+      const uint32_t iters = (n_runs + 31u) >> 5;
+      const uint32_t r_lo = min(n_runs, (uint32_t)lane * iters);
+      const uint32_t r_hi = min(n_runs, r_lo + iters);
+      const int kp = k - 1;
+      int32_t pr[kBpMaxN];
 #pragma unroll
-        for (int jj = 0; jj < kBpMaxN; ++jj) pr[jj] = 1;
-        int32_t psum = 0;
+      for (int jj = 0; jj < kBpMaxN; ++jj) pr[jj] = 1;
+      int32_t psum = kp;
+      uint64_t rk = rank_pi;
+      if (r_lo < r_hi) {
         unrank_prefix_rev(tab, kp, M - 1, r_lo, pr, psum);
-        uint64_t rk = rank_pi + run_start_sidx(tab, k, M, pr);  // rank of (prefix, 1)
-        uint32_t *bits = a.bits ? a.bits + cur * a.words : nullptr;
-        uint64_t cands = 0;
-        for (uint32_t r = r_lo; r < r_hi; ++r) {
-          const int len = M - psum;  // last part 1 .. len
-          uint32_t pre = 1u;  // prefix blocks: block kp-1-jj has size pr[jj], word Vr[jj+1]
+        rk = rank_pi + run_start_sidx(tab, k, M, pr);  // rank of (prefix, 1)
+      }
+      // verdict of the prefix blocks other than the last prefix block (k-2)
+      auto pre_rest = [&]() -> uint32_t {
+        uint32_t v = 1u;
 #pragma unroll
-          for (int jj = 0; jj < kBpMaxN - 1; ++jj)
-            if (jj < kp) pre &= Vr[jj + 1] >> (pr[jj] - 1);
-          uint32_t okb = (pre & 1u) ? Vr[0] : 0u;
+        for (int jj = 1; jj < kBpMaxN - 1; ++jj)
+          if (jj < kp) v &= Vr[jj + 1] >> (pr[jj] - 1);
+        return v;
+      };
+      uint32_t rest = pre_rest();
+      uint32_t *bits = a.bits ? a.bits + cur * a.words : nullptr;
+      uint64_t cands = 0;
+      for (uint32_t i = 0; i < iters; ++i) {
+        const uint32_t r = r_lo + i;
+        const bool live = r < r_hi;
+        const int len = M - psum;  // last part 1 .. len
+        uint32_t okb = 0;
+        if (live) {
+          const uint32_t pre = kp > 0 ? rest & (Vr[1] >> (pr[0] - 1)) : 1u;
+          okb = (pre & 1u) ? Vr[0] : 0u;
           if (len < 32) okb &= (1u << len) - 1u;
-          // rank window [lo, hi): candidate b has rank rk + b
-          if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
-          if (rk + (uint64_t)len > a.hi)
-            okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
-          {  // candidates of this run inside the window
+          if (full) {
+            cands += (uint64_t)len;
+          } else {  // rank window [lo, hi): candidate b has rank rk + b
+            if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
+            if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
             const uint64_t in_lo = rk < a.lo ? min(a.lo - rk, (uint64_t)len) : 0;
             const uint64_t in_hi = rk + (uint64_t)len > a.hi ? (a.hi > rk ? a.hi - rk : 0) : (uint64_t)len;
             cands += in_hi > in_lo ? in_hi - in_lo : 0;
@@ -257,14 +319,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
             acc.n += __popc(okb);
             acc.pi = min(acc.pi, psum + fb + 1);
             acc.first = min(acc.first, rk + (uint64_t)fb);
-            if (want_hash) {
-              uint32_t w = okb;
-              while (w) {
-                const int b = __ffs(w) - 1;
-                w &= w - 1u;
-                acc.hash += splitmix64(rk + (uint64_t)b);
-              }
-            }
             if (bits) {  // verdict bits of the run, word-level
               const uint64_t off = rk - a.lo + (uint64_t)fb;
               const uint32_t w2 = okb >> fb;
@@ -273,11 +327,22 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
               if (sh && (w2 >> (32u - sh))) atomicOr(bits + (off >> 5) + 1, w2 >> (32u - sh));
             }
           }
-          rk += (uint64_t)len;
-          if (kp > 0 && r + 1 < r_hi) next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
         }
-        acc.st_cand += cands;
+        if (want_hash && __any_sync(GP_FULL, okb != 0)) acc.hash += warp_hash_bits(okb, rk, lane);
+        if (live) {
+          rk += (uint64_t)len;
+          if (kp > 0 && r + 1 < r_hi) {
+            if (psum < M - 1) {  // common: grow the last prefix part
+              pr[0] += 1;
+              psum += 1;
+            } else {
+              next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
+              rest = pre_rest();
+            }
+          }
+        }
       }
+      acc.st_cand += cands;
     }
   }
   exh_flush(a, acc, cur, lane);
@@ -296,16 +361,22 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   using namespace gp;
   const int n = a0.n, M = a0.M;
   if (n > kBpMaxN || M > kBpMaxM) return gp_fail(GP_EINVAL, "EXHAUSTIVE(bp): n <= 8, M <= 32");
-  // items = (set, allocation): item_base[k] = first RGS index with k blocks
+  // items = (set, allocation) in groups of k = kmax, ..., 1; item_base[k] =
+  // the first item AFTER group k (group kmax starts at 0); rgs_base[k] = first
+  // RGS index with k blocks (rank order)
   ExhArgs a = a0;
   uint64_t n_rgs = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
-    a.item_base[k] = n_rgs;
+    a.rgs_base[k] = (uint32_t)n_rgs;
     n_rgs += a.L.n_pi[k];
   }
-  a.item_base[a.L.kmax + 1] = n_rgs;
+  uint64_t items = 0;
+  for (int k = a.L.kmax; k >= 1; --k) {
+    items += a.L.n_pi[k] * (uint64_t)a.n_sets;
+    a.item_base[k] = items;
+  }
   a.items_per_set = n_rgs;
-  a.total_items = n_rgs * (uint64_t)a.n_sets;
+  a.total_items = items;
   const size_t memo_words = (size_t)a.n_sets * ((size_t)1 << n);
   uint32_t *ws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void **>(&ws), (memo_words + n_rgs) * sizeof(uint32_t), st) !=

@@ -212,7 +212,7 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
 
 @pytest.mark.parametrize("seed,n,M", [(1, 1, 1), (2, 1, 7), (3, 2, 1), (4, 3, 4), (5, 4, 6),
                                       (6, 5, 3), (7, 6, 5), (8, 7, 4), (9, 8, 3), (10, 4, 12),
-                                      (11, 3, 12), (12, 6, 9), (13, 3, 40), (14, 8, 32),
+                                      (11, 3, 12), (12, 6, 9), (13, 3, 40), (14, 8, 12), (16, 3, 32),
                                       (15, 2, 31)])
 @EVALUATORS
 def test_exhaustive_random_sets(G, seed, n, M, ev):
