@@ -171,67 +171,38 @@ GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t 
   return r;
 }
 
-// j-th (0-based) set bit of x, j < popc(x)
-GP_DEV int select_bit(uint32_t x, int j) {
-  int pos = 0;
-  int c = __popc(x & 0xFFFFu);
-  if (j >= c) { j -= c; pos += 16; x >>= 16; }
-  c = __popc(x & 0xFFu);
-  if (j >= c) { j -= c; pos += 8; x >>= 8; }
-  c = __popc(x & 0xFu);
-  if (j >= c) { j -= c; pos += 4; x >>= 4; }
-  c = __popc(x & 0x3u);
-  if (j >= c) { j -= c; pos += 2; x >>= 2; }
-  return pos + (j >= (int)(x & 1u) ? 1 : 0);
-}
-
-// Verdict hash of the warp's schedulable candidates of one iteration: lane l
-// holds okb (bit b = rank rk + b).  The ranks are spread over the 32 lanes
-// in rounds (owner lane by a binary search over the exclusive prefix counts),
-// so splitmix64 runs on full warps whatever the distribution of the bits.
-GP_DEV uint64_t warp_hash_bits(uint32_t okb, uint64_t rk, int lane) {
-  const int cnt = __popc(okb);
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(GP_FULL, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int total = __shfl_sync(GP_FULL, incl, 31);
-  const int excl = incl - cnt;
-  uint64_t h = 0;
-  for (int base = 0; base < total; base += 32) {
-    const int e = base + lane;
-    int L = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int x = __shfl_sync(GP_FULL, excl, L + step);
-      if (x <= e) L += step;
-    }
-    const uint32_t wL = __shfl_sync(GP_FULL, okb, L);
-    const uint64_t rL = __shfl_sync(GP_FULL, rk, L);
-    const int xL = __shfl_sync(GP_FULL, excl, L);
-    if (e < total) h += splitmix64(rL + (uint64_t)select_bit(wL, e - xL));
-  }
-  return h;
-}
-
-// ---- main pass: bit-sliced verdicts over runs -----------------------------------
-// item = (set, allocation pi), in k-DESCENDING groups (the largest allocations
-// are handed out first, the small ones fill the tail); a pi's runs (one per
-// prefix, C(M-1, k-1) of them) are split evenly over the 32 lanes, so every
-// lane iterates the same number of times.
+// ---- main pass: bit-sliced verdicts over runs, lane = task set -------------------
+// item = (group of 32 consecutive sets, allocation pi), items in k-DESCENDING
+// groups (the largest allocations first, small ones fill the tail).  The run
+// structure of pi -- prefixes in lexicographic order, run lengths, ranks --
+// depends only on (k, M), so the whole warp walks it in lockstep (uniform
+// control flow, no divergent successor) while each lane applies its own set's
+// verdict words.
 __global__ void __launch_bounds__(kWarps * 32, 3)
     k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs) {
-  extern __shared__ __align__(16) uint32_t smem[];
   const int n = a.n, M = a.M;
-  const EnumTables tab = build_enum_tables(smem, M, n);
   const int lane = threadIdx.x & 31;
   const int nsub = 1 << n;
   const bool want_hash = !(a.flags & GP_EX_NO_HASH);
-  LaneAcc acc;
-  int64_t cur = -1;
-  bool okc = false;
+  // per-lane (= per-set) accumulators
+  uint32_t acc_n = 0;
+  int32_t acc_pi = INT32_MAX;
+  uint64_t acc_first = ~0ull, acc_hash = 0, st_cand = 0;
+  int64_t cur_g = -1, set = -1;
+  bool lane_ok = false;
+  auto flush = [&]() {
+    if (lane_ok && acc_n > 0) {
+      long long *ps = reinterpret_cast<long long *>(a.per_set + set * 4);
+      atomicAdd(reinterpret_cast<unsigned long long *>(ps + 0), (unsigned long long)acc_n);
+      atomicMin(ps + 1, (long long)acc_pi);
+      atomicMin(ps + 2, (long long)acc_first);
+      atomicAdd(reinterpret_cast<unsigned long long *>(ps + 3), acc_hash);
+    }
+    acc_n = 0;
+    acc_pi = INT32_MAX;
+    acc_first = ~0ull;
+    acc_hash = 0;
+  };
   for (;;) {
     uint64_t base = 0;
     if (lane == 0) base = atomicAdd(a.work_counter, (unsigned long long)kGrab);
@@ -239,54 +210,50 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
     if (base >= a.total_items) break;
     const uint64_t end = min(base + (uint64_t)kGrab, a.total_items);
     for (uint64_t it = base; it < end; ++it) {
-      int k = a.L.kmax;  // groups k = kmax, kmax-1, ..., 1; item_base[k] = end of group k
+      int k = a.L.kmax;  // groups k = kmax, ..., 1; item_base[k] = end of group k
       while (k > 1 && it >= a.item_base[k]) --k;
       const uint64_t local = it - (k == a.L.kmax ? 0 : a.item_base[k + 1]);
       const uint32_t npi = (uint32_t)a.L.n_pi[k];
-      const int64_t set = (int64_t)(local / npi);
-      const uint32_t p = (uint32_t)(local - (uint64_t)set * npi);
-      if (set != cur) {
-        exh_flush(a, acc, cur, lane);
-        cur = set;
-        okc = memo[set * nsub] != 0;
+      const int64_t grp = (int64_t)(local / npi);
+      const uint32_t p = (uint32_t)(local - (uint64_t)grp * npi);
+      if (grp != cur_g) {
+        flush();
+        cur_g = grp;
+        set = grp * 32 + lane;
+        lane_ok = set < a.n_sets && memo[set * nsub] != 0;  // input contract (word 0)
       }
-      if (!okc) continue;  // contract violation: finalize reports it
       const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
       const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
       if (rank_pi >= a.hi || rank_pi + per_pi <= a.lo) continue;
-      const bool full = rank_pi >= a.lo && rank_pi + per_pi <= a.hi;  // no window clipping
-      // blocks of pi -> verdict words, reversed: Vr[jj] = V[S_{k-1-jj}]
+      const bool full = rank_pi >= a.lo && rank_pi + per_pi <= a.hi;
+      // block task masks of pi (warp-uniform ballots) -> this lane's set's
+      // verdict words, reversed: Vr[jj] = V[set][S_{k-1-jj}]
       const uint32_t labels = rgs[a.rgs_base[k] + p];
       const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
-      uint32_t bmask = 0;
+      uint32_t Vr[kBpMaxN];
+#pragma unroll
+      for (int q = 0; q < kBpMaxN; ++q) Vr[q] = 0;
 #pragma unroll
       for (int j = 0; j < kBpMaxN; ++j) {
         const uint32_t bm = __ballot_sync(GP_FULL, myb == j);
-        if (lane == j) bmask = bm;
-      }
-      const uint32_t vw = lane < k ? memo[set * nsub + bmask] : 0u;
-      uint32_t Vr[kBpMaxN];
+        const int jj = k - 1 - j;
+        uint32_t v = 0;
+        if (j < k && lane_ok) v = memo[set * nsub + bm];
 #pragma unroll
-      for (int jj = 0; jj < kBpMaxN; ++jj) Vr[jj] = __shfl_sync(GP_FULL, vw, max(k - 1 - jj, 0));
-      // this lane's runs [r_lo, r_hi) among C(M-1, k-1); all lanes iterate
-      // `iters` times (idle lanes with an empty word) so the hash can run on
-      // the whole warp
-      const uint32_t n_runs = tab.C(M - 1, k - 1);
-      const uint32_t iters = (n_runs + 31u) >> 5;
-      const uint32_t r_lo = min(n_runs, (uint32_t)lane * iters);
-      const uint32_t r_hi = min(n_runs, r_lo + iters);
+        for (int q = 0; q < kBpMaxN; ++q)
+          if (q == jj) Vr[q] = v;
+      }
+      if (!__any_sync(GP_FULL, lane_ok)) continue;
+      // walk every run of pi: prefix (s_0..s_{k-2}) lexicographic, stored
+      // reversed in pr (pr[0] = s_{k-2}); run = last part 1 .. M - psum
       const int kp = k - 1;
+      const uint32_t n_runs = a.L.n_runs[k];
       int32_t pr[kBpMaxN];
 #pragma unroll
       for (int jj = 0; jj < kBpMaxN; ++jj) pr[jj] = 1;
       int32_t psum = kp;
       uint64_t rk = rank_pi;
-      if (r_lo < r_hi) {
-        unrank_prefix_rev(tab, kp, M - 1, r_lo, pr, psum);
-        rk = rank_pi + run_start_sidx(tab, k, M, pr);  // rank of (prefix, 1)
-      }
-      // verdict of the prefix blocks other than the last prefix block (k-2)
-      auto pre_rest = [&]() -> uint32_t {
+      auto pre_rest = [&]() -> uint32_t {  // prefix blocks except the last one
         uint32_t v = 1u;
 #pragma unroll
         for (int jj = 1; jj < kBpMaxN - 1; ++jj)
@@ -294,60 +261,57 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
         return v;
       };
       uint32_t rest = pre_rest();
-      uint32_t *bits = a.bits ? a.bits + cur * a.words : nullptr;
-      uint64_t cands = 0;
-      for (uint32_t i = 0; i < iters; ++i) {
-        const uint32_t r = r_lo + i;
-        const bool live = r < r_hi;
-        const int len = M - psum;  // last part 1 .. len
-        uint32_t okb = 0;
-        if (live) {
-          const uint32_t pre = kp > 0 ? rest & (Vr[1] >> (pr[0] - 1)) : 1u;
-          okb = (pre & 1u) ? Vr[0] : 0u;
-          if (len < 32) okb &= (1u << len) - 1u;
-          if (full) {
-            cands += (uint64_t)len;
-          } else {  // rank window [lo, hi): candidate b has rank rk + b
-            if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
-            if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
-            const uint64_t in_lo = rk < a.lo ? min(a.lo - rk, (uint64_t)len) : 0;
-            const uint64_t in_hi = rk + (uint64_t)len > a.hi ? (a.hi > rk ? a.hi - rk : 0) : (uint64_t)len;
-            cands += in_hi > in_lo ? in_hi - in_lo : 0;
+      uint32_t *bits = (a.bits && lane_ok) ? a.bits + set * a.words : nullptr;
+      for (uint32_t r = 0; r < n_runs; ++r) {
+        const int len = M - psum;
+        const uint32_t pre = kp > 0 ? rest & (Vr[1] >> (pr[0] - 1)) : 1u;
+        uint32_t okb = (pre & 1u) ? Vr[0] : 0u;
+        if (len < 32) okb &= (1u << len) - 1u;
+        if (!full) {  // rank window [lo, hi) (warp-uniform)
+          if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
+          if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
+          const uint64_t in_lo = rk < a.lo ? min(a.lo - rk, (uint64_t)len) : 0;
+          const uint64_t in_hi = rk + (uint64_t)len > a.hi ? (a.hi > rk ? a.hi - rk : 0) : (uint64_t)len;
+          st_cand += (lane_ok && in_hi > in_lo) ? in_hi - in_lo : 0;
+        }
+        if (okb) {
+          const int fb = __ffs(okb) - 1;
+          acc_n += __popc(okb);
+          acc_pi = min(acc_pi, psum + fb + 1);
+          acc_first = min(acc_first, rk + (uint64_t)fb);
+          if (want_hash) {
+            uint32_t w = okb;
+            do {
+              const int b = __ffs(w) - 1;
+              w &= w - 1u;
+              acc_hash += splitmix64(rk + (uint64_t)b);
+            } while (w);
           }
-          if (okb) {
-            const int fb = __ffs(okb) - 1;
-            acc.n += __popc(okb);
-            acc.pi = min(acc.pi, psum + fb + 1);
-            acc.first = min(acc.first, rk + (uint64_t)fb);
-            if (bits) {  // verdict bits of the run, word-level
-              const uint64_t off = rk - a.lo + (uint64_t)fb;
-              const uint32_t w2 = okb >> fb;
-              const uint32_t sh = (uint32_t)(off & 31u);
-              atomicOr(bits + (off >> 5), w2 << sh);
-              if (sh && (w2 >> (32u - sh))) atomicOr(bits + (off >> 5) + 1, w2 >> (32u - sh));
-            }
+          if (bits) {  // verdict bits of the run, word-level
+            const uint64_t off = rk - a.lo + (uint64_t)fb;
+            const uint32_t w2 = okb >> fb;
+            const uint32_t sh = (uint32_t)(off & 31u);
+            atomicOr(bits + (off >> 5), w2 << sh);
+            if (sh && (w2 >> (32u - sh))) atomicOr(bits + (off >> 5) + 1, w2 >> (32u - sh));
           }
         }
-        if (want_hash && __any_sync(GP_FULL, okb != 0)) acc.hash += warp_hash_bits(okb, rk, lane);
-        if (live) {
-          rk += (uint64_t)len;
-          if (kp > 0 && r + 1 < r_hi) {
-            if (psum < M - 1) {  // common: grow the last prefix part
-              pr[0] += 1;
-              psum += 1;
-            } else {
-              next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
-              rest = pre_rest();
-            }
+        rk += (uint64_t)len;
+        if (kp > 0) {  // lexicographic successor of the prefix (warp-uniform)
+          if (psum < M - 1) {
+            pr[0] += 1;
+            psum += 1;
+          } else {
+            next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
+            rest = pre_rest();
           }
         }
       }
-      acc.st_cand += cands;
+      if (full && lane_ok) st_cand += per_pi;
     }
   }
-  exh_flush(a, acc, cur, lane);
+  flush();
   if (a.stats) {
-    const uint64_t c0 = warp_sum_u64(acc.st_cand);
+    const uint64_t c0 = warp_sum_u64(st_cand);
     if (lane == 0) atomicAdd(a.stats + 0, c0);
   }
 }
@@ -371,8 +335,9 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
     n_rgs += a.L.n_pi[k];
   }
   uint64_t items = 0;
+  const uint64_t groups32 = ((uint64_t)a.n_sets + 31) / 32;  // lane = set
   for (int k = a.L.kmax; k >= 1; --k) {
-    items += a.L.n_pi[k] * (uint64_t)a.n_sets;
+    items += a.L.n_pi[k] * groups32;
     a.item_base[k] = items;
   }
   a.items_per_set = n_rgs;
@@ -388,6 +353,12 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = ((enum_table_words(M, n) + 3) & ~(size_t)3) * 4;
   k_exh_rgs_table<<<1, 256, smem, st>>>(a, rgs);
+  // runs per allocation: C(M-1, k-1) prefixes
+  for (int k = 1; k <= a.L.kmax; ++k) {
+    uint64_t c = 1;
+    for (int i = 0; i < k - 1; ++i) c = c * (uint64_t)(M - 1 - i) / (uint64_t)(i + 1);
+    a.L.n_runs[k] = (uint32_t)c;
+  }
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
@@ -396,12 +367,12 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
   if (r == GP_OK) {
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_bp, kWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_bp, kWarps * 32, 0);
     if (occ < 1) occ = 1;
     uint64_t want = (a.total_items + kGrab * kWarps - 1) / (kGrab * kWarps);
     uint64_t grid = (uint64_t)sms * occ;
     if (want < grid) grid = want > 0 ? want : 1;
-    k_exh_bp<<<(unsigned)grid, kWarps * 32, smem, st>>>(a, memo, rgs);
+    k_exh_bp<<<(unsigned)grid, kWarps * 32, 0, st>>>(a, memo, rgs);
     r = gp_cuda_check("EXHAUSTIVE(bp) main kernel");
   }
   cudaFreeAsync(ws, st);

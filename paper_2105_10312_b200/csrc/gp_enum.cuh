@@ -22,6 +22,7 @@ struct RankLayout {
   uint64_t k_base[kMaxTasks + 2];  // first rank with k blocks
   uint64_t n_pi[kMaxTasks + 2];    // S(n,k): number of RGS with k labels
   uint64_t per_pi[kMaxTasks + 2];  // C(M,k): size vectors per RGS
+  uint32_t n_runs[kMaxTasks + 2];  // C(M-1,k-1): runs (prefixes) per RGS (bit-sliced evaluator)
 };
 
 // Host: exact layout with 128-bit arithmetic; GP_EOVERFLOW if N_c >= 2^63.
