@@ -29,26 +29,35 @@ namespace gp {
 constexpr int kBpMaxN = 8;   // tasks per set (2^8 subset words per set)
 constexpr int kBpMaxM = 32;  // sizes per verdict word
 
-// ---- pre-pass: V[set][S] for every subset S, one warp per set, lane = size --
+// ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
+// The (subset, size) pairs of a set are spread over the lanes (C3: 63 x 20 =
+// 1,260 pairs, 40 per lane); the verdict bits meet in a shared-memory word per
+// subset and are written out once.
+template <int NT>
 __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *memo) {
-  const int lane = threadIdx.x & 31;
+  __shared__ uint32_t vs_all[8][1 << kBpMaxN];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t *vs = vs_all[wid];
   const int n = a.n, M = a.M;
   const int nsub = 1 << n;
+  const int npairs = (nsub - 1) * M;
   uint64_t st_tests = 0, st_tasks = 0;
   uint32_t st_events = 0;
   for (int64_t set = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < a.n_sets;
        set += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t H = set_contract(a, set);
     uint32_t *V = memo + set * nsub;
-    if (lane == 0) V[0] = H > 0 ? 1u : 0u;  // word 0: the set's input contract
-    if (H <= 0) continue;
+    if (H <= 0) {
+      if (lane == 0) V[0] = 0u;  // word 0: the set's input contract
+      continue;
+    }
     const int32_t H32 = (int32_t)H;
-    // task i's fields in registers of every lane (n <= 8)
-    int32_t T[kBpMaxN], D[kBpMaxN], B[kBpMaxN], cn[kBpMaxN], cc[kBpMaxN], fn[kBpMaxN],
-        fc[kBpMaxN], q[kBpMaxN];
+    for (int S = lane; S < nsub; S += 32) vs[S] = 0u;
+    // task i's fields in registers of every lane (n <= NT)
+    int32_t T[NT], D[NT], B[NT], cn[NT], cc[NT], fn[NT], fc[NT], q[NT];
     uint32_t mem = 0;
 #pragma unroll
-    for (int i = 0; i < kBpMaxN; ++i) {
+    for (int i = 0; i < NT; ++i) {
       const bool v = i < n;
       const int64_t o = set * n + (v ? i : 0);
       T[i] = v ? a.T[o] : INT32_MAX;
@@ -61,43 +70,45 @@ __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *mem
       q[i] = v ? (int32_t)(H / T[i]) : 0;
       mem |= (v && a.type[o] == 1) ? 1u << i : 0u;
     }
-    const int32_t m = lane + 1;  // this lane's size
-    for (int S = 1; S < nsub; ++S) {
+    __syncwarp();
+    for (int pq = lane; pq < npairs; pq += 32) {
+      const int S = pq / M + 1;
+      const int32_t m = pq - (S - 1) * M + 1;
+      const int cnt = __popc((unsigned)S);
+      int32_t C[NT], Dv[NT], Tv[NT], qv[NT];
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const bool in = (S >> i) & 1;
+        const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
+        const bool x = __popc((unsigned)S & same) > 1;  // conflict
+        C[i] = in ? (x ? wcet_sat(B[i], cc[i], fc[i], m) : wcet_sat(B[i], cn[i], fn[i], m)) : 0;
+        Dv[i] = in ? D[i] : INT32_MAX;
+        Tv[i] = in ? T[i] : INT32_MAX;
+        qv[i] = in ? q[i] : 0;
+        bad |= C[i] > Dv[i];
+      }
+      ++st_tests;
+      st_tasks += cnt;
       bool ok = false;
-      if (m <= M) {
-        const int cnt = __popc((unsigned)S);
-        int32_t C[kBpMaxN], Dv[kBpMaxN], Tv[kBpMaxN], qv[kBpMaxN];
-        bool bad = false;
+      if (!bad) {
+        if (cnt == 1) {
+          ok = true;  // a single task: C <= D decides (gp_edf.cuh shortcut 1)
+        } else {
+          int32_t UH = 0;
 #pragma unroll
-        for (int i = 0; i < kBpMaxN; ++i) {
-          const bool in = (S >> i) & 1;
-          const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
-          const bool x = __popc((unsigned)S & same) > 1;  // conflict
-          C[i] = in ? (x ? wcet_sat(B[i], cc[i], fc[i], m) : wcet_sat(B[i], cn[i], fn[i], m)) : 0;
-          Dv[i] = in ? D[i] : INT32_MAX;
-          Tv[i] = in ? T[i] : INT32_MAX;
-          qv[i] = in ? q[i] : 0;
-          bad |= C[i] > Dv[i];
-        }
-        ++st_tests;
-        st_tasks += cnt;
-        if (!bad) {
-          if (cnt == 1) {
-            ok = true;  // a single task: C <= D decides (gp_edf.cuh shortcut 1)
-          } else {
-            int32_t UH = 0;
-#pragma unroll
-            for (int i = 0; i < kBpMaxN; ++i) UH += C[i] * qv[i];
-            if (UH <= H32) {
-              const int32_t lcut = pdc_cutoff<kBpMaxN>(C, Dv, Tv, qv, H32, UH);
-              ok = pdc_walk<kBpMaxN>(C, Dv, Tv, lcut, st_events);
-            }
+          for (int i = 0; i < NT; ++i) UH += C[i] * qv[i];
+          if (UH <= H32) {
+            const int32_t lcut = pdc_cutoff<NT>(C, Dv, Tv, qv, H32, UH);
+            ok = pdc_walk<NT>(C, Dv, Tv, lcut, st_events);
           }
         }
       }
-      const uint32_t word = __ballot_sync(GP_FULL, ok);
-      if (lane == (S & 31)) V[S] = word;
+      if (ok) atomicOr(&vs[S], 1u << (m - 1));
     }
+    __syncwarp();
+    for (int S = lane; S < nsub; S += 32) V[S] = S == 0 ? 1u : vs[S];
+    __syncwarp();
   }
   if (a.stats) {
     const uint64_t t0 = warp_sum_u64(st_tests), t1 = warp_sum_u64(st_tasks);
@@ -205,11 +216,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
   };
   for (;;) {
     uint64_t base = 0;
-    if (lane == 0) base = atomicAdd(a.work_counter, (unsigned long long)kGrab);
+    if (lane == 0) base = atomicAdd(a.work_counter, 1ull);  // items are large: one per grab
     base = __shfl_sync(GP_FULL, base, 0);
     if (base >= a.total_items) break;
-    const uint64_t end = min(base + (uint64_t)kGrab, a.total_items);
-    for (uint64_t it = base; it < end; ++it) {
+    {
+      const uint64_t it = base;
       int k = a.L.kmax;  // groups k = kmax, ..., 1; item_base[k] = end of group k
       while (k > 1 && it >= a.item_base[k]) --k;
       const uint64_t local = it - (k == a.L.kmax ? 0 : a.item_base[k + 1]);
@@ -362,14 +373,17 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-    k_exh_memo<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, st>>>(a, memo);
+    const unsigned g = (unsigned)(blocks > 0 ? blocks : 1);
+    if (n <= 4) k_exh_memo<4><<<g, 256, 0, st>>>(a, memo);
+    else if (n <= 6) k_exh_memo<6><<<g, 256, 0, st>>>(a, memo);
+    else k_exh_memo<8><<<g, 256, 0, st>>>(a, memo);
   }
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
   if (r == GP_OK) {
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_bp, kWarps * 32, 0);
     if (occ < 1) occ = 1;
-    uint64_t want = (a.total_items + kGrab * kWarps - 1) / (kGrab * kWarps);
+    uint64_t want = (a.total_items + kWarps - 1) / kWarps;
     uint64_t grid = (uint64_t)sms * occ;
     if (want < grid) grid = want > 0 ? want : 1;
     k_exh_bp<<<(unsigned)grid, kWarps * 32, 0, st>>>(a, memo, rgs);
