@@ -182,6 +182,70 @@ GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t 
   return r;
 }
 
+// ---- verdict-hash prefix table: P[r] = sum_{x < r} splitmix64(x) mod 2^64 -------
+// The hash of a set is sum of splitmix64(rank) over its schedulable ranks; a run
+// segment of consecutive ranks [r0, r1) then contributes P[r1] - P[r0] (exact in
+// mod-2^64 arithmetic), so the main pass needs two table reads per contiguous
+// range of schedulable candidates instead of one splitmix64 per candidate.
+constexpr int kScanBlock = 1024;
+constexpr uint32_t kMaxHashTable = 1u << 24;  // ranks per set covered by the table
+
+GP_DEV uint64_t block_incl_scan_u64(uint64_t v, uint64_t *wsum) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t u = __shfl_up_sync(GP_FULL, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) wsum[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t u = __shfl_up_sync(GP_FULL, w, o);
+      if (lane >= o) w += u;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  return v + (wid > 0 ? wsum[wid - 1] : 0ull);
+}
+
+// pass 1: P[r + 1] = inclusive sum within the block; block totals
+__global__ void __launch_bounds__(kScanBlock) k_hash_scan_local(uint64_t *P, uint64_t n_ranks,
+                                                                uint64_t *btot) {
+  __shared__ uint64_t wsum[32];
+  const uint64_t r = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  const uint64_t v = r < n_ranks ? splitmix64(r) : 0ull;
+  const uint64_t incl = block_incl_scan_u64(v, wsum);
+  if (r < n_ranks) P[r + 1] = incl;
+  if (threadIdx.x == kScanBlock - 1) btot[blockIdx.x] = incl;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P[0] = 0ull;
+}
+
+// pass 2 (one block): exclusive scan of the block totals, in place
+__global__ void __launch_bounds__(kScanBlock) k_hash_scan_blocks(uint64_t *btot, uint32_t nb) {
+  __shared__ uint64_t wsum[32];
+  uint64_t carry = 0;
+  for (uint32_t b0 = 0; b0 < nb; b0 += kScanBlock) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint64_t v = b < nb ? btot[b] : 0ull;
+    const uint64_t incl = block_incl_scan_u64(v, wsum);
+    if (b < nb) btot[b] = carry + incl - v;
+    __syncthreads();
+    carry += wsum[31];
+    __syncthreads();
+  }
+}
+
+// pass 3: add each block's offset
+__global__ void __launch_bounds__(kScanBlock) k_hash_scan_add(uint64_t *P, uint64_t n_ranks,
+                                                              const uint64_t *btot) {
+  const uint64_t r = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  if (r < n_ranks) P[r + 1] += btot[blockIdx.x];
+}
+
 // ---- main pass: bit-sliced verdicts over runs, lane = task set -------------------
 // item = (group of 32 consecutive sets, allocation pi), items in k-DESCENDING
 // groups (the largest allocations first, small ones fill the tail).  The run
@@ -190,7 +254,7 @@ GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t 
 // control flow, no divergent successor) while each lane applies its own set's
 // verdict words.
 __global__ void __launch_bounds__(kWarps * 32, 3)
-    k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs) {
+    k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs, const uint64_t *P) {
   const int n = a.n, M = a.M;
   const int lane = threadIdx.x & 31;
   const int nsub = 1 << n;
@@ -292,11 +356,21 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
           acc_first = min(acc_first, rk + (uint64_t)fb);
           if (want_hash) {
             uint32_t w = okb;
-            do {
-              const int b = __ffs(w) - 1;
-              w &= w - 1u;
-              acc_hash += splitmix64(rk + (uint64_t)b);
-            } while (w);
+            if (P) {  // contiguous ranges of schedulable ranks: P[r1] - P[r0]
+              do {
+                const int b0 = __ffs(w) - 1;
+                const uint32_t t = ~(w >> b0);
+                const int b1 = t ? b0 + __ffs(t) - 1 : 32;
+                acc_hash += P[rk + (uint64_t)b1] - P[rk + (uint64_t)b0];
+                w &= b1 >= 32 ? 0u : ~0u << b1;
+              } while (w);
+            } else {
+              do {
+                const int b = __ffs(w) - 1;
+                w &= w - 1u;
+                acc_hash += splitmix64(rk + (uint64_t)b);
+              } while (w);
+            }
           }
           if (bits) {  // verdict bits of the run, word-level
             const uint64_t off = rk - a.lo + (uint64_t)fb;
@@ -354,11 +428,23 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   a.items_per_set = n_rgs;
   a.total_items = items;
   const size_t memo_words = (size_t)a.n_sets * ((size_t)1 << n);
+  // hash prefix table over the rank space (when it is small enough and wanted)
+  const bool use_P = !(a.flags & GP_EX_NO_HASH) && a.L.total < kMaxHashTable;
+  const uint64_t n_ranks = use_P ? a.L.total : 0;
+  const uint32_t nb = (uint32_t)((n_ranks + kScanBlock - 1) / kScanBlock);
+  const size_t words32 = (memo_words + n_rgs + 1) & ~(size_t)1;  // 8-byte alignment after
+  const size_t bytes = words32 * 4 + (use_P ? (n_ranks + 1 + nb) * 8 : 0);
   uint32_t *ws = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void **>(&ws), (memo_words + n_rgs) * sizeof(uint32_t), st) !=
-      cudaSuccess)
+  if (cudaMallocAsync(reinterpret_cast<void **>(&ws), bytes, st) != cudaSuccess)
     return gp_cuda_check("EXHAUSTIVE(bp): workspace allocation");
   uint32_t *memo = ws, *rgs = ws + memo_words;
+  uint64_t *P = use_P ? reinterpret_cast<uint64_t *>(ws + words32) : nullptr;
+  if (use_P) {
+    uint64_t *btot = P + n_ranks + 1;
+    k_hash_scan_local<<<nb, kScanBlock, 0, st>>>(P, n_ranks, btot);
+    k_hash_scan_blocks<<<1, kScanBlock, 0, st>>>(btot, nb);
+    k_hash_scan_add<<<nb, kScanBlock, 0, st>>>(P, n_ranks, btot);
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -386,7 +472,7 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
     uint64_t want = (a.total_items + kWarps - 1) / kWarps;
     uint64_t grid = (uint64_t)sms * occ;
     if (want < grid) grid = want > 0 ? want : 1;
-    k_exh_bp<<<(unsigned)grid, kWarps * 32, 0, st>>>(a, memo, rgs);
+    k_exh_bp<<<(unsigned)grid, kWarps * 32, 0, st>>>(a, memo, rgs, P);
     r = gp_cuda_check("EXHAUSTIVE(bp) main kernel");
   }
   cudaFreeAsync(ws, st);
