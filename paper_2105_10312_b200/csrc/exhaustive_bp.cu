@@ -435,6 +435,19 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   const size_t words32 = (memo_words + n_rgs + 1) & ~(size_t)1;  // 8-byte alignment after
   const size_t bytes = words32 * 4 + (use_P ? (n_ranks + 1 + nb) * 8 : 0);
   uint32_t *ws = nullptr;
+  {  // keep freed workspace in the device's default pool (no unmap/remap per call)
+    static int configured = -1;
+    int cur_dev = 0;
+    cudaGetDevice(&cur_dev);
+    if (configured != cur_dev) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, cur_dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      configured = cur_dev;
+    }
+  }
   if (cudaMallocAsync(reinterpret_cast<void **>(&ws), bytes, st) != cudaSuccess)
     return gp_cuda_check("EXHAUSTIVE(bp): workspace allocation");
   uint32_t *memo = ws, *rgs = ws + memo_words;
