@@ -327,7 +327,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
 #pragma unroll
       for (int jj = 0; jj < kBpMaxN; ++jj) pr[jj] = 1;
       int32_t psum = kp;
-      uint64_t rk = rank_pi;
       auto pre_rest = [&]() -> uint32_t {  // prefix blocks except the last one
         uint32_t v = 1u;
 #pragma unroll
@@ -335,63 +334,86 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
           if (jj < kp) v &= Vr[jj + 1] >> (pr[jj] - 1);
         return v;
       };
+      // candidates of pi inside the rank window (all evaluated, bit-sliced)
+      {
+        const uint64_t w_lo = max(a.lo, rank_pi), w_hi = min(a.hi, rank_pi + per_pi);
+        if (lane_ok) st_cand += w_hi > w_lo ? w_hi - w_lo : 0;
+      }
+      // a block never schedulable at any size: every candidate of pi fails
+      bool dead = !lane_ok;
+#pragma unroll
+      for (int jj = 0; jj < kBpMaxN; ++jj)
+        if (jj < k) dead |= Vr[jj] == 0u;
+      if (__all_sync(GP_FULL, dead)) continue;
       uint32_t rest = pre_rest();
       uint32_t *bits = (a.bits && lane_ok) ? a.bits + set * a.words : nullptr;
-      for (uint32_t r = 0; r < n_runs; ++r) {
-        const int len = M - psum;
-        const uint32_t pre = kp > 0 ? rest & (Vr[1] >> (pr[0] - 1)) : 1u;
-        uint32_t okb = (pre & 1u) ? Vr[0] : 0u;
-        if (len < 32) okb &= (1u << len) - 1u;
-        if (!full) {  // rank window [lo, hi) (warp-uniform)
-          if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
-          if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
-          const uint64_t in_lo = rk < a.lo ? min(a.lo - rk, (uint64_t)len) : 0;
-          const uint64_t in_hi = rk + (uint64_t)len > a.hi ? (a.hi > rk ? a.hi - rk : 0) : (uint64_t)len;
-          st_cand += (lane_ok && in_hi > in_lo) ? in_hi - in_lo : 0;
-        }
-        if (okb) {
-          const int fb = __ffs(okb) - 1;
-          acc_n += __popc(okb);
-          acc_pi = min(acc_pi, psum + fb + 1);
-          acc_first = min(acc_first, rk + (uint64_t)fb);
-          if (want_hash) {
-            uint32_t w = okb;
-            if (P) {  // contiguous ranges of schedulable ranks: P[r1] - P[r0]
-              do {
-                const int b0 = __ffs(w) - 1;
-                const uint32_t t = ~(w >> b0);
-                const int b1 = t ? b0 + __ffs(t) - 1 : 32;
-                acc_hash += P[rk + (uint64_t)b1] - P[rk + (uint64_t)b0];
-                w &= b1 >= 32 ? 0u : ~0u << b1;
-              } while (w);
-            } else {
-              do {
-                const int b = __ffs(w) - 1;
-                w &= w - 1u;
-                acc_hash += splitmix64(rk + (uint64_t)b);
-              } while (w);
+      uint32_t off = 0;  // s-index (within pi) of the current run's first candidate
+      uint32_t r = 0;
+      for (;;) {
+        // a sweep: the last prefix part grows from pr[0] while psum <= M - 1;
+        // run i of the sweep has last part 1 .. len_i, len_i = M - psum0 - i
+        const int psum0 = psum;
+        const int steps = kp > 0 ? M - psum0 : 1;
+        if (__any_sync(GP_FULL, (rest & 1u) != 0u)) {
+          uint32_t w1 = kp > 0 ? Vr[1] >> (pr[0] - 1) : 1u;  // bit i: block k-2 at pr[0] + i
+          const uint32_t live = 0u - (rest & 1u);
+          int len = M - psum0;
+          uint32_t lmask = len >= 32 ? ~0u : (1u << len) - 1u;
+          for (int i = 0; i < steps; ++i) {
+            uint32_t okb = Vr[0] & lmask & live & (0u - (w1 & 1u));
+            if (!full) {  // rank window [lo, hi) (warp-uniform)
+              const uint64_t rk = rank_pi + off;
+              if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
+              if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
             }
+            if (okb) {
+              const uint64_t rk = rank_pi + off;
+              const int fb = __ffs(okb) - 1;
+              acc_n += __popc(okb);
+              acc_pi = min(acc_pi, psum0 + i + fb + 1);
+              acc_first = min(acc_first, rk + (uint64_t)fb);
+              if (want_hash) {
+                uint32_t w = okb;
+                if (P) {  // contiguous ranges of schedulable ranks: P[r1] - P[r0]
+                  do {
+                    const int b0 = __ffs(w) - 1;
+                    const uint32_t t = ~(w >> b0);
+                    const int b1 = t ? b0 + __ffs(t) - 1 : 32;
+                    acc_hash += P[rk + (uint64_t)b1] - P[rk + (uint64_t)b0];
+                    w &= b1 >= 32 ? 0u : ~0u << b1;
+                  } while (w);
+                } else {
+                  do {
+                    const int b = __ffs(w) - 1;
+                    w &= w - 1u;
+                    acc_hash += splitmix64(rk + (uint64_t)b);
+                  } while (w);
+                }
+              }
+              if (bits) {  // verdict bits of the run, word-level
+                const uint64_t o2 = rk - a.lo + (uint64_t)fb;
+                const uint32_t w2 = okb >> fb;
+                const uint32_t sh = (uint32_t)(o2 & 31u);
+                atomicOr(bits + (o2 >> 5), w2 << sh);
+                if (sh && (w2 >> (32u - sh))) atomicOr(bits + (o2 >> 5) + 1, w2 >> (32u - sh));
+              }
+            }
+            off += (uint32_t)len;
+            len -= 1;
+            lmask >>= 1;
+            w1 >>= 1;
           }
-          if (bits) {  // verdict bits of the run, word-level
-            const uint64_t off = rk - a.lo + (uint64_t)fb;
-            const uint32_t w2 = okb >> fb;
-            const uint32_t sh = (uint32_t)(off & 31u);
-            atomicOr(bits + (off >> 5), w2 << sh);
-            if (sh && (w2 >> (32u - sh))) atomicOr(bits + (off >> 5) + 1, w2 >> (32u - sh));
-          }
+        } else {  // no set has its other prefix blocks schedulable: skip the sweep
+          off += (uint32_t)(steps * (M - psum0) - steps * (steps - 1) / 2);
         }
-        rk += (uint64_t)len;
-        if (kp > 0) {  // lexicographic successor of the prefix (warp-uniform)
-          if (psum < M - 1) {
-            pr[0] += 1;
-            psum += 1;
-          } else {
-            next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
-            rest = pre_rest();
-          }
-        }
+        r += (uint32_t)steps;
+        if (r >= n_runs) break;
+        // general successor of the prefix from (pr[0] + steps - 1, psum = M - 1)
+        pr[0] += steps - 1;
+        psum = M - 1;
+        next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
+        rest = pre_rest();
       }
-      if (full && lane_ok) st_cand += per_pi;
     }
   }
   flush();
