@@ -21,6 +21,7 @@ synchronize on both sides of the K timed steps, max over ranks.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -55,6 +56,8 @@ def parse():
     ap.add_argument("--f3", action="store_true",
                     help="use the subset-threshold evaluator (SURVEY §8(f) f3, a different work "
                          "unit, reported separately) instead of the direct per-candidate path")
+    ap.add_argument("--per-candidate", action="store_true",
+                    help="time the per-candidate EXHAUSTIVE evaluator instead of the bit-sliced one")
     ap.add_argument("--f3-hash", action="store_true",
                     help="with --f3, also enumerate the schedulable candidates for the verdict "
                          "hash (parity check; counts and ratios do not need it)")
@@ -86,6 +89,14 @@ def ncu_entry(workload):
         if isinstance(e, dict) and e.get("dram_bytes") is not None:
             return e, os.path.relpath(path, ROOT)
     return None, None
+
+
+def stirling2(n, k):
+    """Stirling numbers of the second kind (number of allocations with k blocks)."""
+    row = [1] + [0] * k
+    for i in range(1, n + 1):
+        row = [0] + [row[j - 1] + j * (row[j] if j < len(row) else 0) for j in range(1, k + 1)]
+    return row[k]
 
 
 def peak_lane_ops():
@@ -247,6 +258,8 @@ def main():
     alloc_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     exh_mode = G.GP_THRESHOLD if args.f3 else G.GP_EXHAUSTIVE
     exh_flags = G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0
+    if args.per_candidate:
+        exh_flags |= G.GP_EX_PER_CANDIDATE
     if args.f3 and not pipe.exhaustive:
         raise SystemExit("--f3 needs an exhaustive config (c2, c3)")
     dom_ev = []  # events around the dominant kernel's launches
@@ -292,6 +305,17 @@ def main():
     torch.cuda.synchronize()
     exh_stats = pipe.stats.cpu().numpy().tolist() if pipe.exhaustive else [0, 0, 0, 0]
     al_stats = alloc_stats.cpu().numpy().tolist()
+    # §8(d)'s per-candidate work (the direct evaluation's W lookups, utilisation
+    # passes and demand-walk events), counted by the per-candidate evaluator on
+    # the same sets (deterministic; untimed)
+    direct_stats = exh_stats
+    if pipe.exhaustive and not args.f3 and not args.per_candidate:
+        pst = torch.zeros(4, dtype=torch.int64, device="cuda")
+        G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, pipe.counts, slot0=0, n_slots=pipe.n_slots,
+                         setting=0, per_set=pipe.per_set, work_counter=pipe.work, stats=pst,
+                         stream=stream, flags=G.GP_EX_PER_CANDIDATE)
+        torch.cuda.synchronize()
+        direct_stats = pst.cpu().numpy().tolist()
     pipe.reset_counts()
     if world > 1:
         dist.barrier()
@@ -342,13 +366,30 @@ def main():
                  "deadlines_per_launch": st[2], "schedulable_enumerated_per_launch": st[3],
                  "ops_per_unit_is": "per set"}
     elif pipe.exhaustive:
-        st = exh_stats
+        # achieved = §8(d)'s per-candidate work x candidates (the direct
+        # evaluation's counters on the same sets); "executed" = the work of the
+        # evaluator that ran: for the bit-sliced one, the memo pass's EDF tests
+        # (3/task + 4/deadline) plus 4 word ops per run of candidates.
+        st = direct_stats
         ops = 3 * st[3] + 4 * st[2] + 4 * st[0]
         launches = 1
-        kname = f"k_exhaustive<{pipe.n if pipe.n > 3 else 3}>"
         per_unit = ops / max(st[0], 1)
-        extra = {"candidates_per_launch": st[0], "block_tests_per_launch": st[1],
-                 "deadlines_per_launch": st[2], "events_per_candidate": st[2] / max(st[0], 1)}
+        if args.per_candidate:
+            kname = f"k_exhaustive<{pipe.n if pipe.n > 3 else 3}> (per-candidate evaluator)"
+            ops_exec = ops
+        else:
+            kname = "k_exh_memo + k_exh_bp (bit-sliced evaluator)"
+            runs = pipe.ts.n_sets * sum(stirling2(pipe.n, k) * math.comb(pipe.M - 1, k - 1)
+                                        for k in range(1, min(pipe.n, pipe.M) + 1))
+            ops_exec = 3 * exh_stats[3] + 4 * exh_stats[2] + 4 * runs
+        extra = {"candidates_per_launch": st[0], "direct_block_tests": st[1],
+                 "direct_deadlines": st[2], "events_per_candidate": st[2] / max(st[0], 1),
+                 "ops_basis": "SURVEY 8(d) per-candidate work of the direct evaluation "
+                              "(3/task tested + 4/deadline examined + 4/candidate), counted by "
+                              "the per-candidate evaluator on the same sets",
+                 "executed": {"ops_per_step": float(ops_exec),
+                              "memo_edf_tests": exh_stats[1], "memo_deadlines": exh_stats[2],
+                              "frac": None}}
     else:
         st = al_stats
         ops = 3 * st[1] + 4 * st[2]
@@ -358,6 +399,8 @@ def main():
         extra = {"edf_tests_per_step": st[0], "tasks_tested_per_step": st[1],
                  "deadlines_per_step": st[2], "sets_per_step": st[3]}
     dom_s = sum(dom_ms) / args.steps / 1e3  # per step (sum of the dominant launches)
+    if "executed" in extra:
+        extra["executed"]["frac"] = extra["executed"]["ops_per_step"] / dom_s / peak
     prof, prof_src = (ncu_entry(wl["name"]) if pipe.exhaustive and not args.f3
                       else (None, None))
     traffic = prof["dram_bytes"] if prof else None
@@ -393,7 +436,7 @@ def main():
                    "l2": "flushed between steps (256 MiB memset outside the events)",
                    "seed": W.SEED},
         "roofline": roof,
-        "gpu_launches": launches_per_step(pipe) * args.steps,
+        "gpu_launches": launches_per_step(pipe, args) * args.steps,
         "clocks": clk,
     }
     if e2e:
@@ -407,9 +450,16 @@ def main():
     return 0
 
 
-def launches_per_step(pipe):
-    # per setting: gp_generate 1 + gp_allocate x V + ratio 1; + EXHAUSTIVE (init, main, finalize)
-    return len(pipe.gens) * (2 + len(pipe.variants)) + (3 if pipe.exhaustive else 0)
+def launches_per_step(pipe, args=None):
+    """Our kernels per step: per setting gp_generate 1 + gp_allocate x V + ratio 1;
+    + EXHAUSTIVE: per-candidate (init, main, finalize) or bit-sliced (init, RGS table,
+    memo, main, finalize, + 3 hash-prefix scan kernels when the hash is computed)."""
+    n = len(pipe.gens) * (2 + len(pipe.variants))
+    if not pipe.exhaustive:
+        return n
+    if (args is not None and (args.f3 or args.per_candidate)) or pipe.n > 8 or pipe.M > 32:
+        return n + 3
+    return n + 5 + (3 if pipe.n_cand < (1 << 24) else 0)
 
 
 def run_e2e(G, pipe, stream, args, world, evals_rank):
