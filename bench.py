@@ -114,12 +114,40 @@ def peak_lane_ops():
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms during the timed region."""
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML
+    polled every 2 ms from a thread (so even a ~30 ms region gets samples);
+    nvidia-smi -lms 200 as the fallback when pynvml is missing."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
+        self.rows, self.p, self.thread = [], None, None
+        try:
+            import threading
+
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            self.stop_ev = threading.Event()
+
+            def poll():
+                while True:
+                    sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, [bool(r & b) for b in bits]))
+                    if self.stop_ev.wait(0.002):
+                        break
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self.thread = None
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
@@ -129,30 +157,41 @@ class ClockSampler:
             self.p = None
 
     def stop(self):
-        if self.p is None:
-            return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.p.kill()
-        self.f.flush()
-        rows = []
-        with open(self.f.name) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
-                    rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
-            return None
-        sm = [float(r[1]) for r in rows]
-        mx = max(float(r[2]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        if self.thread is not None:
+            self.stop_ev.set()
+            self.thread.join(timeout=5)
+            rows = self.rows
+            if not rows:
+                return None
+            sm = [r[0] for r in rows]
+            mx = self.mx
+            reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[1][i]})
+            src = "nvml 2 ms"
+        else:
+            if self.p is None:
+                return None
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+            self.f.flush()
+            raw = []
+            with open(self.f.name) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                        raw.append(parts)
+            os.unlink(self.f.name)
+            if not raw:
+                return None
+            sm = [float(r[1]) for r in raw]
+            mx = max(float(r[2]) for r in raw)
+            reasons = sorted({self.NAMES[i] for r in raw for i in range(4) if r[5 + i].lower() == "active"})
+            src = "nvidia-smi 200 ms"
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(sm), "source": src}
 
 
 # --------------------------------------------------------------------------- CPU oracle
@@ -401,7 +440,8 @@ def main():
     dom_s = sum(dom_ms) / args.steps / 1e3  # per step (sum of the dominant launches)
     if "executed" in extra:
         extra["executed"]["frac"] = extra["executed"]["ops_per_step"] / dom_s / peak
-    prof, prof_src = (ncu_entry(wl["name"]) if pipe.exhaustive and not args.f3
+    prof, prof_src = (ncu_entry(wl["name"] + ("_per_candidate" if args.per_candidate else ""))
+                      if pipe.exhaustive and not args.f3
                       else (None, None))
     traffic = prof["dram_bytes"] if prof else None
     roof = {"bound": "alu", "achieved": ops / dom_s / 1e12, "peak": peak / 1e12,
