@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kScanBlock) k_hash_scan_add(uint64_t *P, uint6
 // depends only on (k, M), so the whole warp walks it in lockstep (uniform
 // control flow, no divergent successor) while each lane applies its own set's
 // verdict words.
-__global__ void __launch_bounds__(kWarps * 32, 3)
+__global__ void __launch_bounds__(kWarps * 32, 4)
     k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs, const uint64_t *P) {
   const int n = a.n, M = a.M;
   const int lane = threadIdx.x & 31;
