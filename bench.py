@@ -2,8 +2,9 @@
 """bench.py -- candidate (task set, partition, allocation) evals/s on B200.
 
 Default workload: C3 (BASELINE.json configs[2], the largest enumeration
-config): M = 20 SMs, n = 6 tasks, 10 utilisation bins x 1,000 task sets per
-GPU per step (weak scaling: every rank adds its own 10,000 sets), all
+config, its scaling size): M = 20 SMs, n = 6 tasks, 10 utilisation bins x
+10,000 task sets per GPU per step (weak scaling: every rank adds its own
+100,000 sets), all
 694,755 canonical candidates of every set evaluated exactly.  One step = the
 whole hot path: gp_generate -> gp_sched_ratio(EXHAUSTIVE) (enumerate + WCET +
 EDF fused) -> gp_allocate x {1G, SMS_ACT, SMS_INA, BF_ACT, BF_INA} ->
@@ -40,7 +41,7 @@ UNIT = "candidate evals/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 B200_SMS, SMSP_PER_SM, LANES = 148, 4, 32
 FALLBACK_SM_MHZ = 1965.0  # clocks.max.sm of B200 (B200_PROFILING.md)
-DEFAULT_REPS = {"c2": 1000, "c3": 1000, "c4": 2000, "c5": 1000}
+DEFAULT_REPS = {"c2": 10000, "c3": 10000, "c4": 20000, "c5": 10000}  # SURVEY §8(d) sizes
 
 
 def parse():
@@ -342,7 +343,7 @@ def main():
     alloc_stats.zero_()
     step(False, stats=True)
     torch.cuda.synchronize()
-    exh_stats = pipe.stats.cpu().numpy().tolist() if pipe.exhaustive else [0, 0, 0, 0]
+    exh_stats = pipe.stats.cpu().numpy().tolist() if pipe.exhaustive else [0] * 6
     al_stats = alloc_stats.cpu().numpy().tolist()
     # §8(d)'s per-candidate work (the direct evaluation's W lookups, utilisation
     # passes and demand-walk events), counted by the per-candidate evaluator on
@@ -415,12 +416,16 @@ def main():
         per_unit = ops / max(st[0], 1)
         if args.per_candidate:
             kname = f"k_exhaustive<{pipe.n if pipe.n > 3 else 3}> (per-candidate evaluator)"
-            ops_exec = ops
+            ops_exec, runs = ops, None
         else:
             kname = "k_exh_memo + k_exh_bp (bit-sliced evaluator)"
             runs = pipe.ts.n_sets * sum(stirling2(pipe.n, k) * math.comb(pipe.M - 1, k - 1)
                                         for k in range(1, min(pipe.n, pipe.M) + 1))
-            ops_exec = 3 * exh_stats[3] + 4 * exh_stats[2] + 4 * runs
+            # memo EDF tests (3/task + 4/deadline) + 2 ops per (set, run) walked (verdict
+            # word AND, zero test) + 6 per live run (count, pi* min, first min, two
+            # hash-table reads, difference-add)
+            ops_exec = (3 * exh_stats[3] + 4 * exh_stats[2] + 2 * exh_stats[4]
+                        + 6 * exh_stats[5])
         extra = {"candidates_per_launch": st[0], "direct_block_tests": st[1],
                  "direct_deadlines": st[2], "events_per_candidate": st[2] / max(st[0], 1),
                  "ops_basis": "SURVEY 8(d) per-candidate work of the direct evaluation "
@@ -428,6 +433,8 @@ def main():
                               "the per-candidate evaluator on the same sets",
                  "executed": {"ops_per_step": float(ops_exec),
                               "memo_edf_tests": exh_stats[1], "memo_deadlines": exh_stats[2],
+                              "runs_total": runs,
+                              "runs_walked": exh_stats[4], "live_runs": exh_stats[5],
                               "frac": None}}
     else:
         st = al_stats

@@ -264,13 +264,19 @@ typedef struct {
   unsigned long long *stats;  /* device [4] or NULL: += {candidates, block tests,
                                  deadline points examined, tasks in tested blocks}
                                  (THRESHOLD: {sets, threshold tests, deadline points,
-                                 schedulable candidates enumerated for the hash})              */
+                                 schedulable candidates enumerated for the hash});
+                                 [6] with GP_EX_STATS_EXT: [4] += (set, run) pairs the
+                                 bit-sliced evaluator walked, [5] += those with a non-zero
+                                 verdict word (a run = the candidates of one allocation that
+                                 differ in the last part only); 0 for the other evaluators  */
   uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0);
                                  GP_EX_PER_CANDIDATE (EXHAUSTIVE): force the per-candidate
-                                 evaluator; unknown bits -> GP_EINVAL                          */
+                                 evaluator; GP_EX_STATS_EXT: stats has 6 slots (above);
+                                 unknown bits -> GP_EINVAL                                     */
 } gp_exhaustive_opts;
 #define GP_EX_NO_HASH 1u
 #define GP_EX_PER_CANDIDATE 2u
+#define GP_EX_STATS_EXT 4u
 
 gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode, const uint8_t *verdicts,
                          int32_t n_rows, int32_t slot0, int32_t n_slots, int32_t setting,

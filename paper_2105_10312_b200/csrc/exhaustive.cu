@@ -787,7 +787,7 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   a.per_set = ex->per_set; a.bits = ex->verdict_bits; a.words = ex->words_per_set;
   a.counts = counts; a.slot0 = slot0; a.n_slots = n_slots; a.setting = setting;
   a.stats = ex->stats; a.work_counter = ex->work_counter;
-  if (ex->flags & ~(uint32_t)(GP_EX_NO_HASH | GP_EX_PER_CANDIDATE))
+  if (ex->flags & ~(uint32_t)(GP_EX_NO_HASH | GP_EX_PER_CANDIDATE | GP_EX_STATS_EXT))
     return gp_fail(GP_EINVAL, "EXHAUSTIVE: unknown flags 0x%x", ex->flags);
   a.flags = ex->flags;
   uint64_t items = 0;

@@ -19,6 +19,8 @@
 //   verdict hash bit by bit; verdict bits with word-level atomics).
 // Outputs are byte-identical to the per-candidate evaluator (GP_EX_PER_CANDIDATE
 // selects that one, for A/B runs and parity).
+#include <stdlib.h>
+
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
 #include "gp_enum.cuh"
@@ -31,13 +33,18 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 
 // ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
 // The (subset, size) pairs of a set are spread over the lanes (C3: 63 x 20 =
-// 1,260 pairs, 40 per lane); the verdict bits meet in a shared-memory word per
-// subset and are written out once.
+// 1,260 pairs, 40 per lane; lane pairs pq = lane + 32j, consecutive pairs share
+// a subset); the verdict bits meet in a shared-memory word per subset and are
+// written out once.  The set's WCETs W_i(m, x) (C.1.3) are tabulated once per
+// set in shared memory (n x 2 x M entries), so a test reads its tasks' WCETs
+// instead of recomputing ceil(B/m) per (pair, task).
 template <int NT>
-__global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *memo) {
+__global__ void __launch_bounds__(256, 3) k_exh_memo(const ExhArgs a, uint32_t *memo) {
   __shared__ uint32_t vs_all[8][1 << kBpMaxN];
+  __shared__ int32_t wt_all[8][kBpMaxN * 2 * kBpMaxM];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t *vs = vs_all[wid];
+  int32_t *Wt = wt_all[wid];  // [i][x][m-1], x = 1: conflict
   const int n = a.n, M = a.M;
   const int nsub = 1 << n;
   const int npairs = (nsub - 1) * M;
@@ -53,8 +60,14 @@ __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *mem
     }
     const int32_t H32 = (int32_t)H;
     for (int S = lane; S < nsub; S += 32) vs[S] = 0u;
-    // task i's fields in registers of every lane (n <= NT)
-    int32_t T[NT], D[NT], B[NT], cn[NT], cc[NT], fn[NT], fc[NT], q[NT];
+    for (int e = lane; e < n * 2 * M; e += 32) {  // W_i(m, x) table
+      const int i = e / (2 * M), r = e - i * 2 * M, x = r >= M ? 1 : 0, m = r - x * M + 1;
+      const int64_t o = set * n + i;
+      Wt[(i * 2 + x) * kBpMaxM + m - 1] =
+          x ? wcet_sat(a.B[o], a.cc[o], a.fc[o], m) : wcet_sat(a.B[o], a.cn[o], a.fn[o], m);
+    }
+    // task i's deadline, period, H/T_i and type in registers of every lane (n <= NT)
+    int32_t T[NT], D[NT], q[NT];
     uint32_t mem = 0;
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
@@ -62,18 +75,16 @@ __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *mem
       const int64_t o = set * n + (v ? i : 0);
       T[i] = v ? a.T[o] : INT32_MAX;
       D[i] = v ? a.D[o] : INT32_MAX;
-      B[i] = v ? a.B[o] : 1;
-      cn[i] = v ? a.cn[o] : 0;
-      cc[i] = v ? a.cc[o] : 0;
-      fn[i] = v ? a.fn[o] : 0;
-      fc[i] = v ? a.fc[o] : 0;
       q[i] = v ? (int32_t)(H / T[i]) : 0;
       mem |= (v && a.type[o] == 1) ? 1u << i : 0u;
     }
     __syncwarp();
+    int S = 1, m = lane + 1;  // pair pq = (S - 1) * M + (m - 1), pq = lane + 32 j
+    while (m > M) {
+      m -= M;
+      ++S;
+    }
     for (int pq = lane; pq < npairs; pq += 32) {
-      const int S = pq / M + 1;
-      const int32_t m = pq - (S - 1) * M + 1;
       const int cnt = __popc((unsigned)S);
       int32_t C[NT], Dv[NT], Tv[NT], qv[NT];
       bool bad = false;
@@ -81,8 +92,8 @@ __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *mem
       for (int i = 0; i < NT; ++i) {
         const bool in = (S >> i) & 1;
         const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
-        const bool x = __popc((unsigned)S & same) > 1;  // conflict
-        C[i] = in ? (x ? wcet_sat(B[i], cc[i], fc[i], m) : wcet_sat(B[i], cn[i], fn[i], m)) : 0;
+        const int x = __popc((unsigned)S & same) > 1 ? 1 : 0;  // conflict
+        C[i] = in ? Wt[(i * 2 + x) * kBpMaxM + m - 1] : 0;
         Dv[i] = in ? D[i] : INT32_MAX;
         Tv[i] = in ? T[i] : INT32_MAX;
         qv[i] = in ? q[i] : 0;
@@ -105,9 +116,14 @@ __global__ void __launch_bounds__(256) k_exh_memo(const ExhArgs a, uint32_t *mem
         }
       }
       if (ok) atomicOr(&vs[S], 1u << (m - 1));
+      m += 32;  // next pair of this lane
+      while (m > M) {
+        m -= M;
+        ++S;
+      }
     }
     __syncwarp();
-    for (int S = lane; S < nsub; S += 32) V[S] = S == 0 ? 1u : vs[S];
+    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : vs[S2];
     __syncwarp();
   }
   if (a.stats) {
@@ -253,16 +269,34 @@ __global__ void __launch_bounds__(kScanBlock) k_hash_scan_add(uint64_t *P, uint6
 // depends only on (k, M), so the whole warp walks it in lockstep (uniform
 // control flow, no divergent successor) while each lane applies its own set's
 // verdict words.
+//
+// Specialised on the call's shape: kWin (a rank window narrower than the whole
+// space), kHash (0: no hash, 1: prefix table P, 2: splitmix64 per schedulable
+// rank) and kBits (verdict bits wanted), so the common call carries none of
+// the other modes' per-run checks.
+//
+// Per sweep (the last prefix part grows, runs i = 0 .. steps-1 of lengths
+// len0 - i), run i can hold a schedulable candidate of a lane's set only if
+// bit i of w1 (block k-2 at size pr[0] + i) is set and len0 - i exceeds the
+// lowest set bit of the last block's word; the warp walks only the runs
+// between the lowest such i and the highest over its lanes (warp min/max),
+// skipping the others in closed form -- their verdict words are zero.
+//
+// Verdict hash: a run's schedulable candidates are the set bits of
+// okb = V_last & len_mask (rank rk + b for bit b).  When the last block's word
+// of every lane's set is one contiguous bit range (checked per item, never
+// assumed), okb is one contiguous range [fb, e) and adds P[rk + e] - P[rk + fb];
+// otherwise the contiguous ranges of okb are walked one by one.
+template <bool kWin, int kHash, bool kBits, bool kStats>
 __global__ void __launch_bounds__(kWarps * 32, 4)
     k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs, const uint64_t *P) {
   const int n = a.n, M = a.M;
   const int lane = threadIdx.x & 31;
   const int nsub = 1 << n;
-  const bool want_hash = !(a.flags & GP_EX_NO_HASH);
   // per-lane (= per-set) accumulators
   uint32_t acc_n = 0;
   int32_t acc_pi = INT32_MAX;
-  uint64_t acc_first = ~0ull, acc_hash = 0, st_cand = 0;
+  uint64_t acc_first = ~0ull, acc_hash = 0, st_cand = 0, st_runs = 0, st_live = 0;
   int64_t cur_g = -1, set = -1;
   bool lane_ok = false;
   auto flush = [&]() {
@@ -271,7 +305,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
       atomicAdd(reinterpret_cast<unsigned long long *>(ps + 0), (unsigned long long)acc_n);
       atomicMin(ps + 1, (long long)acc_pi);
       atomicMin(ps + 2, (long long)acc_first);
-      atomicAdd(reinterpret_cast<unsigned long long *>(ps + 3), acc_hash);
+      if (kHash) atomicAdd(reinterpret_cast<unsigned long long *>(ps + 3), acc_hash);
     }
     acc_n = 0;
     acc_pi = INT32_MAX;
@@ -283,144 +317,276 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
     if (lane == 0) base = atomicAdd(a.work_counter, 1ull);  // items are large: one per grab
     base = __shfl_sync(GP_FULL, base, 0);
     if (base >= a.total_items) break;
-    {
-      const uint64_t it = base;
-      int k = a.L.kmax;  // groups k = kmax, ..., 1; item_base[k] = end of group k
-      while (k > 1 && it >= a.item_base[k]) --k;
-      const uint64_t local = it - (k == a.L.kmax ? 0 : a.item_base[k + 1]);
-      const uint32_t npi = (uint32_t)a.L.n_pi[k];
-      const int64_t grp = (int64_t)(local / npi);
-      const uint32_t p = (uint32_t)(local - (uint64_t)grp * npi);
-      if (grp != cur_g) {
-        flush();
-        cur_g = grp;
-        set = grp * 32 + lane;
-        lane_ok = set < a.n_sets && memo[set * nsub] != 0;  // input contract (word 0)
-      }
-      const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
-      const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
+    const uint64_t it = base;
+    int k = a.L.kmax;  // groups k = kmax, ..., 1; item_base[k] = end of group k
+    while (k > 1 && it >= a.item_base[k]) --k;
+    const uint64_t local = it - (k == a.L.kmax ? 0 : a.item_base[k + 1]);
+    const uint32_t npi = (uint32_t)a.L.n_pi[k];
+    const int64_t grp = (int64_t)(local / npi);
+    const uint32_t p = (uint32_t)(local - (uint64_t)grp * npi);
+    if (grp != cur_g) {
+      flush();
+      cur_g = grp;
+      set = grp * 32 + lane;
+      lane_ok = set < a.n_sets && memo[set * nsub] != 0;  // input contract (word 0)
+    }
+    const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
+    const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
+    bool full = true;
+    if constexpr (kWin) {
       if (rank_pi >= a.hi || rank_pi + per_pi <= a.lo) continue;
-      const bool full = rank_pi >= a.lo && rank_pi + per_pi <= a.hi;
-      // block task masks of pi (warp-uniform ballots) -> this lane's set's
-      // verdict words, reversed: Vr[jj] = V[set][S_{k-1-jj}]
-      const uint32_t labels = rgs[a.rgs_base[k] + p];
-      const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
-      uint32_t Vr[kBpMaxN];
+      full = rank_pi >= a.lo && rank_pi + per_pi <= a.hi;
+    }
+    // block task masks of pi (warp-uniform ballots) -> this lane's set's
+    // verdict words, reversed: Vr[jj] = V[set][S_{k-1-jj}]
+    const uint32_t labels = rgs[a.rgs_base[k] + p];
+    const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
+    uint32_t Vr[kBpMaxN];
 #pragma unroll
-      for (int q = 0; q < kBpMaxN; ++q) Vr[q] = 0;
+    for (int q = 0; q < kBpMaxN; ++q) Vr[q] = 0;
 #pragma unroll
-      for (int j = 0; j < kBpMaxN; ++j) {
-        const uint32_t bm = __ballot_sync(GP_FULL, myb == j);
-        const int jj = k - 1 - j;
-        uint32_t v = 0;
-        if (j < k && lane_ok) v = memo[set * nsub + bm];
+    for (int j = 0; j < kBpMaxN; ++j) {
+      const uint32_t bm = __ballot_sync(GP_FULL, myb == j);
+      const int jj = k - 1 - j;
+      uint32_t v = 0;
+      if (j < k && lane_ok) v = memo[set * nsub + bm];
 #pragma unroll
-        for (int q = 0; q < kBpMaxN; ++q)
-          if (q == jj) Vr[q] = v;
-      }
-      if (!__any_sync(GP_FULL, lane_ok)) continue;
-      // walk every run of pi: prefix (s_0..s_{k-2}) lexicographic, stored
-      // reversed in pr (pr[0] = s_{k-2}); run = last part 1 .. M - psum
-      const int kp = k - 1;
-      const uint32_t n_runs = a.L.n_runs[k];
-      int32_t pr[kBpMaxN];
-#pragma unroll
-      for (int jj = 0; jj < kBpMaxN; ++jj) pr[jj] = 1;
-      int32_t psum = kp;
-      auto pre_rest = [&]() -> uint32_t {  // prefix blocks except the last one
-        uint32_t v = 1u;
-#pragma unroll
-        for (int jj = 1; jj < kBpMaxN - 1; ++jj)
-          if (jj < kp) v &= Vr[jj + 1] >> (pr[jj] - 1);
-        return v;
-      };
-      // candidates of pi inside the rank window (all evaluated, bit-sliced)
-      {
+      for (int q = 0; q < kBpMaxN; ++q)
+        if (q == jj) Vr[q] = v;
+    }
+    if (!__any_sync(GP_FULL, lane_ok)) continue;
+    const int kp = k - 1;
+    // candidates of pi inside the rank window (all evaluated, bit-sliced)
+    if (lane_ok) {
+      if constexpr (kWin) {
         const uint64_t w_lo = max(a.lo, rank_pi), w_hi = min(a.hi, rank_pi + per_pi);
-        if (lane_ok) st_cand += w_hi > w_lo ? w_hi - w_lo : 0;
+        st_cand += w_hi > w_lo ? w_hi - w_lo : 0;
+      } else {
+        st_cand += per_pi;
       }
-      // a block never schedulable at any size: every candidate of pi fails
-      bool dead = !lane_ok;
+    }
+    // a block never schedulable at any size: every candidate of pi fails
+    bool dead = !lane_ok;
 #pragma unroll
-      for (int jj = 0; jj < kBpMaxN; ++jj)
-        if (jj < k) dead |= Vr[jj] == 0u;
-      if (__all_sync(GP_FULL, dead)) continue;
-      uint32_t rest = pre_rest();
-      uint32_t *bits = (a.bits && lane_ok) ? a.bits + set * a.words : nullptr;
-      uint32_t off = 0;  // s-index (within pi) of the current run's first candidate
-      uint32_t r = 0;
-      for (;;) {
-        // a sweep: the last prefix part grows from pr[0] while psum <= M - 1;
-        // run i of the sweep has last part 1 .. len_i, len_i = M - psum0 - i
-        const int psum0 = psum;
-        const int steps = kp > 0 ? M - psum0 : 1;
-        if (__any_sync(GP_FULL, (rest & 1u) != 0u)) {
-          uint32_t w1 = kp > 0 ? Vr[1] >> (pr[0] - 1) : 1u;  // bit i: block k-2 at pr[0] + i
-          const uint32_t live = 0u - (rest & 1u);
-          int len = M - psum0;
-          uint32_t lmask = len >= 32 ? ~0u : (1u << len) - 1u;
-          for (int i = 0; i < steps; ++i) {
-            uint32_t okb = Vr[0] & lmask & live & (0u - (w1 & 1u));
-            if (!full) {  // rank window [lo, hi) (warp-uniform)
-              const uint64_t rk = rank_pi + off;
-              if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
-              if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
+    for (int jj = 0; jj < kBpMaxN; ++jj)
+      if (jj < k) dead |= Vr[jj] == 0u;
+    if (__all_sync(GP_FULL, dead)) continue;
+    const uint32_t V0 = dead ? 0u : Vr[0];
+    // lowest size index of the last block that can pass; contiguity of its word
+    const int a0 = V0 ? __ffs(V0) - 1 : 32;
+    const uint32_t v0s = V0 >> (a0 & 31);
+    const bool contig = !a.force_ranges && __all_sync(GP_FULL, (v0s & (v0s + 1u)) == 0u);
+    const int b0 = a0 + __popc(V0);  // end of the last block's range when contiguous
+    uint32_t *bits = nullptr;
+    if constexpr (kBits) bits = lane_ok ? a.bits + set * a.words : nullptr;
+    uint32_t first_off = UINT32_MAX;  // s-index of pi's first schedulable candidate
+    // One sweep: every prefix part but s_{k-2} fixed (their blocks pass in the
+    // lanes where w1 != 0), s_{k-2} = 1 + i for runs i = 0 .. steps-1, run i with
+    // last part 1 .. len0 - i.  w1 bit i: block k-2 passes at size 1 + i.
+    // `off` = s-index (within pi) of the sweep's first candidate.
+    auto sweep = [&](int len0, int steps, uint32_t w1, uint32_t off) {
+      // runs [i_lo, i_hi) can hold schedulable candidates of some lane's set
+      const int lo_l = w1 ? __ffs(w1) - 1 : steps;
+      const int hi_l = w1 ? min(steps, len0 - a0) : 0;
+      const int i_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)lo_l);
+      const int i_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(hi_l, 0));
+      if (i_lo >= i_hi) return;
+      if constexpr (kStats) st_runs += lane_ok ? (uint64_t)(i_hi - i_lo) : 0;
+      int len = len0 - i_lo;
+      uint32_t o2 = off + (uint32_t)(i_lo * len0 - i_lo * (i_lo - 1) / 2);
+      uint32_t lmask = len >= 32 ? ~0u : (1u << len) - 1u;
+      w1 >>= i_lo;
+      const int psb = M - len0 + 1;  // (sum of the prefix parts but s_{k-2}) + 1 + 1
+      if constexpr (!kWin && kHash == 1) {
+        if (contig) {
+          // every lane's okb is [a0, min(b0, len)) when non-zero: the two hash-table
+          // reads of run i+1 are issued while run i is evaluated
+          const uint64_t *Pb = P + rank_pi;
+          uint64_t pa = Pb[o2 + (uint32_t)min(a0, len)], pe = Pb[o2 + (uint32_t)min(b0, len)];
+          for (int i = i_lo; i < i_hi; ++i) {
+            const uint32_t o2n = o2 + (uint32_t)len;
+            const int lenn = len - 1;
+            uint64_t pan = 0, pen = 0;
+            if (i + 1 < i_hi) {
+              pan = Pb[o2n + (uint32_t)min(a0, lenn)];
+              pen = Pb[o2n + (uint32_t)min(b0, lenn)];
             }
+            const uint32_t okb = V0 & lmask & (0u - (w1 & 1u));
             if (okb) {
-              const uint64_t rk = rank_pi + off;
-              const int fb = __ffs(okb) - 1;
-              acc_n += __popc(okb);
-              acc_pi = min(acc_pi, psum0 + i + fb + 1);
-              acc_first = min(acc_first, rk + (uint64_t)fb);
-              if (want_hash) {
-                uint32_t w = okb;
-                if (P) {  // contiguous ranges of schedulable ranks: P[r1] - P[r0]
-                  do {
-                    const int b0 = __ffs(w) - 1;
-                    const uint32_t t = ~(w >> b0);
-                    const int b1 = t ? b0 + __ffs(t) - 1 : 32;
-                    acc_hash += P[rk + (uint64_t)b1] - P[rk + (uint64_t)b0];
-                    w &= b1 >= 32 ? 0u : ~0u << b1;
-                  } while (w);
-                } else {
-                  do {
-                    const int b = __ffs(w) - 1;
-                    w &= w - 1u;
-                    acc_hash += splitmix64(rk + (uint64_t)b);
-                  } while (w);
-                }
-              }
-              if (bits) {  // verdict bits of the run, word-level
-                const uint64_t o2 = rk - a.lo + (uint64_t)fb;
-                const uint32_t w2 = okb >> fb;
-                const uint32_t sh = (uint32_t)(o2 & 31u);
-                atomicOr(bits + (o2 >> 5), w2 << sh);
-                if (sh && (w2 >> (32u - sh))) atomicOr(bits + (o2 >> 5) + 1, w2 >> (32u - sh));
+              if constexpr (kStats) ++st_live;
+              acc_n += (uint32_t)(min(b0, len) - a0);
+              acc_pi = min(acc_pi, psb + i + a0);
+              first_off = min(first_off, o2 + (uint32_t)a0);
+              acc_hash += pe - pa;
+              if constexpr (kBits) {
+                const uint64_t ob = rank_pi + o2 + (uint64_t)a0;
+                const uint32_t w2 = okb >> a0;
+                const uint32_t sh = (uint32_t)(ob & 31u);
+                atomicOr(bits + (ob >> 5), w2 << sh);
+                if (sh && (w2 >> (32u - sh))) atomicOr(bits + (ob >> 5) + 1, w2 >> (32u - sh));
               }
             }
-            off += (uint32_t)len;
-            len -= 1;
+            pa = pan;
+            pe = pen;
+            o2 = o2n;
+            len = lenn;
             lmask >>= 1;
             w1 >>= 1;
           }
-        } else {  // no set has its other prefix blocks schedulable: skip the sweep
-          off += (uint32_t)(steps * (M - psum0) - steps * (steps - 1) / 2);
+          return;
         }
-        r += (uint32_t)steps;
-        if (r >= n_runs) break;
-        // general successor of the prefix from (pr[0] + steps - 1, psum = M - 1)
-        pr[0] += steps - 1;
-        psum = M - 1;
-        next_sizes_rev<kBpMaxN>(M - 1, kp, pr, psum);
-        rest = pre_rest();
+      }
+      for (int i = i_lo; i < i_hi; ++i) {
+        uint32_t okb = V0 & lmask & (0u - (w1 & 1u));
+        if constexpr (kWin) {
+          if (!full) {  // rank window [lo, hi) (warp-uniform)
+            const uint64_t rk = rank_pi + o2;
+            if (rk < a.lo) okb &= a.lo - rk >= (uint64_t)len ? 0u : ~0u << (uint32_t)(a.lo - rk);
+            if (rk + (uint64_t)len > a.hi) okb &= a.hi <= rk ? 0u : (1u << (uint32_t)(a.hi - rk)) - 1u;
+          }
+        }
+        if (okb) {
+          if constexpr (kStats) ++st_live;
+          const int fb = __ffs(okb) - 1;
+          acc_pi = min(acc_pi, psb + i + fb);
+          first_off = min(first_off, o2 + (uint32_t)fb);
+          if constexpr (kHash == 1) {
+            const uint64_t *Pr = P + rank_pi + o2;
+            if (contig) {  // one range [fb, e)
+              const int e = 32 - __clz(okb);
+              acc_n += (uint32_t)(e - fb);
+              acc_hash += Pr[e] - Pr[fb];
+            } else {  // contiguous ranges of schedulable ranks: P[r1] - P[r0]
+              acc_n += __popc(okb);
+              uint32_t w = okb;
+              do {
+                const int c0 = __ffs(w) - 1;
+                const uint32_t t = ~(w >> c0);
+                const int c1 = t ? c0 + __ffs(t) - 1 : 32;
+                acc_hash += Pr[c1] - Pr[c0];
+                w &= c1 >= 32 ? 0u : ~0u << c1;
+              } while (w);
+            }
+          } else {
+            acc_n += __popc(okb);
+            if constexpr (kHash == 2) {
+              const uint64_t rk = rank_pi + o2;
+              uint32_t w = okb;
+              do {
+                const int b = __ffs(w) - 1;
+                w &= w - 1u;
+                acc_hash += splitmix64(rk + (uint64_t)b);
+              } while (w);
+            }
+          }
+          if constexpr (kBits) {  // verdict bits of the run, word-level
+            const uint64_t ob = rank_pi + o2 - a.lo + (uint64_t)fb;
+            const uint32_t w2 = okb >> fb;
+            const uint32_t sh = (uint32_t)(ob & 31u);
+            atomicOr(bits + (ob >> 5), w2 << sh);
+            if (sh && (w2 >> (32u - sh))) atomicOr(bits + (ob >> 5) + 1, w2 >> (32u - sh));
+          }
+        }
+        o2 += (uint32_t)len;
+        len -= 1;
+        lmask >>= 1;
+        w1 >>= 1;
+      }
+    };
+    if (kp == 0) {  // k = 1: one run, the single block at 1 .. M
+      sweep(M, 1, dead ? 0u : 1u, 0u);
+    } else if (kp == 1) {  // k = 2: one sweep over s_0
+      sweep(M - 1, M - 1, dead ? 0u : Vr[1], 0u);
+    } else {
+      // k >= 3: the outer parts s_0 .. s_{k-4} (reversed: q[0] = s_{k-4}) in
+      // lexicographic order (sum <= M - 3 leaves room for s_{k-3}, s_{k-2}, s_{k-1});
+      // for each, s_{k-3} = v walks its sweeps with the verdict word of block k-3
+      // shifted one bit per step, skipping v's no lane can pass at (the skipped
+      // sweeps' candidates are counted in closed form: a sweep of len0 = L holds
+      // L(L+1)/2 candidates, consecutive sweeps L, L-1, ... sum to tetrahedral numbers)
+      const int k2 = kp - 2;
+      int32_t q[kBpMaxN];
+#pragma unroll
+      for (int t = 0; t < kBpMaxN; ++t) q[t] = 1;
+      int qsum = k2;
+      uint32_t off2 = 0;
+      for (;;) {
+        uint32_t rh = dead ? 0u : 1u;  // outer blocks pass at q
+#pragma unroll
+        for (int t = 0; t < kBpMaxN - 3; ++t)
+          if (t < k2) rh &= Vr[t + 3] >> (q[t] - 1);
+        const int L1 = M - qsum - 2;  // len0 of the sweep with s_{k-3} = 1; s_{k-3} <= L1
+        const uint32_t w2 = (rh & 1u) ? Vr[2] : 0u;  // bit v-1: block k-3 passes at v
+        const int vlo_l = w2 ? __ffs(w2) : 99;
+        const int vhi_l = w2 ? min(L1, L1 - a0) : 0;
+        const int v_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)vlo_l);
+        const int v_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(vhi_l, 0));
+        const uint32_t tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);
+        for (int v = v_lo; v <= v_hi; ++v) {
+          const int len0 = L1 - v + 1;
+          const uint32_t offv = off2 + tet1 - (uint32_t)(len0 * (len0 + 1) * (len0 + 2) / 6);
+          sweep(len0, len0, ((w2 >> (v - 1)) & 1u) ? Vr[1] : 0u, offv);
+        }
+        off2 += tet1;
+        // lexicographic successor of the outer parts (sum <= M - 3)
+        if (k2 == 0) break;
+        if (qsum < M - 3) {
+          q[0] += 1;
+          qsum += 1;
+        } else {
+          int prefix = 0, pick = -1;
+#pragma unroll
+          for (int t = 1; t < kBpMaxN; ++t) {
+            prefix += q[t - 1];
+            if (pick < 0 && t < k2 && prefix > t) pick = t;
+          }
+          if (pick < 0) break;
+          int ns = 0;
+#pragma unroll
+          for (int t = 0; t < kBpMaxN; ++t) {
+            q[t] = t < pick ? 1 : (t == pick ? q[t] + 1 : q[t]);
+            ns += t < k2 ? q[t] : 0;
+          }
+          qsum = ns;
+        }
+      }
+    }
+    if (first_off != UINT32_MAX) acc_first = min(acc_first, rank_pi + first_off);
+  }
+  flush();
+  if constexpr (kStats) {
+    const uint64_t c0 = warp_sum_u64(st_cand);
+    const uint64_t c4 = warp_sum_u64(st_runs), c5 = warp_sum_u64(st_live);
+    if (lane == 0) {
+      atomicAdd(a.stats + 0, c0);
+      if (a.flags & GP_EX_STATS_EXT) {
+        atomicAdd(a.stats + 4, c4);
+        atomicAdd(a.stats + 5, c5);
       }
     }
   }
-  flush();
-  if (a.stats) {
-    const uint64_t c0 = warp_sum_u64(st_cand);
-    if (lane == 0) atomicAdd(a.stats + 0, c0);
-  }
+}
+
+template <bool kWin, int kHash, bool kBits>
+static void launch_bp(unsigned grid, const ExhArgs &a, const uint32_t *memo, const uint32_t *rgs,
+                      const uint64_t *P, cudaStream_t st) {
+  if (a.stats) k_exh_bp<kWin, kHash, kBits, true><<<grid, kWarps * 32, 0, st>>>(a, memo, rgs, P);
+  else k_exh_bp<kWin, kHash, kBits, false><<<grid, kWarps * 32, 0, st>>>(a, memo, rgs, P);
+}
+
+template <bool kWin, int kHash>
+static void launch_bp_b(unsigned grid, const ExhArgs &a, const uint32_t *memo,
+                        const uint32_t *rgs, const uint64_t *P, cudaStream_t st) {
+  if (a.bits) launch_bp<kWin, kHash, true>(grid, a, memo, rgs, P, st);
+  else launch_bp<kWin, kHash, false>(grid, a, memo, rgs, P, st);
+}
+
+template <bool kWin>
+static void launch_bp_h(unsigned grid, const ExhArgs &a, const uint32_t *memo,
+                        const uint32_t *rgs, const uint64_t *P, cudaStream_t st) {
+  if (a.flags & GP_EX_NO_HASH) launch_bp_b<kWin, 0>(grid, a, memo, rgs, P, st);
+  else if (P) launch_bp_b<kWin, 1>(grid, a, memo, rgs, P, st);
+  else launch_bp_b<kWin, 2>(grid, a, memo, rgs, P, st);
 }
 
 }  // namespace gp
@@ -436,6 +602,8 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   // the first item AFTER group k (group kmax starts at 0); rgs_base[k] = first
   // RGS index with k blocks (rank order)
   ExhArgs a = a0;
+  // test hook: take the range-by-range hash path even for contiguous verdict words
+  a.force_ranges = getenv("GP_EXH_RANGES") != nullptr;
   uint64_t n_rgs = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
     a.rgs_base[k] = (uint32_t)n_rgs;
@@ -502,12 +670,14 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
   if (r == GP_OK) {
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_bp, kWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exh_bp<false, 1, false, false>, kWarps * 32, 0);
     if (occ < 1) occ = 1;
     uint64_t want = (a.total_items + kWarps - 1) / kWarps;
     uint64_t grid = (uint64_t)sms * occ;
     if (want < grid) grid = want > 0 ? want : 1;
-    k_exh_bp<<<(unsigned)grid, kWarps * 32, 0, st>>>(a, memo, rgs, P);
+    const bool win = !(a.lo == 0 && a.hi >= a.L.total);
+    if (win) launch_bp_h<true>((unsigned)grid, a, memo, rgs, P, st);
+    else launch_bp_h<false>((unsigned)grid, a, memo, rgs, P, st);
     r = gp_cuda_check("EXHAUSTIVE(bp) main kernel");
   }
   cudaFreeAsync(ws, st);

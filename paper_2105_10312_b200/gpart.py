@@ -23,6 +23,7 @@ VARIANTS = {"1G": GP_1G, "SMS_ACT": GP_SMS_ACT, "SMS_INA": GP_SMS_INA, "BF_ACT":
 GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD = 0, 1, 2
 GP_EX_NO_HASH = 1
 GP_EX_PER_CANDIDATE = 2  # force the per-candidate EXHAUSTIVE evaluator
+GP_EX_STATS_EXT = 4  # stats has 6 slots: + (set, run) pairs walked, live runs (bit-sliced)
 UINT64_MAX = 2**64 - 1
 
 FIELDS_I32 = ("T", "D", "B", "cn", "cc", "fn", "fc")
@@ -256,8 +257,10 @@ def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=N
                    stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None, flags=0):
     """FROM_VERDICTS: verdicts uint8 [n_rows][n_sets]; EXHAUSTIVE: per_set int64 [n_sets][4]
     (+ work_counter int64 [>=1], optional verdict_bits int32/uint32 [n_sets][words], stats
-    int64 [4]).  counts int64 [n_settings][n_groups][n_slots][3] is accumulated."""
+    int64 [4], or [6] for the bit-sliced evaluator's run counters).  counts int64 [n_settings][n_groups][n_slots][3] is accumulated."""
     s = ts.struct()
+    if stats is not None and stats.numel() >= 6 and mode == GP_EXHAUSTIVE:
+        flags |= GP_EX_STATS_EXT
     if mode in (GP_EXHAUSTIVE, GP_THRESHOLD):
         n_rows = 1
         ex = _ExOptsC(rank_lo, rank_hi, _ptr(per_set), _ptr(verdict_bits), words_per_set,

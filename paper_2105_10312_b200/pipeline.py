@@ -54,7 +54,7 @@ class Pipeline:
             self.n_cand = G.gp_count_candidates(self.M, self.n)
             self.per_set = torch.zeros((S, 4), dtype=torch.int64, device=device)
             self.work = torch.zeros(1, dtype=torch.int64, device=device)
-            self.stats = torch.zeros(4, dtype=torch.int64, device=device) if stats else None
+            self.stats = torch.zeros(6, dtype=torch.int64, device=device) if stats else None
         else:
             self.n_cand = 0
 

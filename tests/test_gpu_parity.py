@@ -210,6 +210,33 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
     assert ((per[:, 0] == 0) == (per[:, 2] == -1)).all()
 
 
+def test_exhaustive_bitsliced_range_walk(G, monkeypatch):
+    """The bit-sliced evaluator's range-by-range hash walk (taken when a set's
+    last-block verdict word is not one contiguous range; forced here by the
+    GP_EXH_RANGES test hook) gives the oracle's outputs: C2 bitmaps, the
+    no-bits / prefix-table call of the bench, rank windows and random sets."""
+    monkeypatch.setenv("GP_EXH_RANGES", "1")
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 100, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 100, ts)
+    host = to_oracle(ts)
+    ref, rbits = oracle.exhaustive(host, bits=True)
+    per, vb, _ = run_exhaustive(G, ts, bits=True)
+    assert (per == ref).all() and (vb == rbits).all()
+    per, _, _ = run_exhaustive(G, ts)
+    assert (per == ref).all()
+    for lo, hi in [(5, 37), (100, 4100), (31, 65)]:
+        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi)
+        r2, b2 = oracle.exhaustive(host, lo, hi, bits=True)
+        assert (per == r2).all() and (vb == b2).all(), (lo, hi)
+    for seed, n, M in [(4, 3, 4), (12, 6, 9), (14, 8, 12), (16, 3, 32)]:
+        d = W.random_sets(np.random.default_rng(seed), 37, n, M, periods=(4, 6, 8, 12, 24),
+                          b_max=2 * M + 3, cost_max=3)
+        per, vb, _ = run_exhaustive(G, gpu_sets(G, d), bits=True)
+        r2, b2 = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
+        assert (per == r2).all() and (vb == b2).all(), (seed, n, M)
+
+
 @pytest.mark.parametrize("seed,n,M", [(1, 1, 1), (2, 1, 7), (3, 2, 1), (4, 3, 4), (5, 4, 6),
                                       (6, 5, 3), (7, 6, 5), (8, 7, 4), (9, 8, 3), (10, 4, 12),
                                       (11, 3, 12), (12, 6, 9), (13, 3, 40), (14, 8, 12), (16, 3, 32),
