@@ -190,7 +190,7 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, const SizeSpa
 }
 
 template <bool kGen>
-__global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
+__global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
   __shared__ WarpScratch scr_all[8];
   extern __shared__ __align__(16) uint16_t wtab_all[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -242,12 +242,13 @@ __global__ void __launch_bounds__(256) k_allocate(const AllocArgs a) {
     scr.cc[lane] = t.cc; scr.fn[lane] = t.fn; scr.fc[lane] = t.fc; scr.q[lane] = t.q;
     scr.same[lane] = t.same;
     // per-set table of ceil(B_i/m) (the wave counts of C.1.3), if B fits 16 bits
-    const bool tab_ok = wtab && __all_sync(GP_FULL, !t.in || t.B <= 65535);
+    // (1G tests one size only: no table)
+    const bool tab_ok = wtab && a.variant != GP_1G && __all_sync(GP_FULL, !t.in || t.B <= 65535);
     __syncwarp();
     if (tab_ok) {
-      for (int e = lane; e < n * M; e += 32) {
-        const int i = e / M, m = e - i * M + 1;
-        wtab[e] = (uint16_t)ceil_div_pos(scr.B[i], m);
+      for (int i = 0; i < n; ++i) {
+        const int32_t Bi = scr.B[i];
+        for (int m = lane + 1; m <= M; m += 32) wtab[i * M + m - 1] = (uint16_t)ceil_div_pos(Bi, m);
       }
     }
     t.wv.tab = tab_ok ? wtab : nullptr;

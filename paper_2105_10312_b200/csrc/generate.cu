@@ -85,8 +85,8 @@ GP_DEV TaskDraw task_fields(const GenArgs &a, uint64_t u, int32_t pidx, int32_t 
   return d;
 }
 
+template <int G>
 __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
-  const int G = a.G;
   const int lane = threadIdx.x & 31;
   const int j = lane & (G - 1);  // task slot inside the group
   const int64_t l = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;  // local set
@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(256) k_generate(const GenArgs a) {
     // spacing point; lanes >= n-1 carry the pad U_q so they sort last (U_q < 2^31)
     uint32_t pt = (j < n - 1) ? (uint32_t)(((uint64_t)x3 * (uint64_t)(Uq + 1)) >> 32) : (uint32_t)Uq;
     // bitonic sort ascending across the G lanes of the group
+#pragma unroll
     for (int kk = 2; kk <= G; kk <<= 1) {
+#pragma unroll
       for (int s = kk >> 1; s > 0; s >>= 1) {
         const uint32_t o = __shfl_xor_sync(GP_FULL, pt, s);
         const bool asc = (j & kk) == 0, lower = (j & s) == 0;
@@ -317,6 +319,13 @@ extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t
   const int64_t threads = (int64_t)out->n_sets * G;
   const int block = 256;
   const int64_t grid = (threads + block - 1) / block;
-  k_generate<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a);
+  switch (G) {  // group width: the sort network is unrolled for it
+    case 1: k_generate<1><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a); break;
+    case 2: k_generate<2><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a); break;
+    case 4: k_generate<4><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a); break;
+    case 8: k_generate<8><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a); break;
+    case 16: k_generate<16><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a); break;
+    default: k_generate<32><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(a); break;
+  }
   return gp_cuda_check("gp_generate");
 }

@@ -28,9 +28,32 @@ GP_DEV int64_t gcd64(int64_t a, int64_t b) {
   return a;
 }
 
-// lcm with saturation: returns -1 when it would exceed `cap`
+// Binary (Stein) gcd of 32-bit values: shifts and subtractions only.
+GP_DEV uint32_t gcd32(uint32_t u, uint32_t v) {
+  if (u == 0) return v;
+  if (v == 0) return u;
+  const int sh = __ffs(u | v) - 1;
+  u >>= __ffs(u) - 1;
+  do {
+    v >>= __ffs(v) - 1;
+    const uint32_t lo = min(u, v), hi = max(u, v);
+    u = lo;
+    v = hi - lo;
+  } while (v);
+  return u << sh;
+}
+
+// lcm with saturation: returns -1 when it would exceed `cap` (q * b > cap
+// <=> q > floor(cap / b) for positive integers).  32-bit path when every
+// operand fits (every hyperperiod the contract admits: cap < 2^31).
 GP_DEV int64_t lcm_capped(int64_t a, int64_t b, int64_t cap) {
   if (a < 0 || b < 0) return -1;
+  if (((a | b | cap) >> 31) == 0) {
+    const uint32_t g = gcd32((uint32_t)a, (uint32_t)b);
+    if (g == 0) return 0;
+    const uint64_t r = (uint64_t)((uint32_t)a / g) * (uint64_t)b;
+    return r > (uint64_t)cap ? -1 : (int64_t)r;
+  }
   int64_t g = gcd64(a, b);
   int64_t q = a / g;
   if (q > cap / b) return -1;
