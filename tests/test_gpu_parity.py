@@ -139,7 +139,8 @@ def test_wcet_batch(G):
 EVALUATORS = pytest.mark.parametrize("ev", [0, 2], ids=["bitsliced", "per_candidate"])
 
 
-def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1, flags=0):
+def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1, flags=0,
+                   with_stats=True):
     S = ts.n_sets
     total = G.gp_count_candidates(ts.M, ts.n_tasks)
     hi_ = total if hi is None else hi
@@ -150,7 +151,7 @@ def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slo
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, counts, slot0=slot0, n_slots=n_slots, per_set=per,
                      verdict_bits=vb, words_per_set=words if bits else 0, work_counter=work,
-                     stats=stats, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi,
+                     stats=stats if with_stats else None, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi,
                      flags=flags)
     torch.cuda.synchronize()
     out = per.cpu().numpy()
@@ -180,6 +181,9 @@ def test_exhaustive_c2_bitmaps(G, ev):
     assert (per == ref).all()
     assert (vb == rbits).all()
     assert st[0] == 1000 * 11334
+    # the bench's launch configuration: no verdict bits, no stats
+    per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
+    assert (per2 == ref).all()
 
 
 @EVALUATORS
@@ -193,6 +197,8 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
     counts = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
     per, _, st = run_exhaustive(G, ts, counts=counts, flags=ev)
     assert st[0] == 10 * 1000 * 694755
+    per_timed, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)  # bench's timed call
+    assert (per_timed == per).all()
     host = to_oracle(ts)
     rng = np.random.default_rng(13)
     sample = sorted(set([0, 999, 5000, 9999] + [int(x) for x in rng.integers(0, 10000, 12)]))
@@ -249,6 +255,8 @@ def test_exhaustive_random_sets(G, seed, n, M, ev):
     per, vb, _ = run_exhaustive(G, ts, bits=True, flags=ev)
     ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
     assert (per == ref).all() and (vb == rbits).all()
+    per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
+    assert (per2 == ref).all()
 
 
 @EVALUATORS
