@@ -47,12 +47,20 @@ def details(rep):
 
 def raw(rep):
     rows = list(csv.reader(ncu("-i", rep, "--page", "raw", "--csv").splitlines()))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
         d = dict(zip(h, r))
-        res.append({k: d.get(k) for k in RAW if k in d} | {"Kernel Name": d.get("Kernel Name", "")[:60],
-                                                          "ID": d.get("ID")})
+        e = {k: d.get(k) for k in RAW if k in d} | {"Kernel Name": d.get("Kernel Name", "")[:60],
+                                                   "ID": d.get("ID")}
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):  # -> bytes
+            u = units[h.index(k)] if k in h else "byte"
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+            try:
+                e[k] = str(float(e[k].replace(",", "")) * sc)
+            except (KeyError, AttributeError, ValueError):
+                pass
+        res.append(e)
     return res
 
 
