@@ -21,6 +21,8 @@
 // (P:704-706), increasing par_list order, admissible partition
 // sizes -- compiled into a second instantiation (kGen) so that the
 // paper's default path keeps its plain linear scan.
+#include <stdlib.h>
+
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
 #include "gp_sizes.cuh"
@@ -420,9 +422,12 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
               int32_t got = 0, uh = 0;
               if (lane < E) {
                 const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
-                got = maxcnt <= 4
-                          ? serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events)
-                          : serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                if (maxcnt <= 2)
+                  got = serial_merge<2, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                else if (maxcnt <= 4)
+                  got = serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                else
+                  got = serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
               }
               const uint32_t succ = __ballot_sync(GP_FULL, lane < E && got > 0);
               int cut = E;  // partners whose tests the sequential order performs
@@ -571,6 +576,12 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
 
 }  // namespace gp
 
+// per-warp wave-table budget per CTA (A/B switch GP_ALLOC_TAB_KB, default 100 KB)
+static int tab_limit_kb() {
+  const char *e = getenv("GP_ALLOC_TAB_KB");
+  return e ? atoi(e) : 100;
+}
+
 extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *opts,
                                  uint8_t *ok, int16_t *block_of_task, int16_t *block_size,
                                  int32_t *pi, int32_t *k, int64_t *n_tests, int64_t *efficiency,
@@ -607,7 +618,7 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
                                   n_tests, efficiency, stats, (cudaStream_t)stream);
   // per-warp ceil(B/m) table: 8 warps x n x M x 2 bytes when it fits (C4: 76 KB)
   size_t tab = (size_t)8 * ts->n_tasks * ts->M * sizeof(uint16_t);
-  const bool use_tab = tab <= 100 * 1024;
+  const bool use_tab = tab <= (size_t)tab_limit_kb() * 1024;
   if (!use_tab) tab = 0;
   const bool gen = vo.flags != 0 || vo.masked;
   size_t smem = tab;

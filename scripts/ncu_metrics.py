@@ -37,6 +37,8 @@ def f(r, k):
         v = float(r[k].replace(",", ""))
     except (KeyError, ValueError, AttributeError):
         return None
+    if v != v:  # NaN: metric not collected for this launch
+        return None
     return v * SCALE.get(UNITS.get(k, ""), 1)
 
 
@@ -60,18 +62,24 @@ def main():
             "fma_pipe_pct": f(r, "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
             "warp_inst_executed": f(r, "smsp__inst_executed.sum"),
             "active_threads_per_inst": f(r, "smsp__thread_inst_executed_per_inst_executed.ratio"),
-            "dram_bytes": (f(r, "dram__bytes_read.sum") or 0) + (f(r, "dram__bytes_write.sum") or 0),
+            "dram_bytes": (None if f(r, "dram__bytes_read.sum") is None
+                       else f(r, "dram__bytes_read.sum") + (f(r, "dram__bytes_write.sum") or 0)),
         })
     T = sum(p["duration_ms"] or 0 for p in per)
-    tw = lambda k: sum((p[k] or 0) * (p["duration_ms"] or 0) for p in per) / T if T else None  # noqa
+
+    def tw(k):  # time-weighted over the launches that have the metric
+        have = [p for p in per if p[k] is not None and p["duration_ms"]]
+        t = sum(p["duration_ms"] for p in have)
+        return sum(p[k] * p["duration_ms"] for p in have) / t if t else None
     ent = {
         "kernel": " + ".join(p["kernel"] for p in per),
-        "dram_bytes": sum(p["dram_bytes"] for p in per),
+        "dram_bytes": sum(p["dram_bytes"] for p in per if p["dram_bytes"] is not None),
         "duration_ms": T,
         "inst_issued_pct": tw("inst_issued_pct"),
         "alu_pipe_pct": tw("alu_pipe_pct"),
         "fma_pipe_pct": tw("fma_pipe_pct"),
         "warp_inst_executed": sum(p["warp_inst_executed"] or 0 for p in per),
+        "launches_missing_metrics": sum(1 for p in per if p["inst_issued_pct"] is None),
         "active_threads_per_inst": tw("active_threads_per_inst"),
         "per_kernel": per,
         "note": a.note,
