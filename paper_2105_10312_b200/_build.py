@@ -30,9 +30,9 @@ def _deps_mtime():
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src, verbose):
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    cmd = ["nvcc", *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src, verbose, bdir=BUILD, extra=()):
+    obj = os.path.join(bdir, src.replace(".cu", ".o"))
+    cmd = ["nvcc", *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -41,20 +41,27 @@ def _compile(src, verbose):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps_mtime():
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out: str = OUT, extra=()) -> str:
+    """Build libgpart.so; `out` / `extra` (nvcc -D flags) make A/B variants of the library
+    (loaded through GP_LIB) without touching the default build."""
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= _deps_mtime():
+        return out
+    bdir = BUILD if out == OUT else out + ".build"
+    os.makedirs(bdir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+        results = list(ex.map(lambda s: _compile(s, verbose, bdir, extra), SOURCES))
     if verbose:
         for obj, log in results:
             sys.stderr.write(f"== {os.path.basename(obj)}\n{log}")
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", tmp, *[o for o, _ in results]])
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2105_10312_b200._build [--force] [-v] [--out PATH -DNAME=VAL ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else OUT
+    print(build(force="--force" in args, verbose="-v" in args, out=out,
+                extra=[a for a in args if a.startswith("-D")]))

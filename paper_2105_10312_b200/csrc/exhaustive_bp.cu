@@ -30,6 +30,13 @@ namespace gp {
 
 constexpr int kBpMaxN = 8;   // tasks per set (2^8 subset words per set)
 constexpr int kBpMaxM = 32;  // sizes per verdict word
+#ifndef GP_BP_UNROLL
+#define GP_BP_UNROLL 2
+#endif
+#ifndef GP_BP_PREFETCH
+#define GP_BP_PREFETCH 0
+#endif
+constexpr int kBpUnroll = GP_BP_UNROLL;  // run loop unroll (A/B builds: -DGP_BP_UNROLL=n)
 
 // ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
 // The (subset, size) pairs of a set are spread over the lanes (C3: 63 x 20 =
@@ -204,6 +211,7 @@ GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t 
 // mod-2^64 arithmetic), so the main pass needs two table reads per contiguous
 // range of schedulable candidates instead of one splitmix64 per candidate.
 constexpr int kScanBlock = 1024;
+constexpr int kPpad = 32;  // slack entries after the hash prefix table
 constexpr uint32_t kMaxHashTable = 1u << 24;  // ranks per set covered by the table
 
 GP_DEV uint64_t block_incl_scan_u64(uint64_t v, uint64_t *wsum) {
@@ -377,6 +385,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
     const uint32_t v0s = V0 >> (a0 & 31);
     const bool contig = !a.force_ranges && __all_sync(GP_FULL, (v0s & (v0s + 1u)) == 0u);
     const int b0 = a0 + __popc(V0);  // end of the last block's range when contiguous
+    // the last block's word reaches size M in every live lane: a non-zero okb is then the
+    // range [a0, len) -- its end is the next run's start, the same rank in every lane
+    const bool top = contig && __all_sync(GP_FULL, V0 == 0u || b0 >= M);
     uint32_t *bits = nullptr;
     if constexpr (kBits) bits = lane_ok ? a.bits + set * a.words : nullptr;
     uint32_t first_off = UINT32_MAX;  // s-index of pi's first schedulable candidate
@@ -398,23 +409,26 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
       w1 >>= i_lo;
       const int psb = M - len0 + 1;  // (sum of the prefix parts but s_{k-2}) + 1 + 1
       if constexpr (!kWin && kHash == 1) {
-        if (contig) {
-          // every lane's okb is [a0, min(b0, len)) when non-zero: the two hash-table
-          // reads of run i+1 are issued while run i is evaluated
-          const uint64_t *Pb = P + rank_pi;
-          uint64_t pa = Pb[o2 + (uint32_t)min(a0, len)], pe = Pb[o2 + (uint32_t)min(b0, len)];
+        if (top) {
+          // per live run: n += len - a0, hash += P[next run start] - P[run start + a0]
+          const uint64_t *Pu = P + rank_pi;       // run start + 0 (warp-uniform)
+          const uint64_t *Pl = Pu + (a0 & 31);    // run start + a0 (per lane; slack-padded)
+#if GP_BP_PREFETCH
+          uint64_t pa = Pl[o2], pe = Pu[o2 + (uint32_t)len];
+#endif
+#pragma unroll kBpUnroll
           for (int i = i_lo; i < i_hi; ++i) {
             const uint32_t o2n = o2 + (uint32_t)len;
-            const int lenn = len - 1;
-            uint64_t pan = 0, pen = 0;
-            if (i + 1 < i_hi) {
-              pan = Pb[o2n + (uint32_t)min(a0, lenn)];
-              pen = Pb[o2n + (uint32_t)min(b0, lenn)];
-            }
+#if GP_BP_PREFETCH
+            const uint64_t pan = Pl[o2n], pen = Pu[o2n + (uint32_t)(len - 1)];
+#endif
             const uint32_t okb = V0 & lmask & (0u - (w1 & 1u));
             if (okb) {
+#if !GP_BP_PREFETCH
+              const uint64_t pa = Pl[o2], pe = Pu[o2n];
+#endif
               if constexpr (kStats) ++st_live;
-              acc_n += (uint32_t)(min(b0, len) - a0);
+              acc_n += (uint32_t)(len - a0);
               acc_pi = min(acc_pi, psb + i + a0);
               first_off = min(first_off, o2 + (uint32_t)a0);
               acc_hash += pe - pa;
@@ -426,10 +440,12 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
                 if (sh && (w2 >> (32u - sh))) atomicOr(bits + (ob >> 5) + 1, w2 >> (32u - sh));
               }
             }
+#if GP_BP_PREFETCH
             pa = pan;
             pe = pen;
+#endif
             o2 = o2n;
-            len = lenn;
+            len -= 1;
             lmask >>= 1;
             w1 >>= 1;
           }
@@ -623,7 +639,9 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   const uint64_t n_ranks = use_P ? a.L.total : 0;
   const uint32_t nb = (uint32_t)((n_ranks + kScanBlock - 1) / kScanBlock);
   const size_t words32 = (memo_words + n_rgs + 1) & ~(size_t)1;  // 8-byte alignment after
-  const size_t bytes = words32 * 4 + (use_P ? (n_ranks + 1 + nb) * 8 : 0);
+  // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
+  // entries past a run's end in lanes whose verdict word is zero there; never summed)
+  const size_t bytes = words32 * 4 + (use_P ? (n_ranks + 1 + kPpad + nb) * 8 : 0);
   uint32_t *ws = nullptr;
   {  // keep freed workspace in the device's default pool (no unmap/remap per call)
     static int configured = -1;
@@ -643,7 +661,7 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   uint32_t *memo = ws, *rgs = ws + memo_words;
   uint64_t *P = use_P ? reinterpret_cast<uint64_t *>(ws + words32) : nullptr;
   if (use_P) {
-    uint64_t *btot = P + n_ranks + 1;
+    uint64_t *btot = P + n_ranks + 1 + kPpad;
     k_hash_scan_local<<<nb, kScanBlock, 0, st>>>(P, n_ranks, btot);
     k_hash_scan_blocks<<<1, kScanBlock, 0, st>>>(btot, nb);
     k_hash_scan_add<<<nb, kScanBlock, 0, st>>>(P, n_ranks, btot);

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpart.so")
+LIB_PATH = os.environ.get("GP_LIB") or os.path.join(_HERE, "libgpart.so")  # GP_LIB: A/B builds
 
 GP_OK, GP_EINVAL, GP_EOVERFLOW, GP_ECUDA = 0, 1, 2, 3
 GP_1G, GP_SMS_ACT, GP_SMS_INA, GP_BF_ACT, GP_BF_INA = range(5)
