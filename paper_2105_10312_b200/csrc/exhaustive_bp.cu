@@ -40,21 +40,67 @@ constexpr int kBpUnroll = GP_BP_UNROLL;  // run loop unroll (A/B builds: -DGP_BP
 
 // ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
 // The (subset, size) pairs of a set are spread over the lanes (C3: 63 x 20 =
-// 1,260 pairs, 40 per lane; lane pairs pq = lane + 32j, consecutive pairs share
-// a subset); the verdict bits meet in a shared-memory word per subset and are
-// written out once.  The set's WCETs W_i(m, x) (C.1.3) are tabulated once per
-// set in shared memory (n x 2 x M entries), so a test reads its tasks' WCETs
-// instead of recomputing ceil(B/m) per (pair, task).
+// 1,260 pairs, 40 per lane; lane pairs pq = lane + 32j).  Subsets are taken in
+// order of increasing size (a per-CTA table), so consecutive pairs -- the 32 of
+// one warp step -- mostly test subsets of the same size, and each test runs on
+// its c tasks only (compacted, templated on c) instead of NT padded slots.  The
+// verdict bits meet in a shared-memory word per subset and are written out once.
+// The set's WCETs W_i(m, x) (C.1.3) are tabulated once per set in shared memory
+// (n x 2 x M entries), so a test reads its tasks' WCETs instead of recomputing
+// ceil(B/m) per (pair, task).
+struct MemoWarp {
+  uint32_t vs[1 << kBpMaxN];          // verdict word per subset
+  int32_t wt[kBpMaxN * 2 * kBpMaxM];  // W_i(m, x) at [(i*2 + x)*32 + m-1], x = 1: conflict
+  int32_t T[kBpMaxN], D[kBpMaxN], q[kBpMaxN];
+};
+
+// EDF-PDC of the c tasks of S at size m (gp_edf.cuh shortcuts), lane-serial.
+template <int c>
+GP_DEV bool memo_test(const MemoWarp &w, uint32_t S, int m, uint32_t mem, int32_t H,
+                      uint32_t &events) {
+  int32_t C[c], D[c], T[c], q[c];
+  uint32_t bits = S;
+  bool bad = false;
+#pragma unroll
+  for (int a = 0; a < c; ++a) {
+    const int i = __ffs(bits) - 1;
+    bits &= bits - 1u;
+    const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
+    const int x = __popc(S & same) > 1 ? 1 : 0;  // conflict
+    C[a] = w.wt[(i * 2 + x) * kBpMaxM + m - 1];
+    D[a] = w.D[i];
+    T[a] = w.T[i];
+    q[a] = w.q[i];
+    bad |= C[a] > D[a];
+  }
+  if (bad) return false;
+  int32_t UH = 0;
+#pragma unroll
+  for (int a = 0; a < c; ++a) UH += C[a] * q[a];
+  if (UH > H) return false;
+  const int32_t lcut = pdc_cutoff<c>(C, D, T, q, H, UH);
+  return pdc_walk<c>(C, D, T, lcut, events);
+}
+
 template <int NT>
 __global__ void __launch_bounds__(256, 3) k_exh_memo(const ExhArgs a, uint32_t *memo) {
-  __shared__ uint32_t vs_all[8][1 << kBpMaxN];
-  __shared__ int32_t wt_all[8][kBpMaxN * 2 * kBpMaxM];
+  __shared__ MemoWarp mw_all[8];
+  __shared__ uint8_t sorder[1 << kBpMaxN];  // subsets 1 .. 2^n - 1 by (size, value)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t *vs = vs_all[wid];
-  int32_t *Wt = wt_all[wid];  // [i][x][m-1], x = 1: conflict
+  MemoWarp &w = mw_all[wid];
   const int n = a.n, M = a.M;
   const int nsub = 1 << n;
   const int npairs = (nsub - 1) * M;
+  for (int S = threadIdx.x + 1; S < nsub; S += blockDim.x) {  // rank of S in the order
+    const int c = __popc((unsigned)S);
+    int r = 0;
+    for (int S2 = 1; S2 < nsub; ++S2) {
+      const int c2 = __popc((unsigned)S2);
+      r += c2 < c || (c2 == c && S2 < S);
+    }
+    sorder[r] = (uint8_t)S;
+  }
+  __syncthreads();
   uint64_t st_tests = 0, st_tasks = 0;
   uint32_t st_events = 0;
   for (int64_t set = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < a.n_sets;
@@ -66,71 +112,56 @@ __global__ void __launch_bounds__(256, 3) k_exh_memo(const ExhArgs a, uint32_t *
       continue;
     }
     const int32_t H32 = (int32_t)H;
-    for (int S = lane; S < nsub; S += 32) vs[S] = 0u;
+    for (int S = lane; S < nsub; S += 32) w.vs[S] = 0u;
     for (int e = lane; e < n * 2 * M; e += 32) {  // W_i(m, x) table
       const int i = e / (2 * M), r = e - i * 2 * M, x = r >= M ? 1 : 0, m = r - x * M + 1;
       const int64_t o = set * n + i;
-      Wt[(i * 2 + x) * kBpMaxM + m - 1] =
+      w.wt[(i * 2 + x) * kBpMaxM + m - 1] =
           x ? wcet_sat(a.B[o], a.cc[o], a.fc[o], m) : wcet_sat(a.B[o], a.cn[o], a.fn[o], m);
     }
-    // task i's deadline, period, H/T_i and type in registers of every lane (n <= NT)
-    int32_t T[NT], D[NT], q[NT];
-    uint32_t mem = 0;
-#pragma unroll
-    for (int i = 0; i < NT; ++i) {
-      const bool v = i < n;
-      const int64_t o = set * n + (v ? i : 0);
-      T[i] = v ? a.T[o] : INT32_MAX;
-      D[i] = v ? a.D[o] : INT32_MAX;
-      q[i] = v ? (int32_t)(H / T[i]) : 0;
-      mem |= (v && a.type[o] == 1) ? 1u << i : 0u;
+    uint32_t mem = 0;  // type mask (memory-intensive tasks)
+    if (lane < n) {
+      const int64_t o = set * n + lane;
+      w.T[lane] = a.T[o];
+      w.D[lane] = a.D[o];
+      w.q[lane] = (int32_t)(H / a.T[o]);
     }
+    mem = __ballot_sync(GP_FULL, lane < n && a.type[set * n + min(lane, n - 1)] == 1);
     __syncwarp();
-    int S = 1, m = lane + 1;  // pair pq = (S - 1) * M + (m - 1), pq = lane + 32 j
+    int idx = 0, m = lane + 1;  // pair pq = idx * M + (m - 1), pq = lane + 32 j
     while (m > M) {
       m -= M;
-      ++S;
+      ++idx;
     }
     for (int pq = lane; pq < npairs; pq += 32) {
-      const int cnt = __popc((unsigned)S);
-      int32_t C[NT], Dv[NT], Tv[NT], qv[NT];
-      bool bad = false;
-#pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        const bool in = (S >> i) & 1;
-        const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
-        const int x = __popc((unsigned)S & same) > 1 ? 1 : 0;  // conflict
-        C[i] = in ? Wt[(i * 2 + x) * kBpMaxM + m - 1] : 0;
-        Dv[i] = in ? D[i] : INT32_MAX;
-        Tv[i] = in ? T[i] : INT32_MAX;
-        qv[i] = in ? q[i] : 0;
-        bad |= C[i] > Dv[i];
-      }
+      const uint32_t S = sorder[idx];
+      const int cnt = __popc(S);
       ++st_tests;
       st_tasks += cnt;
-      bool ok = false;
-      if (!bad) {
-        if (cnt == 1) {
-          ok = true;  // a single task: C <= D decides (gp_edf.cuh shortcut 1)
-        } else {
-          int32_t UH = 0;
-#pragma unroll
-          for (int i = 0; i < NT; ++i) UH += C[i] * qv[i];
-          if (UH <= H32) {
-            const int32_t lcut = pdc_cutoff<NT>(C, Dv, Tv, qv, H32, UH);
-            ok = pdc_walk<NT>(C, Dv, Tv, lcut, st_events);
-          }
+      bool ok;
+      if (cnt == 1) {
+        const int i = __ffs(S) - 1;  // a single task: C <= D decides (no conflict)
+        ok = w.wt[(i * 2) * kBpMaxM + m - 1] <= w.D[i];
+      } else {
+        switch (cnt) {
+          case 2: ok = memo_test<2>(w, S, m, mem, H32, st_events); break;
+          case 3: ok = memo_test<3>(w, S, m, mem, H32, st_events); break;
+          case 4: ok = memo_test<4>(w, S, m, mem, H32, st_events); break;
+          case 5: ok = memo_test<(NT >= 5 ? 5 : 2)>(w, S, m, mem, H32, st_events); break;
+          case 6: ok = memo_test<(NT >= 6 ? 6 : 2)>(w, S, m, mem, H32, st_events); break;
+          case 7: ok = memo_test<(NT >= 7 ? 7 : 2)>(w, S, m, mem, H32, st_events); break;
+          default: ok = memo_test<(NT >= 8 ? 8 : 2)>(w, S, m, mem, H32, st_events); break;
         }
       }
-      if (ok) atomicOr(&vs[S], 1u << (m - 1));
+      if (ok) atomicOr(&w.vs[S], 1u << (m - 1));
       m += 32;  // next pair of this lane
       while (m > M) {
         m -= M;
-        ++S;
+        ++idx;
       }
     }
     __syncwarp();
-    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : vs[S2];
+    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
     __syncwarp();
   }
   if (a.stats) {
