@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
               livemask = __ballot_sync(GP_FULL, live);
               rank = 0;
               int brank = 0;
-              for (int s2 = 0; s2 < 32; ++s2) {
+              for (int s2 = 0; s2 < n; ++s2) {
                 const int32_t u2 = __shfl_sync(GP_FULL, puh, s2);
                 const bool lv = (livemask >> s2) & 1u;
                 brank += lv && (u2 > puh || (u2 == puh && s2 < lane));
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 }
               forb_slots = 0;
               if (act)
-                for (int s2 = 0; s2 < 32; ++s2) {
+                for (int s2 = 0; s2 < n; ++s2) {
                   const uint32_t m2 = __shfl_sync(GP_FULL, pm, s2);
                   if (m2 & F) forb_slots |= 1u << s2;
                 }
