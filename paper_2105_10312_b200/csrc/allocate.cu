@@ -46,6 +46,7 @@ struct AllocArgs {
   int64_t *eff;               // optional [n_sets][4]: scheduled workload (f2)
   unsigned long long *stats;  // optional: += {EDF tests, tasks tested, deadlines examined, sets}
   int32_t use_tab;            // per-warp table of ceil(B_i/m) in dynamic shared memory
+  unsigned long long *next_set;  // work counter (zeroed per launch)
   AllocVariantOpts vo;        // f4
 };
 
@@ -217,7 +218,13 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
   uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // warp-uniform
   uint64_t st_pair_tasks = 0;                                        // per lane
   uint32_t st_pair_events = 0;                                       // per lane
-  for (int64_t set = (int64_t)blockIdx.x * 8 + wid; set < a.n_sets; set += (int64_t)gridDim.x * 8) {
+  // persistent warps: each grabs its next set from a global counter (sets differ widely in
+  // work -- utilisation bin, variant -- so a static stride leaves warps idle at the tail)
+  for (;;) {
+    int64_t set = 0;
+    if (lane == 0) set = (int64_t)atomicAdd(a.next_set, 1ull);
+    set = __shfl_sync(GP_FULL, set, 0);
+    if (set >= a.n_sets) break;
     const int64_t o = set * n + lane;
     TaskLane t;
     t.in = lane < n;
@@ -625,12 +632,23 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   if (gen && vo.masked) smem = ((tab + 15) & ~(size_t)15) + sizeof(SizeTables);
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-              efficiency, stats, use_tab ? 1 : 0, vo};
+              efficiency, stats, use_tab ? 1 : 0, nullptr, vo};
   auto kern = gen ? k_allocate<true> : k_allocate<false>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // persistent grid: one wave of resident CTAs; the set counter lives in a stream-ordered
+  // 8-byte allocation from the default pool
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  if (occ < 1) occ = 1;
   int64_t grid = ((int64_t)ts->n_sets + 7) / 8;
-  if (grid > 148 * 64) grid = 148 * 64;
+  if (grid > (int64_t)sms * occ) grid = (int64_t)sms * occ;
+  if (cudaMallocAsync(reinterpret_cast<void **>(&a.next_set), 8, (cudaStream_t)stream) != cudaSuccess)
+    return gp_cuda_check("gp_allocate: work counter");
+  cudaMemsetAsync(a.next_set, 0, 8, (cudaStream_t)stream);
   kern<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(a);
+  cudaFreeAsync(a.next_set, (cudaStream_t)stream);
   return gp_cuda_check("gp_allocate");
 }
