@@ -33,10 +33,12 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_UNROLL
 #define GP_BP_UNROLL 2
 #endif
-#ifndef GP_BP_PREFETCH
-#define GP_BP_PREFETCH 0
-#endif
 constexpr int kBpUnroll = GP_BP_UNROLL;  // run loop unroll (A/B builds: -DGP_BP_UNROLL=n)
+
+// 64-bit table entry at byte address base + 8 * idx (one IMAD.WIDE + one load)
+GP_DEV uint64_t ld_u64(uint64_t base, uint32_t idx) {
+  return __ldg(reinterpret_cast<const unsigned long long *>(base + 8ull * idx));
+}
 
 // ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
 // The (subset, size) pairs of a set are spread over the lanes (C3: 63 x 20 =
@@ -419,6 +421,10 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
     // the last block's word reaches size M in every live lane: a non-zero okb is then the
     // range [a0, len) -- its end is the next run's start, the same rank in every lane
     const bool top = contig && __all_sync(GP_FULL, V0 == 0u || b0 >= M);
+    // hash-table byte addresses of pi's first rank (+ a0 in this lane; the table has
+    // kPpad entries of slack for lanes whose a0 runs past a run's end)
+    const uint64_t pu_addr = reinterpret_cast<uint64_t>(P) + 8ull * rank_pi;
+    const uint64_t pl_addr = pu_addr + 8ull * (uint32_t)(a0 & 31);
     uint32_t *bits = nullptr;
     if constexpr (kBits) bits = lane_ok ? a.bits + set * a.words : nullptr;
     uint32_t first_off = UINT32_MAX;  // s-index of pi's first schedulable candidate
@@ -442,27 +448,16 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
       if constexpr (!kWin && kHash == 1) {
         if (top) {
           // per live run: n += len - a0, hash += P[next run start] - P[run start + a0]
-          const uint64_t *Pu = P + rank_pi;       // run start + 0 (warp-uniform)
-          const uint64_t *Pl = Pu + (a0 & 31);    // run start + a0 (per lane; slack-padded)
-#if GP_BP_PREFETCH
-          uint64_t pa = Pl[o2], pe = Pu[o2 + (uint32_t)len];
-#endif
 #pragma unroll kBpUnroll
           for (int i = i_lo; i < i_hi; ++i) {
             const uint32_t o2n = o2 + (uint32_t)len;
-#if GP_BP_PREFETCH
-            const uint64_t pan = Pl[o2n], pen = Pu[o2n + (uint32_t)(len - 1)];
-#endif
             const uint32_t okb = V0 & lmask & (0u - (w1 & 1u));
             if (okb) {
-#if !GP_BP_PREFETCH
-              const uint64_t pa = Pl[o2], pe = Pu[o2n];
-#endif
               if constexpr (kStats) ++st_live;
               acc_n += (uint32_t)(len - a0);
               acc_pi = min(acc_pi, psb + i + a0);
               first_off = min(first_off, o2 + (uint32_t)a0);
-              acc_hash += pe - pa;
+              acc_hash += ld_u64(pu_addr, o2n) - ld_u64(pl_addr, o2);
               if constexpr (kBits) {
                 const uint64_t ob = rank_pi + o2 + (uint64_t)a0;
                 const uint32_t w2 = okb >> a0;
@@ -471,10 +466,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
                 if (sh && (w2 >> (32u - sh))) atomicOr(bits + (ob >> 5) + 1, w2 >> (32u - sh));
               }
             }
-#if GP_BP_PREFETCH
-            pa = pan;
-            pe = pen;
-#endif
             o2 = o2n;
             len -= 1;
             lmask >>= 1;
