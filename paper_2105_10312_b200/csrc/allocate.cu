@@ -50,6 +50,48 @@ struct AllocArgs {
   AllocVariantOpts vo;        // f4
 };
 
+// A group of G lanes of one warp works on one task set (G = 8, 16 or 32: the
+// smallest power of two >= n), so small sets share a warp.  Every collective is
+// over the group's lanes (mask gmask, shuffles of width G); groups of a warp may
+// diverge freely.
+template <int G>
+struct Grp {
+  uint32_t gmask;
+  int gl;  // lane within the group
+  GP_DEV Grp() {
+    const int lane = threadIdx.x & 31;
+    gl = lane & (G - 1);
+    gmask = G == 32 ? GP_FULL : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  }
+  GP_DEV uint32_t ballot(bool p) const {
+    const uint32_t b = __ballot_sync(gmask, p);
+    return G == 32 ? b : (b >> ((threadIdx.x & 31) & ~(G - 1))) & ((1u << G) - 1u);
+  }
+  template <class T> GP_DEV T shfl(T v, int src) const { return __shfl_sync(gmask, v, src, G); }
+  template <class T> GP_DEV T shfl_xor(T v, int o) const { return __shfl_xor_sync(gmask, v, o, G); }
+  GP_DEV bool all(bool p) const { return __all_sync(gmask, p); }
+  GP_DEV void sync() const { __syncwarp(gmask); }
+  GP_DEV unsigned reduce_max(unsigned v) const { return __reduce_max_sync(gmask, v); }
+  template <class T> GP_DEV T sum(T v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += shfl_xor(v, o);
+    return v;
+  }
+  GP_DEV int32_t sum_i32(int32_t v) const { return sum<int32_t>(v); }
+  GP_DEV int64_t sum_i64(int64_t v) const { return sum<int64_t>(v); }
+  GP_DEV uint64_t sum_u64(uint64_t v) const { return sum<uint64_t>(v); }
+  GP_DEV int32_t min_i32(int32_t v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = min(v, shfl_xor(v, o));
+    return v;
+  }
+  GP_DEV uint32_t or_u32(uint32_t v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v |= shfl_xor(v, o);
+    return v;
+  }
+};
+
 // ceil(B_i / m) from the warp's per-set table (uint16, built once per set)
 // or computed directly when the table is off or B does not fit 16 bits.
 struct Waves {
@@ -73,49 +115,51 @@ struct TaskLane {
   Waves wv;
 };
 
-GP_DEV int32_t task_w(const TaskLane &t, int32_t m, bool x) {
-  const int32_t wv = t.wv(threadIdx.x & 31, t.B, m);
+GP_DEV int32_t task_w(const TaskLane &t, int lane, int32_t m, bool x) {
+  const int32_t wv = t.wv(lane, t.B, m);
   return x ? w_from_waves(wv, t.cc, t.fc) : w_from_waves(wv, t.cn, t.fn);
 }
 
-// Warp-cooperative EDF-PDC of partition S at size m (C.1.7).
-GP_DEV bool warp_pdc(const TaskLane &t, uint32_t S, int32_t m, int32_t H, uint64_t &st_tasks,
-                     uint64_t &st_events) {
-  const int lane = threadIdx.x & 31;
+// Group-cooperative EDF-PDC of partition S at size m (C.1.7).
+template <int G>
+GP_DEV bool warp_pdc(const Grp<G> &g, const TaskLane &t, uint32_t S, int32_t m, int32_t H,
+                     uint64_t &st_tasks, uint64_t &st_events) {
+  const int lane = g.gl;
   st_tasks += __popc(S);
   const bool in = (S >> lane) & 1u;
   const bool x = __popc(S & t.same) > 1;  // conflict
-  const int32_t C = in ? task_w(t, m, x) : 0;
-  if (__ballot_sync(GP_FULL, in && C > t.D)) return false;
+  const int32_t C = in ? task_w(t, lane, m, x) : 0;
+  if (g.ballot(in && C > t.D)) return false;
   if (__popc(S) == 1) return true;
-  const int32_t UH = warp_sum_i32(in ? C * t.q : 0);
+  const int32_t UH = g.sum_i32(in ? C * t.q : 0);
   if (UH > H) return false;
   int32_t lcut = H;
   if (UH < H) {
     float X = in ? (float)(t.T - t.D) * (float)(C * t.q) : 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) X += __shfl_xor_sync(GP_FULL, X, o);
+    for (int o = G / 2; o > 0; o >>= 1) X += g.shfl_xor(X, o);
     const float L = X / (float)(H - UH) * 1.0001f + 2.0f;
     lcut = L >= (float)H ? H : (int32_t)L;
   }
   int32_t nx = in ? t.D : INT32_MAX, dem = 0;
   for (;;) {
-    const int32_t tt = warp_min_i32(nx);
+    const int32_t tt = g.min_i32(nx);
     if (tt > lcut) return true;
     const bool hit = nx == tt;
     ++st_events;
-    dem += warp_sum_i32(hit ? C : 0);
+    dem += g.sum_i32(hit ? C : 0);
     nx += hit ? t.T : 0;
     if (dem > tt) return false;
   }
 }
 
 // U(P)*H of partition S at size m (Def. 5 with /T_i, reading A-19).
-GP_DEV int32_t warp_uh(const TaskLane &t, uint32_t S, int32_t m) {
-  const int lane = threadIdx.x & 31;
+template <int G>
+GP_DEV int32_t warp_uh(const Grp<G> &g, const TaskLane &t, uint32_t S, int32_t m) {
+  const int lane = g.gl;
   const bool in = (S >> lane) & 1u;
   const bool x = __popc(S & t.same) > 1;
-  return warp_sum_i32(in ? task_w(t, m, x) * t.q : 0);
+  return g.sum_i32(in ? task_w(t, lane, m, x) * t.q : 0);
 }
 
 // Per-lane two-task EDF-PDC (ACT prefill), same exact shortcuts.
@@ -128,24 +172,25 @@ GP_DEV bool pair_pdc(const int32_t (&C)[2], const int32_t (&D)[2], const int32_t
   return pdc_walk<2>(C, D, T, lcut, ev);
 }
 
+template <int G>
 struct WarpScratch {
-  int32_t ord[32];    // ord[r] = slot with par_list rank r
-  int32_t bord[32];   // bord[r] = slot with best-fit rank r (U*H desc, A-21)
-  int32_t lab[32];    // output label of task i
-  int32_t size[32];   // size of output label j
-  uint32_t forb[32];  // ACT: forbidden task row
-  int32_t plist[32];  // eligible partners of the selected partition, par_list order
-  uint32_t pmask[32]; // task mask of output label j
+  int32_t ord[G];    // ord[r] = slot with par_list rank r
+  int32_t bord[G];   // bord[r] = slot with best-fit rank r (U*H desc, A-21)
+  int32_t lab[G];    // output label of task i
+  int32_t size[G];   // size of output label j
+  uint32_t forb[G];  // ACT: forbidden task row
+  int32_t plist[G];  // eligible partners of the selected partition, par_list order
+  uint32_t pmask[G]; // task mask of output label j
   // the set's tasks, for the lane-serial merge tests
-  int32_t T[32], D[32], B[32], cn[32], cc[32], fn[32], fc[32], q[32];
-  uint32_t same[32];
+  int32_t T[G], D[G], B[G], cn[G], cc[G], fn[G], fc[G], q[G];
+  uint32_t same[G];
 };
 
 // Algorithm 2 merge of partition S (<= NS tasks) by ONE lane: sizes
 // m = lo .. hi in order (Def. 3 bound hi = |P1| + |P2| - 1), an EDF-PDC test
 // each.  Returns the first schedulable m (0 if none) and U*H there.
-template <int NS, bool kGen>
-GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, const SizeSpace &z, uint32_t S,
+template <int NS, bool kGen, class WS>
+GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, uint32_t S,
                             int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
                             uint64_t &st_tasks, uint32_t &st_events) {
   int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
@@ -192,12 +237,13 @@ GP_DEV int32_t serial_merge(const WarpScratch &w, const Waves &wv, const SizeSpa
   return search_sizes<kGen>(z, lo, hi, test);
 }
 
-template <bool kGen>
+template <bool kGen, int G>
 __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
-  __shared__ WarpScratch scr_all[8];
+  __shared__ WarpScratch<G> scr_all[256 / G];
   extern __shared__ __align__(16) uint16_t wtab_all[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpScratch &scr = scr_all[wid];
+  const Grp<G> g;
+  const int lane = g.gl, wid = threadIdx.x / G;  // lane within the group, group in the CTA
+  WarpScratch<G> &scr = scr_all[wid];
   const int n = a.n, M = a.M;
   uint16_t *wtab = a.use_tab ? wtab_all + (size_t)wid * n * M : nullptr;
   // f4: admissible-size tables after the ceil(B/m) tables
@@ -207,7 +253,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
     z.binary = (a.vo.flags & GP_AL_BINARY_MERGE) != 0;
     incr = (a.vo.flags & GP_AL_INCREASING) != 0;
     if (a.vo.masked) {
-      const size_t off = a.use_tab ? (size_t)8 * n * M : 0;
+      const size_t off = a.use_tab ? (size_t)(256 / G) * n * M : 0;
       SizeTables *tb = reinterpret_cast<SizeTables *>(wtab_all + ((off + 7) & ~(size_t)7));
       build_size_tables(*tb, a.vo.mask, M);
       z.tab = tb;
@@ -223,7 +269,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
   for (;;) {
     int64_t set = 0;
     if (lane == 0) set = (int64_t)atomicAdd(a.next_set, 1ull);
-    set = __shfl_sync(GP_FULL, set, 0);
+    set = g.shfl(set, 0);
     if (set >= a.n_sets) break;
     const int64_t o = set * n + lane;
     TaskLane t;
@@ -232,7 +278,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
     t.T = a.T[oo]; t.D = a.D[oo]; t.B = a.B[oo]; t.cn = a.cn[oo]; t.cc = a.cc[oo];
     t.fn = a.fn[oo]; t.fc = a.fc[oo];
     const bool mem = t.in && a.type[oo] == 1;
-    const uint32_t memmask = __ballot_sync(GP_FULL, mem);
+    const uint32_t memmask = g.ballot(mem);
     t.same = mem ? memmask : (all & ~memmask);
     // input contract and H = lcm of all periods (capped)
     const bool fields_ok = !t.in || (t.T >= 1 && t.D >= 1 && t.D <= t.T && t.B >= 1 && t.cn >= 1 &&
@@ -240,11 +286,11 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
     const int64_t cap = ((int64_t)1 << 31) / (n + 1) - 1;
     int64_t h = (t.in && fields_ok) ? t.T : (t.in ? -1 : 1);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const int64_t other = __shfl_xor_sync(GP_FULL, h, off);
+    for (int off = G / 2; off > 0; off >>= 1) {
+      const int64_t other = g.shfl_xor(h, off);
       h = (h < 0 || other < 0) ? -1 : lcm_capped(h, other, cap);
     }
-    const bool contract = __all_sync(GP_FULL, fields_ok) && h > 0;
+    const bool contract = g.all(fields_ok) && h > 0;
     const int32_t H = contract ? (int32_t)h : 1;
     t.q = (contract && t.in) ? H / t.T : 0;
     scr.T[lane] = t.T; scr.D[lane] = t.D; scr.B[lane] = t.B; scr.cn[lane] = t.cn;
@@ -252,17 +298,17 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
     scr.same[lane] = t.same;
     // per-set table of ceil(B_i/m) (the wave counts of C.1.3), if B fits 16 bits
     // (1G tests one size only: no table)
-    const bool tab_ok = wtab && a.variant != GP_1G && __all_sync(GP_FULL, !t.in || t.B <= 65535);
-    __syncwarp();
+    const bool tab_ok = wtab && a.variant != GP_1G && g.all(!t.in || t.B <= 65535);
+    g.sync();
     if (tab_ok) {
       for (int i = 0; i < n; ++i) {
         const int32_t Bi = scr.B[i];
-        for (int m = lane + 1; m <= M; m += 32) wtab[i * M + m - 1] = (uint16_t)ceil_div_pos(Bi, m);
+        for (int m = lane + 1; m <= M; m += G) wtab[i * M + m - 1] = (uint16_t)ceil_div_pos(Bi, m);
       }
     }
     t.wv.tab = tab_ok ? wtab : nullptr;
     t.wv.M = M;
-    __syncwarp();
+    g.sync();
 
     int64_t tests = 0;
     bool ok = false;
@@ -277,7 +323,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
       // 1G: the whole GPU as one partition
       tests = 1;
       const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
-      ok = warp_pdc(t, all, m1, H, st_tasks, st_events);
+      ok = warp_pdc(g, t, all, m1, H, st_tasks, st_events);
       pm = lane == 0 ? all : 0;
       psz = lane == 0 ? m1 : 0;
       stage = 1;
@@ -286,7 +332,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
       const bool sms = a.variant == GP_SMS_ACT || a.variant == GP_SMS_INA;
       // Lemma 1: sum_i W_i(1,n) * (H/T_i) > M*H  =>  reject
       const int64_t w1 = t.in ? ((int64_t)t.B * t.cn + t.fn) * (int64_t)t.q : 0;
-      const bool lemma1 = warp_sum_i64(w1) <= (int64_t)M * H;
+      const bool lemma1 = g.sum_i64(w1) <= (int64_t)M * H;
       // Lemma 2: m_i = min{m : ceil(B/m) cn + fn <= D}
       int32_t mi = 0;
       if (t.in && t.D - t.fn >= t.cn) {
@@ -295,23 +341,23 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
         mi = m0 <= M ? (m0 < 1 ? 1 : m0) : 0;
         if (kGen && mi) mi = z.round_up(mi);  // f4: smallest admissible size >= m0
       }
-      const bool lemma2 = !__ballot_sync(GP_FULL, t.in && mi == 0);
+      const bool lemma2 = !g.ballot(t.in && mi == 0);
       if (lemma1 && lemma2) {
         stage = 1;
         pm = t.in ? (1u << lane) : 0;
         psz = mi;
-        puh = t.in ? task_w(t, mi, false) * t.q : 0;
-        int32_t Pi = warp_sum_i32(psz);
+        puh = t.in ? task_w(t, lane, mi, false) * t.q : 0;
+        int32_t Pi = g.sum_i32(psz);
         if (Pi <= M) {
           ok = true;  // Lemma 3: exit on success at any time (A-24)
         } else {
           uint32_t forb_row = 0;
           if (act) {  // §5.3: test every couple of tasks
             scr.forb[lane] = 0;
-            __syncwarp();
+            g.sync();
             const int np = n * (n - 1) / 2;
             int64_t my_tests = 0;
-            for (int base = 0; base < np; base += 32) {
+            for (int base = 0; base < np; base += G) {
               int idx = base + lane;
               int i = 0;
               int rem = idx < np ? idx : 0;
@@ -320,17 +366,17 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 ++i;
               }
               const int j = i + 1 + rem;
-              const int32_t Ti = __shfl_sync(GP_FULL, t.T, i), Tj = __shfl_sync(GP_FULL, t.T, j);
-              const int32_t Di = __shfl_sync(GP_FULL, t.D, i), Dj = __shfl_sync(GP_FULL, t.D, j);
-              const int32_t Bi = __shfl_sync(GP_FULL, t.B, i), Bj = __shfl_sync(GP_FULL, t.B, j);
-              const int32_t qi = __shfl_sync(GP_FULL, t.q, i), qj = __shfl_sync(GP_FULL, t.q, j);
-              const int32_t mi_ = __shfl_sync(GP_FULL, mi, i), mj_ = __shfl_sync(GP_FULL, mi, j);
-              const uint32_t si = __shfl_sync(GP_FULL, t.same, i);
+              const int32_t Ti = g.shfl(t.T, i), Tj = g.shfl(t.T, j);
+              const int32_t Di = g.shfl(t.D, i), Dj = g.shfl(t.D, j);
+              const int32_t Bi = g.shfl(t.B, i), Bj = g.shfl(t.B, j);
+              const int32_t qi = g.shfl(t.q, i), qj = g.shfl(t.q, j);
+              const int32_t mi_ = g.shfl(mi, i), mj_ = g.shfl(mi, j);
+              const uint32_t si = g.shfl(t.same, i);
               const bool x = (si >> j) & 1u;  // same type -> both in conflict
-              const int32_t cni = __shfl_sync(GP_FULL, t.cn, i), cci = __shfl_sync(GP_FULL, t.cc, i);
-              const int32_t cnj = __shfl_sync(GP_FULL, t.cn, j), ccj = __shfl_sync(GP_FULL, t.cc, j);
-              const int32_t fni = __shfl_sync(GP_FULL, t.fn, i), fci = __shfl_sync(GP_FULL, t.fc, i);
-              const int32_t fnj = __shfl_sync(GP_FULL, t.fn, j), fcj = __shfl_sync(GP_FULL, t.fc, j);
+              const int32_t cni = g.shfl(t.cn, i), cci = g.shfl(t.cc, i);
+              const int32_t cnj = g.shfl(t.cn, j), ccj = g.shfl(t.cc, j);
+              const int32_t fni = g.shfl(t.fn, i), fci = g.shfl(t.fc, i);
+              const int32_t fnj = g.shfl(t.fn, j), fcj = g.shfl(t.fc, j);
               const int32_t ci = x ? cci : cni, cj = x ? ccj : cnj;
               const int32_t fi = x ? fci : fni, fj = x ? fcj : fnj;
               if (idx < np) {
@@ -350,8 +396,8 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 }
               }
             }
-            tests += warp_sum_i64(my_tests);
-            __syncwarp();
+            tests += g.sum_i64(my_tests);
+            g.sync();
             forb_row = scr.forb[lane];
           }
           // Algorithm 1 main loop.  par_list order and the ACT exclusions depend
@@ -365,11 +411,11 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
               // par_list order: (U*H desc, slot asc), or U*H asc (f4 increasing);
               // best-fit partner order: always U*H desc (A-21)
               live = pm != 0;
-              livemask = __ballot_sync(GP_FULL, live);
+              livemask = g.ballot(live);
               rank = 0;
               int brank = 0;
               for (int s2 = 0; s2 < n; ++s2) {
-                const int32_t u2 = __shfl_sync(GP_FULL, puh, s2);
+                const int32_t u2 = g.shfl(puh, s2);
                 const bool lv = (livemask >> s2) & 1u;
                 brank += lv && (u2 > puh || (u2 == puh && s2 < lane));
                 if (kGen && incr) rank += lv && (u2 < puh || (u2 == puh && s2 < lane));
@@ -379,18 +425,18 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 scr.ord[rank] = lane;
                 scr.bord[brank] = lane;
               }
-              __syncwarp();
+              g.sync();
               len = __popc(livemask);
               uint32_t F = 0;  // tasks forbidden with a task of my partition (ACT)
               if (act)
                 for (int a2 = 0; a2 < n; ++a2) {
-                  const uint32_t fr = __shfl_sync(GP_FULL, forb_row, a2);
+                  const uint32_t fr = g.shfl(forb_row, a2);
                   if ((pm >> a2) & 1u) F |= fr;
                 }
               forb_slots = 0;
               if (act)
                 for (int s2 = 0; s2 < n; ++s2) {
-                  const uint32_t m2 = __shfl_sync(GP_FULL, pm, s2);
+                  const uint32_t m2 = g.shfl(pm, s2);
                   if (m2 & F) forb_slots |= 1u << s2;
                 }
               dirty = false;
@@ -401,26 +447,26 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
             }
             // Algorithm 3: eligibility of every slot, pick the first in order
             const uint32_t elig_mine = live ? (livemask & ~(1u << lane) & ~pex & ~forb_slots) : 0;
-            const int cand_rank = warp_min_i32(elig_mine ? rank : 99);
+            const int cand_rank = g.min_i32(elig_mine ? rank : 99);
             if (cand_rank == 99) break;  // no selectable partition: fail (Alg. 1 l.6-7)
             const int P = scr.ord[cand_rank];
-            const uint32_t elig = __shfl_sync(GP_FULL, elig_mine, P);
-            const uint32_t pmP = __shfl_sync(GP_FULL, pm, P);
-            const int32_t szP = __shfl_sync(GP_FULL, psz, P);
+            const uint32_t elig = g.shfl(elig_mine, P);
+            const uint32_t pmP = g.shfl(pm, P);
+            const int32_t szP = g.shfl(psz, P);
             int best = -1;
             int32_t best_m = 0, best_uh = 0;
             // eligible partners in best-fit order -> lane e holds partner plist[e]
             const int Qr = lane < len ? scr.bord[lane] : 0;
             const bool el = lane < len && ((elig >> Qr) & 1u);
-            const uint32_t elb = __ballot_sync(GP_FULL, el);
+            const uint32_t elb = g.ballot(el);
             if (el) scr.plist[__popc(elb & ((1u << lane) - 1u))] = Qr;
-            __syncwarp();
+            g.sync();
             const int E = __popc(elb);
             const int Qe = lane < E ? scr.plist[lane] : 0;
-            const uint32_t pmQe = __shfl_sync(GP_FULL, pm, Qe);
-            const int32_t szQe = __shfl_sync(GP_FULL, psz, Qe);
+            const uint32_t pmQe = g.shfl(pm, Qe);
+            const int32_t szQe = g.shfl(psz, Qe);
             const uint32_t Se = pmP | pmQe;
-            const int maxcnt = __reduce_max_sync(GP_FULL, lane < E ? (unsigned)__popc(Se) : 0u);
+            const int maxcnt = g.reduce_max(lane < E ? (unsigned)__popc(Se) : 0u);
             bool done_round = false;
             if (maxcnt <= 8) {
               // every partner's merge scan runs on its own lane (exact: the scans
@@ -436,15 +482,15 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 else
                   got = serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
               }
-              const uint32_t succ = __ballot_sync(GP_FULL, lane < E && got > 0);
+              const uint32_t succ = g.ballot(lane < E && got > 0);
               int cut = E;  // partners whose tests the sequential order performs
               if (sms) {
                 uint64_t key = (lane < E && got > 0)
                                    ? ((uint64_t)got << 40) | ((uint64_t)(uint32_t)uh << 8) | (uint64_t)Qe
                                    : ~0ull;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                  const uint64_t k2 = __shfl_xor_sync(GP_FULL, key, o);
+                for (int o = G / 2; o > 0; o >>= 1) {
+                  const uint64_t k2 = g.shfl_xor(key, o);
                   key = k2 < key ? k2 : key;
                 }
                 if (key != ~0ull) {
@@ -455,13 +501,13 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
               } else if (succ) {  // BF: the first success in par_list order commits
                 cut = __ffs(succ);  // partners 0 .. cut-1 were tried
                 const int e0 = cut - 1;
-                best = __shfl_sync(GP_FULL, Qe, e0);
-                best_m = __shfl_sync(GP_FULL, got, e0);
-                best_uh = __shfl_sync(GP_FULL, uh, e0);
+                best = g.shfl(Qe, e0);
+                best_m = g.shfl(got, e0);
+                best_uh = g.shfl(uh, e0);
               }
-              tests += warp_sum_i64(lane < cut ? my_tests : 0);
+              tests += g.sum_i64(lane < cut ? my_tests : 0);
               const bool failed = lane < cut && lane < E && got == 0;
-              const uint32_t failQ = warp_or_u32(failed ? (1u << Qe) : 0u);
+              const uint32_t failQ = g.or_u32(failed ? (1u << Qe) : 0u);
               if (lane == P) pex |= failQ;                 // add_to_forbidden_moves(P, Q)
               if ((failQ >> lane) & 1u) pex |= 1u << P;
               done_round = true;
@@ -469,13 +515,13 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
             for (int r = 0; r < len && !done_round; ++r) {
               const int Q = scr.bord[r];
               if (!((elig >> Q) & 1u)) continue;
-              const uint32_t pmQ = __shfl_sync(GP_FULL, pm, Q);
-              const int32_t szQ = __shfl_sync(GP_FULL, psz, Q);
+              const uint32_t pmQ = g.shfl(pm, Q);
+              const int32_t szQ = g.shfl(psz, Q);
               const uint32_t S = pmP | pmQ;
               // Algorithm 2: m < |P1| + |P2| (Def. 3), warp-cooperative tests
               auto wtest = [&](int32_t m) -> bool {
                 ++tests;
-                return warp_pdc(t, S, m, H, st_tasks, st_events);
+                return warp_pdc(g, t, S, m, H, st_tasks, st_events);
               };
               const int32_t got = search_sizes<kGen>(z, max(szP, szQ), szP + szQ - 1, wtest);
               if (!got) {  // add_to_forbidden_moves(P, Q)
@@ -483,7 +529,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 if (lane == Q) pex |= 1u << P;
                 continue;
               }
-              const int32_t uh = warp_uh(t, S, got);
+              const int32_t uh = warp_uh(g, t, S, got);
               if (sms) {  // Def. 4 order >>: smallest size, then U*H, then min id
                 if (best < 0 || got < best_m || (got == best_m && (uh < best_uh ||
                                                                     (uh == best_uh && Q < best)))) {
@@ -498,11 +544,11 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
                 break;
               }
             }
-            __syncwarp();
+            g.sync();
             if (best >= 0) {  // commit: P u Q replaces P and Q in par_list
               const int Q = best;
-              const int32_t szQ = __shfl_sync(GP_FULL, psz, Q);
-              const uint32_t pmQ = __shfl_sync(GP_FULL, pm, Q);
+              const int32_t szQ = g.shfl(psz, Q);
+              const uint32_t pmQ = g.shfl(pm, Q);
               const int keep = min(P, Q), drop = max(P, Q);
               Pi -= szP + szQ - best_m;
               if (lane == keep) {
@@ -524,7 +570,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
       }
     }
     // outputs: labels numbered by lowest task id (= slot index)
-    const uint32_t livemask = __ballot_sync(GP_FULL, pm != 0);
+    const uint32_t livemask = g.ballot(pm != 0);
     const int kk = stage ? __popc(livemask) : 0;
     if (pm) {
       const int label = __popc(livemask & ((1u << lane) - 1u));
@@ -537,8 +583,8 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
         scr.lab[tsk] = label;
       }
     }
-    __syncwarp();
-    const int32_t Pi_out = stage ? warp_sum_i32(psz) : 0;
+    g.sync();
+    const int32_t Pi_out = stage ? g.sum_i32(psz) : 0;
     if (t.in) {
       a.bot[o] = (int16_t)(stage ? scr.lab[lane] : -1);
       a.bs[o] = (int16_t)((stage && lane < kk) ? scr.size[lane] : 0);
@@ -548,13 +594,13 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
     if (a.eff) {
       // f2: work c^x * B per period, x H
       const int64_t w = t.in ? (int64_t)t.B * t.q : 0;
-      const int64_t lo = warp_sum_i64(w * t.cn), up = warp_sum_i64(w * t.cc);
+      const int64_t lo = g.sum_i64(w * t.cn), up = g.sum_i64(w * t.cc);
       int64_t mine = 0;
       if (stage && t.in) {
         const bool x = __popc(scr.pmask[scr.lab[lane]] & t.same) > 1;  // conflict
         mine = w * (x ? t.cc : t.cn);
       }
-      const int64_t ach = warp_sum_i64(mine);
+      const int64_t ach = g.sum_i64(mine);
       if (lane == 0) {
         a.eff[set * 4 + 0] = lo;
         a.eff[set * 4 + 1] = up;
@@ -568,10 +614,10 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
       a.k[set] = kk;
       a.n_tests[set] = tests;
     }
-    __syncwarp();
+    g.sync();
   }
   if (a.stats) {
-    const uint64_t pt = warp_sum_u64(st_pair_tasks), pe = warp_sum_u64(st_pair_events);
+    const uint64_t pt = g.sum_u64(st_pair_tasks), pe = g.sum_u64(st_pair_events);
     if (lane == 0) {
       atomicAdd(a.stats + 0, (unsigned long long)st_tests);
       atomicAdd(a.stats + 1, (unsigned long long)(st_tasks + pt));
@@ -623,8 +669,12 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   if (ts->n_tasks > kMaxTasks)  // 33..256 tasks: one CTA per set (allocate_big.cu)
     return gp_allocate_big_launch(ts, (int32_t)v, vo, ok, block_of_task, block_size, pi, k,
                                   n_tests, efficiency, stats, (cudaStream_t)stream);
-  // per-warp ceil(B/m) table: 8 warps x n x M x 2 bytes when it fits (C4: 76 KB)
-  size_t tab = (size_t)8 * ts->n_tasks * ts->M * sizeof(uint16_t);
+  // group width: the smallest of 8, 16, 32 lanes that holds the set's tasks (A/B switch
+  // GP_ALLOC_G forces a width >= that)
+  int G = ts->n_tasks <= 8 ? 8 : (ts->n_tasks <= 16 ? 16 : 32);
+  if (const char *e = getenv("GP_ALLOC_G")) G = max(G, atoi(e) >= 32 ? 32 : (atoi(e) >= 16 ? 16 : 8));
+  // per-group ceil(B/m) table: 256/G groups x n x M x 2 bytes when it fits (C4: 76 KB)
+  size_t tab = (size_t)(256 / G) * ts->n_tasks * ts->M * sizeof(uint16_t);
   const bool use_tab = tab <= (size_t)tab_limit_kb() * 1024;
   if (!use_tab) tab = 0;
   const bool gen = vo.flags != 0 || vo.masked;
@@ -633,9 +683,11 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
               efficiency, stats, use_tab ? 1 : 0, nullptr, vo};
-  auto kern = gen ? k_allocate<true> : k_allocate<false>;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = G == 8 ? (gen ? k_allocate<true, 8> : k_allocate<false, 8>)
+              : G == 16 ? (gen ? k_allocate<true, 16> : k_allocate<false, 16>)
+                        : (gen ? k_allocate<true, 32> : k_allocate<false, 32>);
+  // dynamic + static shared memory may pass 48 KB (e.g. 16-lane groups: 16 scratches + tables)
+  if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // persistent grid: one wave of resident CTAs; the set counter lives in a stream-ordered
   // 8-byte allocation from the default pool
   int dev = 0, sms = 148, occ = 1;
@@ -643,7 +695,7 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
   if (occ < 1) occ = 1;
-  int64_t grid = ((int64_t)ts->n_sets + 7) / 8;
+  int64_t grid = ((int64_t)ts->n_sets + 256 / G - 1) / (256 / G);
   if (grid > (int64_t)sms * occ) grid = (int64_t)sms * occ;
   if (cudaMallocAsync(reinterpret_cast<void **>(&a.next_set), 8, (cudaStream_t)stream) != cudaSuccess)
     return gp_cuda_check("gp_allocate: work counter");
