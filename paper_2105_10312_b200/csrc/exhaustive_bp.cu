@@ -303,6 +303,54 @@ __global__ void __launch_bounds__(kScanBlock) k_hash_scan_add(uint64_t *P, uint6
   if (r < n_ranks) P[r + 1] += btot[blockIdx.x];
 }
 
+// ---- per-subset lane order: for every subset S, the sets ordered by (utilisation group,
+// first size at which S passes): sets of one group have similar loads in every subset,
+// and within it the lanes of a warp share the upper end of their live run ranges.  A
+// counting sort per subset (global histogram, one scan per subset, a scatter); the order
+// inside a key is arbitrary (atomics), which no output depends on (per-set results are
+// sums and minima).
+constexpr int kThrBins = kBpMaxM + 1;
+
+GP_DEV int first_pass(uint32_t v) { return v ? __ffs(v) - 1 : kBpMaxM; }
+
+GP_DEV int sp_key(const ExhArgs &a, const uint32_t *V, int64_t set, int S) {
+  if (V[0] == 0u) return a.n_groups * kThrBins;  // contract violated: last
+  const int g = a.group[set];
+  return (g >= 0 && g < a.n_groups ? g : 0) * kThrBins + first_pass(V[S]);
+}
+
+__global__ void __launch_bounds__(256) k_sp_hist(const ExhArgs a, const uint32_t *memo, int nsub,
+                                                 int nkeys, uint32_t *hist) {
+  for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
+       set += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t *V = memo + set * nsub;
+    for (int S = 1; S < nsub; ++S) atomicAdd(&hist[(size_t)S * nkeys + sp_key(a, V, set, S)], 1u);
+  }
+}
+
+__global__ void k_sp_scan(uint32_t *hist, int nsub, int nkeys) {  // exclusive scan per subset
+  for (int S = threadIdx.x + 1; S < nsub; S += blockDim.x) {
+    uint32_t run = 0;
+    for (int b = 0; b < nkeys; ++b) {
+      const uint32_t c = hist[(size_t)S * nkeys + b];
+      hist[(size_t)S * nkeys + b] = run;
+      run += c;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sp_scatter(const ExhArgs a, const uint32_t *memo, int nsub,
+                                                    int nkeys, uint32_t *offs, uint32_t *sperm) {
+  for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
+       set += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t *V = memo + set * nsub;
+    for (int S = 1; S < nsub; ++S) {
+      const uint32_t pos = atomicAdd(&offs[(size_t)S * nkeys + sp_key(a, V, set, S)], 1u);
+      sperm[(size_t)S * a.n_sets + pos] = (uint32_t)set;
+    }
+  }
+}
+
 // ---- main pass: bit-sliced verdicts over runs, lane = task set -------------------
 // item = (group of 32 consecutive sets, allocation pi), items in k-DESCENDING
 // groups (the largest allocations first, small ones fill the tail).  The run
@@ -365,7 +413,18 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
     const uint32_t npi = (uint32_t)a.L.n_pi[k];
     const int64_t grp = (int64_t)(local / npi);
     const uint32_t p = (uint32_t)(local - (uint64_t)grp * npi);
-    if (grp != cur_g) {
+    const uint32_t labels = rgs[a.rgs_base[k] + p];
+    const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
+    if (a.sperm) {
+      // lane slots of this item follow the permutation of the sets by the first size at
+      // which pi's LAST block passes, so a warp's lanes share the upper end of their
+      // live run ranges; per-set results are flushed per item
+      flush();
+      const uint32_t S_last = __ballot_sync(GP_FULL, myb == k - 1);
+      const int64_t slot = grp * 32 + lane;
+      set = slot < a.n_sets ? (int64_t)a.sperm[(size_t)S_last * a.n_sets + slot] : slot;
+      lane_ok = slot < a.n_sets && memo[set * nsub] != 0;  // input contract (word 0)
+    } else if (grp != cur_g) {
       flush();
       cur_g = grp;
       set = grp * 32 + lane;
@@ -380,8 +439,6 @@ __global__ void __launch_bounds__(kWarps * 32, 4)
     }
     // block task masks of pi (warp-uniform ballots) -> this lane's set's
     // verdict words, reversed: Vr[jj] = V[set][S_{k-1-jj}]
-    const uint32_t labels = rgs[a.rgs_base[k] + p];
-    const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
     uint32_t Vr[kBpMaxN];
 #pragma unroll
     for (int q = 0; q < kBpMaxN; ++q) Vr[q] = 0;
@@ -660,7 +717,13 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   const bool use_P = !(a.flags & GP_EX_NO_HASH) && a.L.total < kMaxHashTable;
   const uint64_t n_ranks = use_P ? a.L.total : 0;
   const uint32_t nb = (uint32_t)((n_ranks + kScanBlock - 1) / kScanBlock);
-  const size_t words32 = (memo_words + n_rgs + 1) & ~(size_t)1;  // 8-byte alignment after
+  // per-subset lane order (GP_EXH_NO_GROUPING: off): nsub x n_sets slots + histograms
+  const size_t sp_words = (size_t)(1 << n) * a.n_sets;
+  const bool use_sp = getenv("GP_EXH_NO_GROUPING") == nullptr && a.n_sets > 32 &&
+                      sp_words * 4 <= ((size_t)256 << 20);
+  const int sp_keys = (a.n_groups > 0 ? a.n_groups : 1) * kThrBins + 1;
+  const size_t sp_total = use_sp ? sp_words + (size_t)(1 << n) * sp_keys : 0;
+  const size_t words32 = (memo_words + n_rgs + sp_total + 1) & ~(size_t)1;  // 8-byte alignment after
   // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
   // entries past a run's end in lanes whose verdict word is zero there; never summed)
   const size_t bytes = words32 * 4 + (use_P ? (n_ranks + 1 + kPpad + nb) * 8 : 0);
@@ -681,6 +744,7 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   if (cudaMallocAsync(reinterpret_cast<void **>(&ws), bytes, st) != cudaSuccess)
     return gp_cuda_check("EXHAUSTIVE(bp): workspace allocation");
   uint32_t *memo = ws, *rgs = ws + memo_words;
+  uint32_t *sperm = use_sp ? rgs + n_rgs : nullptr, *sphist = use_sp ? sperm + sp_words : nullptr;
   uint64_t *P = use_P ? reinterpret_cast<uint64_t *>(ws + words32) : nullptr;
   if (use_P) {
     uint64_t *btot = P + n_ranks + 1 + kPpad;
@@ -706,6 +770,17 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
     if (n <= 4) k_exh_memo<4><<<g, 256, 0, st>>>(a, memo);
     else if (n <= 6) k_exh_memo<6><<<g, 256, 0, st>>>(a, memo);
     else k_exh_memo<8><<<g, 256, 0, st>>>(a, memo);
+  }
+  a.sperm = nullptr;
+  if (use_sp) {
+    const int nsub = 1 << n;
+    cudaMemsetAsync(sphist, 0, (size_t)nsub * sp_keys * 4, st);
+    int64_t gk = ((int64_t)a.n_sets + 255) / 256;
+    if (gk > (int64_t)sms * 4) gk = (int64_t)sms * 4;
+    k_sp_hist<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist);
+    k_sp_scan<<<1, 256, 0, st>>>(sphist, nsub, sp_keys);
+    k_sp_scatter<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm);
+    a.sperm = sperm;
   }
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
   if (r == GP_OK) {

@@ -26,6 +26,7 @@ struct ExhArgs {
   unsigned long long *work_counter;
   uint32_t flags;  // gp_exhaustive_opts.flags
   int32_t force_ranges;  // bit-sliced evaluator: walk okb range by range (env GP_EXH_RANGES, tests)
+  const uint32_t *sperm;  // bit-sliced evaluator: [subset][slot] -> set, sets by that subset's first passing size
   uint32_t rgs_base[kEnumMaxTasks + 2];  // bit-sliced evaluator: first RGS index with k blocks
   uint64_t items_per_set, total_items;
   uint64_t item_base[kEnumMaxTasks + 2];

@@ -199,6 +199,13 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
     assert st[0] == 10 * 1000 * 694755
     per_timed, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)  # bench's timed call
     assert (per_timed == per).all()
+    if ev == 0:  # the bit-sliced evaluator without its per-subset lane order
+        os.environ["GP_EXH_NO_GROUPING"] = "1"
+        try:
+            per_id, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
+        finally:
+            del os.environ["GP_EXH_NO_GROUPING"]
+        assert (per_id == per).all()
     host = to_oracle(ts)
     rng = np.random.default_rng(13)
     sample = sorted(set([0, 999, 5000, 9999] + [int(x) for x in rng.integers(0, 10000, 12)]))
