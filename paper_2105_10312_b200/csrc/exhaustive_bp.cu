@@ -313,18 +313,37 @@ constexpr int kThrBins = kBpMaxM + 1;
 
 GP_DEV int first_pass(uint32_t v) { return v ? __ffs(v) - 1 : kBpMaxM; }
 
-GP_DEV int sp_key(const ExhArgs &a, const uint32_t *V, int64_t set, int S) {
-  if (V[0] == 0u) return a.n_groups * kThrBins;  // contract violated: last
+#ifndef GP_SP_LEVELS
+#define GP_SP_LEVELS 4
+#endif
+constexpr int kSpLevels = GP_SP_LEVELS;  // load levels inside a (group, first size) key
+
+// key = (group, first passing size of S, load level of the set); load level = the set's
+// number of schedulable (subset, size) pairs, quantised
+GP_DEV int sp_key(const ExhArgs &a, const uint32_t *V, int64_t set, int S, const uint8_t *lvl) {
+  if (V[0] == 0u) return a.n_groups * kThrBins * kSpLevels;  // contract violated: last
   const int g = a.group[set];
-  return (g >= 0 && g < a.n_groups ? g : 0) * kThrBins + first_pass(V[S]);
+  return ((g >= 0 && g < a.n_groups ? g : 0) * kThrBins + first_pass(V[S])) * kSpLevels + lvl[set];
 }
 
-__global__ void __launch_bounds__(256) k_sp_hist(const ExhArgs a, const uint32_t *memo, int nsub,
-                                                 int nkeys, uint32_t *hist) {
+__global__ void k_sp_level(const ExhArgs a, const uint32_t *memo, int nsub, uint8_t *lvl) {
+  const uint32_t mmask = a.M >= 32 ? ~0u : (1u << a.M) - 1u;
+  const uint32_t cap = (uint32_t)(nsub - 1) * (uint32_t)a.M + 1u;
   for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
        set += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t *V = memo + set * nsub;
-    for (int S = 1; S < nsub; ++S) atomicAdd(&hist[(size_t)S * nkeys + sp_key(a, V, set, S)], 1u);
+    uint32_t c = 0;
+    for (int S = 1; S < nsub; ++S) c += __popc(V[S] & mmask);
+    lvl[set] = (uint8_t)(c * (uint32_t)kSpLevels / cap);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sp_hist(const ExhArgs a, const uint32_t *memo, int nsub,
+                                                 int nkeys, uint32_t *hist, const uint8_t *lvl) {
+  for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
+       set += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t *V = memo + set * nsub;
+    for (int S = 1; S < nsub; ++S) atomicAdd(&hist[(size_t)S * nkeys + sp_key(a, V, set, S, lvl)], 1u);
   }
 }
 
@@ -340,12 +359,13 @@ __global__ void k_sp_scan(uint32_t *hist, int nsub, int nkeys) {  // exclusive s
 }
 
 __global__ void __launch_bounds__(256) k_sp_scatter(const ExhArgs a, const uint32_t *memo, int nsub,
-                                                    int nkeys, uint32_t *offs, uint32_t *sperm) {
+                                                    int nkeys, uint32_t *offs, uint32_t *sperm,
+                                                    const uint8_t *lvl) {
   for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
        set += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t *V = memo + set * nsub;
     for (int S = 1; S < nsub; ++S) {
-      const uint32_t pos = atomicAdd(&offs[(size_t)S * nkeys + sp_key(a, V, set, S)], 1u);
+      const uint32_t pos = atomicAdd(&offs[(size_t)S * nkeys + sp_key(a, V, set, S, lvl)], 1u);
       sperm[(size_t)S * a.n_sets + pos] = (uint32_t)set;
     }
   }
@@ -721,8 +741,9 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   const size_t sp_words = (size_t)(1 << n) * a.n_sets;
   const bool use_sp = getenv("GP_EXH_NO_GROUPING") == nullptr && a.n_sets > 32 &&
                       sp_words * 4 <= ((size_t)256 << 20);
-  const int sp_keys = (a.n_groups > 0 ? a.n_groups : 1) * kThrBins + 1;
-  const size_t sp_total = use_sp ? sp_words + (size_t)(1 << n) * sp_keys : 0;
+  const int sp_keys = (a.n_groups > 0 ? a.n_groups : 1) * kThrBins * kSpLevels + 1;
+  const size_t sp_total =
+      use_sp ? sp_words + (size_t)(1 << n) * sp_keys + ((size_t)a.n_sets + 3) / 4 : 0;
   const size_t words32 = (memo_words + n_rgs + sp_total + 1) & ~(size_t)1;  // 8-byte alignment after
   // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
   // entries past a run's end in lanes whose verdict word is zero there; never summed)
@@ -777,9 +798,11 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
     cudaMemsetAsync(sphist, 0, (size_t)nsub * sp_keys * 4, st);
     int64_t gk = ((int64_t)a.n_sets + 255) / 256;
     if (gk > (int64_t)sms * 4) gk = (int64_t)sms * 4;
-    k_sp_hist<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist);
+    uint8_t *lvl = reinterpret_cast<uint8_t *>(sphist + (size_t)nsub * sp_keys);
+    k_sp_level<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, lvl);
+    k_sp_hist<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, lvl);
     k_sp_scan<<<1, 256, 0, st>>>(sphist, nsub, sp_keys);
-    k_sp_scatter<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm);
+    k_sp_scatter<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm, lvl);
     a.sperm = sperm;
   }
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
