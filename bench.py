@@ -511,13 +511,15 @@ def main():
 def launches_per_step(pipe, args=None):
     """Our kernels per step: per setting gp_generate 1 + gp_allocate x V + ratio 1;
     + EXHAUSTIVE: per-candidate (init, main, finalize) or bit-sliced (init, RGS table,
-    memo, main, finalize, + 3 hash-prefix scan kernels when the hash is computed)."""
+    memo, main, finalize, + 3 hash-prefix scan kernels when the hash is computed, + 4
+    lane-order kernels)."""
     n = len(pipe.gens) * (2 + len(pipe.variants))
     if not pipe.exhaustive:
         return n
     if (args is not None and (args.f3 or args.per_candidate)) or pipe.n > 8 or pipe.M > 32:
         return n + 3
-    return n + 5 + (3 if pipe.n_cand < (1 << 24) else 0)
+    # + 4 lane-order kernels (load level, histogram, scan, scatter) when n_sets > 32
+    return n + 5 + (3 if pipe.n_cand < (1 << 24) else 0) + (4 if pipe.ts.n_sets > 32 else 0)
 
 
 def run_e2e(G, pipe, stream, args, world, evals_rank):

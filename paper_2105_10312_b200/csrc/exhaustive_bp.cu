@@ -340,34 +340,47 @@ __global__ void k_sp_level(const ExhArgs a, const uint32_t *memo, int nsub, uint
 
 __global__ void __launch_bounds__(256) k_sp_hist(const ExhArgs a, const uint32_t *memo, int nsub,
                                                  int nkeys, uint32_t *hist, const uint8_t *lvl) {
-  for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
-       set += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t *V = memo + set * nsub;
-    for (int S = 1; S < nsub; ++S) atomicAdd(&hist[(size_t)S * nkeys + sp_key(a, V, set, S, lvl)], 1u);
+  // thread = (set, subset), subset fastest: a warp's atomics go to different subsets' bins
+  const int64_t total = a.n_sets * (int64_t)(nsub - 1);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t set = e / (nsub - 1);
+    const int S = (int)(e - set * (nsub - 1)) + 1;
+    atomicAdd(&hist[(size_t)S * nkeys + sp_key(a, memo + set * nsub, set, S, lvl)], 1u);
   }
 }
 
-__global__ void k_sp_scan(uint32_t *hist, int nsub, int nkeys) {  // exclusive scan per subset
-  for (int S = threadIdx.x + 1; S < nsub; S += blockDim.x) {
-    uint32_t run = 0;
-    for (int b = 0; b < nkeys; ++b) {
-      const uint32_t c = hist[(size_t)S * nkeys + b];
-      hist[(size_t)S * nkeys + b] = run;
-      run += c;
-    }
+// exclusive scan per subset, in place: one warp per subset (block = 32 threads, grid = nsub - 1)
+__global__ void __launch_bounds__(32) k_sp_scan(uint32_t *hist, int nkeys) {
+  uint32_t *h = hist + (size_t)(blockIdx.x + 1) * nkeys;
+  const int lane = threadIdx.x, per = (nkeys + 31) / 32, b0 = lane * per;
+  uint32_t loc = 0;
+  for (int b = b0; b < b0 + per && b < nkeys; ++b) loc += h[b];
+  uint32_t incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(GP_FULL, incl, o);
+    if (lane >= o) incl += u;
+  }
+  uint32_t run = incl - loc;
+  for (int b = b0; b < b0 + per && b < nkeys; ++b) {
+    const uint32_t c = h[b];
+    h[b] = run;
+    run += c;
   }
 }
 
 __global__ void __launch_bounds__(256) k_sp_scatter(const ExhArgs a, const uint32_t *memo, int nsub,
                                                     int nkeys, uint32_t *offs, uint32_t *sperm,
                                                     const uint8_t *lvl) {
-  for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
-       set += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t *V = memo + set * nsub;
-    for (int S = 1; S < nsub; ++S) {
-      const uint32_t pos = atomicAdd(&offs[(size_t)S * nkeys + sp_key(a, V, set, S, lvl)], 1u);
-      sperm[(size_t)S * a.n_sets + pos] = (uint32_t)set;
-    }
+  const int64_t total = a.n_sets * (int64_t)(nsub - 1);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t set = e / (nsub - 1);
+    const int S = (int)(e - set * (nsub - 1)) + 1;
+    const uint32_t pos =
+        atomicAdd(&offs[(size_t)S * nkeys + sp_key(a, memo + set * nsub, set, S, lvl)], 1u);
+    sperm[(size_t)S * a.n_sets + pos] = (uint32_t)set;
   }
 }
 
@@ -796,12 +809,12 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   if (use_sp) {
     const int nsub = 1 << n;
     cudaMemsetAsync(sphist, 0, (size_t)nsub * sp_keys * 4, st);
-    int64_t gk = ((int64_t)a.n_sets + 255) / 256;
-    if (gk > (int64_t)sms * 4) gk = (int64_t)sms * 4;
+    int64_t gk = ((int64_t)a.n_sets * (nsub - 1) + 255) / 256;
+    if (gk > (int64_t)sms * 8) gk = (int64_t)sms * 8;
     uint8_t *lvl = reinterpret_cast<uint8_t *>(sphist + (size_t)nsub * sp_keys);
     k_sp_level<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, lvl);
     k_sp_hist<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, lvl);
-    k_sp_scan<<<1, 256, 0, st>>>(sphist, nsub, sp_keys);
+    k_sp_scan<<<nsub - 1, 32, 0, st>>>(sphist, sp_keys);
     k_sp_scatter<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm, lvl);
     a.sperm = sperm;
   }
