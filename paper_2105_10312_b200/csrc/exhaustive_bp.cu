@@ -30,6 +30,9 @@ namespace gp {
 
 constexpr int kBpMaxN = 8;   // tasks per set (2^8 subset words per set)
 constexpr int kBpMaxM = 32;  // sizes per verdict word
+#ifndef GP_BP_MINB
+#define GP_BP_MINB 4  // main-pass CTAs per SM the register budget targets (A/B: -DGP_BP_MINB=n)
+#endif
 #ifndef GP_BP_UNROLL
 #define GP_BP_UNROLL 2
 #endif
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(256) k_sp_scatter(const ExhArgs a, const uint3
 // assumed), okb is one contiguous range [fb, e) and adds P[rk + e] - P[rk + fb];
 // otherwise the contiguous ranges of okb are walked one by one.
 template <bool kWin, int kHash, bool kBits, bool kStats>
-__global__ void __launch_bounds__(kWarps * 32, 4)
+__global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     k_exh_bp(const ExhArgs a, const uint32_t *memo, const uint32_t *rgs, const uint64_t *P) {
   const int n = a.n, M = a.M;
   const int lane = threadIdx.x & 31;
