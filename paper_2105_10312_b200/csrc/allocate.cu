@@ -50,6 +50,17 @@ struct AllocArgs {
   AllocVariantOpts vo;        // f4
 };
 
+#ifndef GP_ALLOC_NS2
+#define GP_ALLOC_NS2 0
+#endif
+#ifndef GP_ALLOC_NS4
+#define GP_ALLOC_NS4 1
+#endif
+// lane-serial merge instantiations for <= 2 and <= 4 tasks (each one is more code for the
+// instruction cache, which the divergent groups of a warp already stress: A/B-measured)
+constexpr bool kAllocNs2 = GP_ALLOC_NS2;
+constexpr bool kAllocNs4 = GP_ALLOC_NS4;
+
 // A group of G lanes of one warp works on one task set (G = 8, 16 or 32: the
 // smallest power of two >= n), so small sets share a warp.  Every collective is
 // over the group's lanes (mask gmask, shuffles of width G); groups of a warp may
@@ -475,9 +486,9 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
               int32_t got = 0, uh = 0;
               if (lane < E) {
                 const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
-                if (maxcnt <= 2)
+                if (kAllocNs2 && maxcnt <= 2)
                   got = serial_merge<2, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
-                else if (maxcnt <= 4)
+                else if (kAllocNs4 && maxcnt <= 4)
                   got = serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
                 else
                   got = serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
@@ -512,7 +523,9 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
               if ((failQ >> lane) & 1u) pex |= 1u << P;
               done_round = true;
             }
-            for (int r = 0; r < len && !done_round; ++r) {
+            // (groups of 8 lanes hold <= 8 tasks: every merge is lane-parallel, the
+            // group-cooperative fallback is compiled out -- smaller code, fewer I-cache misses)
+            for (int r = 0; G > 8 && r < len && !done_round; ++r) {
               const int Q = scr.bord[r];
               if (!((elig >> Q) & 1u)) continue;
               const uint32_t pmQ = g.shfl(pm, Q);
