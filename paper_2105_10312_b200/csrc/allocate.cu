@@ -248,8 +248,12 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
   return search_sizes<kGen>(z, lo, hi, test);
 }
 
-template <bool kGen, int G>
+// kV >= 0: the variant is a compile-time constant (one kernel per variant: each carries only
+// its own code, e.g. no ACT prefill in INA, which keeps the instruction working set small);
+// kV = -1: runtime variant (the f4 kGen kernels)
+template <bool kGen, int G, int kV>
 __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
+  const int variant = kV >= 0 ? kV : a.variant;
   __shared__ WarpScratch<G> scr_all[256 / G];
   extern __shared__ __align__(16) uint16_t wtab_all[];
   const Grp<G> g;
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
     scr.same[lane] = t.same;
     // per-set table of ceil(B_i/m) (the wave counts of C.1.3), if B fits 16 bits
     // (1G tests one size only: no table)
-    const bool tab_ok = wtab && a.variant != GP_1G && g.all(!t.in || t.B <= 65535);
+    const bool tab_ok = wtab && variant != GP_1G && g.all(!t.in || t.B <= 65535);
     g.sync();
     if (tab_ok) {
       for (int i = 0; i < n; ++i) {
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
 
     if (!contract) {
       tests = -1;
-    } else if (a.variant == GP_1G) {
+    } else if (variant == GP_1G) {
       // 1G: the whole GPU as one partition
       tests = 1;
       const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
@@ -339,8 +343,8 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
       psz = lane == 0 ? m1 : 0;
       stage = 1;
     } else {
-      const bool act = a.variant == GP_SMS_ACT || a.variant == GP_BF_ACT;
-      const bool sms = a.variant == GP_SMS_ACT || a.variant == GP_SMS_INA;
+      const bool act = variant == GP_SMS_ACT || variant == GP_BF_ACT;
+      const bool sms = variant == GP_SMS_ACT || variant == GP_SMS_INA;
       // Lemma 1: sum_i W_i(1,n) * (H/T_i) > M*H  =>  reject
       const int64_t w1 = t.in ? ((int64_t)t.B * t.cn + t.fn) * (int64_t)t.q : 0;
       const bool lemma1 = g.sum_i64(w1) <= (int64_t)M * H;
@@ -696,9 +700,18 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
               efficiency, stats, use_tab ? 1 : 0, nullptr, vo};
-  auto kern = G == 8 ? (gen ? k_allocate<true, 8> : k_allocate<false, 8>)
-              : G == 16 ? (gen ? k_allocate<true, 16> : k_allocate<false, 16>)
-                        : (gen ? k_allocate<true, 32> : k_allocate<false, 32>);
+  using KernFn = void (*)(AllocArgs);
+  static const KernFn kdef[3][5] = {
+      {k_allocate<false, 8, 0>, k_allocate<false, 8, 1>, k_allocate<false, 8, 2>,
+       k_allocate<false, 8, 3>, k_allocate<false, 8, 4>},
+      {k_allocate<false, 16, 0>, k_allocate<false, 16, 1>, k_allocate<false, 16, 2>,
+       k_allocate<false, 16, 3>, k_allocate<false, 16, 4>},
+      {k_allocate<false, 32, 0>, k_allocate<false, 32, 1>, k_allocate<false, 32, 2>,
+       k_allocate<false, 32, 3>, k_allocate<false, 32, 4>}};
+  const int gi = G == 8 ? 0 : (G == 16 ? 1 : 2);
+  const KernFn kern = gen ? (G == 8 ? k_allocate<true, 8, -1>
+                             : G == 16 ? k_allocate<true, 16, -1> : k_allocate<true, 32, -1>)
+                          : kdef[gi][(int)v];
   // dynamic + static shared memory may pass 48 KB (e.g. 16-lane groups: 16 scratches + tables)
   if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // persistent grid: one wave of resident CTAs; the set counter lives in a stream-ordered
