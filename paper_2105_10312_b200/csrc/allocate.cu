@@ -646,10 +646,11 @@ __global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
 
 }  // namespace gp
 
-// per-warp wave-table budget per CTA (A/B switch GP_ALLOC_TAB_KB, default 100 KB)
+// per-CTA wave-table budget (A/B switch GP_ALLOC_TAB_KB, default 40 KB: 3 CTAs per SM stay
+// resident next to the groups' scratch)
 static int tab_limit_kb() {
   const char *e = getenv("GP_ALLOC_TAB_KB");
-  return e ? atoi(e) : 100;
+  return e ? atoi(e) : 40;
 }
 
 extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *opts,
@@ -692,7 +693,9 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   if (const char *e = getenv("GP_ALLOC_G")) G = max(G, atoi(e) >= 32 ? 32 : (atoi(e) >= 16 ? 16 : 8));
   // per-group ceil(B/m) table: 256/G groups x n x M x 2 bytes when it fits (C4: 76 KB)
   size_t tab = (size_t)(256 / G) * ts->n_tasks * ts->M * sizeof(uint16_t);
-  const bool use_tab = tab <= (size_t)tab_limit_kb() * 1024;
+  // the table pays for itself only in the INA variants (most WCET evaluations per set), and
+  // only while it does not cost resident CTAs (A/B-measured on C2-C5)
+  const bool use_tab = (v == GP_SMS_INA || v == GP_BF_INA) && tab <= (size_t)tab_limit_kb() * 1024;
   if (!use_tab) tab = 0;
   const bool gen = vo.flags != 0 || vo.masked;
   size_t smem = tab;
