@@ -252,7 +252,9 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
 // its own code, e.g. no ACT prefill in INA, which keeps the instruction working set small);
 // kV = -1: runtime variant (the f4 kGen kernels)
 template <bool kGen, int G, int kV>
-__global__ void __launch_bounds__(256, 3) k_allocate(const AllocArgs a) {
+// register budget: 4 CTAs per SM for 8-lane groups (64 registers), 3 otherwise (80): A/B
+// measured -- the small-set kernels gain occupancy, the larger ones lose more to spills
+__global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArgs a) {
   const int variant = kV >= 0 ? kV : a.variant;
   __shared__ WarpScratch<G> scr_all[256 / G];
   extern __shared__ __align__(16) uint16_t wtab_all[];
