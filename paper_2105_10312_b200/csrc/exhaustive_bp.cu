@@ -30,6 +30,9 @@ namespace gp {
 
 constexpr int kBpMaxN = 8;   // tasks per set (2^8 subset words per set)
 constexpr int kBpMaxM = 32;  // sizes per verdict word
+#ifndef GP_MEMO_MINB
+#define GP_MEMO_MINB 4  // memo-pass CTAs per SM the register budget targets (A/B)
+#endif
 #ifndef GP_BP_MINB
 #define GP_BP_MINB 4  // main-pass CTAs per SM the register budget targets (A/B: -DGP_BP_MINB=n)
 #endif
@@ -88,7 +91,7 @@ GP_DEV bool memo_test(const MemoWarp &w, uint32_t S, int m, uint32_t mem, int32_
 }
 
 template <int NT>
-__global__ void __launch_bounds__(256, 3) k_exh_memo(const ExhArgs a, uint32_t *memo) {
+__global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a, uint32_t *memo) {
   __shared__ MemoWarp mw_all[8];
   __shared__ uint8_t sorder[1 << kBpMaxN];  // subsets 1 .. 2^n - 1 by (size, value)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
