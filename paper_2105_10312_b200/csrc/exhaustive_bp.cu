@@ -9,14 +9,19 @@
 //   m SMs) for all 2^n - 1 task subsets S -- C3: 63 x 20 = 1,260 EDF tests per
 //   set where the per-candidate evaluator runs ~2.3 million.  Every (S, m) is
 //   tested; no monotonicity in m is assumed (that is f3's GP_THRESHOLD).
-//   k_exh_bp: the same work items, rank windows and lexicographic candidate
-//   order as the per-candidate kernel (exhaustive.cu).  Candidates of one
-//   allocation with a common prefix (s_0..s_{k-2}) form a RUN in which only
-//   the last part moves (1 .. M - prefix sum); a lane evaluates a whole run
-//   segment in one word:  prefix_ok ? (V_{k-1} >> (s_{k-1} - 1)) & seg_mask : 0,
-//   i.e. up to 32 candidate verdicts per word operation, then records the set
-//   bits (count by popcount; pi* and first rank from the lowest bit; the
-//   verdict hash bit by bit; verdict bits with word-level atomics).
+//   k_sp_*: per subset, the sets ordered by (utilisation group, first passing
+//   size, load level): the lane order of the main pass (below).
+//   k_exh_bp: items = (32 sets, allocation pi), candidates in the rank order of
+//   C.1.6.  Candidates of pi that differ in the last part only form a RUN
+//   (last part 1 .. len); its verdicts are one word V_last & len_mask when the
+//   other blocks pass, i.e. up to 32 candidate verdicts per word operation.
+//   The warp walks pi's runs in lockstep -- outer parts by a successor, the
+//   third-to-last part with its block's word shifted per step, the
+//   second-to-last likewise per run -- visiting only the runs some lane's set
+//   can pass, and records the set bits: count by popcount (or range length),
+//   pi* and the first rank from the lowest bit, the verdict hash from a prefix
+//   table of splitmix64 over the rank space, verdict bits with word-level
+//   atomics (tests).
 // Outputs are byte-identical to the per-candidate evaluator (GP_EX_PER_CANDIDATE
 // selects that one, for A/B runs and parity).
 #include <stdlib.h>
@@ -195,53 +200,6 @@ __global__ void k_exh_rgs_table(const ExhArgs a, uint32_t *rgs) {
     while (g >= base + (uint32_t)a.L.n_pi[k]) base += (uint32_t)a.L.n_pi[k++];
     rgs[g] = (uint32_t)unrank_rgs(tab, k, g - base);  // 4 bits per task, n <= 8
   }
-}
-
-// Prefix index -> prefix (p_0..p_{kp-1}), parts >= 1, sum <= Mx, lexicographic;
-// stored reversed (pr[0] = p_{kp-1}).  C(Mx - c, r) counts the completions.
-GP_DEV void unrank_prefix_rev(const EnumTables &t, int kp, int Mx, uint32_t rho,
-                              int32_t (&pr)[kBpMaxN], int32_t &psum) {
-  int prev = 0;
-#pragma unroll
-  for (int j = 0; j < kBpMaxN; ++j) {
-    if (j < kp) {
-      int v = prev + 1;
-      for (;;) {
-        const uint32_t cnt = t.binom[(Mx - v) * (t.n + 1) + (kp - 1 - j)];
-        if (rho < cnt) break;
-        rho -= cnt;
-        ++v;
-      }
-#pragma unroll
-      for (int jj = 0; jj < kBpMaxN; ++jj)
-        if (jj == kp - 1 - j) pr[jj] = v - prev;
-      prev = v;
-    }
-  }
-  psum = prev;
-}
-
-// s-index (lexicographic rank among k-part size vectors, sum <= M) of the
-// vector (prefix, 1): sum over parts j of the vectors that differ first at j
-// with a smaller part, by the hockey-stick identity
-//   sum_{v=c_{j-1}+1}^{c_j - 1} C(M - v, k-1-j) = C(M - c_{j-1}, k-j) - C(M - c_j + 1, k-j)
-// (c_j = prefix sums).
-GP_DEV uint32_t run_start_sidx(const EnumTables &t, int k, int M, const int32_t (&pr)[kBpMaxN]) {
-  uint32_t r = 0;
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < kBpMaxN - 1; ++j) {
-    if (j < k - 1) {
-      int part = 0;
-#pragma unroll
-      for (int jj = 0; jj < kBpMaxN; ++jj)
-        if (jj == k - 2 - j) part = pr[jj];
-      const int cn = c + part;
-      r += t.C(M - c, k - j) - t.C(M - cn + 1, k - j);
-      c = cn;
-    }
-  }
-  return r;
 }
 
 // ---- verdict-hash prefix table: P[r] = sum_{x < r} splitmix64(x) mod 2^64 -------
