@@ -203,7 +203,7 @@ struct WarpScratch {
 template <int NS, bool kGen, class WS>
 GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, uint32_t S,
                             int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
-                            uint64_t &st_tasks, uint32_t &st_events) {
+                            uint64_t &st_tasks, uint32_t &st_events, int32_t stride = 1) {
   int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   const int cnt = __popc(S);
   uint32_t bits = S;
@@ -245,7 +245,13 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
     uh_out = UH;
     return true;
   };
-  return search_sizes<kGen>(z, lo, hi, test);
+  if constexpr (!kGen) {  // linear scan, every stride-th size (the packed rounds below)
+    for (int32_t m = lo; m <= hi; m += stride)
+      if (test(m)) return m;
+    return 0;
+  } else {
+    return search_sizes<kGen>(z, lo, hi, test);
+  }
 }
 
 // kV >= 0: the variant is a compile-time constant (one kernel per variant: each carries only
@@ -488,16 +494,39 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             if (maxcnt <= 8) {
               // every partner's merge scan runs on its own lane (exact: the scans
               // of one round are independent; only failures feed later rounds)
+              // With E <= G/2 partners, R = G/E lanes share each partner's linear scan:
+              // lane e + jE tests sizes lo + j, lo + j + R, ... and stops at its first
+              // success; the partner's first schedulable size is the minimum over its R
+              // lanes (the sequential scan's answer), and the tests the sequential scan
+              // performs -- first success - lo + 1, or all -- are what is counted.  (The
+              // f4 kGen scans keep one lane per partner.)
               int64_t my_tests = 0;
               int32_t got = 0, uh = 0;
-              if (lane < E) {
-                const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
+              const int R = (!kGen && E > 0 && E <= G / 2) ? G / E : 1;
+              const int eL = E > 0 ? lane % E : 0, rL = E > 0 ? lane / E : G;
+              const int QeL = g.shfl(Qe, eL);
+              const uint32_t SeL = pmP | g.shfl(pm, QeL);
+              const int32_t szQL = g.shfl(psz, QeL);
+              if (rL < R) {
+                const int32_t lo = max(szP, szQL) + rL, hi = szP + szQL - 1;
                 if (kAllocNs2 && maxcnt <= 2)
-                  got = serial_merge<2, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                  got = serial_merge<2, kGen>(scr, t.wv, z, SeL, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, R);
                 else if (kAllocNs4 && maxcnt <= 4)
-                  got = serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                  got = serial_merge<4, kGen>(scr, t.wv, z, SeL, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, R);
                 else
-                  got = serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events);
+                  got = serial_merge<8, kGen>(scr, t.wv, z, SeL, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, R);
+              }
+              for (int j = 1; j < R; ++j) {  // partner e's other lanes e + jE
+                const int src = min(lane + j * E, G - 1);
+                const int32_t g2 = g.shfl(got, src), u2 = g.shfl(uh, src);
+                if (lane < E && lane + j * E < G && g2 > 0 && (got == 0 || g2 < got)) {
+                  got = g2;
+                  uh = u2;
+                }
+              }
+              if (!kGen && lane < E) {
+                const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
+                my_tests = got > 0 ? got - lo + 1 : max(hi - lo + 1, 0);
               }
               const uint32_t succ = g.ballot(lane < E && got > 0);
               int cut = E;  // partners whose tests the sequential order performs
