@@ -302,15 +302,29 @@ __global__ void k_sp_level(const ExhArgs a, const uint32_t *memo, int nsub, uint
   }
 }
 
+// thread = (subset, set), sets fastest: the 32 sets of a warp mostly share a key (same
+// group, similar first passing size), so each warp adds once per distinct key
+// (warp-aggregated atomics via __match_any_sync).  The grid-stride loop keeps whole warps
+// in step (total is rounded up to a multiple of 32; lanes past the end carry no key).
+GP_DEV uint32_t sp_slot(const ExhArgs &a, const uint32_t *memo, int nsub, int nkeys, int64_t e,
+                        const uint8_t *lvl, int64_t &set, int &S) {
+  S = (int)(e / a.n_sets) + 1;
+  set = e - (int64_t)(S - 1) * a.n_sets;
+  return (uint32_t)S * (uint32_t)nkeys + (uint32_t)sp_key(a, memo + set * nsub, set, S, lvl);
+}
+
 __global__ void __launch_bounds__(256) k_sp_hist(const ExhArgs a, const uint32_t *memo, int nsub,
                                                  int nkeys, uint32_t *hist, const uint8_t *lvl) {
-  // thread = (set, subset), subset fastest: a warp's atomics go to different subsets' bins
   const int64_t total = a.n_sets * (int64_t)(nsub - 1);
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+  const int64_t total32 = (total + 31) & ~(int64_t)31;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total32;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t set = e / (nsub - 1);
-    const int S = (int)(e - set * (nsub - 1)) + 1;
-    atomicAdd(&hist[(size_t)S * nkeys + sp_key(a, memo + set * nsub, set, S, lvl)], 1u);
+    int64_t set;
+    int S;
+    const uint32_t slot = e < total ? sp_slot(a, memo, nsub, nkeys, e, lvl, set, S) : ~0u;
+    const uint32_t peers = __match_any_sync(GP_FULL, slot);
+    if (slot != ~0u && lane == __ffs(peers) - 1) atomicAdd(&hist[slot], (uint32_t)__popc(peers));
   }
 }
 
@@ -338,13 +352,20 @@ __global__ void __launch_bounds__(256) k_sp_scatter(const ExhArgs a, const uint3
                                                     int nkeys, uint32_t *offs, uint32_t *sperm,
                                                     const uint8_t *lvl) {
   const int64_t total = a.n_sets * (int64_t)(nsub - 1);
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+  const int64_t total32 = (total + 31) & ~(int64_t)31;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total32;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t set = e / (nsub - 1);
-    const int S = (int)(e - set * (nsub - 1)) + 1;
-    const uint32_t pos =
-        atomicAdd(&offs[(size_t)S * nkeys + sp_key(a, memo + set * nsub, set, S, lvl)], 1u);
-    sperm[(size_t)S * a.n_sets + pos] = (uint32_t)set;
+    int64_t set = 0;
+    int S = 0;
+    const uint32_t slot = e < total ? sp_slot(a, memo, nsub, nkeys, e, lvl, set, S) : ~0u;
+    const uint32_t peers = __match_any_sync(GP_FULL, slot);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (slot != ~0u && lane == leader) base = atomicAdd(&offs[slot], (uint32_t)__popc(peers));
+    base = __shfl_sync(GP_FULL, base, leader);
+    if (slot != ~0u)
+      sperm[(size_t)S * a.n_sets + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)set;
   }
 }
 
