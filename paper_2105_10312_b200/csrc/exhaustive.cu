@@ -626,26 +626,38 @@ __global__ void k_exh_init(int64_t *per_set, int32_t n_sets) {
 }
 
 __global__ void k_exh_finalize(const ExhArgs a) {
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.n_sets;
+  // whole warps iterate together (bound rounded up to 32) so the counts can be added once
+  // per distinct group per warp (__match_any_sync): consecutive sets share their group
+  const int lane = threadIdx.x & 31;
+  const int64_t n32 = ((int64_t)a.n_sets + 31) & ~(int64_t)31;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n32;
        g += (int64_t)gridDim.x * blockDim.x) {
-    int64_t *ps = a.per_set + g * 4;
-    const bool okc = set_contract(a, g) > 0;
-    if (!okc) {
-      ps[0] = -1; ps[1] = 0; ps[2] = -1; ps[3] = 0;
-    } else {
-      if (ps[1] == INT64_MAX) ps[1] = 0;
-      if (ps[2] == INT64_MAX) ps[2] = -1;
+    const bool in = g < a.n_sets;
+    bool okc = false;
+    if (in) {
+      int64_t *ps = a.per_set + g * 4;
+      okc = set_contract(a, g) > 0;
+      if (!okc) {
+        ps[0] = -1; ps[1] = 0; ps[2] = -1; ps[3] = 0;
+      } else {
+        if (ps[1] == INT64_MAX) ps[1] = 0;
+        if (ps[2] == INT64_MAX) ps[2] = -1;
+      }
     }
     if (a.counts) {
-      const int32_t grp = a.group[g];
-      if (grp < 0 || grp >= a.n_groups) continue;
-      const bool valid = okc && a.valid[g];
-      const bool exists = okc && ps[0] > 0;
-      unsigned long long *c = reinterpret_cast<unsigned long long *>(
-          a.counts + (((int64_t)a.setting * a.n_groups + grp) * a.n_slots + a.slot0) * 3);
-      if (exists && valid) atomicAdd(c + 0, 1ull);
-      atomicAdd(c + 1, 1ull);
-      if (!valid) atomicAdd(c + 2, 1ull);
+      const int32_t grp = in ? a.group[g] : -1;
+      const bool counted = grp >= 0 && grp < a.n_groups;
+      const bool valid = counted && okc && a.valid[g];
+      const bool exists = valid && a.per_set[g * 4] > 0;
+      const uint32_t peers = __match_any_sync(GP_FULL, counted ? grp : -1);
+      const uint32_t b_ok = __ballot_sync(GP_FULL, exists), b_inv = __ballot_sync(GP_FULL, counted && !valid);
+      if (counted && lane == __ffs(peers) - 1) {
+        unsigned long long *c = reinterpret_cast<unsigned long long *>(
+            a.counts + (((int64_t)a.setting * a.n_groups + grp) * a.n_slots + a.slot0) * 3);
+        if (b_ok & peers) atomicAdd(c + 0, (unsigned long long)__popc(b_ok & peers));
+        atomicAdd(c + 1, (unsigned long long)__popc(peers));
+        if (b_inv & peers) atomicAdd(c + 2, (unsigned long long)__popc(b_inv & peers));
+      }
     }
   }
 }

@@ -27,19 +27,33 @@ __global__ void __launch_bounds__(256) k_ratio(const RatioArgs a) {
   const int bins = a.n_groups * a.n_rows * 3;
   for (int e = threadIdx.x; e < bins; e += blockDim.x) hist[e] = 0;
   __syncthreads();
+  // whole warps iterate together; each warp adds once per distinct (group, row) bin
+  const int lane = threadIdx.x & 31;
   const int64_t total = (int64_t)a.n_sets * a.n_rows;
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+  const int64_t total32 = (total + 31) & ~(int64_t)31;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total32;
        x += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(x / a.n_sets);
-    const int64_t set = x - (int64_t)row * a.n_sets;
-    const int32_t g = a.group[set];
-    if (g < 0 || g >= a.n_groups) continue;
-    const bool valid = a.valid[set] != 0;
-    const bool ok = a.verdicts[x] != 0;
-    unsigned long long *h = hist + ((int64_t)g * a.n_rows + row) * 3;
-    if (ok && valid) atomicAdd(h + 0, 1ull);
-    atomicAdd(h + 1, 1ull);
-    if (!valid) atomicAdd(h + 2, 1ull);
+    int bin = -1;
+    bool valid = false, ok = false;
+    if (x < total) {
+      const int row = (int)(x / a.n_sets);
+      const int64_t set = x - (int64_t)row * a.n_sets;
+      const int32_t g = a.group[set];
+      if (g >= 0 && g < a.n_groups) {
+        bin = g * a.n_rows + row;
+        valid = a.valid[set] != 0;
+        ok = a.verdicts[x] != 0;
+      }
+    }
+    const uint32_t peers = __match_any_sync(GP_FULL, bin);
+    const uint32_t b_ok = __ballot_sync(GP_FULL, bin >= 0 && ok && valid);
+    const uint32_t b_inv = __ballot_sync(GP_FULL, bin >= 0 && !valid);
+    if (bin >= 0 && lane == __ffs(peers) - 1) {
+      unsigned long long *h = hist + (int64_t)bin * 3;
+      if (b_ok & peers) atomicAdd(h + 0, (unsigned long long)__popc(b_ok & peers));
+      atomicAdd(h + 1, (unsigned long long)__popc(peers));
+      if (b_inv & peers) atomicAdd(h + 2, (unsigned long long)__popc(b_inv & peers));
+    }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < bins; e += blockDim.x) {
