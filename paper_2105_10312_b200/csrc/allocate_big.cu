@@ -32,6 +32,7 @@ struct BigArgs {
   int64_t *n_tests;
   int64_t *eff;
   unsigned long long *stats;
+  unsigned long long *next_set;  // work counter (zeroed per launch)
   AllocVariantOpts vo;  // f4
 };
 
@@ -200,7 +201,13 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
   uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // thread 0's copies
   uint64_t my_tasks = 0;
   uint32_t my_events = 0;
-  for (int64_t set = blockIdx.x; set < a.n_sets; set += gridDim.x) {
+  // persistent CTAs grabbing their next set from a counter (work per set varies widely)
+  for (;;) {
+    if (threadIdx.x == 0) s.bcast[3] = (int32_t)atomicAdd(a.next_set, 1ull);
+    __syncthreads();
+    const int64_t set = s.bcast[3];
+    __syncthreads();
+    if (set >= a.n_sets) break;
     // ---- load, contract, hyperperiod
     const bool in = t < n;
     const int64_t o = set * n + t;
@@ -598,7 +605,7 @@ gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, const gp::All
                                  cudaStream_t st) {
   using namespace gp;
   BigArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
-            ts->n_tasks, ts->M, v, ok, bot, bs, pi, k, n_tests, eff, stats, vo};
+            ts->n_tasks, ts->M, v, ok, bot, bs, pi, k, n_tests, eff, stats, nullptr, vo};
   const bool gen = vo.flags != 0 || vo.masked;
   size_t smem = sizeof(BigSmem);
   if (gen && vo.masked) smem = ((smem + 15) & ~(size_t)15) + sizeof(SizeTables);
@@ -609,6 +616,10 @@ gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, const gp::All
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)148 * occ;
   if (grid > ts->n_sets) grid = ts->n_sets;
+  if (cudaMallocAsync(reinterpret_cast<void **>(&a.next_set), 8, st) != cudaSuccess)
+    return gp_cuda_check("gp_allocate (n > 32): work counter");
+  cudaMemsetAsync(a.next_set, 0, 8, st);
   kern<<<(unsigned)grid, 256, smem, st>>>(a);
+  cudaFreeAsync(a.next_set, st);
   return gp_cuda_check("gp_allocate (n > 32)");
 }
