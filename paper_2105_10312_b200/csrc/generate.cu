@@ -21,6 +21,7 @@ struct GenArgs {
   int32_t M, n, n_bins, n_prm, sets_per_group, Q, n_periods, b_max;
   int32_t beta_c, beta_m, beta_den, kc, km, k_den, max_attempts, G, curve_gran;
   int32_t rep_count, n_sets;
+  uint32_t bden_mlo, bden_mhi;  // division by beta_den as a multiply: M = floor(2^64/d) + 1
   uint64_t rep_begin, seed;
   int32_t menu[kMaxMenu];
   uint64_t prm_q[kMaxPrm];
@@ -43,6 +44,16 @@ GP_DEV void philox4x32_10(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
+}
+
+// floor(n / d) for n < 2^32 and 2 <= d < 2^32 as floor(n * M / 2^64), M = floor(2^64/d) + 1
+// (or 2^64/d when d is a power of two): n*M/2^64 lies in [n/d, n/d + n/2^64] and the
+// fractional part of n/d is at most 1 - 1/d < 1 - 2^-32, so the floor is exact.
+// M = mhi * 2^32 + mlo; d = 1 is passed as mhi = mlo = 0 and returns n.
+GP_DEV uint32_t div_by_magic(uint32_t n, uint32_t mlo, uint32_t mhi) {
+  if ((mlo | mhi) == 0u) return n;
+  const uint64_t t = ((uint64_t)n * mlo) >> 32;
+  return (uint32_t)(((uint64_t)n * mhi + t) >> 32);
 }
 
 // One task of §7.1 from its draws; the discard test of A-9.
@@ -78,8 +89,8 @@ GP_DEV TaskDraw task_fields(const GenArgs &a, uint64_t u, int32_t pidx, int32_t 
   }
   // fn = ceil(a * beta_num / beta_den) without 64-bit division: a = qd*den + r
   const uint32_t bnum = typ ? (uint32_t)a.beta_m : (uint32_t)a.beta_c, bden = (uint32_t)a.beta_den;
-  const uint32_t qd = a32 / bden, rd = a32 - qd * bden;
-  d.fn = qd * bnum + (rd * bnum + bden - 1u) / bden;
+  const uint32_t qd = div_by_magic(a32, a.bden_mlo, a.bden_mhi), rd = a32 - qd * bden;
+  d.fn = qd * bnum + div_by_magic(rd * bnum + bden - 1u, a.bden_mlo, a.bden_mhi);
   const uint32_t waves = (uint32_t)ceil_div_pos(d.B, a.M);
   d.feasible = (uint64_t)waves * d.cn + d.fn <= (uint64_t)d.D;                   // A-9
   return d;
@@ -301,6 +312,12 @@ extern "C" gp_status gp_generate(const gp_gen_params *p, uint64_t seed, uint64_t
   a.M = p->M; a.n = p->n_tasks; a.n_bins = p->n_bins; a.n_prm = p->n_prm;
   a.sets_per_group = p->sets_per_group; a.Q = p->ticks_per_unit; a.n_periods = p->n_periods;
   a.b_max = p->b_max; a.beta_c = p->beta_c_num; a.beta_m = p->beta_m_num; a.beta_den = p->beta_den;
+  {
+    const uint64_t d = (uint64_t)p->beta_den;
+    const uint64_t mg = d >= 2 ? (~0ull) / d + 1ull : 0ull;  // exact: see div_by_magic
+    a.bden_mlo = (uint32_t)mg;
+    a.bden_mhi = (uint32_t)(mg >> 32);
+  }
   a.kc = p->kc_num; a.km = p->km_num; a.k_den = p->k_den; a.max_attempts = p->max_attempts;
   a.curve_gran = p->curve_gran;
   int G = 1;
