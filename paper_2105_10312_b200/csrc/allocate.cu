@@ -1,16 +1,20 @@
 // allocate.cu -- A5: the paper's partition-and-allocate heuristics and the 1G
-// baseline, one WARP per task set (gp_allocate).
+// baseline, one GROUP of G = 8, 16 or 32 lanes per task set (gp_allocate; the
+// smallest power of two >= n, so small sets share a warp; every collective is
+// group-masked), persistent warps grabbing sets from a counter, one kernel per
+// variant.
 //
 // Lane roles: lane i holds task i (its parameters, its Lemma 2 size, its
 // ACT forbidden row); lane s also holds partition SLOT s.  A live slot's index
 // is always the lowest task id of its partition (a merge keeps the lower
 // slot), so the par_list tie-break "lower min task id" (A-17) is the slot
 // index and canonical output labels are popcounts.  The per-partition EDF
-// test is warp-cooperative (lane = task of the partition): conflict flags via
+// test is group-cooperative (lane = task of the partition): conflict flags via
 // popcount on the type mask, U*H via a shuffle sum, the demand walk with a
 // shuffle-min over the next deadlines (gp_edf.cuh explains the exact L_a
 // cut-off).  The ACT prefill runs the n(n-1)/2 pair merges lane-parallel with
-// a per-lane two-task test.
+// a per-lane two-task test; Algorithm 2's merge scans of one round run one
+// partner per lane (G/E lanes per partner when E <= G/2, strided).
 //
 // Algorithm 1, Lemma 1, Lemma 2 (the minimal m is
 // computed in closed form m = ceil(B / floor((D - f)/c)), exact for the W
