@@ -16,6 +16,13 @@ import torch
 
 import gp_workloads as W
 import oracle
+from math import comb
+
+
+def W_stirling(n, k):
+    """Stirling numbers of the second kind (allocations with k blocks)."""
+    from math import factorial
+    return sum((-1) ** j * comb(k, j) * (k - j) ** n for j in range(k + 1)) // factorial(k)
 
 pytestmark = pytest.mark.gpu
 
@@ -184,6 +191,19 @@ def test_exhaustive_c2_bitmaps(G, ev):
     # the bench's launch configuration: no verdict bits, no stats
     per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
     assert (per2 == ref).all()
+    if ev == 0:  # GP_EX_STATS_EXT: 6 counters, + (set, run) pairs walked and live runs
+        st6 = torch.zeros(6, dtype=torch.int64, device="cuda")
+        per3 = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
+        G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per3,
+                         work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"), stats=st6)
+        torch.cuda.synchronize()
+        s6 = st6.cpu().numpy()
+        assert (per3.cpu().numpy() == ref).all()
+        assert s6[0] == 1000 * 11334 and s6[1] == 1000 * 63 * 8  # candidates, memo tests
+        # every run holding a schedulable candidate is live; live runs <= runs walked
+        n_runs = 1000 * sum(W_stirling(6, k) * comb(7, k - 1) for k in range(1, 7))
+        assert 0 < s6[5] <= s6[4] <= n_runs
+        assert s6[5] >= (ref[:, 0] > 0).sum()
 
 
 @EVALUATORS
