@@ -643,3 +643,41 @@ def test_allocate_f4_hand_traces(G):
     assert list(r["block_of_task"][0]) == [0, 1, 0]
     r = G.gp_allocate(gpu_sets(G, pair), "SMS_ACT", sizes=[2, 4, 8, 10]).to_host()
     assert r["ok"][0] == 1 and r["block_size"][0][0] == 10
+
+
+# ------------------------------------------------------- bench-size launch configurations
+def test_exhaustive_c3_bench_size_sampled(G):
+    """C3 at the bench's size (10 bins x 10,000 sets = 6.95e10 candidates, the lane order
+    and every kernel of the timed call): 12 sets recomputed by the oracle, counts vs
+    per-set outputs on all 10^5 sets."""
+    gen = W.WORKLOADS["c3"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 10000, 6, 20, 10)
+    G.gp_generate(gen, W.SEED, 0, 10000, ts)
+    counts = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
+    per, _, st = run_exhaustive(G, ts, counts=counts, with_stats=False)
+    host = to_oracle(ts)
+    rng = np.random.default_rng(29)
+    sample = sorted(set([0, 31, 32, 9999, 50000, 99999] + [int(x) for x in rng.integers(0, 10**5, 6)]))
+    assert (per[sample] == oracle.exhaustive(host.subset(sample))).all()
+    c = counts.cpu().numpy()[0, :, 0]
+    exists = per[:, 0] > 0
+    for b in range(10):
+        rows = host.group == b
+        assert c[b, 1] == rows.sum() == 10000
+        assert c[b, 0] == (exists & rows & (host.valid == 1)).sum()
+
+
+def test_allocate_c4_bench_size_sampled(G):
+    """C4 at the bench's size (5 prm x 10 bins x 20,000 = 10^6 sets of 32 tasks, M = 148):
+    every output of 40 sampled sets per variant recomputed by the oracle."""
+    gen = W.WORKLOADS["c4"]["gen"](R=20000)
+    ts = G.TaskSets(50 * 20000, 32, 148, 50)
+    G.gp_generate(gen, W.SEED, 0, 20000, ts)
+    rng = np.random.default_rng(31)
+    sample = sorted(set([0, 1, 999999] + [int(x) for x in rng.integers(0, 10**6, 37)]))
+    host = to_oracle(ts).subset(sample)
+    for v in VARIANTS:
+        got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
+        ref = oracle.allocate(host, v)
+        for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
+            assert (got[key][sample] == ref[key]).all(), (v, key)
