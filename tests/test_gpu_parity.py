@@ -681,3 +681,38 @@ def test_allocate_c4_bench_size_sampled(G):
         ref = oracle.allocate(host, v)
         for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
             assert (got[key][sample] == ref[key]).all(), (v, key)
+
+
+def test_exhaustive_and_allocate_c2_bench_size_sampled(G):
+    """C2 at the bench's size (10^5 sets, M = 8): 200 sampled sets' exhaustive outputs and
+    heuristic outputs recomputed by the oracle."""
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 10000, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 10000, ts)
+    per, _, _ = run_exhaustive(G, ts, with_stats=False)
+    rng = np.random.default_rng(37)
+    sample = sorted(set([0, 99999] + [int(x) for x in rng.integers(0, 10**5, 198)]))
+    host = to_oracle(ts).subset(sample)
+    assert (per[sample] == oracle.exhaustive(host)).all()
+    for v in VARIANTS:
+        got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
+        ref = oracle.allocate(host, v)
+        for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
+            assert (got[key][sample] == ref[key]).all(), (v, key)
+
+
+def test_allocate_c5_bench_size_sampled(G):
+    """C5 at the bench's size (10^5 sets of 16 tasks, M = 68) for 3 of the 16 coefficient
+    settings: 40 sampled sets per variant recomputed by the oracle."""
+    rng = np.random.default_rng(41)
+    sample = sorted(set([0, 99999] + [int(x) for x in rng.integers(0, 10**5, 38)]))
+    for kc, km in (W.C5_SETTINGS[0], W.C5_SETTINGS[6], W.C5_SETTINGS[15]):
+        gen = W.WORKLOADS["c5"]["gen"](R=10000, kc=kc, km=km)
+        ts = G.TaskSets(10 * 10000, 16, 68, 10)
+        G.gp_generate(gen, W.SEED, 0, 10000, ts)
+        host = to_oracle(ts).subset(sample)
+        for v in VARIANTS:
+            got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
+            ref = oracle.allocate(host, v)
+            for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
+                assert (got[key][sample] == ref[key]).all(), (kc, km, v, key)
