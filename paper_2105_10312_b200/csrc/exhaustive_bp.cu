@@ -126,11 +126,13 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
     }
     const int32_t H32 = (int32_t)H;
     for (int S = lane; S < nsub; S += 32) w.vs[S] = 0u;
-    for (int e = lane; e < n * 2 * M; e += 32) {  // W_i(m, x) table
-      const int i = e / (2 * M), r = e - i * 2 * M, x = r >= M ? 1 : 0, m = r - x * M + 1;
+    for (int i = 0; i < n; ++i) {  // W_i(m, x) table: lane = size (M <= 32)
       const int64_t o = set * n + i;
-      w.wt[(i * 2 + x) * kBpMaxM + m - 1] =
-          x ? wcet_sat(a.B[o], a.cc[o], a.fc[o], m) : wcet_sat(a.B[o], a.cn[o], a.fn[o], m);
+      const int32_t Bi = a.B[o], cni = a.cn[o], cci = a.cc[o], fni = a.fn[o], fci = a.fc[o];
+      if (lane < M) {
+        w.wt[(i * 2) * kBpMaxM + lane] = wcet_sat(Bi, cni, fni, lane + 1);
+        w.wt[(i * 2 + 1) * kBpMaxM + lane] = wcet_sat(Bi, cci, fci, lane + 1);
+      }
     }
     uint32_t mem = 0;  // type mask (memory-intensive tasks)
     if (lane < n) {
