@@ -90,6 +90,9 @@ def _declare(L):
     L.gpref_uunisort.argtypes = [C.c_int32, C.c_int64, P, P]
     L.gpref_task_fields.argtypes = [P, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P]
     L.gpref_efficiency.argtypes = [P, P, P]
+    L.gpref_fill_forbidden_list.argtypes = [P, C.c_int32, P, P]
+    L.gpref_select_partitions.argtypes = [P, C.c_int32, C.c_int32, P, P, C.c_int32, P, P, P,
+                                          C.c_int32, P, P, P]
     L.gpref_splitmix64.argtypes = [C.c_uint64]
     L.gpref_splitmix64.restype = C.c_uint64
 
@@ -341,6 +344,43 @@ def allocate(sets: Sets, variant, threads=None, flags=0, sizes=None):
     _check(lib().gpref_allocate_ex(C.byref(cs), v, C.byref(opts), _p(ok), _p(bot), _p(bs), _p(pi),
                                    _p(k), _p(nt), th), "allocate")
     return dict(ok=ok, block_of_task=bot, block_size=bs, pi=pi, k=k, n_tests=nt)
+
+
+def fill_forbidden_list(sets: Sets, set_idx=0):
+    """ACT prefill: (forbidden task-pair matrix [n][n], EDF tests run)."""
+    n = sets.n_tasks
+    forb = np.zeros((n, n), np.uint8)
+    nt = np.zeros(1, np.int64)
+    cs = sets._c()
+    _check(lib().gpref_fill_forbidden_list(C.byref(cs), set_idx, _p(forb), _p(nt)),
+           "fill_forbidden_list")
+    return forb, int(nt[0])
+
+
+def select_partitions(sets: Sets, parts, snapshots=(), forb=None, best_fit=False, set_idx=0):
+    """Algorithm 3 on a given state.  parts: list of (task-id
+    list, size); snapshots: list of (task-id list, task-id list) INA failures; forb:
+    ACT task-pair matrix or None.  Returns (selected task-id list or None, [elig
+    task-id lists in order])."""
+    def m(ids):
+        return sum(1 << i for i in ids)
+
+    def ids(mask):
+        return [i for i in range(64) if (int(mask) >> i) & 1]
+    masks = np.array([m(p) for p, _ in parts], np.uint64)
+    sizes = np.array([sz for _, sz in parts], np.int32)
+    sa = np.array([m(a) for a, _ in snapshots] or [0], np.uint64)
+    sb = np.array([m(b) for _, b in snapshots] or [0], np.uint64)
+    fb = None if forb is None else np.ascontiguousarray(forb, dtype=np.uint8)
+    sel = np.zeros(1, np.uint64)
+    elig = np.zeros(max(1, len(parts)), np.uint64)
+    ne = np.zeros(1, np.int32)
+    cs = sets._c()
+    _check(lib().gpref_select_partitions(C.byref(cs), set_idx, len(parts), _p(masks), _p(sizes),
+                                         len(snapshots), _p(sa), _p(sb),
+                                         None if fb is None else _p(fb), int(best_fit), _p(sel),
+                                         _p(elig), _p(ne)), "select_partitions")
+    return (ids(sel[0]) if sel[0] else None), [ids(x) for x in elig[:int(ne[0])]]
 
 
 def efficiency(sets: Sets, block_of_task):

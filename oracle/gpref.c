@@ -765,6 +765,76 @@ static int forbidden(const heur_t *h, const tmask *p, const tmask *q) {
   return 0;
 }
 
+/* init_partitions, Lemma 2: one singleton partition per task with
+ * |P| = min{m in 1..M : C^n(m) <= D} (f4: m admissible), inserted into
+ * par_list in order.  Returns Pi = sum of the sizes, or -1 if some task has
+ * no feasible size.                                                          */
+static int32_t init_partitions(heur_t *h) {
+  const gpref_sets *s = h->s;
+  int32_t n = h->n, set = h->set, Pi = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    int64_t b = (int64_t)set * n + i;
+    int32_t size = 0;
+    for (int32_t m = 1; m <= h->M; ++m) {
+      if (size_ok(h, m) && gpref_wcet(s->B[b], s->cn[b], s->fn[b], m) - s->D[b] <= 0) {
+        size = m;
+        break;
+      }
+    }
+    if (size == 0) return -1;
+    part_t p = {tm_single(i), size, 0};
+    p.uh = part_uh(h, &p.mask, size);
+    list_insert(h, p);
+    Pi += size;
+  }
+  return Pi;
+}
+
+/* Def. 5 order > as best fit (A-21): insertion sort of the eligible partners
+ * by their U*H descending, ties lower min task id.                          */
+static void sort_best_fit(part_t *cand, int32_t n_elig) {
+  for (int32_t x = 1; x < n_elig; ++x)
+    for (int32_t y = x; y > 0 && part_before(&cand[y], &cand[y - 1]); --y) {
+      part_t t = cand[y]; cand[y] = cand[y - 1]; cand[y - 1] = t;
+    }
+}
+
+/* §5.3 fill_forbidden_list (ACT, Alg. 1 line 3): "every couple of
+ * tasks is tested to check if they are mergeable" -- the Lemma-2 singleton
+ * partitions of every pair i < j (in task-id order) go through Algorithm 2;
+ * a failing pair is recorded as a forbidden TASK pair.  The
+ * singletons are the entries of par_list (one per task before any merge). */
+static void fill_forbidden_list(heur_t *h) {
+  int32_t n = h->n;
+  h->forb = (uint8_t *)calloc((size_t)n * n, 1);
+  part_t *single = (part_t *)calloc((size_t)n, sizeof(part_t));
+  for (int32_t q = 0; q < h->len; ++q) single[min_task(&h->list[q].mask)] = h->list[q];
+  for (int32_t i = 0; i < n; ++i)
+    for (int32_t j = i + 1; j < n; ++j)
+      if (merge(h, &single[i], &single[j]) == 0) h->forb[i * n + j] = h->forb[j * n + i] = 1;
+  free(single);
+}
+
+/* Algorithm 3 select_partitions: candidates in par_list order,
+ * choose_from = the head (A-18); forbidden(P) per Alg. 3 line 7 (snapshots,
+ * plus ACT's task pairs); elig = par_list minus P (A-26) minus
+ * forbidden(P), in par_list order (SMS evaluates every merge, so its order
+ * does not matter; BF sorts it afterwards, A-21).  Returns the index of P in
+ * par_list, or -1 when every candidate has an empty elig list.              */
+static int32_t select_partitions(const heur_t *h, part_t *cand, int32_t *n_elig) {
+  for (int32_t c = 0; c < h->len; ++c) {
+    *n_elig = 0;
+    for (int32_t q = 0; q < h->len; ++q) {
+      if (q == c) continue; /* P itself is not eligible (A-26) */
+      if (forbidden(h, &h->list[c].mask, &h->list[q].mask)) continue;
+      cand[(*n_elig)++] = h->list[q];
+    }
+    if (*n_elig > 0) return c;
+  }
+  *n_elig = 0;
+  return -1;
+}
+
 static void write_solution(const heur_t *h, int ok, uint8_t *okp, int16_t *bot, int16_t *bs,
                            int32_t *pi, int32_t *k, int64_t *nt, int with_parts) {
   int32_t n = h->n, set = h->set;
@@ -842,27 +912,11 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant,
     free(h);
     return;
   }
-  /* init_partitions, Lemma 2: |P| = min{m in 1..M : C^n(m) <= D}
-   * (f4: m admissible)                                                       */
-  int32_t Pi = 0;
-  for (int32_t i = 0; i < n; ++i) {
-    int64_t b = (int64_t)set * n + i;
-    int32_t size = 0;
-    for (int32_t m = 1; m <= M; ++m) {
-      if (size_ok(h, m) && gpref_wcet(s->B[b], s->cn[b], s->fn[b], m) - s->D[b] <= 0) {
-        size = m;
-        break;
-      }
-    }
-    if (size == 0) { /* no feasible size: fail */
-      write_solution(h, 0, okp, bot, bs, pi, kk, nt, 0);
-      free(h);
-      return;
-    }
-    part_t p = {tm_single(i), size, 0};
-    p.uh = part_uh(h, &p.mask, size);
-    list_insert(h, p);
-    Pi += size;
+  int32_t Pi = init_partitions(h);
+  if (Pi < 0) { /* no feasible size: fail */
+    write_solution(h, 0, okp, bot, bs, pi, kk, nt, 0);
+    free(h);
+    return;
   }
   /* Lemma 3: exit on success at any time -- before the ACT
    * prefill (reading A-24).                                                  */
@@ -872,30 +926,12 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant,
     return;
   }
   /* Alg. 1 line 3 / §5.3: ACT tests every couple of tasks. */
-  if (h->act) {
-    h->forb = (uint8_t *)calloc((size_t)n * n, 1);
-    part_t *single = (part_t *)calloc((size_t)n, sizeof(part_t));
-    for (int32_t q = 0; q < h->len; ++q) single[min_task(&h->list[q].mask)] = h->list[q];
-    for (int32_t i = 0; i < n; ++i)
-      for (int32_t j = i + 1; j < n; ++j)
-        if (merge(h, &single[i], &single[j]) == 0) h->forb[i * n + j] = h->forb[j * n + i] = 1;
-    free(single);
-  }
+  if (h->act) fill_forbidden_list(h);
   /* Alg. 1 lines 4-18 */
   while (Pi > M) {
-    /* Algorithm 3: select_partitions -- choose_from takes the head (A-18). */
-    int32_t sel = -1;
     int32_t n_elig = 0;
     part_t cand[GPREF_MAX_TASKS];
-    for (int32_t c = 0; c < h->len && sel < 0; ++c) {
-      n_elig = 0;
-      for (int32_t q = 0; q < h->len; ++q) {
-        if (q == c) continue; /* P itself is not eligible (A-26) */
-        if (forbidden(h, &h->list[c].mask, &h->list[q].mask)) continue;
-        cand[n_elig++] = h->list[q];
-      }
-      if (n_elig > 0) sel = c;
-    }
+    int32_t sel = select_partitions(h, cand, &n_elig);
     if (sel < 0) { /* Alg. 1 line 6-7: return false */
       write_solution(h, 0, okp, bot, bs, pi, kk, nt, 1);
       free(h->snaps);
@@ -936,10 +972,7 @@ static void allocate_one(const gpref_sets *s, int32_t set, int32_t variant,
       /* Def. 5 order > as best fit (A-21): sort the eligible partners by
        * their U*H descending, ties lower min task id; Alg. 1 repeat-loop:
        * try in order, record failures, commit the first success.           */
-      for (int32_t x = 1; x < n_elig; ++x) /* insertion sort */
-        for (int32_t y = x; y > 0 && part_before(&cand[y], &cand[y - 1]); --y) {
-          part_t t = cand[y]; cand[y] = cand[y - 1]; cand[y - 1] = t;
-        }
+      sort_best_fit(cand, n_elig);
       for (int32_t e = 0; e < n_elig; ++e) {
         int32_t m = merge(h, &P, &cand[e]);
         if (m == 0) {
@@ -1015,6 +1048,86 @@ int gpref_allocate_ex(const gpref_sets *s, int32_t variant, const gpref_alloc_op
   for (int32_t t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
   pthread_mutex_destroy(&j.mu);
   return 0;
+}
+
+/* Test entry points of two steps of Algorithm 1 in isolation (SPEC's
+ * select_partitions and fill_forbidden_list examples).  Both run
+ * the same static functions as gpref_allocate_ex.  Tasks < 64 (masks are
+ * one uint64 word).                                                         */
+static int heur_setup(heur_t *h, const gpref_sets *s, int32_t set) {
+  if (set < 0 || set >= s->n_sets || s->n_tasks < 1 || s->n_tasks > 64) return 1;
+  h->s = s; h->set = set; h->n = s->n_tasks; h->M = s->M;
+  int64_t Tv[64];
+  for (int32_t i = 0; i < h->n; ++i) Tv[i] = s->T[(int64_t)set * h->n + i];
+  return gpref_hyperperiod(h->n, Tv, &h->H) != 0 ? 2 : 0;
+}
+
+static tmask tm_from64(uint64_t w) {
+  tmask m;
+  memset(&m, 0, sizeof(m));
+  m.w[0] = w;
+  return m;
+}
+
+/* fill_forbidden_list: forb[i*n + j] = 1 iff the Lemma-2
+ * singletons of tasks i and j fail Algorithm 2; *n_tests = EDF tests run.
+ * Returns 3 if some task has no Lemma-2 size.                               */
+int gpref_fill_forbidden_list(const gpref_sets *s, int32_t set, uint8_t *forb,
+                              int64_t *n_tests) {
+  heur_t *h = (heur_t *)calloc(1, sizeof(heur_t));
+  int rc = heur_setup(h, s, set);
+  if (!rc && init_partitions(h) < 0) rc = 3;
+  if (!rc) {
+    fill_forbidden_list(h);
+    memcpy(forb, h->forb, (size_t)h->n * h->n);
+    *n_tests = h->n_tests;
+  }
+  free(h->forb);
+  free(h);
+  return rc;
+}
+
+/* select_partitions (Algorithm 3) on a given state: par_list =
+ * the n_parts partitions (task masks, sizes; inserted in par_list order by
+ * their U*H, so the input order does not matter), the INA snapshot pairs
+ * (snap_a[x], snap_b[x]) and, if forb != NULL, ACT's forbidden task pairs
+ * (n x n).  best_fit != 0 sorts elig as BF does (A-21).  Outputs the mask of
+ * the selected P (0 = none) and the elig masks in order.                    */
+int gpref_select_partitions(const gpref_sets *s, int32_t set, int32_t n_parts,
+                            const uint64_t *masks, const int32_t *sizes, int32_t n_snaps,
+                            const uint64_t *snap_a, const uint64_t *snap_b,
+                            const uint8_t *forb, int32_t best_fit, uint64_t *sel_mask,
+                            uint64_t *elig_masks, int32_t *n_elig) {
+  heur_t *h = (heur_t *)calloc(1, sizeof(heur_t));
+  int rc = heur_setup(h, s, set);
+  if (!rc && (n_parts < 1 || n_parts > 64)) rc = 1;
+  if (!rc) {
+    for (int32_t q = 0; q < n_parts; ++q) {
+      part_t p = {tm_from64(masks[q]), sizes[q], 0};
+      p.uh = part_uh(h, &p.mask, sizes[q]);
+      list_insert(h, p);
+    }
+    for (int32_t x = 0; x < n_snaps; ++x) {
+      tmask a = tm_from64(snap_a[x]), b = tm_from64(snap_b[x]);
+      add_to_forbidden_moves(h, &a, &b);
+    }
+    if (forb) {
+      h->act = 1;
+      h->forb = (uint8_t *)malloc((size_t)h->n * h->n);
+      memcpy(h->forb, forb, (size_t)h->n * h->n);
+    }
+    part_t cand[64];
+    int32_t ne = 0;
+    int32_t sel = select_partitions(h, cand, &ne);
+    if (best_fit) sort_best_fit(cand, ne);
+    *sel_mask = sel < 0 ? 0 : h->list[sel].mask.w[0];
+    for (int32_t e = 0; e < ne; ++e) elig_masks[e] = cand[e].mask.w[0];
+    *n_elig = ne;
+  }
+  free(h->snaps);
+  free(h->forb);
+  free(h);
+  return rc;
 }
 
 /* §8(f) f2: scheduled workload ("efficiency") of an allocation (P:965-966,

@@ -91,6 +91,15 @@ int gpref_allocate(const gpref_sets *s, int32_t variant, uint8_t *ok, int16_t *b
                    int16_t *block_size, int32_t *pi, int32_t *k, int64_t *n_tests,
                    int32_t n_threads);
 
+/* Two steps of Algorithm 1 in isolation (tests of SPEC S:280-296; tasks < 64) */
+int gpref_fill_forbidden_list(const gpref_sets *s, int32_t set, uint8_t *forb /*[n][n]*/,
+                              int64_t *n_tests);
+int gpref_select_partitions(const gpref_sets *s, int32_t set, int32_t n_parts,
+                            const uint64_t *masks, const int32_t *sizes, int32_t n_snaps,
+                            const uint64_t *snap_a, const uint64_t *snap_b,
+                            const uint8_t *forb /*[n][n] or NULL (INA)*/, int32_t best_fit,
+                            uint64_t *sel_mask, uint64_t *elig_masks, int32_t *n_elig);
+
 /* ---- f4: the variants the paper names ---- */
 enum { GPREF_AL_BINARY_MERGE = 1, /* Algorithm 2 by binary search */
        GPREF_AL_INCREASING = 2 }; /* par_list in increasing utilisation */
