@@ -317,7 +317,7 @@ def main():
                 G.gp_sched_ratio(pipe.ts, exh_mode, pipe.counts, slot0=0,
                                  n_slots=pipe.n_slots, setting=0, per_set=pipe.per_set,
                                  work_counter=pipe.work, stats=pipe.stats if stats else None,
-                                 stream=stream, flags=exh_flags)
+                                 stream=stream, flags=exh_flags, workspace=pipe.workspace)
                 if timed:
                     e1.record(stream)
                     dom_ev.append((e0, e1))
@@ -555,7 +555,8 @@ def run_e2e(G, pipe, stream, args, world, evals_rank):
                              flags=(G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0)
                              | (G.GP_EX_PER_CANDIDATE if args.per_candidate else 0),
                              slot0=0, n_slots=pipe.n_slots,
-                             per_set=pipe.per_set, work_counter=pipe.work, stream=stream)
+                             per_set=pipe.per_set, work_counter=pipe.work, stream=stream,
+                             workspace=pipe.workspace)
         for vi, v in enumerate(pipe.variants):
             G.gp_allocate(dev, v, pipe.alloc[vi], stream, stats=stats if with_stats else None)
         G.gp_sched_ratio(dev, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts,

@@ -13,7 +13,19 @@
  *    on the same thread) describes the first failing check.
  *  - Ownership: the CALLER allocates and frees every buffer.  Buffers marked
  *    "device" must be device (or managed) memory; "host" buffers are read
- *    during the call only.  The library makes no persistent allocations.
+ *    during the call only.  The library makes no persistent allocations and
+ *    changes no device or memory-pool attribute.  Scratch the caller does not
+ *    provide (gp_allocate's 8-byte set counter; gp_sched_ratio(EXHAUSTIVE)'s
+ *    workspace when gp_exhaustive_opts.workspace is NULL) is a stream-ordered
+ *    temporary: cudaMallocAsync on `stream` from the device's current memory
+ *    pool, cudaFreeAsync on `stream` after the call's last kernel.
+ *  - Reentrancy: no host-side mutable state (no static caches); calls may run
+ *    concurrently from several host threads on different streams / devices.
+ *    Kernel attributes (dynamic shared memory limits) are set per call.
+ *  - Configuration: there are no environment-variable switches.  Behaviour is
+ *    selected by arguments only (flags below); performance A/B variants are
+ *    compile-time macros of the build (-DGP_ALLOC_TAB_KB, -DGP_ALLOC_MIN_G,
+ *    -DGP_BP_MINB, -DGP_MEMO_MINB, -DGP_SP_LEVELS; defaults are the product).
  *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
  *    default stream).  Every device call only ENQUEUES work on that stream
  *    and returns; none synchronises.  Outputs are valid once the stream has
@@ -234,8 +246,8 @@ gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *
  *   verdicts are memoised per (task subset, size) -- 2^n - 1 subsets x M
  *   sizes, every one tested -- and each candidate's verdict is the AND of its
  *   blocks' memoised verdicts, evaluated 32 candidates per word along runs of
- *   the last part (a stream-ordered workspace of n_sets * 2^n * 4 bytes is
- *   allocated and freed on `stream`); GP_EX_PER_CANDIDATE forces the
+ *   the last part (workspace: gp_exhaustive_opts.workspace, or a stream-ordered
+ *   temporary, see gp_exhaustive_workspace_size); GP_EX_PER_CANDIDATE forces the
  *   per-candidate EDF tests.  Both give identical outputs.  Per set it writes ex->per_set[set][4] =
  *   {n_sched, pi_star = min sum(s) over schedulable candidates (0 if none),
  *   first_rank (-1 if none), hash = sum of splitmix64(rank) mod 2^64 over
@@ -272,11 +284,36 @@ typedef struct {
   uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0);
                                  GP_EX_PER_CANDIDATE (EXHAUSTIVE): force the per-candidate
                                  evaluator; GP_EX_STATS_EXT: stats has 6 slots (above);
-                                 unknown bits -> GP_EINVAL                                     */
+                                 test hooks (same outputs, other code paths):
+                                 GP_EX_FORCE_RANGES: the bit-sliced evaluator walks every
+                                 verdict word range by range (no contiguous fast path);
+                                 GP_EX_NATURAL_ORDER: the bit-sliced evaluator's lanes take
+                                 sets in index order (no per-subset lane order);
+                                 GP_EX_GENERIC: the per-candidate evaluator with runtime
+                                 block structure (no shape specialisation), implies
+                                 GP_EX_PER_CANDIDATE; unknown bits -> GP_EINVAL              */
+  void *workspace;            /* device scratch, 256-byte aligned, of at least
+                                 gp_exhaustive_workspace_size() bytes for this call's shapes
+                                 and flags, owned by the caller; NULL: a stream-ordered
+                                 temporary of that size is allocated and released on `stream` */
+  uint64_t workspace_bytes;   /* size of `workspace` (GP_EINVAL if too small)                  */
 } gp_exhaustive_opts;
 #define GP_EX_NO_HASH 1u
 #define GP_EX_PER_CANDIDATE 2u
 #define GP_EX_STATS_EXT 4u
+#define GP_EX_FORCE_RANGES 8u
+#define GP_EX_NATURAL_ORDER 16u
+#define GP_EX_GENERIC 32u
+
+/* HOST ONLY (no CUDA call): device workspace bytes gp_sched_ratio(mode, flags) needs
+ * for n_sets sets of n_tasks tasks on M SMs in n_groups groups -- the bit-sliced
+ * evaluator's memo words (n_sets * 2^n * 4 B), RGS labels, per-subset lane order and
+ * verdict-hash prefix table (8 B per rank when N_c < 2^24 and the hash is wanted);
+ * 0 for the per-candidate and threshold evaluators and for FROM_VERDICTS.  C3 with
+ * 10^5 sets: about 58 MB.  Errors: GP_EINVAL (shapes outside the EXHAUSTIVE limits). */
+gp_status gp_exhaustive_workspace_size(int32_t n_sets, int32_t n_tasks, int32_t M,
+                                       int32_t n_groups, gp_ratio_mode mode, uint32_t flags,
+                                       uint64_t *bytes /*host*/);
 
 gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode, const uint8_t *verdicts,
                          int32_t n_rows, int32_t slot0, int32_t n_slots, int32_t setting,

@@ -24,6 +24,11 @@ gp_status gp_cuda_check(const char *what) {
   return GP_OK;
 }
 
+gp_status gp_ok(void) {
+  g_err[0] = '\0';
+  return GP_OK;
+}
+
 extern "C" const char *gp_last_error(void) { return g_err; }
 
 // N_c(M, n) = sum_k S(n,k) C(M,k) (C.1.6), host-only, exact with 128-bit checks.

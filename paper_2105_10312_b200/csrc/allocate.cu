@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
       int32_t mi = 0;
       if (t.in && t.D - t.fn >= t.cn) {
         const int32_t K = (t.D - t.fn) / t.cn;  // waves allowed: ceil(B/m) <= K
-        const int32_t m0 = (t.B + K - 1) / K;
-        mi = m0 <= M ? (m0 < 1 ? 1 : m0) : 0;
+        const int64_t m0 = ((int64_t)t.B + K - 1) / K;  // 64-bit: B may reach INT32_MAX
+        mi = m0 <= M ? (m0 < 1 ? 1 : (int32_t)m0) : 0;
         if (kGen && mi) mi = z.round_up(mi);  // f4: smallest admissible size >= m0
       }
       const bool lemma2 = !g.ballot(t.in && mi == 0);
@@ -681,12 +681,15 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
 
 }  // namespace gp
 
-// per-CTA wave-table budget (A/B switch GP_ALLOC_TAB_KB, default 40 KB: 3 CTAs per SM stay
-// resident next to the groups' scratch)
-static int tab_limit_kb() {
-  const char *e = getenv("GP_ALLOC_TAB_KB");
-  return e ? atoi(e) : 40;
-}
+// per-CTA wave-table budget (compile-time A/B switch -DGP_ALLOC_TAB_KB=n, default 40 KB:
+// 3 CTAs per SM stay resident next to the groups' scratch)
+#ifndef GP_ALLOC_TAB_KB
+#define GP_ALLOC_TAB_KB 40
+#endif
+// minimum group width (compile-time A/B switch -DGP_ALLOC_MIN_G=8|16|32, default 8)
+#ifndef GP_ALLOC_MIN_G
+#define GP_ALLOC_MIN_G 8
+#endif
 
 extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *opts,
                                  uint8_t *ok, int16_t *block_of_task, int16_t *block_size,
@@ -722,15 +725,15 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   if (ts->n_tasks > kMaxTasks)  // 33..256 tasks: one CTA per set (allocate_big.cu)
     return gp_allocate_big_launch(ts, (int32_t)v, vo, ok, block_of_task, block_size, pi, k,
                                   n_tests, efficiency, stats, (cudaStream_t)stream);
-  // group width: the smallest of 8, 16, 32 lanes that holds the set's tasks (A/B switch
-  // GP_ALLOC_G forces a width >= that)
+  // group width: the smallest of 8, 16, 32 lanes that holds the set's tasks (and is at
+  // least GP_ALLOC_MIN_G)
   int G = ts->n_tasks <= 8 ? 8 : (ts->n_tasks <= 16 ? 16 : 32);
-  if (const char *e = getenv("GP_ALLOC_G")) G = max(G, atoi(e) >= 32 ? 32 : (atoi(e) >= 16 ? 16 : 8));
+  G = max(G, GP_ALLOC_MIN_G);
   // per-group ceil(B/m) table: 256/G groups x n x M x 2 bytes when it fits (C4: 76 KB)
   size_t tab = (size_t)(256 / G) * ts->n_tasks * ts->M * sizeof(uint16_t);
   // the table pays for itself only in the INA variants (most WCET evaluations per set), and
   // only while it does not cost resident CTAs (A/B-measured on C2-C5)
-  const bool use_tab = (v == GP_SMS_INA || v == GP_BF_INA) && tab <= (size_t)tab_limit_kb() * 1024;
+  const bool use_tab = (v == GP_SMS_INA || v == GP_BF_INA) && tab <= (size_t)GP_ALLOC_TAB_KB * 1024;
   if (!use_tab) tab = 0;
   const bool gen = vo.flags != 0 || vo.masked;
   size_t smem = tab;

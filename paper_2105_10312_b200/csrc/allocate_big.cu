@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
       int32_t mi = 0;
       if (in && s.D[t] - s.fn[t] >= s.cn[t]) {
         const int32_t K = (s.D[t] - s.fn[t]) / s.cn[t];
-        const int32_t m0 = (s.B[t] + K - 1) / K;
-        mi = m0 <= M ? max(m0, 1) : 0;
+        const int64_t m0 = ((int64_t)s.B[t] + K - 1) / K;  // 64-bit: B may reach INT32_MAX
+        mi = m0 <= M ? max((int32_t)m0, 1) : 0;
         if (kGen && mi) mi = z.round_up(mi);  // f4: smallest admissible size >= m0
       }
       const bool lemma2 = !__syncthreads_or(in && mi == 0);

@@ -662,17 +662,15 @@ __global__ void k_exh_finalize(const ExhArgs a) {
   }
 }
 
+// No host-side caches: the attribute and the occupancy are queried per call (per device,
+// thread-safe; microseconds against a launch of milliseconds).
 template <int NT>
 static gp_status launch_exh(ExhArgs &a, size_t smem, cudaStream_t st) {
-  static int occ = -1;
-  static size_t occ_smem = 0;
-  if (occ < 0 || occ_smem != smem) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_exhaustive<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exhaustive<NT>, kWarps * 32, smem);
-    occ_smem = smem;
-    if (occ < 1) occ = 1;
-  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_exhaustive<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exhaustive<NT>, kWarps * 32, smem);
+  if (occ < 1) occ = 1;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -749,7 +747,7 @@ static void build_shape_table(int n, const ExhArgs &a, ShapeTable &sh) {
 
 template <int N>
 static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
-  static ShapeTable sh;  // host staging, copied into the kernel parameters
+  ShapeTable sh;  // host staging (per call), copied into the kernel parameters
   build_shape_table(N, a, sh);
   if (sh.item_base[sh.n_shapes] != a.total_items)
     return gp_fail(GP_EINVAL, "EXHAUSTIVE: shape table does not cover the candidate space");
@@ -771,7 +769,29 @@ static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
 
 }  // namespace gp
 
-gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a, cudaStream_t st);
+gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a, void *ws, uint64_t ws_bytes,
+                                  cudaStream_t st);
+size_t gp_exhaustive_bp_workspace(const gp::RankLayout &L, int n, int M, int32_t n_sets,
+                                  int32_t n_groups, uint32_t flags);
+
+// Workspace of gp_sched_ratio for these shapes (gpart.h): the bit-sliced evaluator's
+// memo / lane-order / hash tables; 0 for the per-candidate and threshold evaluators.
+extern "C" gp_status gp_exhaustive_workspace_size(int32_t n_sets, int32_t n_tasks, int32_t M,
+                                                  int32_t n_groups, gp_ratio_mode mode,
+                                                  uint32_t flags, uint64_t *bytes) {
+  using namespace gp;
+  if (!bytes) return gp_fail(GP_EINVAL, "gp_exhaustive_workspace_size: null output");
+  if (n_sets < 0 || n_tasks < 1 || n_tasks > kEnumMaxTasks || M < 1 || M > kEnumMaxM)
+    return gp_fail(GP_EINVAL, "gp_exhaustive_workspace_size: need n_tasks <= 12, M <= 256");
+  *bytes = 0;
+  if (mode == GP_EXHAUSTIVE && !(flags & (GP_EX_PER_CANDIDATE | GP_EX_GENERIC))) {
+    RankLayout L;
+    gp_status s = rank_layout(M, n_tasks, &L, true);
+    if (s != GP_OK) return s;
+    *bytes = gp_exhaustive_bp_workspace(L, n_tasks, M, n_sets, n_groups, flags);
+  }
+  return gp_ok();
+}
 
 // Called by gp_sched_ratio (ratio.cu) for GP_EXHAUSTIVE.
 gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_slots,
@@ -799,7 +819,8 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   a.per_set = ex->per_set; a.bits = ex->verdict_bits; a.words = ex->words_per_set;
   a.counts = counts; a.slot0 = slot0; a.n_slots = n_slots; a.setting = setting;
   a.stats = ex->stats; a.work_counter = ex->work_counter;
-  if (ex->flags & ~(uint32_t)(GP_EX_NO_HASH | GP_EX_PER_CANDIDATE | GP_EX_STATS_EXT))
+  if (ex->flags & ~(uint32_t)(GP_EX_NO_HASH | GP_EX_PER_CANDIDATE | GP_EX_STATS_EXT |
+                              GP_EX_FORCE_RANGES | GP_EX_NATURAL_ORDER | GP_EX_GENERIC))
     return gp_fail(GP_EINVAL, "EXHAUSTIVE: unknown flags 0x%x", ex->flags);
   a.flags = ex->flags;
   uint64_t items = 0;
@@ -823,9 +844,8 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   k_exh_init<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(ex->per_set, ts->n_sets);
   // default for n <= 8, M <= 32: bit-sliced verdicts over memoised block
   // verdicts (exhaustive_bp.cu); otherwise, or on request, per candidate
-  static const bool percand_env = getenv("GP_EXH_PERCAND") != nullptr;  // A/B switch
-  if (n <= 8 && M <= 32 && !(ex->flags & GP_EX_PER_CANDIDATE) && !percand_env) {
-    gp_status r = gp_exhaustive_bp_launch(a, st);
+  if (n <= 8 && M <= 32 && !(ex->flags & (GP_EX_PER_CANDIDATE | GP_EX_GENERIC))) {
+    gp_status r = gp_exhaustive_bp_launch(a, ex->workspace, ex->workspace_bytes, st);
     if (r != GP_OK) return r;
     k_exh_finalize<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(a);
     return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) finalize");
@@ -835,8 +855,7 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   const size_t smem = (((enum_table_words(M, n) + 3) & ~(size_t)3) + per_warp * kWarps) * 4;
   if (smem > 227 * 1024) return gp_fail(GP_EINVAL, "EXHAUSTIVE: shared memory need %zu B too large", smem);
   gp_status r;
-  static const bool generic_only = getenv("GP_EXH_GENERIC") != nullptr;  // A/B switch
-  if (n <= kMaxShapeN && !generic_only) {
+  if (n <= kMaxShapeN && !(ex->flags & GP_EX_GENERIC)) {
     switch (n) {
       case 1: r = launch_shaped<1>(a, smem, st); break;
       case 2: r = launch_shaped<2>(a, smem, st); break;

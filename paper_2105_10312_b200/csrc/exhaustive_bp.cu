@@ -706,10 +706,55 @@ static void launch_bp_h(unsigned grid, const ExhArgs &a, const uint32_t *memo,
 
 }  // namespace gp
 
+namespace gp {
+// Workspace of one bit-sliced call, carved from one buffer (caller-provided or a
+// stream-ordered temporary): memo words [n_sets][2^n], RGS labels, the per-subset
+// lane order (slots, histograms, load levels) and the hash prefix table.
+struct BpLayout {
+  size_t memo_words, sp_words, sp_total, words32, bytes;
+  uint64_t n_rgs, n_ranks;
+  uint32_t nb;
+  int sp_keys;
+  bool use_sp, use_P;
+};
+
+static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_groups,
+                          uint32_t flags) {
+  BpLayout b{};
+  b.n_rgs = 0;
+  for (int k = 1; k <= L.kmax; ++k) b.n_rgs += L.n_pi[k];
+  b.memo_words = (size_t)n_sets * ((size_t)1 << n);
+  // hash prefix table over the rank space (when it is small enough and wanted)
+  b.use_P = !(flags & GP_EX_NO_HASH) && L.total < kMaxHashTable;
+  b.n_ranks = b.use_P ? L.total : 0;
+  b.nb = (uint32_t)((b.n_ranks + kScanBlock - 1) / kScanBlock);
+  // per-subset lane order (GP_EX_NATURAL_ORDER: off): nsub x n_sets slots + histograms
+  b.sp_words = (size_t)(1 << n) * n_sets;
+  b.use_sp = !(flags & GP_EX_NATURAL_ORDER) && n_sets > 32 && b.sp_words * 4 <= ((size_t)256 << 20);
+  b.sp_keys = (n_groups > 0 ? n_groups : 1) * kThrBins * kSpLevels + 1;
+  b.sp_total = b.use_sp ? b.sp_words + (size_t)(1 << n) * b.sp_keys + ((size_t)n_sets + 3) / 4 : 0;
+  b.words32 = (b.memo_words + b.n_rgs + b.sp_total + 1) & ~(size_t)1;  // 8-byte alignment after
+  // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
+  // entries past a run's end in lanes whose verdict word is zero there; never summed)
+  b.bytes = b.words32 * 4 + (b.use_P ? (b.n_ranks + 1 + kPpad + b.nb) * 8 : 0);
+  return b;
+}
+}  // namespace gp
+
+// Workspace bytes of the bit-sliced evaluator (0 when it would not run).
+size_t gp_exhaustive_bp_workspace(const gp::RankLayout &L, int n, int M, int32_t n_sets,
+                                  int32_t n_groups, uint32_t flags) {
+  if (n > gp::kBpMaxN || M > gp::kBpMaxM) return 0;
+  return gp::bp_layout(L, n, n_sets, n_groups, flags).bytes;
+}
+
 // Called by gp_exhaustive_launch (exhaustive.cu) when n <= 8, M <= 32 and the
 // caller did not ask for the per-candidate evaluator.  `a` is fully set up
-// (items, rank window, per_set initialised); finalize runs after.
-gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
+// (items, rank window, per_set initialised); finalize runs after.  `ws_user` /
+// `ws_bytes`: the caller's workspace (gp_exhaustive_opts), or NULL for a
+// stream-ordered temporary allocation released on `st`.
+gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t ws_bytes,
+                                  cudaStream_t st) {
   using namespace gp;
   const int n = a0.n, M = a0.M;
   if (n > kBpMaxN || M > kBpMaxM) return gp_fail(GP_EINVAL, "EXHAUSTIVE(bp): n <= 8, M <= 32");
@@ -718,7 +763,8 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   // RGS index with k blocks (rank order)
   ExhArgs a = a0;
   // test hook: take the range-by-range hash path even for contiguous verdict words
-  a.force_ranges = getenv("GP_EXH_RANGES") != nullptr;
+  a.force_ranges = (a.flags & GP_EX_FORCE_RANGES) != 0;
+  const BpLayout b = bp_layout(a.L, n, a.n_sets, a.n_groups, a.flags);
   uint64_t n_rgs = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
     a.rgs_base[k] = (uint32_t)n_rgs;
@@ -732,41 +778,25 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
   }
   a.items_per_set = n_rgs;
   a.total_items = items;
-  const size_t memo_words = (size_t)a.n_sets * ((size_t)1 << n);
-  // hash prefix table over the rank space (when it is small enough and wanted)
-  const bool use_P = !(a.flags & GP_EX_NO_HASH) && a.L.total < kMaxHashTable;
-  const uint64_t n_ranks = use_P ? a.L.total : 0;
-  const uint32_t nb = (uint32_t)((n_ranks + kScanBlock - 1) / kScanBlock);
-  // per-subset lane order (GP_EXH_NO_GROUPING: off): nsub x n_sets slots + histograms
-  const size_t sp_words = (size_t)(1 << n) * a.n_sets;
-  const bool use_sp = getenv("GP_EXH_NO_GROUPING") == nullptr && a.n_sets > 32 &&
-                      sp_words * 4 <= ((size_t)256 << 20);
-  const int sp_keys = (a.n_groups > 0 ? a.n_groups : 1) * kThrBins * kSpLevels + 1;
-  const size_t sp_total =
-      use_sp ? sp_words + (size_t)(1 << n) * sp_keys + ((size_t)a.n_sets + 3) / 4 : 0;
-  const size_t words32 = (memo_words + n_rgs + sp_total + 1) & ~(size_t)1;  // 8-byte alignment after
-  // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
-  // entries past a run's end in lanes whose verdict word is zero there; never summed)
-  const size_t bytes = words32 * 4 + (use_P ? (n_ranks + 1 + kPpad + nb) * 8 : 0);
+  const size_t memo_words = b.memo_words, sp_words = b.sp_words;
+  const bool use_P = b.use_P, use_sp = b.use_sp;
+  const uint64_t n_ranks = b.n_ranks;
+  const uint32_t nb = b.nb;
+  const int sp_keys = b.sp_keys;
   uint32_t *ws = nullptr;
-  {  // keep freed workspace in the device's default pool (no unmap/remap per call)
-    static int configured = -1;
-    int cur_dev = 0;
-    cudaGetDevice(&cur_dev);
-    if (configured != cur_dev) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, cur_dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      configured = cur_dev;
-    }
-  }
-  if (cudaMallocAsync(reinterpret_cast<void **>(&ws), bytes, st) != cudaSuccess)
+  if (ws_user) {
+    if (ws_bytes < b.bytes)
+      return gp_fail(GP_EINVAL, "EXHAUSTIVE: workspace of %llu B < the %zu B needed",
+                     (unsigned long long)ws_bytes, b.bytes);
+    if (reinterpret_cast<uintptr_t>(ws_user) & 255)
+      return gp_fail(GP_EINVAL, "EXHAUSTIVE: workspace must be 256-byte aligned");
+    ws = static_cast<uint32_t *>(ws_user);
+  } else if (cudaMallocAsync(reinterpret_cast<void **>(&ws), b.bytes, st) != cudaSuccess) {
     return gp_cuda_check("EXHAUSTIVE(bp): workspace allocation");
+  }
   uint32_t *memo = ws, *rgs = ws + memo_words;
   uint32_t *sperm = use_sp ? rgs + n_rgs : nullptr, *sphist = use_sp ? sperm + sp_words : nullptr;
-  uint64_t *P = use_P ? reinterpret_cast<uint64_t *>(ws + words32) : nullptr;
+  uint64_t *P = use_P ? reinterpret_cast<uint64_t *>(ws + b.words32) : nullptr;
   if (use_P) {
     uint64_t *btot = P + n_ranks + 1 + kPpad;
     k_hash_scan_local<<<nb, kScanBlock, 0, st>>>(P, n_ranks, btot);
@@ -818,6 +848,6 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, cudaStream_t st) {
     else launch_bp_h<false>((unsigned)grid, a, memo, rgs, P, st);
     r = gp_cuda_check("EXHAUSTIVE(bp) main kernel");
   }
-  cudaFreeAsync(ws, st);
+  if (!ws_user) cudaFreeAsync(ws, st);
   return r;
 }

@@ -60,19 +60,19 @@ GP_DEV int64_t lcm_capped(int64_t a, int64_t b, int64_t cap) {
   return q * b;
 }
 
-// ceil(B/m) for 0 <= B, 1 <= m <= 1024 without an integer division when B is
-// small (< 2^22: every generated set, b_max <= 4096): a float reciprocal
-// estimate is within 1 of the quotient and one correction each way makes it
-// exact.
+// ceil(B/m) for 0 <= B <= INT32_MAX, 1 <= m <= 1024 without an integer division
+// when B is small (< 2^22: every generated set, b_max <= 4096): a float
+// reciprocal estimate is within 1 of the quotient and one correction each way
+// makes it exact.  Larger B take a 64-bit division (B + m - 1 may exceed int32).
 GP_DEV int32_t ceil_div_pos(int32_t B, int32_t m) {
-  const int32_t num = B + m - 1;
   if (B < (1 << 22)) {
+    const int32_t num = B + m - 1;
     int32_t q = (int32_t)((float)num * __frcp_rn((float)m));
     q += (q + 1) * m <= num;
     q -= q * m > num;
     return q;
   }
-  return num / m;
+  return (int32_t)(((int64_t)B + m - 1) / m);
 }
 
 // W(m) = ceil(B/m)*c + f in 64-bit, saturated to INT32_MAX (C.1.3).
@@ -129,3 +129,4 @@ GP_DEV uint64_t splitmix64(uint64_t x) {
 // ---- host-side error plumbing (abi.cu) ---------------------------------------
 gp_status gp_fail(gp_status st, const char *fmt, ...);
 gp_status gp_cuda_check(const char *what);
+gp_status gp_ok(void);  // clears gp_last_error() (host-only calls: no CUDA API touched)

@@ -24,6 +24,9 @@ GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD = 0, 1, 2
 GP_EX_NO_HASH = 1
 GP_EX_PER_CANDIDATE = 2  # force the per-candidate EXHAUSTIVE evaluator
 GP_EX_STATS_EXT = 4  # stats has 6 slots: + (set, run) pairs walked, live runs (bit-sliced)
+GP_EX_FORCE_RANGES = 8  # test hook: bit-sliced evaluator walks verdict words range by range
+GP_EX_NATURAL_ORDER = 16  # test hook: bit-sliced evaluator without the per-subset lane order
+GP_EX_GENERIC = 32  # test hook: per-candidate evaluator without shape specialisation
 UINT64_MAX = 2**64 - 1
 
 FIELDS_I32 = ("T", "D", "B", "cn", "cc", "fn", "fc")
@@ -60,7 +63,8 @@ class _GenC(C.Structure):
 class _ExOptsC(C.Structure):
     _fields_ = [("rank_lo", C.c_uint64), ("rank_hi", C.c_uint64), ("per_set", C.c_void_p),
                 ("verdict_bits", C.c_void_p), ("words_per_set", C.c_int64),
-                ("work_counter", C.c_void_p), ("stats", C.c_void_p), ("flags", C.c_uint32)]
+                ("work_counter", C.c_void_p), ("stats", C.c_void_p), ("flags", C.c_uint32),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64)]
 
 
 _P = C.c_void_p
@@ -73,12 +77,14 @@ _lib.gp_wcet_per_sm.argtypes = [C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P]
 _lib.gp_allocate.argtypes = [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.gp_sched_ratio.argtypes = [_P, C.c_int32, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 _P, _P, _P]
+_lib.gp_exhaustive_workspace_size.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int32, C.c_uint32, _P]
 for _f in ("gp_generate", "gp_count_candidates", "gp_enumerate", "gp_wcet", "gp_wcet_per_sm",
-           "gp_allocate", "gp_sched_ratio"):
+           "gp_allocate", "gp_sched_ratio", "gp_exhaustive_workspace_size"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTS = ("gp_last_error", "gp_generate", "gp_count_candidates", "gp_enumerate", "gp_wcet",
-           "gp_wcet_per_sm", "gp_allocate", "gp_sched_ratio")
+           "gp_wcet_per_sm", "gp_allocate", "gp_sched_ratio", "gp_exhaustive_workspace_size")
 
 
 def gp_last_error() -> str:
@@ -165,6 +171,21 @@ def gp_count_candidates(M: int, n: int) -> int:
     out = C.c_uint64(0)
     _check(_lib.gp_count_candidates(M, n, C.byref(out)))
     return out.value
+
+
+def gp_exhaustive_workspace_size(n_sets, n_tasks, M, n_groups, mode=None, flags=0) -> int:
+    """Host-only: device workspace bytes of gp_sched_ratio(mode, flags) for these shapes."""
+    out = C.c_uint64(0)
+    mode = GP_EXHAUSTIVE if mode is None else mode
+    _check(_lib.gp_exhaustive_workspace_size(n_sets, n_tasks, M, n_groups, mode, flags,
+                                             C.byref(out)))
+    return out.value
+
+
+def exhaustive_workspace(ts, mode=None, flags=0, device="cuda"):
+    """A caller-owned workspace tensor for gp_sched_ratio on ``ts`` (None if 0 bytes)."""
+    nb = gp_exhaustive_workspace_size(ts.n_sets, ts.n_tasks, ts.M, ts.n_groups, mode, flags)
+    return torch.empty(nb, dtype=torch.uint8, device=device) if nb else None
 
 
 def gp_enumerate(M, n, first_rank, count, block_of_task=None, block_size=None, stream=None):
@@ -254,17 +275,22 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
 
 def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=None, setting=0,
                    per_set=None, verdict_bits=None, words_per_set=0, work_counter=None,
-                   stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None, flags=0):
+                   stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None, flags=0,
+                   workspace=None):
     """FROM_VERDICTS: verdicts uint8 [n_rows][n_sets]; EXHAUSTIVE: per_set int64 [n_sets][4]
     (+ work_counter int64 [>=1], optional verdict_bits int32/uint32 [n_sets][words], stats
-    int64 [4], or [6] for the bit-sliced evaluator's run counters).  counts int64 [n_settings][n_groups][n_slots][3] is accumulated."""
+    int64 [4], or [6] for the bit-sliced evaluator's run counters; optional workspace: a
+    uint8 device tensor of >= gp_exhaustive_workspace_size() bytes, else the call makes a
+    stream-ordered temporary).  counts int64 [n_settings][n_groups][n_slots][3] is
+    accumulated."""
     s = ts.struct()
     if stats is not None and stats.numel() >= 6 and mode == GP_EXHAUSTIVE:
         flags |= GP_EX_STATS_EXT
     if mode in (GP_EXHAUSTIVE, GP_THRESHOLD):
         n_rows = 1
         ex = _ExOptsC(rank_lo, rank_hi, _ptr(per_set), _ptr(verdict_bits), words_per_set,
-                      _ptr(work_counter), _ptr(stats), flags)
+                      _ptr(work_counter), _ptr(stats), flags, _ptr(workspace),
+                      0 if workspace is None else workspace.numel() * workspace.element_size())
         exp = C.byref(ex)
         vp = None
     else:

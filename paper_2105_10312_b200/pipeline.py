@@ -55,6 +55,8 @@ class Pipeline:
             self.per_set = torch.zeros((S, 4), dtype=torch.int64, device=device)
             self.work = torch.zeros(1, dtype=torch.int64, device=device)
             self.stats = torch.zeros(6, dtype=torch.int64, device=device) if stats else None
+            # caller-owned evaluator workspace (gpart.h: no hidden persistent allocations)
+            self.workspace = G.exhaustive_workspace(self.ts, device=device)
         else:
             self.n_cand = 0
 
@@ -78,7 +80,8 @@ class Pipeline:
             if self.exhaustive and si == 0:
                 G.gp_sched_ratio(self.ts, G.GP_EXHAUSTIVE, self.counts, slot0=0,
                                  n_slots=self.n_slots, setting=si, per_set=self.per_set,
-                                 work_counter=self.work, stats=self.stats, stream=stream)
+                                 work_counter=self.work, stats=self.stats, stream=stream,
+                                 workspace=self.workspace)
             for vi, v in enumerate(self.variants):
                 G.gp_allocate(self.ts, v, self.alloc[vi], stream)
             if self.variants:

@@ -147,7 +147,7 @@ EVALUATORS = pytest.mark.parametrize("ev", [0, 2], ids=["bitsliced", "per_candid
 
 
 def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1, flags=0,
-                   with_stats=True):
+                   with_stats=True, workspace=False):
     S = ts.n_sets
     total = G.gp_count_candidates(ts.M, ts.n_tasks)
     hi_ = total if hi is None else hi
@@ -159,7 +159,7 @@ def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slo
     G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, counts, slot0=slot0, n_slots=n_slots, per_set=per,
                      verdict_bits=vb, words_per_set=words if bits else 0, work_counter=work,
                      stats=stats if with_stats else None, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi,
-                     flags=flags)
+                     flags=flags, workspace=G.exhaustive_workspace(ts, flags=flags) if workspace else None)
     torch.cuda.synchronize()
     out = per.cpu().numpy()
     if bits:
@@ -220,12 +220,11 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
     per_timed, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)  # bench's timed call
     assert (per_timed == per).all()
     if ev == 0:  # the bit-sliced evaluator without its per-subset lane order
-        os.environ["GP_EXH_NO_GROUPING"] = "1"
-        try:
-            per_id, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
-        finally:
-            del os.environ["GP_EXH_NO_GROUPING"]
+        per_id, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NATURAL_ORDER, with_stats=False)
         assert (per_id == per).all()
+        # and with a caller-owned workspace (the pipeline's call) instead of the temporary
+        per_ws, _, _ = run_exhaustive(G, ts, with_stats=False, workspace=True)
+        assert (per_ws == per).all()
     host = to_oracle(ts)
     rng = np.random.default_rng(13)
     sample = sorted(set([0, 999, 5000, 9999] + [int(x) for x in rng.integers(0, 10000, 12)]))
@@ -243,29 +242,29 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
     assert ((per[:, 0] == 0) == (per[:, 2] == -1)).all()
 
 
-def test_exhaustive_bitsliced_range_walk(G, monkeypatch):
+def test_exhaustive_bitsliced_range_walk(G):
     """The bit-sliced evaluator's range-by-range hash walk (taken when a set's
     last-block verdict word is not one contiguous range; forced here by the
-    GP_EXH_RANGES test hook) gives the oracle's outputs: C2 bitmaps, the
+    GP_EX_FORCE_RANGES test hook) gives the oracle's outputs: C2 bitmaps, the
     no-bits / prefix-table call of the bench, rank windows and random sets."""
-    monkeypatch.setenv("GP_EXH_RANGES", "1")
+    FR = G.GP_EX_FORCE_RANGES
     gen = W.WORKLOADS["c2"]["gen"](R=10000)
     ts = G.TaskSets(10 * 100, 6, 8, 10)
     G.gp_generate(gen, W.SEED, 0, 100, ts)
     host = to_oracle(ts)
     ref, rbits = oracle.exhaustive(host, bits=True)
-    per, vb, _ = run_exhaustive(G, ts, bits=True)
+    per, vb, _ = run_exhaustive(G, ts, bits=True, flags=FR)
     assert (per == ref).all() and (vb == rbits).all()
-    per, _, _ = run_exhaustive(G, ts)
+    per, _, _ = run_exhaustive(G, ts, flags=FR)
     assert (per == ref).all()
     for lo, hi in [(5, 37), (100, 4100), (31, 65)]:
-        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi)
+        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi, flags=FR)
         r2, b2 = oracle.exhaustive(host, lo, hi, bits=True)
         assert (per == r2).all() and (vb == b2).all(), (lo, hi)
     for seed, n, M in [(4, 3, 4), (12, 6, 9), (14, 8, 12), (16, 3, 32)]:
         d = W.random_sets(np.random.default_rng(seed), 37, n, M, periods=(4, 6, 8, 12, 24),
                           b_max=2 * M + 3, cost_max=3)
-        per, vb, _ = run_exhaustive(G, gpu_sets(G, d), bits=True)
+        per, vb, _ = run_exhaustive(G, gpu_sets(G, d), bits=True, flags=FR)
         r2, b2 = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
         assert (per == r2).all() and (vb == b2).all(), (seed, n, M)
 
@@ -323,7 +322,86 @@ def test_exhaustive_no_hash_and_flag_validation(G):
     nh, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NO_HASH)
     assert (nh[:, :3] == full[:, :3]).all() and (nh[:, 3] == 0).all()
     with pytest.raises(G.GpError):
-        run_exhaustive(G, ts, flags=8)
+        run_exhaustive(G, ts, flags=64)
+
+
+def test_exhaustive_workspace_contract(G):
+    """gpart.h workspace convention: the host query sizes the bit-sliced evaluator's
+    scratch (0 for the per-candidate / threshold evaluators); a caller workspace gives
+    the temporary's outputs; a too-small or misaligned one is GP_EINVAL."""
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 20, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 20, ts)
+    nb = G.gp_exhaustive_workspace_size(ts.n_sets, 6, 8, 10)
+    assert nb >= ts.n_sets * 64 * 4  # memo words alone
+    assert G.gp_exhaustive_workspace_size(ts.n_sets, 6, 8, 10, flags=G.GP_EX_PER_CANDIDATE) == 0
+    assert G.gp_exhaustive_workspace_size(ts.n_sets, 6, 8, 10, mode=G.GP_THRESHOLD) == 0
+    assert G.gp_exhaustive_workspace_size(ts.n_sets, 6, 8, 10, flags=G.GP_EX_NO_HASH) < nb
+    ref, _, _ = run_exhaustive(G, ts)
+    got, _, _ = run_exhaustive(G, ts, workspace=True)
+    assert (got == ref).all()
+    per = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
+    work = torch.zeros(1, dtype=torch.int64, device="cuda")
+    small = torch.empty(nb - 8, dtype=torch.uint8, device="cuda")
+    with pytest.raises(G.GpError):
+        G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per, work_counter=work, workspace=small)
+    big = torch.empty(nb + 512, dtype=torch.uint8, device="cuda")
+    with pytest.raises(G.GpError):
+        G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per, work_counter=work,
+                         workspace=big[8:])
+
+
+@pytest.mark.parametrize("seed,n,M", [(21, 3, 5), (22, 5, 7), (23, 6, 9)])
+def test_exhaustive_generic_kernel_hook(G, seed, n, M):
+    """GP_EX_GENERIC (test hook): the per-candidate evaluator without shape
+    specialisation gives the oracle's bitmaps for n <= 6 too."""
+    d = W.random_sets(np.random.default_rng(seed), 37, n, M, periods=(4, 6, 8, 12, 24),
+                      b_max=2 * M + 3, cost_max=3)
+    per, vb, _ = run_exhaustive(G, gpu_sets(G, d), bits=True, flags=G.GP_EX_GENERIC)
+    ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
+    assert (per == ref).all() and (vb == rbits).all()
+
+
+def _huge_b_sets():
+    """Two tasks, T = D = 4e8 ticks (H (n+1) < 2^31), task 0 with B near INT32_MAX and
+    c = 1: W_0(m) = ceil(B/m) crosses D = 4e8 between m = 5 and m = 6, and B + m - 1
+    overflows int32 (the wave count must not wrap negative)."""
+    Bs = [2**31 - 1, 2**31 - 2, 2**31 - 8, 2**30 + 1, (1 << 22), (1 << 22) - 1, 1999999999]
+    S = len(Bs)
+    full = lambda x: np.full((S, 2), x, np.int32)  # noqa: E731
+    d = dict(M=8, n_groups=1, T=full(400_000_000), D=full(400_000_000), B=full(1), cn=full(1),
+             cc=full(2), fn=full(0), fc=full(0), type=np.tile(np.array([0, 1], np.uint8), (S, 1)),
+             valid=np.ones(S, np.uint8), group=np.zeros(S, np.int32))
+    d["B"][:, 0] = Bs
+    return d
+
+
+@EVALUATORS
+def test_exhaustive_huge_block_counts(G, ev):
+    d = _huge_b_sets()
+    per, vb, _ = run_exhaustive(G, gpu_sets(G, d), bits=True, flags=ev)
+    ref, rbits = oracle.exhaustive(oracle.Sets.from_dict(d), bits=True)
+    assert (per == ref).all() and (vb == rbits).all()
+    # the B ~ 2^31 sets are schedulable only where task 0 gets >= 6 SMs
+    assert (ref[:, 0] > 0).all() and (ref[:3, 0] < G.gp_count_candidates(8, 2)).all()
+
+
+def test_wcet_and_allocate_huge_block_counts(G):
+    d = _huge_b_sets()
+    ts = gpu_sets(G, d)
+    host = oracle.Sets.from_dict(d)
+    soc, bot, bs = [], [], []
+    for s_ in range(ts.n_sets):
+        for m in range(1, 9):
+            soc.append(s_)
+            bot.append([0, 1])
+            bs.append([m, 1])
+    w, cf = G.gp_wcet(ts, torch.tensor(soc, dtype=torch.int32, device="cuda"),
+                      torch.tensor(bot, dtype=torch.int8, device="cuda"),
+                      torch.tensor(bs, dtype=torch.int16, device="cuda"))
+    rw, rcf = oracle.wcet_batch(host, soc, bot, bs)
+    assert (w.cpu().numpy() == rw).all() and (cf.cpu().numpy() == rcf).all()
+    check_allocate(G, ts, host)
 
 
 # ------------------------------------------------------------------ A5
