@@ -36,6 +36,11 @@ def test_bench_line_contract(config):
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in r, k
     assert r["bound"] == "alu" and r["peak"] > 0 and r["frac"] > 0
+    # a roofline fraction: the timed kernels' own counted work cannot beat the issue peak
+    assert r["frac"] <= 1.0 and r["ops_per_step"] / (r["dominant_ms_per_step"] / 1e3) <= r["peak"] * 1e12
+    if config == "c3":  # the direct (per-candidate) path, measured in the same run
+        dr = r["direct"]
+        assert dr["value"] > 0 and 0 < dr["frac"] <= 1.0 and dr["ms_per_launch"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     cb = d["cpu_baseline"]
