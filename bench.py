@@ -51,7 +51,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c2", "c3", "c4", "c5"])
-    ap.add_argument("--reps", type=int, default=0, help="sets per (prm, bin) group per GPU")
+    ap.add_argument("--reps", type=int, default=0,
+                    help="sets per (prm, bin) group: per GPU (--split weak) or global")
+    ap.add_argument("--split", default="weak", choices=["weak", "sets", "ranks"],
+                    help="multi-GPU sharding (SURVEY 8(e)): weak = R sets/group per GPU; "
+                         "sets = R global sets/group split by set range (strong); ranks = all "
+                         "R global sets on every GPU, candidate-rank windows + per-set merge")
+    ap.add_argument("--strong", action="store_true", help="alias of --split sets")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-direct", action="store_true",
@@ -66,6 +72,8 @@ def parse():
                          "hash (parity check; counts and ratios do not need it)")
     a = ap.parse_args()
     a.reps = a.reps or DEFAULT_REPS[a.config]
+    if a.strong:
+        a.split = "sets"
     return a
 
 
@@ -296,11 +304,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; GP_BENCH_BACKEND=gloo lets several ranks share a GPU (a test of
+    # the N > 1 code path on a one-GPU box; timings from such a run are not scaling data)
+    backend = os.environ.get("GP_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     wl = W.WORKLOADS[args.config]
-    pipe = Pipeline(args.config, reps=args.reps, rank=rank, world=world)
+    pipe = Pipeline(args.config, reps=args.reps, rank=rank, world=world, split=args.split)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     alloc_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
@@ -310,39 +325,24 @@ def main():
         exh_flags |= G.GP_EX_PER_CANDIDATE
     if args.f3 and not pipe.exhaustive:
         raise SystemExit("--f3 needs an exhaustive config (c2, c3)")
+    if args.f3 and args.split == "ranks":
+        raise SystemExit("--f3 evaluates whole rank spaces: use --split weak|sets")
     dom_ev = []  # events around the dominant kernel's launches
 
     def step(timed, stats=False):
-        """One full step.  The dominant kernel is the exhaustive evaluator
-        when present, else the heuristics (gp_allocate)."""
-        for si, gen in enumerate(pipe.gens):
-            G.gp_generate(gen, pipe.seed, pipe.rep_begin, pipe.reps, pipe.ts, stream)
-            if pipe.exhaustive and si == 0:
-                e0 = e1 = None
-                if timed:
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                G.gp_sched_ratio(pipe.ts, exh_mode, pipe.counts, slot0=0,
-                                 n_slots=pipe.n_slots, setting=0, per_set=pipe.per_set,
-                                 work_counter=pipe.work, stats=pipe.stats if stats else None,
-                                 stream=stream, flags=exh_flags, workspace=pipe.workspace)
-                if timed:
-                    e1.record(stream)
-                    dom_ev.append((e0, e1))
-            a0 = a1 = None
-            if timed and not pipe.exhaustive:
-                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a0.record(stream)
-            for vi, v in enumerate(pipe.variants):
-                G.gp_allocate(pipe.ts, v, pipe.alloc[vi], stream,
-                              stats=alloc_stats if stats else None)
-            if a1 is not None:
-                a1.record(stream)
-                dom_ev.append((a0, a1))
-            G.gp_sched_ratio(pipe.ts, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts,
-                             slot0=1 if pipe.exhaustive else 0, n_slots=pipe.n_slots,
-                             setting=si, stream=stream)
-        allreduce_counts(pipe.counts)
+        """One full step (Pipeline.run).  The dominant kernel is the exhaustive evaluator
+        when present, else the heuristics (gp_allocate); its launches are bracketed by CUDA
+        events on the launching stream."""
+        ev = []
+
+        def hook(phase):
+            if timed:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                ev.append(e)
+        pipe.run(stream, mode=exh_mode, flags=exh_flags, stats=stats,
+                 alloc_stats=alloc_stats if stats else None, on_dominant=hook)
+        dom_ev.extend(zip(ev[0::2], ev[1::2]))
 
     for _ in range(args.warmup):
         step(False)
@@ -359,9 +359,10 @@ def main():
     direct_stats = exh_stats
     if pipe.exhaustive and not args.f3 and not args.per_candidate:
         pst = torch.zeros(4, dtype=torch.int64, device="cuda")
-        G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, pipe.counts, slot0=0, n_slots=pipe.n_slots,
-                         setting=0, per_set=pipe.per_set, work_counter=pipe.work, stats=pst,
-                         stream=stream, flags=G.GP_EX_PER_CANDIDATE)
+        G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, None, per_set=pipe.per_set,
+                         work_counter=pipe.work, stats=pst, stream=stream,
+                         flags=G.GP_EX_PER_CANDIDATE, rank_lo=pipe.rank_lo,
+                         rank_hi=pipe.rank_hi)
         torch.cuda.synchronize()
         direct_stats = pst.cpu().numpy().tolist()
     pipe.reset_counts()
@@ -397,7 +398,12 @@ def main():
     else:
         evals_rank = int(al_stats[0])
         unit_def = "one EDF-PDC test of a (task subset, size) pair run by the heuristics"
-    value = evals_rank * world * args.steps / (total_ms / 1e3)
+    # whole-job work: the sum over ranks (uneven strong splits differ per rank)
+    ev_t = torch.tensor([evals_rank], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ev_t, op=dist.ReduceOp.SUM)
+    evals_total = int(ev_t.item())
+    value = evals_total * args.steps / (total_ms / 1e3)
 
     # ---- roofline of the dominant kernel: essential int32 lane-ops per launch
     # (DESIGN.md "Roofline"): 3 per task of every tested block (W lookup,
@@ -481,21 +487,25 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(G, pipe, stream, args, world, evals_rank)
+        e2e = run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": "weak" if args.split == "weak" else "strong", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic",
         "config": {"workload": wl["name"] + ("+f3_threshold" if args.f3 else "")
                    + ("_hash" if args.f3 and args.f3_hash else ""),
                    "M": wl["M"], "n": wl["n"],
                    "sets_per_gpu": pipe.ts.n_sets, "global_sets": pipe.ts.n_sets * world,
                    "coefficient_settings": len(pipe.gens),
                    "candidates_per_set": pipe.n_cand if pipe.exhaustive else None,
-                   "evals_per_step": evals_rank * world, "eval_unit": unit_def,
+                   "evals_per_step": evals_total, "eval_unit": unit_def,
+                   "split": args.split,
                    "heuristic_edf_tests_per_step": int(al_stats[0]) * world,
-                   "variants": list(pipe.variants), "parallelism": f"dp{world}",
+                   "variants": list(pipe.variants),
+                   "parallelism": f"dp{world}" + ("" if args.split != "ranks"
+                                                  else " (candidate-rank windows)"),
                    "l2": "flushed between steps (256 MiB memset outside the events)",
                    "seed": W.SEED},
         "roofline": roof,
@@ -527,7 +537,8 @@ def time_direct(G, pipe, stream, flush, args, peak, direct_stats, world):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         G.gp_sched_ratio(pipe.ts, G.GP_EXHAUSTIVE, None, per_set=pipe.per_set,
-                         work_counter=pipe.work, stream=stream, flags=G.GP_EX_PER_CANDIDATE)
+                         work_counter=pipe.work, stream=stream, flags=G.GP_EX_PER_CANDIDATE,
+                         rank_lo=pipe.rank_lo, rank_hi=pipe.rank_hi)
         e1.record(stream)
         ms.append((e0, e1))
     torch.cuda.synchronize()
@@ -562,12 +573,14 @@ def launches_per_step(pipe, args=None):
     return n + 5 + (3 if pipe.n_cand < (1 << 24) else 0) + (4 if pipe.ts.n_sets > 32 else 0)
 
 
-def run_e2e(G, pipe, stream, args, world, evals_rank):
+def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
     """Host task sets (pinned) -> H2D -> evaluation -> D2H, through the C ABI.
     The host inputs are the first setting's task sets of this rank.  Every step copies
     its inputs H2D and its results D2H inside the timed region; the inputs of step k+1
     are copied on a second stream into a second device buffer while step k computes
-    (double buffering), so the copies overlap the evaluation."""
+    (double buffering), so the copies overlap the evaluation.  The evaluation is
+    Pipeline.run on the uploaded sets (same calls and collectives as the device-only
+    step, minus gp_generate)."""
     import torch
     fields = ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group")
     G.gp_generate(pipe.gens[0], pipe.seed, pipe.rep_begin, pipe.reps, pipe.ts, stream)
@@ -580,6 +593,8 @@ def run_e2e(G, pipe, stream, args, world, evals_rank):
     d2h = sum(t.numel() * t.element_size() for t in host_out)
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     copy_stream = torch.cuda.Stream()
+    settings = pipe.settings
+    pipe.settings = settings[:1]  # the host inputs are one setting's task sets
 
     def upload(dev, s):
         with torch.cuda.stream(s):
@@ -590,17 +605,8 @@ def run_e2e(G, pipe, stream, args, world, evals_rank):
         """The step's ABI calls on `stream`, then the D2H of its results."""
         with torch.cuda.stream(stream):
             pipe.counts.zero_()
-        if pipe.exhaustive:
-            G.gp_sched_ratio(dev, G.GP_THRESHOLD if args.f3 else G.GP_EXHAUSTIVE, pipe.counts,
-                             flags=(G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0)
-                             | (G.GP_EX_PER_CANDIDATE if args.per_candidate else 0),
-                             slot0=0, n_slots=pipe.n_slots,
-                             per_set=pipe.per_set, work_counter=pipe.work, stream=stream,
-                             workspace=pipe.workspace)
-        for vi, v in enumerate(pipe.variants):
-            G.gp_allocate(dev, v, pipe.alloc[vi], stream, stats=stats if with_stats else None)
-        G.gp_sched_ratio(dev, G.GP_FROM_VERDICTS, pipe.counts, verdicts=pipe.verdicts,
-                         slot0=1 if pipe.exhaustive else 0, n_slots=pipe.n_slots, stream=stream)
+        pipe.run(stream, mode=exh_mode, flags=exh_flags,
+                 alloc_stats=stats if with_stats else None, ts=dev)
         with torch.cuda.stream(stream):
             for h, d in zip(host_out, outs):
                 h.copy_(d, non_blocking=True)
@@ -631,17 +637,23 @@ def run_e2e(G, pipe, stream, args, world, evals_rank):
     run(1, with_stats=True)
     torch.cuda.synchronize()
     evals = pipe.candidates_per_step() if pipe.exhaustive else int(stats[0].item())
+    ev_t = torch.tensor([evals], dtype=torch.int64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ev_t, op=dist.ReduceOp.SUM)
+    evals = int(ev_t.item())
     run(2)
     torch.cuda.synchronize()
     a, b = run(args.steps)
     torch.cuda.synchronize()
+    pipe.settings = settings
     ms = a.elapsed_time(b)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"value": evals * world * args.steps / (ms / 1e3), "unit": UNIT,
+    return {"value": evals * args.steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.steps,
             "path": "pinned host task sets -> H2D (double-buffered on a copy stream) -> "
                     "gp_sched_ratio(EXHAUSTIVE) + gp_allocate x5 + gp_sched_ratio -> D2H counts, "

@@ -100,7 +100,9 @@ typedef struct {
 } gp_gen_params;
 
 typedef enum { GP_1G = 0, GP_SMS_ACT = 1, GP_SMS_INA = 2, GP_BF_ACT = 3, GP_BF_INA = 4 } gp_variant;
-typedef enum { GP_FROM_VERDICTS = 0, GP_EXHAUSTIVE = 1, GP_THRESHOLD = 2 } gp_ratio_mode;
+typedef enum {
+  GP_FROM_VERDICTS = 0, GP_EXHAUSTIVE = 1, GP_THRESHOLD = 2, GP_FROM_PER_SET = 3
+} gp_ratio_mode;
 
 /* ---------------------------------------------------------------------------
  * A1. gp_generate -- counter-based synthetic task sets (§7.1; C.1.10).
@@ -257,6 +259,12 @@ gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *
  *   per-window per_set rows merge by sum / min / min / sum).
  *   Limits: n_tasks <= 12, M <= 256, C(M,k) < 2^32; else GP_EINVAL; N_c >=
  *   2^63 -> GP_EOVERFLOW.
+ * mode GP_FROM_PER_SET: the EXHAUSTIVE counting from per-set outputs computed
+ *   elsewhere (ex->per_set, READ-ONLY [n_sets][4] in the EXHAUSTIVE convention, e.g.
+ *   the per-set merge of candidate-rank shards over several GPUs):
+ *   exists = n_sched > 0, a set with n_sched < 0 (contract violated) or valid = 0 is
+ *   counted invalid -- the counts equal those of one full-window EXHAUSTIVE call.
+ *   verdicts NULL, n_rows 1; only ex->per_set is read.
  * mode GP_THRESHOLD (a different work unit, reported
  *   separately): the same per_set outputs and counts as GP_EXHAUSTIVE, exact by
  *   resource monotonicity: per set, m*(S) = min{s : EDF-PDC(S,s)}

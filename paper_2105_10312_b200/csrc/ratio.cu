@@ -65,6 +65,41 @@ __global__ void __launch_bounds__(256) k_ratio(const RatioArgs a) {
   }
 }
 
+// GP_FROM_PER_SET: the EXHAUSTIVE finalize's counting from per-set outputs that were
+// produced elsewhere (e.g. merged over candidate-rank shards, §8(e)): exists = n_sched > 0;
+// n_sched < 0 (input contract violated) or valid = 0 counts as invalid.
+struct PerSetArgs {
+  const int64_t *per_set;
+  const uint8_t *valid;
+  const int32_t *group;
+  int32_t n_sets, n_groups, slot0, n_slots, setting;
+  int64_t *counts;
+};
+
+__global__ void __launch_bounds__(256) k_ratio_per_set(const PerSetArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n32 = ((int64_t)a.n_sets + 31) & ~(int64_t)31;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n32;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = g < a.n_sets;
+    const int32_t grp = in ? a.group[g] : -1;
+    const bool counted = grp >= 0 && grp < a.n_groups;
+    const int64_t ns = counted ? a.per_set[g * 4] : 0;
+    const bool valid = counted && ns >= 0 && a.valid[g];
+    const bool exists = valid && ns > 0;
+    const uint32_t peers = __match_any_sync(GP_FULL, counted ? grp : -1);
+    const uint32_t b_ok = __ballot_sync(GP_FULL, exists);
+    const uint32_t b_inv = __ballot_sync(GP_FULL, counted && !valid);
+    if (counted && lane == __ffs(peers) - 1) {
+      unsigned long long *c = reinterpret_cast<unsigned long long *>(
+          a.counts + (((int64_t)a.setting * a.n_groups + grp) * a.n_slots + a.slot0) * 3);
+      if (b_ok & peers) atomicAdd(c + 0, (unsigned long long)__popc(b_ok & peers));
+      atomicAdd(c + 1, (unsigned long long)__popc(peers));
+      if (b_inv & peers) atomicAdd(c + 2, (unsigned long long)__popc(b_inv & peers));
+    }
+  }
+}
+
 }  // namespace gp
 
 extern "C" gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode,
@@ -83,6 +118,17 @@ extern "C" gp_status gp_sched_ratio(const gp_tasksets *ts, gp_ratio_mode mode,
     if (verdicts || n_rows != 1) return gp_fail(GP_EINVAL, "EXHAUSTIVE: verdicts must be NULL, n_rows 1");
     if (mode == GP_THRESHOLD) return gp_threshold_launch(ts, slot0, n_slots, setting, counts, ex, st);
     return gp_exhaustive_launch(ts, slot0, n_slots, setting, counts, ex, st);
+  }
+  if (mode == GP_FROM_PER_SET) {
+    if (verdicts || n_rows != 1) return gp_fail(GP_EINVAL, "FROM_PER_SET: verdicts must be NULL, n_rows 1");
+    if (!ex || !ex->per_set || !counts)
+      return gp_fail(GP_EINVAL, "FROM_PER_SET: opts->per_set and counts are required");
+    if (ts->n_sets == 0) return gp_cuda_check("gp_sched_ratio");
+    PerSetArgs a{ex->per_set, ts->valid, ts->group, ts->n_sets, ts->n_groups, slot0, n_slots,
+                 setting, counts};
+    int64_t g1 = (ts->n_sets + 255) / 256;
+    k_ratio_per_set<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(a);
+    return gp_cuda_check("gp_sched_ratio(FROM_PER_SET)");
   }
   if (mode != GP_FROM_VERDICTS) return gp_fail(GP_EINVAL, "gp_sched_ratio: bad mode");
   if (ex) return gp_fail(GP_EINVAL, "FROM_VERDICTS: exhaustive options must be NULL");

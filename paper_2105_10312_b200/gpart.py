@@ -20,7 +20,7 @@ GP_OK, GP_EINVAL, GP_EOVERFLOW, GP_ECUDA = 0, 1, 2, 3
 GP_1G, GP_SMS_ACT, GP_SMS_INA, GP_BF_ACT, GP_BF_INA = range(5)
 VARIANTS = {"1G": GP_1G, "SMS_ACT": GP_SMS_ACT, "SMS_INA": GP_SMS_INA, "BF_ACT": GP_BF_ACT,
             "BF_INA": GP_BF_INA}
-GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD = 0, 1, 2
+GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD, GP_FROM_PER_SET = 0, 1, 2, 3
 GP_EX_NO_HASH = 1
 GP_EX_PER_CANDIDATE = 2  # force the per-candidate EXHAUSTIVE evaluator
 GP_EX_STATS_EXT = 4  # stats has 6 slots: + (set, run) pairs walked, live runs (bit-sliced)
@@ -135,6 +135,14 @@ class TaskSets:
         for f in ("type", "valid"):
             setattr(ts, f, torch.as_tensor(np.ascontiguousarray(d[f], np.uint8)).to(
                 device, non_blocking=non_blocking))
+        return ts
+
+    def slice(self, a: int, b: int) -> "TaskSets":
+        """Sets [a, b) as a view (no copy): the same device memory, offset pointers."""
+        ts = TaskSets.__new__(TaskSets)
+        ts.n_sets, ts.n_tasks, ts.M, ts.n_groups = b - a, self.n_tasks, self.M, self.n_groups
+        for f in FIELDS_I32 + ("type", "valid", "group"):
+            setattr(ts, f, getattr(self, f)[a:b])
         return ts
 
     def to_host(self) -> dict:
@@ -286,7 +294,7 @@ def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=N
     s = ts.struct()
     if stats is not None and stats.numel() >= 6 and mode == GP_EXHAUSTIVE:
         flags |= GP_EX_STATS_EXT
-    if mode in (GP_EXHAUSTIVE, GP_THRESHOLD):
+    if mode in (GP_EXHAUSTIVE, GP_THRESHOLD, GP_FROM_PER_SET):
         n_rows = 1
         ex = _ExOptsC(rank_lo, rank_hi, _ptr(per_set), _ptr(verdict_bits), words_per_set,
                       _ptr(work_counter), _ptr(stats), flags, _ptr(workspace),

@@ -2,10 +2,25 @@
 + WCET + EDF, fused) -> allocate (1G + 4 heuristics) -> ratio counts.
 
 Every stage is one C-ABI call (libgpart.so); this module only owns the
-device buffers (torch) and orders the calls on one stream.  Multi-GPU: rank r
-of W takes repetitions [r*reps, (r+1)*reps) of every (prm, bin) group, so all
-ranks see the same utilisation mix; the per-group counts are integers and
-one all-reduce (NCCL) sums them (``allreduce_counts``).
+device buffers (torch), orders the calls on one stream and issues the
+collectives of the multi-GPU modes:
+
+* ``split="weak"`` (default): rank r of W takes repetitions [r*R, (r+1)*R) of
+  every (prm, bin) group, R = ``reps`` per rank (per-GPU work fixed), so all
+  ranks see the same utilisation mix; one all-reduce sums the integer counts.
+* ``split="sets"`` (strong): ``reps`` is the GLOBAL number of repetitions per
+  group; rank r takes [floor(r R / W), floor((r+1) R / W)) of every group.
+* ``split="ranks"`` (strong, for few sets): every rank holds all ``reps``
+  global repetitions and evaluates the candidate-rank window
+  [floor(r N_c / W), floor((r+1) N_c / W)) of every set; the per-set outputs
+  are merged across ranks (sum n_sched, min pi*, min first_rank, sum hash mod
+  2^64: ``merge_window_shards``) before the exhaustive counts are taken
+  (gp_sched_ratio GP_FROM_PER_SET); the heuristics take set range
+  [floor(r S / W), floor((r+1) S / W)).
+
+Counter-based generation makes every shard byte-identical to the same sets of
+a one-process run, and integer sums / minima are order-independent, so every
+mode's counts (and, for "ranks", per-set outputs) equal one process's.
 """
 from __future__ import annotations
 
@@ -16,13 +31,26 @@ import gp_workloads as W
 
 from . import gpart as G
 
+SPLITS = ("weak", "sets", "ranks")
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+INT64_MAX = (1 << 63) - 1
+
 
 class Pipeline:
     def __init__(self, key: str, reps: int = None, rank: int = 0, world: int = 1,
                  device="cuda", exhaustive: bool = None, variants=None, settings=None,
-                 seed: int = W.SEED, stats: bool = True):
+                 seed: int = W.SEED, stats: bool = True, split: str = "weak"):
+        if split not in SPLITS:
+            raise ValueError(f"split must be one of {SPLITS}")
         wl = W.WORKLOADS[key]
-        self.key, self.wl, self.seed = key, wl, seed
+        self.key, self.wl, self.seed, self.split = key, wl, seed, split
         self.rank, self.world = rank, world
         self.M, self.n = wl["M"], wl["n"]
         self.exhaustive = wl["exhaustive"] if exhaustive is None else exhaustive
@@ -30,28 +58,40 @@ class Pipeline:
         self.device = device
         if key == "c1":
             self.host_sets = wl["sets"]()
-            self.gen = None
+            self.gens = []
             self.ts = G.TaskSets.from_host(self.host_sets, device)
             self.settings = [None]
+            self.rep_begin, self.reps = 0, 1
         else:
-            self.reps = reps
+            if split == "weak":
+                self.rep_begin, self.reps, R = shard_plan(rank, world, reps)
+            elif split == "sets":
+                self.rep_begin, self.reps, R = strong_shard_plan(rank, world, reps)
+            else:  # "ranks": all sets on every rank
+                self.rep_begin, self.reps, R = 0, reps, reps
             self.settings = settings or ([(12, 23)] if key != "c5" else W.C5_SETTINGS)
-            self.gens = [self._gen(kc, km) for kc, km in self.settings]
+            self.gens = [self._gen(kc, km, R) for kc, km in self.settings]
             g0 = self.gens[0]
             n_groups = g0["n_prm"] * g0["n_bins"]
-            self.ts = G.TaskSets(n_groups * reps, self.n, self.M, n_groups, device)
+            self.ts = G.TaskSets(n_groups * self.reps, self.n, self.M, n_groups, device)
         S = self.ts.n_sets
+        # the sets this rank's heuristics evaluate (all but in "ranks" mode)
+        self.h_lo, self.h_hi = (range_split(rank, world, S) if split == "ranks" else (0, S))
+        self.ts_h = self.ts.slice(self.h_lo, self.h_hi) if split == "ranks" else self.ts
+        Sh = self.h_hi - self.h_lo
         self.n_slots = (1 if self.exhaustive else 0) + len(self.variants)
         self.counts = torch.zeros((len(self.settings), self.ts.n_groups, self.n_slots, 3),
                                   dtype=torch.int64, device=device)
-        self.verdicts = torch.zeros((len(self.variants), S), dtype=torch.uint8, device=device)
+        self.verdicts = torch.zeros((len(self.variants), Sh), dtype=torch.uint8, device=device)
         self.alloc = []
         for vi in range(len(self.variants)):
-            out = G.AllocOut(S, self.n, device)
+            out = G.AllocOut(Sh, self.n, device)
             out.ok = self.verdicts[vi]  # gp_allocate writes its verdict row in place
             self.alloc.append(out)
         if self.exhaustive:
             self.n_cand = G.gp_count_candidates(self.M, self.n)
+            self.rank_lo, self.rank_hi = (range_split(rank, world, self.n_cand)
+                                          if split == "ranks" else (0, self.n_cand))
             self.per_set = torch.zeros((S, 4), dtype=torch.int64, device=device)
             self.work = torch.zeros(1, dtype=torch.int64, device=device)
             self.stats = torch.zeros(6, dtype=torch.int64, device=device) if stats else None
@@ -59,43 +99,65 @@ class Pipeline:
             self.workspace = G.exhaustive_workspace(self.ts, device=device)
         else:
             self.n_cand = 0
+            self.workspace = None
 
-    def _gen(self, kc, km):
+    def _gen(self, kc, km, R):
         wl = self.wl
         if self.key == "c5":
-            return wl["gen"](R=self.reps * self.world, kc=kc, km=km)
-        g = wl["gen"](R=self.reps * self.world)
+            return wl["gen"](R=R, kc=kc, km=km)
+        g = wl["gen"](R=R)
         g["kc_num"], g["km_num"] = kc, km
         return g
 
-    @property
-    def rep_begin(self):
-        return shard_plan(self.rank, self.world, self.reps)[0]
-
-    def run(self, stream=None):
-        """Enqueue one full step (no host synchronisation)."""
+    def run(self, stream=None, mode=G.GP_EXHAUSTIVE, flags=0, stats=False, alloc_stats=None,
+            on_dominant=None, ts=None):
+        """Enqueue one full step (no host synchronisation except the collectives of the
+        "ranks" split).  ``on_dominant(phase)`` is called with "begin"/"end" around the
+        exhaustive call (or around the heuristics when there is none): bench.py records its
+        CUDA events there.  ``ts``: evaluate these (already resident) task sets of the
+        same shape instead of generating (bench.py's end-to-end path: host -> device)."""
+        hook = on_dominant or (lambda phase: None)
+        generate = ts is None
+        ts = self.ts if ts is None else ts
+        ts_h = ts.slice(self.h_lo, self.h_hi) if self.split == "ranks" else ts
         for si, _ in enumerate(self.settings):
-            if self.gens_present:
-                G.gp_generate(self.gens[si], self.seed, self.rep_begin, self.reps, self.ts, stream)
+            if self.gens and generate:
+                G.gp_generate(self.gens[si], self.seed, self.rep_begin, self.reps, ts, stream)
             if self.exhaustive and si == 0:
-                G.gp_sched_ratio(self.ts, G.GP_EXHAUSTIVE, self.counts, slot0=0,
+                window = self.split == "ranks"
+                hook("begin")
+                G.gp_sched_ratio(ts, mode, None if window else self.counts, slot0=0,
                                  n_slots=self.n_slots, setting=si, per_set=self.per_set,
-                                 work_counter=self.work, stats=self.stats, stream=stream,
-                                 workspace=self.workspace)
+                                 work_counter=self.work,
+                                 stats=self.stats if stats else None, stream=stream,
+                                 flags=flags, workspace=self.workspace,
+                                 rank_lo=self.rank_lo,
+                                 rank_hi=G.UINT64_MAX if not window else self.rank_hi)
+                hook("end")
+                if window:
+                    with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                        merge_window_shards(self.per_set)
+                    if self.rank == 0:  # counted once, from the merged per-set outputs
+                        G.gp_sched_ratio(ts, G.GP_FROM_PER_SET, self.counts, slot0=0,
+                                         n_slots=self.n_slots, setting=si,
+                                         per_set=self.per_set, stream=stream)
+            if not self.exhaustive:
+                hook("begin")
             for vi, v in enumerate(self.variants):
-                G.gp_allocate(self.ts, v, self.alloc[vi], stream)
-            if self.variants:
-                G.gp_sched_ratio(self.ts, G.GP_FROM_VERDICTS, self.counts, verdicts=self.verdicts,
-                                 slot0=1 if self.exhaustive else 0, n_slots=self.n_slots,
-                                 setting=si, stream=stream)
-
-    @property
-    def gens_present(self):
-        return self.key != "c1"
+                G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats)
+            if not self.exhaustive:
+                hook("end")
+            if self.variants and ts_h.n_sets > 0:
+                G.gp_sched_ratio(ts_h, G.GP_FROM_VERDICTS, self.counts,
+                                 verdicts=self.verdicts, slot0=1 if self.exhaustive else 0,
+                                 n_slots=self.n_slots, setting=si, stream=stream)
+        allreduce_counts(self.counts)
 
     def candidates_per_step(self) -> int:
-        """Exhaustive candidate evaluations per step (the metric's unit)."""
-        return self.ts.n_sets * self.n_cand if self.exhaustive else 0
+        """Exhaustive candidate evaluations per step on this rank (the metric's unit)."""
+        if not self.exhaustive:
+            return 0
+        return self.ts.n_sets * (self.rank_hi - self.rank_lo)
 
     def heuristic_tests(self) -> int:
         return int(sum(int(a.n_tests.clamp(min=0).sum()) for a in self.alloc))
@@ -115,6 +177,65 @@ def shard_plan(rank: int, world: int, reps_per_rank: int):
     if not (0 <= rank < world) or reps_per_rank < 1:
         raise ValueError("bad shard")
     return rank * reps_per_rank, reps_per_rank, reps_per_rank * world
+
+
+def range_split(rank: int, world: int, total: int):
+    """[floor(r T / W), floor((r+1) T / W)): contiguous, disjoint, covering [0, T)."""
+    if not (0 <= rank < world) or total < 0:
+        raise ValueError("bad range split")
+    return rank * total // world, (rank + 1) * total // world
+
+
+def strong_shard_plan(rank: int, world: int, reps_global: int):
+    """Strong-scaling shard: the GLOBAL repetitions per group are fixed and rank r
+    takes its contiguous share of every group.  Returns (rep_begin, rep_count,
+    sets_per_group); needs reps_global >= world so that no rank is empty."""
+    if reps_global < world:
+        raise ValueError("strong split needs at least one repetition per rank")
+    lo, hi = range_split(rank, world, reps_global)
+    return lo, hi - lo, reps_global
+
+
+def pack_window_shard(per_set: torch.Tensor):
+    """One rank-window shard's per-set outputs (gpart.h EXHAUSTIVE convention) ->
+    (sum part [S][3], min part [S][2]) whose elementwise sums / minima over the
+    shards are the full window's: n_sched (a contract violation, -1 in every
+    shard, becomes -2^40 so the sum stays negative), the hash split into 32-bit
+    halves (sums cannot overflow), and pi*, first rank with "none" -> INT64_MAX."""
+    n, pi, first, h = per_set.unbind(1)
+    none = n <= 0
+    big = torch.full_like(n, INT64_MAX)
+    s = torch.stack([torch.where(n < 0, torch.full_like(n, -(1 << 40)), n),
+                     h & 0xFFFFFFFF, (h >> 32) & 0xFFFFFFFF], 1).contiguous()
+    m = torch.stack([torch.where(none, big, pi), torch.where(none, big, first)], 1).contiguous()
+    return s, m
+
+
+def unpack_window_shards(s: torch.Tensor, m: torch.Tensor, out: torch.Tensor):
+    """Inverse of pack_window_shard after the sum / min over shards."""
+    n = s[:, 0]
+    lo = s[:, 1] & 0xFFFFFFFF
+    hi = (s[:, 2] + (s[:, 1] >> 32)) & 0xFFFFFFFF
+    h = lo | (hi << 32)  # mod 2^64, as an int64 bit pattern
+    bad, none = n < 0, n == 0
+    z, m1 = torch.zeros_like(n), torch.full_like(n, -1)
+    out[:, 0] = torch.where(bad, m1, n)
+    out[:, 1] = torch.where(bad | none, z, m[:, 0])
+    out[:, 2] = torch.where(bad | none, m1, m[:, 1])
+    out[:, 3] = torch.where(bad | none, z, h)
+    return out
+
+
+def merge_window_shards(per_set: torch.Tensor, group=None):
+    """§8(e)'s per-set merge of candidate-rank shards, in place: sum n_sched, min pi*,
+    min first_rank, sum hash mod 2^64, over the ranks of the process group (two
+    all-reduces, SUM and MIN; the identity without a process group)."""
+    import torch.distributed as dist
+    s, m = pack_window_shard(per_set)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(m, op=dist.ReduceOp.MIN, group=group)
+    return unpack_window_shards(s, m, per_set)
 
 
 def allreduce_counts(counts: torch.Tensor):
