@@ -318,7 +318,7 @@ def main():
     pipe = Pipeline(args.config, reps=args.reps, rank=rank, world=world, split=args.split)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    alloc_stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    alloc_stats = torch.zeros(8, dtype=torch.int64, device="cuda")  # GP_AL_STATS_EXT layout
     exh_mode = G.GP_THRESHOLD if args.f3 else G.GP_EXHAUSTIVE
     exh_flags = G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0
     if args.per_candidate:
@@ -452,13 +452,22 @@ def main():
                  "direct_ops_per_step": float(direct_ops),
                  "direct_events_per_candidate": st[2] / max(st[0], 1)}
     else:
+        # the heuristics' own essential work, counted by the kernels: per EDF test actually
+        # run 3 ops per task (W lookup, C <= D, U multiply-add) + 4 per deadline examined,
+        # and per Algorithm 3 selection 2 mask ops per partition of par_list (eligibility
+        # test, rank compare) -- SURVEY 8(d)'s "O(k) mask ops per selection"
         st = al_stats
-        ops = 3 * st[1] + 4 * st[2]
+        ops = 3 * st[1] + 4 * st[2] + 2 * st[6]
         launches = len(pipe.variants) * len(pipe.gens)
         kname = "k_allocate (5 variants)"
-        per_unit = ops / max(st[0], 1)
-        extra = {"edf_tests_per_step": st[0], "tasks_tested_per_step": st[1],
-                 "deadlines_per_step": st[2], "sets_per_step": st[3]}
+        per_unit = ops / max(st[4], 1)
+        extra = {"ops_basis": "executed EDF tests (3/task + 4/deadline) + 2 per partition scanned "
+                              "by each Algorithm 3 selection, counted by the kernels",
+                 "edf_tests_per_step": st[0], "edf_tests_run_per_step": st[4],
+                 "tasks_tested_per_step": st[1], "deadlines_per_step": st[2],
+                 "sets_per_step": st[3], "selections_per_step": st[5],
+                 "partitions_scanned_per_step": st[6], "partner_searches_per_step": st[7],
+                 "ops_per_unit_is": "per EDF test run"}
     dom_s = sum(dom_ms) / args.steps / 1e3  # per step (sum of the dominant launches)
     if pipe.exhaustive and not args.f3 and not args.per_candidate:
         extra["effective_vs_direct"] = extra["direct_ops_per_step"] / dom_s / peak

@@ -193,9 +193,15 @@ gp_status gp_wcet_per_sm(int32_t B, int32_t m, const int32_t *cost_per_sm, int32
  * the set's hyperperiod H -- {lower = sum cn_i B_i H/T_i (no conflict),
  * upper = sum cc_i B_i H/T_i (all in conflict), achieved = sum c_i^x B_i H/T_i
  * for the reported partitions (0 when rejected by Lemma 1/2), H}.
- * stats: device uint64 [4] or NULL; += {EDF-PDC tests, tasks in tested
- * partitions, distinct deadlines examined by the demand walks, sets} (the
- * per-launch work figures of the roofline).
+ * Algorithm 2's size search (paper default): the first schedulable m of
+ * max(|P1|,|P2|) .. |P1|+|P2|-1 is found by one test at the top size and a
+ * binary search below it -- exact, since EDF-PDC(P, m) is monotone in m (C.1.3)
+ * -- while n_tests counts the tests of the paper's linear scan (first success -
+ * lo + 1, or the whole range), so every output equals the sequential algorithm's.
+ * stats: device uint64 [4] (or [8] with GP_AL_STATS_EXT) or NULL; += {EDF-PDC
+ * tests as n_tests counts them, tasks in the tests actually run, distinct
+ * deadlines examined by their demand walks, sets} (the per-launch work figures
+ * of the roofline).
  * opts: NULL or the f4 variants below.
  * Errors: GP_EINVAL (bad struct / variant / options), GP_ECUDA.
  * ------------------------------------------------------------------------- */
@@ -205,8 +211,11 @@ typedef enum {
                              candidate sizes (lo = 0, hi = |L|, mid = (lo+hi)/2).  Same
                              partitions as the linear scan (schedulability is monotone in m),
                              fewer EDF tests; only n_tests changes.                         */
-  GP_AL_INCREASING = 2    /* par_list in increasing utilisation order; ties by
+  GP_AL_INCREASING = 2,   /* par_list in increasing utilisation order; ties by
                              lower min task id.  Best-fit partner order stays U*H desc (A-21). */
+  GP_AL_STATS_EXT = 4     /* not a variant: `stats` has 8 slots; [4..7] += {EDF tests actually
+                             run, Algorithm 3 selections, partitions those selections scanned,
+                             Algorithm 2 partner searches} (the roofline's executed work)      */
 } gp_alloc_flag;
 
 /* f4 options of gp_allocate.  Host memory; NULL = the paper's

@@ -34,7 +34,7 @@
 gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, const gp::AllocVariantOpts &vo,
                                  uint8_t *ok, int16_t *bot, int16_t *bs, int32_t *pi, int32_t *k,
                                  int64_t *n_tests, int64_t *eff, unsigned long long *stats,
-                                 cudaStream_t st);
+                                 bool stats_ext, cudaStream_t st);
 
 namespace gp {
 
@@ -48,7 +48,10 @@ struct AllocArgs {
   int32_t *pi, *k;
   int64_t *n_tests;
   int64_t *eff;               // optional [n_sets][4]: scheduled workload (f2)
-  unsigned long long *stats;  // optional: += {EDF tests, tasks tested, deadlines examined, sets}
+  unsigned long long *stats;  // optional: += {EDF tests (paper's count), tasks tested, deadlines
+                              // examined, sets} [+ {tests run, selections, partitions scanned,
+                              // partner searches} with stats_ext]
+  int32_t stats_ext;
   int32_t use_tab;            // per-warp table of ceil(B_i/m) in dynamic shared memory
   unsigned long long *next_set;  // work counter (zeroed per launch)
   AllocVariantOpts vo;        // f4
@@ -201,13 +204,15 @@ struct WarpScratch {
   uint32_t same[G];
 };
 
-// Algorithm 2 merge of partition S (<= NS tasks) by ONE lane: sizes
-// m = lo .. hi in order (Def. 3 bound hi = |P1| + |P2| - 1), an EDF-PDC test
-// each.  Returns the first schedulable m (0 if none) and U*H there.
+// Algorithm 2 merge of partition S (<= NS tasks) by ONE lane: the first
+// schedulable m in lo .. hi (Def. 3 bound hi = |P1| + |P2| - 1; 0 if none) and
+// U*H there.  `counted` += the tests the paper's linear scan performs
+// (alg2_search: one probe at hi + binary search instead of the scan, exact by
+// monotonicity); `st_exec` += the tests actually run.
 template <int NS, bool kGen, class WS>
 GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, uint32_t S,
-                            int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
-                            uint64_t &st_tasks, uint32_t &st_events, int32_t stride = 1) {
+                            int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &counted,
+                            uint64_t &st_tasks, uint32_t &st_events, uint32_t &st_exec) {
   int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   const int cnt = __popc(S);
   uint32_t bits = S;
@@ -228,7 +233,7 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
   // one EDF-PDC test at size m; on success U*H is recorded (the last success
   // of a search is its answer)
   auto test = [&](int32_t m) -> bool {
-    ++tests;
+    ++st_exec;
     st_tasks += cnt;
     int32_t C[NS];
     bool bad = false;
@@ -249,13 +254,7 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
     uh_out = UH;
     return true;
   };
-  if constexpr (!kGen) {  // linear scan, every stride-th size (the packed rounds below)
-    for (int32_t m = lo; m <= hi; m += stride)
-      if (test(m)) return m;
-    return 0;
-  } else {
-    return search_sizes<kGen>(z, lo, hi, test);
-  }
+  return alg2_search<kGen>(z, lo, hi, test, counted);
 }
 
 // kV >= 0: the variant is a compile-time constant (one kernel per variant: each carries only
@@ -288,9 +287,10 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
     }
   }
   const uint32_t all = n == 32 ? GP_FULL : ((1u << n) - 1u);
-  uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // warp-uniform
+  uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // group-uniform
+  uint64_t st_exec = 0, st_rounds = 0, st_scan = 0, st_partners = 0; // group-uniform
   uint64_t st_pair_tasks = 0;                                        // per lane
-  uint32_t st_pair_events = 0;                                       // per lane
+  uint32_t st_pair_events = 0, st_pair_exec = 0;                     // per lane
   // persistent warps: each grabs its next set from a global counter (sets differ widely in
   // work -- utilisation bin, variant -- so a static stride leaves warps idle at the tail)
   for (;;) {
@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
     } else if (variant == GP_1G) {
       // 1G: the whole GPU as one partition
       tests = 1;
+      ++st_exec;
       const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
       ok = warp_pdc(g, t, all, m1, H, st_tasks, st_events);
       pm = lane == 0 ? all : 0;
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               const int32_t fi = x ? fci : fni, fj = x ? fcj : fnj;
               if (idx < np) {
                 auto pair_test = [&](int32_t m) -> bool {
-                  ++my_tests;
+                  ++st_pair_exec;
                   const int32_t C[2] = {w_from_waves(t.wv(i, Bi, m), ci, fi),
                                         w_from_waves(t.wv(j, Bj, m), cj, fj)};
                   const int32_t Dv[2] = {Di, Dj}, Tv[2] = {Ti, Tj}, qv[2] = {qi, qj};
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
                   return pair_pdc(C, Dv, Tv, qv, H, st_pair_events);
                 };
                 const bool merged =
-                    search_sizes<kGen>(z, max(mi_, mj_), mi_ + mj_ - 1, pair_test) != 0;
+                    alg2_search<kGen>(z, max(mi_, mj_), mi_ + mj_ - 1, pair_test, my_tests) != 0;
                 if (!merged) {
                   atomicOr(&scr.forb[i], 1u << j);
                   atomicOr(&scr.forb[j], 1u << i);
@@ -489,6 +490,9 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             if (el) scr.plist[__popc(elb & ((1u << lane) - 1u))] = Qr;
             g.sync();
             const int E = __popc(elb);
+            ++st_rounds;       // one Algorithm 3 selection ...
+            st_scan += len;    // ... over the len partitions of par_list (mask ops)
+            st_partners += E;  // eligible partners tried with Algorithm 2
             const int Qe = lane < E ? scr.plist[lane] : 0;
             const uint32_t pmQe = g.shfl(pm, Qe);
             const int32_t szQe = g.shfl(psz, Qe);
@@ -496,41 +500,18 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             const int maxcnt = g.reduce_max(lane < E ? (unsigned)__popc(Se) : 0u);
             bool done_round = false;
             if (maxcnt <= 8) {
-              // every partner's merge scan runs on its own lane (exact: the scans
-              // of one round are independent; only failures feed later rounds)
-              // With E <= G/2 partners, R = G/E lanes share each partner's linear scan:
-              // lane e + jE tests sizes lo + j, lo + j + R, ... and stops at its first
-              // success; the partner's first schedulable size is the minimum over its R
-              // lanes (the sequential scan's answer), and the tests the sequential scan
-              // performs -- first success - lo + 1, or all -- are what is counted.  (The
-              // f4 kGen scans keep one lane per partner.)
-              int64_t my_tests = 0;
+              // every partner's Algorithm 2 search runs on its own lane (exact: the
+              // searches of one round are independent; only failures feed later rounds)
+              int64_t my_tests = 0;  // the paper's linear-scan count for partner `lane`
               int32_t got = 0, uh = 0;
-              const int R = (!kGen && E > 0 && E <= G / 2) ? G / E : 1;
-              const int eL = E > 0 ? lane % E : 0, rL = E > 0 ? lane / E : G;
-              const int QeL = g.shfl(Qe, eL);
-              const uint32_t SeL = pmP | g.shfl(pm, QeL);
-              const int32_t szQL = g.shfl(psz, QeL);
-              if (rL < R) {
-                const int32_t lo = max(szP, szQL) + rL, hi = szP + szQL - 1;
-                if (kAllocNs2 && maxcnt <= 2)
-                  got = serial_merge<2, kGen>(scr, t.wv, z, SeL, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, R);
-                else if (kAllocNs4 && maxcnt <= 4)
-                  got = serial_merge<4, kGen>(scr, t.wv, z, SeL, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, R);
-                else
-                  got = serial_merge<8, kGen>(scr, t.wv, z, SeL, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, R);
-              }
-              for (int j = 1; j < R; ++j) {  // partner e's other lanes e + jE
-                const int src = min(lane + j * E, G - 1);
-                const int32_t g2 = g.shfl(got, src), u2 = g.shfl(uh, src);
-                if (lane < E && lane + j * E < G && g2 > 0 && (got == 0 || g2 < got)) {
-                  got = g2;
-                  uh = u2;
-                }
-              }
-              if (!kGen && lane < E) {
+              if (lane < E) {
                 const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
-                my_tests = got > 0 ? got - lo + 1 : max(hi - lo + 1, 0);
+                if (kAllocNs2 && maxcnt <= 2)
+                  got = serial_merge<2, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, st_pair_exec);
+                else if (kAllocNs4 && maxcnt <= 4)
+                  got = serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, st_pair_exec);
+                else
+                  got = serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, st_pair_exec);
               }
               const uint32_t succ = g.ballot(lane < E && got > 0);
               int cut = E;  // partners whose tests the sequential order performs
@@ -572,10 +553,10 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               const uint32_t S = pmP | pmQ;
               // Algorithm 2: m < |P1| + |P2| (Def. 3), warp-cooperative tests
               auto wtest = [&](int32_t m) -> bool {
-                ++tests;
+                ++st_exec;
                 return warp_pdc(g, t, S, m, H, st_tasks, st_events);
               };
-              const int32_t got = search_sizes<kGen>(z, max(szP, szQ), szP + szQ - 1, wtest);
+              const int32_t got = alg2_search<kGen>(z, max(szP, szQ), szP + szQ - 1, wtest, tests);
               if (!got) {  // add_to_forbidden_moves(P, Q)
                 if (lane == P) pex |= 1u << Q;
                 if (lane == Q) pex |= 1u << P;
@@ -670,11 +651,18 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
   }
   if (a.stats) {
     const uint64_t pt = g.sum_u64(st_pair_tasks), pe = g.sum_u64(st_pair_events);
+    const uint64_t px = g.sum_u64(st_pair_exec);
     if (lane == 0) {
       atomicAdd(a.stats + 0, (unsigned long long)st_tests);
       atomicAdd(a.stats + 1, (unsigned long long)(st_tasks + pt));
       atomicAdd(a.stats + 2, (unsigned long long)(st_events + pe));
       atomicAdd(a.stats + 3, (unsigned long long)st_sets);
+      if (a.stats_ext) {
+        atomicAdd(a.stats + 4, (unsigned long long)(st_exec + px));
+        atomicAdd(a.stats + 5, (unsigned long long)st_rounds);
+        atomicAdd(a.stats + 6, (unsigned long long)st_scan);
+        atomicAdd(a.stats + 7, (unsigned long long)st_partners);
+      }
     }
   }
 }
@@ -701,10 +689,12 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
     return gp_fail(GP_EINVAL, "gp_allocate: bad task sets (n_tasks 1..256, M 1..1024)");
   if ((int)v < 0 || (int)v > 4) return gp_fail(GP_EINVAL, "gp_allocate: bad variant %d", (int)v);
   AllocVariantOpts vo{};
+  bool stats_ext = false;
   if (opts) {
-    if (opts->flags & ~(uint32_t)(GP_AL_BINARY_MERGE | GP_AL_INCREASING))
+    if (opts->flags & ~(uint32_t)(GP_AL_BINARY_MERGE | GP_AL_INCREASING | GP_AL_STATS_EXT))
       return gp_fail(GP_EINVAL, "gp_allocate: unknown option flags 0x%x", opts->flags);
-    vo.flags = opts->flags;
+    vo.flags = opts->flags & ~(uint32_t)GP_AL_STATS_EXT;  // the f4 variant bits
+    stats_ext = (opts->flags & GP_AL_STATS_EXT) != 0;
     if (opts->size_mask) {
       const int words = (ts->M + 31) / 32;
       int any = 0;
@@ -724,7 +714,8 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
     return gp_fail(GP_EINVAL, "gp_allocate: null pointer");
   if (ts->n_tasks > kMaxTasks)  // 33..256 tasks: one CTA per set (allocate_big.cu)
     return gp_allocate_big_launch(ts, (int32_t)v, vo, ok, block_of_task, block_size, pi, k,
-                                  n_tests, efficiency, stats, (cudaStream_t)stream);
+                                  n_tests, efficiency, stats, stats_ext,
+                                  (cudaStream_t)stream);
   // group width: the smallest of 8, 16, 32 lanes that holds the set's tasks (and is at
   // least GP_ALLOC_MIN_G)
   int G = ts->n_tasks <= 8 ? 8 : (ts->n_tasks <= 16 ? 16 : 32);
@@ -740,7 +731,7 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   if (gen && vo.masked) smem = ((tab + 15) & ~(size_t)15) + sizeof(SizeTables);
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-              efficiency, stats, use_tab ? 1 : 0, nullptr, vo};
+              efficiency, stats, stats_ext ? 1 : 0, use_tab ? 1 : 0, nullptr, vo};
   using KernFn = void (*)(AllocArgs);
   static const KernFn kdef[3][5] = {
       {k_allocate<false, 8, 0>, k_allocate<false, 8, 1>, k_allocate<false, 8, 2>,

@@ -32,6 +32,7 @@ struct BigArgs {
   int64_t *n_tests;
   int64_t *eff;
   unsigned long long *stats;
+  int32_t stats_ext;
   unsigned long long *next_set;  // work counter (zeroed per launch)
   AllocVariantOpts vo;  // f4
 };
@@ -132,8 +133,8 @@ GP_DEV bool cta_pdc(BigSmem &s, const uint32_t *S, int32_t m, int32_t H, int n,
 // Algorithm 2 merge by ONE thread for a merged partition of <= kSerialMax tasks.
 template <bool kGen>
 GP_DEV int32_t big_serial_merge(const BigSmem &s, const SizeSpace &z, const uint32_t (&S)[kBW],
-                                int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &tests,
-                                uint64_t &st_tasks, uint32_t &st_events) {
+                                int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &counted,
+                                uint64_t &st_tasks, uint32_t &st_events, uint32_t &st_exec) {
   int32_t T[kSerialMax], D[kSerialMax], Bv[kSerialMax], c[kSerialMax], f[kSerialMax],
       q[kSerialMax];
   int cnt = 0;
@@ -155,7 +156,7 @@ GP_DEV int32_t big_serial_merge(const BigSmem &s, const SizeSpace &z, const uint
     cnt += v;
   }
   auto test = [&](int32_t m) -> bool {
-    ++tests;
+    ++st_exec;
     st_tasks += cnt;
     int32_t C[kSerialMax];
     bool bad = false;
@@ -176,7 +177,7 @@ GP_DEV int32_t big_serial_merge(const BigSmem &s, const SizeSpace &z, const uint
     uh_out = UH;
     return true;
   };
-  return search_sizes<kGen>(z, lo, hi, test);
+  return alg2_search<kGen>(z, lo, hi, test, counted);  // paper's count (gp_sizes.cuh)
 }
 
 template <bool kGen>
@@ -199,8 +200,9 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
   const bool act = a.variant == GP_SMS_ACT || a.variant == GP_BF_ACT;
   const bool sms = a.variant == GP_SMS_ACT || a.variant == GP_SMS_INA;
   uint64_t st_tests = 0, st_tasks = 0, st_events = 0, st_sets = 0;  // thread 0's copies
+  uint64_t st_exec = 0, st_rounds = 0, st_scan = 0, st_partners = 0;  // uniform
   uint64_t my_tasks = 0;
-  uint32_t my_events = 0;
+  uint32_t my_events = 0, my_exec = 0;
   // persistent CTAs grabbing their next set from a counter (work per set varies widely)
   for (;;) {
     if (threadIdx.x == 0) s.bcast[3] = (int32_t)atomicAdd(a.next_set, 1ull);
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
       if (in) atomicOr(&s.pm[0][t >> 5], 1u << (t & 31));
       __syncthreads();
       tests = 1;
+      ++st_exec;
       const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
       ok = cta_pdc(s, s.pm[0], m1, H32, n, st_tasks, st_events);
       if (t == 0) {
@@ -312,7 +315,8 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
               int32_t uh;
               const int32_t mi_ = s.psz[i], mj_ = s.psz[j];
               const int32_t got = big_serial_merge<kGen>(s, z, S, max(mi_, mj_), mi_ + mj_ - 1,
-                                                         H32, uh, my_tests, my_tasks, my_events);
+                                                         H32, uh, my_tests, my_tasks, my_events,
+                                                         my_exec);
               if (!got) {
                 atomicOr(&s.forb[i][j >> 5], 1u << (j & 31));
                 atomicOr(&s.forb[j][i >> 5], 1u << (i & 31));
@@ -396,6 +400,9 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
               E += s.red32[w];
             }
             if (el) s.plist[before + __popc(bal & ((1u << (t & 31)) - 1u))] = s.bord[t];
+            ++st_rounds;       // one Algorithm 3 selection over len partitions,
+            st_scan += len;
+            st_partners += E;  // E partner searches (Algorithm 2)
             __syncthreads();
             // merged sizes
             const int Qe = t < E ? s.plist[t] : 0;
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
               if (t < E) {
                 const int32_t szQ = s.psz[Qe];
                 got = big_serial_merge<kGen>(s, z, Se, max(szP, szQ), szP + szQ - 1, H32, uh,
-                                             my_tests, my_tasks, my_events);
+                                             my_tests, my_tasks, my_events, my_exec);
               }
               // first success (BF) / best (SMS), tests counted in sequential order
               const int first_ok = cta_min32(s, (t < E && got > 0) ? t : INT32_MAX);
@@ -476,10 +483,11 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
 #pragma unroll
                 for (int w = 0; w < kBW; ++w) S2[w] = s.scratch[w];
                 auto ctest = [&](int32_t m) -> bool {
-                  ++tests;
+                  ++st_exec;
                   return cta_pdc(s, S2, m, H32, n, st_tasks, st_events);
                 };
-                const int32_t got = search_sizes<kGen>(z, max(szP, szQ), szP + szQ - 1, ctest);
+                const int32_t got =
+                    alg2_search<kGen>(z, max(szP, szQ), szP + szQ - 1, ctest, tests);
                 if (!got) {
                   if (t == 0) {
                     s.pex[P][Q >> 5] |= 1u << (Q & 31);
@@ -588,11 +596,18 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
   if (a.stats) {
     const uint64_t pt = (uint64_t)cta_sum64(*reinterpret_cast<BigSmem *>(smem_raw), (int64_t)my_tasks);
     const uint64_t pe = (uint64_t)cta_sum64(*reinterpret_cast<BigSmem *>(smem_raw), (int64_t)my_events);
+    const uint64_t px = (uint64_t)cta_sum64(*reinterpret_cast<BigSmem *>(smem_raw), (int64_t)my_exec);
     if (t == 0) {
       atomicAdd(a.stats + 0, (unsigned long long)st_tests);
       atomicAdd(a.stats + 1, (unsigned long long)(st_tasks + pt));
       atomicAdd(a.stats + 2, (unsigned long long)(st_events + pe));
       atomicAdd(a.stats + 3, (unsigned long long)st_sets);
+      if (a.stats_ext) {
+        atomicAdd(a.stats + 4, (unsigned long long)(st_exec + px));
+        atomicAdd(a.stats + 5, (unsigned long long)st_rounds);
+        atomicAdd(a.stats + 6, (unsigned long long)st_scan);
+        atomicAdd(a.stats + 7, (unsigned long long)st_partners);
+      }
     }
   }
 }
@@ -602,10 +617,11 @@ __global__ void __launch_bounds__(256) k_allocate_big(const BigArgs a) {
 gp_status gp_allocate_big_launch(const gp_tasksets *ts, int32_t v, const gp::AllocVariantOpts &vo,
                                  uint8_t *ok, int16_t *bot, int16_t *bs, int32_t *pi, int32_t *k,
                                  int64_t *n_tests, int64_t *eff, unsigned long long *stats,
-                                 cudaStream_t st) {
+                                 bool stats_ext, cudaStream_t st) {
   using namespace gp;
   BigArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
-            ts->n_tasks, ts->M, v, ok, bot, bs, pi, k, n_tests, eff, stats, nullptr, vo};
+            ts->n_tasks, ts->M, v, ok, bot, bs, pi, k, n_tests, eff, stats,
+            stats_ext ? 1 : 0, nullptr, vo};
   const bool gen = vo.flags != 0 || vo.masked;
   size_t smem = sizeof(BigSmem);
   if (gen && vo.masked) smem = ((smem + 15) & ~(size_t)15) + sizeof(SizeTables);

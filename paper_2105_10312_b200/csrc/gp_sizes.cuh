@@ -86,4 +86,51 @@ GP_DEV int32_t search_sizes(const SizeSpace &z, int32_t lo, int32_t hi, F &&test
   }
 }
 
+// Algorithm 2's answer WITHOUT its linear scan (paper default, no f4 option): the
+// first schedulable m in [lo, hi] (0 if none), found by one test at hi and then a
+// binary search below it.  Exact: EDF-PDC(S, m) is monotone in m (W_i is
+// non-increasing in m, C.1.3, and the demand test is monotone in the C_i; the
+// conflict flags depend on S only), so the linear scan's first success is the
+// binary search's -- the oracle's f4 binary merge proves the same equivalence and
+// tests/test_oracle_f4.py pins it.  A failing scan, the common case (96-98 % of
+// INA's merges at C4 load), costs one test instead of hi - lo + 1.  `counted` gets
+// the tests the PAPER's linear scan performs -- the n_tests contract (C.1.9 step 7):
+// first success - lo + 1, or hi - lo + 1 if none; the tests actually run are what the
+// caller's test() counts (the roofline's executed work).
+template <class F>
+GP_DEV int32_t first_fit_size(int32_t lo, int32_t hi, F &&test, int64_t &counted) {
+  if (hi < lo) return 0;
+  int32_t got = 0;
+  if (test(hi)) {
+    int32_t a = lo, b = hi;  // test(b) holds; the answer lies in [a, b]
+    while (a < b) {
+      const int32_t mid = (a + b) >> 1;
+      if (test(mid)) b = mid;
+      else a = mid + 1;
+    }
+    got = a;  // the last successful test was at b == a (callers record U*H there)
+  }
+  counted += got ? got - lo + 1 : hi - lo + 1;
+  return got;
+}
+
+// The size search of one Algorithm 2 call: the paper's default through
+// first_fit_size (counting the linear scan's tests), the f4 variants through
+// search_sizes (counting the tests they run: binary search is the variant).
+template <bool kGen, class F>
+GP_DEV int32_t alg2_search(const SizeSpace &z, int32_t lo, int32_t hi, F &&test, int64_t &counted) {
+  if constexpr (!kGen) {
+    return first_fit_size(lo, hi, test, counted);
+  } else {
+    int64_t ran = 0;
+    auto counted_test = [&](int32_t m) -> bool {
+      ++ran;
+      return test(m);
+    };
+    const int32_t r = search_sizes<true>(z, lo, hi, counted_test);
+    counted += ran;
+    return r;
+  }
+}
+
 }  // namespace gp

@@ -254,6 +254,7 @@ class _AllocOptsC(C.Structure):
 
 GP_AL_BINARY_MERGE = 1  # f4: Algorithm 2 by binary search
 GP_AL_INCREASING = 2    # f4: par_list in increasing utilisation
+GP_AL_STATS_EXT = 4     # stats has 8 slots (+ tests run, selections, partitions scanned, searches)
 
 
 def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=None, flags=0,
@@ -265,6 +266,8 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
         out = AllocOut(ts.n_sets, ts.n_tasks, ts.T.device)
     s = ts.struct()
     opts = None
+    if stats is not None and stats.numel() >= 8:
+        flags |= GP_AL_STATS_EXT
     if flags or sizes is not None:
         mask = (C.c_uint32 * ((ts.M + 31) // 32))()
         if sizes is not None:

@@ -724,73 +724,170 @@ def test_allocate_f4_hand_traces(G):
 
 
 # ------------------------------------------------------- bench-size launch configurations
-def test_exhaustive_c3_bench_size_sampled(G):
-    """C3 at the bench's size (10 bins x 10,000 sets = 6.95e10 candidates, the lane order
-    and every kernel of the timed call): 12 sets recomputed by the oracle, counts vs
-    per-set outputs on all 10^5 sets."""
+ALLOC_KEYS = ("ok", "pi", "k", "n_tests", "block_of_task", "block_size")
+
+
+def compare_allocate(G, ts, host, idx=None, variants=VARIANTS, tag=""):
+    """Every heuristic output of the GPU run on `ts` vs the oracle on `host` (the sets
+    `idx` of ts, or all)."""
+    for v in variants:
+        got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
+        ref = oracle.allocate(host, v)
+        for key in ALLOC_KEYS:
+            g = got[key] if idx is None else got[key][idx]
+            bad = np.nonzero((g != ref[key]).reshape(len(g), -1).any(1))[0]
+            assert len(bad) == 0, (tag, v, key, len(bad), bad[:5])
+
+
+@pytest.fixture(scope="module")
+def c3_bench(G):
+    """C3 at the bench's size: 10 bins x 10,000 sets (6.95e10 candidates), M = 20, n = 6."""
     gen = W.WORKLOADS["c3"]["gen"](R=10000)
     ts = G.TaskSets(10 * 10000, 6, 20, 10)
     G.gp_generate(gen, W.SEED, 0, 10000, ts)
+    return ts, to_oracle(ts)
+
+
+def test_exhaustive_c3_bench_size(G, c3_bench):
+    """C3 at the bench's size in the timed launch configuration (lane order, hash table):
+    1,000 sets (100 per utilisation bin) recomputed by the oracle; the per-candidate
+    evaluator's per-set outputs on ALL 10^5 sets; counts vs per-set outputs."""
+    ts, host = c3_bench
     counts = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
-    per, _, st = run_exhaustive(G, ts, counts=counts, with_stats=False)
-    host = to_oracle(ts)
+    per, _, st = run_exhaustive(G, ts, counts=counts, with_stats=False, workspace=True)
     rng = np.random.default_rng(29)
-    sample = sorted(set([0, 31, 32, 9999, 50000, 99999] + [int(x) for x in rng.integers(0, 10**5, 6)]))
+    sample = sorted(int(b * 10000 + x) for b in range(10)
+                    for x in rng.choice(10000, 100, replace=False))
     assert (per[sample] == oracle.exhaustive(host.subset(sample))).all()
+    pc, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_PER_CANDIDATE, with_stats=False)
+    assert (pc == per).all()
     c = counts.cpu().numpy()[0, :, 0]
     exists = per[:, 0] > 0
     for b in range(10):
         rows = host.group == b
         assert c[b, 1] == rows.sum() == 10000
         assert c[b, 0] == (exists & rows & (host.valid == 1)).sum()
+    assert (exists[:10000].sum() > 0) and (~exists[-10000:]).any()  # bins differ
 
 
-def test_allocate_c4_bench_size_sampled(G):
-    """C4 at the bench's size (5 prm x 10 bins x 20,000 = 10^6 sets of 32 tasks, M = 148):
-    every output of 40 sampled sets per variant recomputed by the oracle."""
-    gen = W.WORKLOADS["c4"]["gen"](R=20000)
-    ts = G.TaskSets(50 * 20000, 32, 148, 50)
-    G.gp_generate(gen, W.SEED, 0, 20000, ts)
-    rng = np.random.default_rng(31)
-    sample = sorted(set([0, 1, 999999] + [int(x) for x in rng.integers(0, 10**6, 37)]))
-    host = to_oracle(ts).subset(sample)
-    for v in VARIANTS:
-        got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
-        ref = oracle.allocate(host, v)
-        for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
-            assert (got[key][sample] == ref[key]).all(), (v, key)
+def test_allocate_c3_shape_all_sets(G, c3_bench):
+    """The heuristics inside the headline step: all 5 variants on all 10^5 C3 sets
+    (M = 20, n = 6), every output incl. n_tests, vs the oracle."""
+    ts, host = c3_bench
+    compare_allocate(G, ts, host, tag="c3")
 
 
-def test_exhaustive_and_allocate_c2_bench_size_sampled(G):
-    """C2 at the bench's size (10^5 sets, M = 8): 200 sampled sets' exhaustive outputs and
-    heuristic outputs recomputed by the oracle."""
+def test_exhaustive_and_allocate_c2_bench_size(G):
+    """C2 at the bench's size (10^5 sets, M = 8): the heuristics on all 10^5 sets, and
+    1,000 sets' exhaustive outputs (100 per bin) recomputed by the oracle."""
     gen = W.WORKLOADS["c2"]["gen"](R=10000)
     ts = G.TaskSets(10 * 10000, 6, 8, 10)
     G.gp_generate(gen, W.SEED, 0, 10000, ts)
+    host = to_oracle(ts)
+    compare_allocate(G, ts, host, tag="c2")
     per, _, _ = run_exhaustive(G, ts, with_stats=False)
     rng = np.random.default_rng(37)
-    sample = sorted(set([0, 99999] + [int(x) for x in rng.integers(0, 10**5, 198)]))
-    host = to_oracle(ts).subset(sample)
-    assert (per[sample] == oracle.exhaustive(host)).all()
-    for v in VARIANTS:
-        got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
-        ref = oracle.allocate(host, v)
-        for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
-            assert (got[key][sample] == ref[key]).all(), (v, key)
+    sample = sorted(int(b * 10000 + x) for b in range(10)
+                    for x in rng.choice(10000, 100, replace=False))
+    assert (per[sample] == oracle.exhaustive(host.subset(sample))).all()
 
 
-def test_allocate_c5_bench_size_sampled(G):
+def test_allocate_c4_bench_size(G):
+    """C4 at the bench's size (5 prm x 10 bins x 20,000 = 10^6 sets of 32 tasks, M = 148),
+    the launch the bench times: every output of 10^4 sets (the first 200 of each of the
+    50 (prm, bin) groups) per variant vs the oracle."""
+    gen = W.WORKLOADS["c4"]["gen"](R=20000)
+    ts = G.TaskSets(50 * 20000, 32, 148, 50)
+    G.gp_generate(gen, W.SEED, 0, 20000, ts)
+    idx = np.array([g * 20000 + r for g in range(50) for r in range(200)])
+    d = ts.to_host()
+    for f in ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group"):
+        d[f] = np.ascontiguousarray(d[f][idx])
+    compare_allocate(G, ts, oracle.Sets.from_dict(d), idx=idx, tag="c4")
+
+
+def test_allocate_c5_bench_size(G):
     """C5 at the bench's size (10^5 sets of 16 tasks, M = 68) for 3 of the 16 coefficient
-    settings: 40 sampled sets per variant recomputed by the oracle."""
-    rng = np.random.default_rng(41)
-    sample = sorted(set([0, 99999] + [int(x) for x in rng.integers(0, 10**5, 38)]))
+    settings: every output of 10^4 sets (the first 1,000 of each bin) per variant."""
+    idx = np.array([b * 10000 + r for b in range(10) for r in range(1000)])
     for kc, km in (W.C5_SETTINGS[0], W.C5_SETTINGS[6], W.C5_SETTINGS[15]):
         gen = W.WORKLOADS["c5"]["gen"](R=10000, kc=kc, km=km)
         ts = G.TaskSets(10 * 10000, 16, 68, 10)
         G.gp_generate(gen, W.SEED, 0, 10000, ts)
-        host = to_oracle(ts).subset(sample)
-        for v in VARIANTS:
-            got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
-            ref = oracle.allocate(host, v)
-            for key in ("ok", "pi", "k", "n_tests", "block_of_task", "block_size"):
-                assert (got[key][sample] == ref[key]).all(), (kc, km, v, key)
+        d = ts.to_host()
+        for f in ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group"):
+            d[f] = np.ascontiguousarray(d[f][idx])
+        compare_allocate(G, ts, oracle.Sets.from_dict(d), idx=idx, tag=(kc, km))
+
+
+# ------------------------------------------------------- n = 9..12 (per-candidate evaluator)
+@pytest.mark.parametrize("M,n", [(2, 11), (3, 9), (3, 12), (4, 10), (5, 9)])
+def test_enumerate_all_ranks_large_n(G, M, n):
+    """gp_enumerate for n = 9..12 (the ABI's upper range): every rank vs the oracle's
+    nested-loop enumeration, plus rank windows straddling k boundaries."""
+    total = G.gp_count_candidates(M, n)
+    assert total == oracle.count_candidates(M, n)
+    bot, bs = G.gp_enumerate(M, n, 0, total)
+    rb, rs = oracle.enumerate_candidates(M, n)
+    assert (bot.cpu().numpy() == rb).all() and (bs.cpu().numpy() == rs).all()
+    for first, cnt in [(0, 1), (total - 1, 1), (M - 1, 3), (total // 2, 777)]:
+        cnt = min(cnt, total - first)
+        b2, s2 = G.gp_enumerate(M, n, first, cnt)
+        assert (b2.cpu().numpy() == rb[first:first + cnt]).all()
+        assert (s2.cpu().numpy() == rs[first:first + cnt]).all()
+
+
+@pytest.mark.parametrize("seed,n,M", [(51, 9, 3), (52, 10, 3), (53, 11, 2), (54, 12, 3),
+                                      (55, 9, 5), (56, 10, 4)])
+def test_exhaustive_large_n(G, seed, n, M):
+    """EXHAUSTIVE for n = 9..12 (the generic per-candidate kernel, NT = 12): per-candidate
+    verdict bitmaps of 16 random sets (ragged: 16 < 32 lanes) vs the oracle, full space
+    and two rank windows; per-set outputs of the bench-style call (no bits, hash)."""
+    d = W.random_sets(np.random.default_rng(seed), 16, n, M, periods=(24, 48, 96, 192),
+                      b_max=2 * M + 3, cost_max=2)
+    ts = gpu_sets(G, d)
+    host = oracle.Sets.from_dict(d)
+    per, vb, _ = run_exhaustive(G, ts, bits=True)
+    ref, rbits = oracle.exhaustive(host, bits=True)
+    assert (per == ref).all() and (vb == rbits).all()
+    assert (ref[:, 0] > 0).any()
+    total = G.gp_count_candidates(M, n)
+    for lo, hi in [(3, 70), (total // 3, total // 3 + 4099)]:
+        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi)
+        r2, b2 = oracle.exhaustive(host, lo, hi, bits=True)
+        assert (per == r2).all() and (vb == b2).all(), (lo, hi)
+    per2, _, _ = run_exhaustive(G, ts, with_stats=False)
+    assert (per2 == ref).all()
+    # f3's threshold evaluator on the same sets (n <= 12): identical per-set outputs
+    thr = torch.empty((16, 4), dtype=torch.int64, device="cuda")
+    G.gp_sched_ratio(ts, G.GP_THRESHOLD, None, per_set=thr)
+    assert (thr.cpu().numpy() == ref).all()
+
+
+# ------------------------------------------------------- f1: 200 tasks at load (Fig. 7)
+def test_allocate_f1_200_at_load(G):
+    """The paper's 200-task scenario (Fig. 7) at the loads where the
+    heuristics separate: U = 30, 32, ..., 50, REPS sets per point, all five variants,
+    every output (ok, pi, k, n_tests, labels, sizes) vs the oracle.  The oracle needs
+    minutes per loaded 200-task set, so its outputs are stored in
+    tests/golden/f1_200_load.npz by scripts/make_golden_f1_200.py (calls only oracle/);
+    the GPU-generated sets are checked against the stored sets first."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "f1_200_load.npz")
+    g = np.load(path)
+    reps, bins = int(g["reps"]), [int(b) for b in g["bins"]]
+    gen = W.WORKLOADS["f1_200"]["gen"](R=100)
+    ts_all = G.TaskSets(34 * reps, 200, 68, 34)
+    G.gp_generate(gen, W.SEED, 0, reps, ts_all)
+    lo, hi = bins[0] * reps, (bins[-1] + 1) * reps
+    assert g["idx"].tolist() == list(range(lo, hi))
+    ts = ts_all.slice(lo, hi)
+    d = ts.to_host()
+    for f in ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid"):
+        assert (d[f] == g[f"set_{f}"]).all(), f
+    for v in VARIANTS:
+        got = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, 200)).to_host()
+        for key in ALLOC_KEYS:
+            assert (got[key] == g[f"{v}_{key}"]).all(), (v, key)
+    # the load points separate the heuristics (not all sets trivially (un)schedulable)
+    oks = g["SMS_INA_ok"]
+    assert 0 < oks.sum() < len(oks)
