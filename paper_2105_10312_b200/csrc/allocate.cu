@@ -53,19 +53,16 @@ struct AllocArgs {
                               // partner searches} with stats_ext]
   int32_t stats_ext;
   int32_t use_tab;            // per-warp table of ceil(B_i/m) in dynamic shared memory
+  uint32_t pt_off;            // byte offset of the groups' pair tables in dynamic shared memory
   unsigned long long *next_set;  // work counter (zeroed per launch)
   AllocVariantOpts vo;        // f4
 };
 
-#ifndef GP_ALLOC_NS2
-#define GP_ALLOC_NS2 0
-#endif
 #ifndef GP_ALLOC_NS4
 #define GP_ALLOC_NS4 1
 #endif
-// lane-serial merge instantiations for <= 2 and <= 4 tasks (each one is more code for the
+// lane-serial merge instantiation for <= 4 tasks besides <= 8 (more code for the
 // instruction cache, which the divergent groups of a warp already stress: A/B-measured)
-constexpr bool kAllocNs2 = GP_ALLOC_NS2;
 constexpr bool kAllocNs4 = GP_ALLOC_NS4;
 
 // A group of G lanes of one warp works on one task set (G = 8, 16 or 32: the
@@ -199,6 +196,8 @@ struct WarpScratch {
   uint32_t forb[G];  // ACT: forbidden task row
   int32_t plist[G];  // eligible partners of the selected partition, par_list order
   uint32_t pmask[G]; // task mask of output label j
+  uint32_t pmS[G];   // task mask of partition slot s (for the pair evaluations)
+  int32_t szS[G];    // size of partition slot s
   // the set's tasks, for the lane-serial merge tests
   int32_t T[G], D[G], B[G], cn[G], cc[G], fn[G], fc[G], q[G];
   uint32_t same[G];
@@ -257,6 +256,22 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
   return alg2_search<kGen>(z, lo, hi, test, counted);
 }
 
+// Pair-table entry: Algorithm 2's outcome for a pair of partition slots (i < j):
+// the first schedulable size (0 if none), the tests the paper's scan counts and
+// U*H of the merged partition at that size.
+GP_DEV uint64_t pt_pack(int32_t got, int64_t cnt, int32_t uh) {
+  return ((uint64_t)(uint32_t)got & 0xFFFu) | (((uint64_t)cnt & 0xFFFFFu) << 12) |
+         ((uint64_t)(uint32_t)uh << 32);
+}
+GP_DEV void pt_unpack(uint64_t e, int32_t &got, int64_t &cnt, int32_t &uh) {
+  got = (int32_t)(e & 0xFFFu);
+  cnt = (int64_t)((e >> 12) & 0xFFFFFu);
+  uh = (int32_t)(e >> 32);
+}
+GP_DEV int pt_index(int i, int j, int n) { return i * (2 * n - i - 1) / 2 + (j - i - 1); }
+template <int G>
+GP_DEV uint32_t pm_bcast(const Grp<G> &g, uint32_t pm, int src) { return g.shfl(pm, src); }
+
 // kV >= 0: the variant is a compile-time constant (one kernel per variant: each carries only
 // its own code, e.g. no ACT prefill in INA, which keeps the instruction working set small);
 // kV = -1: runtime variant (the f4 kGen kernels)
@@ -272,6 +287,9 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
   WarpScratch<G> &scr = scr_all[wid];
   const int n = a.n, M = a.M;
   uint16_t *wtab = a.use_tab ? wtab_all + (size_t)wid * n * M : nullptr;
+  // this group's pair table (dynamic shared memory after the wave / size tables)
+  uint64_t *pt_tab = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(wtab_all) +
+                                                  a.pt_off) + (size_t)wid * (n * (n - 1) / 2);
   // f4: admissible-size tables after the ceil(B/m) tables
   SizeSpace z{nullptr, M, 0, false};
   bool incr = false;
@@ -379,55 +397,47 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
         if (Pi <= M) {
           ok = true;  // Lemma 3: exit on success at any time (A-24)
         } else {
-          uint32_t forb_row = 0;
-          if (act) {  // §5.3: test every couple of tasks
-            scr.forb[lane] = 0;
-            g.sync();
-            const int np = n * (n - 1) / 2;
-            int64_t my_tests = 0;
-            for (int base = 0; base < np; base += G) {
-              int idx = base + lane;
-              int i = 0;
-              int rem = idx < np ? idx : 0;
-              while (rem >= n - 1 - i) {
-                rem -= n - 1 - i;
-                ++i;
-              }
-              const int j = i + 1 + rem;
-              const int32_t Ti = g.shfl(t.T, i), Tj = g.shfl(t.T, j);
-              const int32_t Di = g.shfl(t.D, i), Dj = g.shfl(t.D, j);
-              const int32_t Bi = g.shfl(t.B, i), Bj = g.shfl(t.B, j);
-              const int32_t qi = g.shfl(t.q, i), qj = g.shfl(t.q, j);
-              const int32_t mi_ = g.shfl(mi, i), mj_ = g.shfl(mi, j);
-              const uint32_t si = g.shfl(t.same, i);
-              const bool x = (si >> j) & 1u;  // same type -> both in conflict
-              const int32_t cni = g.shfl(t.cn, i), cci = g.shfl(t.cc, i);
-              const int32_t cnj = g.shfl(t.cn, j), ccj = g.shfl(t.cc, j);
-              const int32_t fni = g.shfl(t.fn, i), fci = g.shfl(t.fc, i);
-              const int32_t fnj = g.shfl(t.fn, j), fcj = g.shfl(t.fc, j);
-              const int32_t ci = x ? cci : cni, cj = x ? ccj : cnj;
-              const int32_t fi = x ? fci : fni, fj = x ? fcj : fnj;
-              if (idx < np) {
-                auto pair_test = [&](int32_t m) -> bool {
-                  ++st_pair_exec;
-                  const int32_t C[2] = {w_from_waves(t.wv(i, Bi, m), ci, fi),
-                                        w_from_waves(t.wv(j, Bj, m), cj, fj)};
-                  const int32_t Dv[2] = {Di, Dj}, Tv[2] = {Ti, Tj}, qv[2] = {qi, qj};
-                  st_pair_tasks += 2;
-                  return pair_pdc(C, Dv, Tv, qv, H, st_pair_events);
-                };
-                const bool merged =
-                    alg2_search<kGen>(z, max(mi_, mj_), mi_ + mj_ - 1, pair_test, my_tests) != 0;
-                if (!merged) {
-                  atomicOr(&scr.forb[i], 1u << j);
-                  atomicOr(&scr.forb[j], 1u << i);
-                }
+          // ---- the pair table.  Algorithm 2's outcome for a pair of partitions
+          // depends only on the two partitions, and every pair the sequential
+          // algorithm tries is tried at most once per partition state, so the
+          // outcome of every pair of LIVE partitions is computed lane-parallel
+          // (speculatively) and the rounds below read it: the Lemma-2 singletons
+          // first (in ACT this is the prefill itself), then after each
+          // commit the new partition against every live one.  Each entry keeps the
+          // tests the paper's scan counts, so n_tests and every output are the
+          // sequential algorithm's.
+          scr.pmS[lane] = pm;
+          scr.szS[lane] = psz;
+          scr.forb[lane] = 0;
+          g.sync();
+          const int np = n * (n - 1) / 2;
+          int64_t my_tests = 0;
+          for (int base = 0; base < np; base += G) {
+            const int idx = base + lane;
+            int i = 0, rem = idx < np ? idx : 0;
+            while (rem >= n - 1 - i) {
+              rem -= n - 1 - i;
+              ++i;
+            }
+            const int j = i + 1 + rem;
+            if (idx < np) {
+              int32_t uh = 0;
+              int64_t cnt = 0;
+              const int32_t got = serial_merge<2, kGen>(
+                  scr, t.wv, z, (1u << i) | (1u << j), max(scr.szS[i], scr.szS[j]),
+                  scr.szS[i] + scr.szS[j] - 1, H, uh, cnt, st_pair_tasks, st_pair_events,
+                  st_pair_exec);
+              pt_tab[idx] = pt_pack(got, cnt, uh);
+              my_tests += cnt;
+              if (act && !got) {  // §5.3: the couple is forbidden
+                atomicOr(&scr.forb[i], 1u << j);
+                atomicOr(&scr.forb[j], 1u << i);
               }
             }
-            tests += g.sum_i64(my_tests);
-            g.sync();
-            forb_row = scr.forb[lane];
           }
+          if (act) tests += g.sum_i64(my_tests);  // the prefill's tests (INA: speculative)
+          g.sync();
+          const uint32_t forb_row = act ? scr.forb[lane] : 0u;
           // Algorithm 1 main loop.  par_list order and the ACT exclusions depend
           // only on the partitions, so they are recomputed after commits only.
           bool dirty = true;
@@ -479,10 +489,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             if (cand_rank == 99) break;  // no selectable partition: fail (Alg. 1 l.6-7)
             const int P = scr.ord[cand_rank];
             const uint32_t elig = g.shfl(elig_mine, P);
-            const uint32_t pmP = g.shfl(pm, P);
             const int32_t szP = g.shfl(psz, P);
-            int best = -1;
-            int32_t best_m = 0, best_uh = 0;
             // eligible partners in best-fit order -> lane e holds partner plist[e]
             const int Qr = lane < len ? scr.bord[lane] : 0;
             const bool el = lane < len && ((elig >> Qr) & 1u);
@@ -494,94 +501,44 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             st_scan += len;    // ... over the len partitions of par_list (mask ops)
             st_partners += E;  // eligible partners tried with Algorithm 2
             const int Qe = lane < E ? scr.plist[lane] : 0;
-            const uint32_t pmQe = g.shfl(pm, Qe);
-            const int32_t szQe = g.shfl(psz, Qe);
-            const uint32_t Se = pmP | pmQe;
-            const int maxcnt = g.reduce_max(lane < E ? (unsigned)__popc(Se) : 0u);
-            bool done_round = false;
-            if (maxcnt <= 8) {
-              // every partner's Algorithm 2 search runs on its own lane (exact: the
-              // searches of one round are independent; only failures feed later rounds)
-              int64_t my_tests = 0;  // the paper's linear-scan count for partner `lane`
-              int32_t got = 0, uh = 0;
-              if (lane < E) {
-                const int32_t lo = max(szP, szQe), hi = szP + szQe - 1;
-                if (kAllocNs2 && maxcnt <= 2)
-                  got = serial_merge<2, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, st_pair_exec);
-                else if (kAllocNs4 && maxcnt <= 4)
-                  got = serial_merge<4, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, st_pair_exec);
-                else
-                  got = serial_merge<8, kGen>(scr, t.wv, z, Se, lo, hi, H, uh, my_tests, st_pair_tasks, st_pair_events, st_pair_exec);
-              }
-              const uint32_t succ = g.ballot(lane < E && got > 0);
-              int cut = E;  // partners whose tests the sequential order performs
-              if (sms) {
-                uint64_t key = (lane < E && got > 0)
-                                   ? ((uint64_t)got << 40) | ((uint64_t)(uint32_t)uh << 8) | (uint64_t)Qe
-                                   : ~0ull;
+            // Algorithm 2 for (P, Q_e): the pair table's entry
+            int32_t got = 0, uh = 0;
+            int64_t my_tests = 0;  // the paper's scan count for partner `lane`
+            if (lane < E) pt_unpack(pt_tab[pt_index(min(P, Qe), max(P, Qe), n)], got, my_tests, uh);
+            int best = -1;
+            int32_t best_m = 0, best_uh = 0;
+            const uint32_t succ = g.ballot(lane < E && got > 0);
+            int cut = E;  // partners whose tests the sequential order performs
+            if (sms) {  // Def. 4 order >>: smallest size, then U*H, then min id (A-20, A-22)
+              uint64_t key = (lane < E && got > 0)
+                                 ? ((uint64_t)got << 40) | ((uint64_t)(uint32_t)uh << 8) | (uint64_t)Qe
+                                 : ~0ull;
 #pragma unroll
-                for (int o = G / 2; o > 0; o >>= 1) {
-                  const uint64_t k2 = g.shfl_xor(key, o);
-                  key = k2 < key ? k2 : key;
-                }
-                if (key != ~0ull) {
-                  best = (int)(key & 0xFF);
-                  best_m = (int32_t)(key >> 40);
-                  best_uh = (int32_t)((key >> 8) & 0xFFFFFFFFu);
-                }
-              } else if (succ) {  // BF: the first success in par_list order commits
-                cut = __ffs(succ);  // partners 0 .. cut-1 were tried
-                const int e0 = cut - 1;
-                best = g.shfl(Qe, e0);
-                best_m = g.shfl(got, e0);
-                best_uh = g.shfl(uh, e0);
+              for (int o = G / 2; o > 0; o >>= 1) {
+                const uint64_t k2 = g.shfl_xor(key, o);
+                key = k2 < key ? k2 : key;
               }
-              tests += g.sum_i64(lane < cut ? my_tests : 0);
-              const bool failed = lane < cut && lane < E && got == 0;
-              const uint32_t failQ = g.or_u32(failed ? (1u << Qe) : 0u);
-              if (lane == P) pex |= failQ;                 // add_to_forbidden_moves(P, Q)
-              if ((failQ >> lane) & 1u) pex |= 1u << P;
-              done_round = true;
+              if (key != ~0ull) {
+                best = (int)(key & 0xFF);
+                best_m = (int32_t)(key >> 40);
+                best_uh = (int32_t)((key >> 8) & 0xFFFFFFFFu);
+              }
+            } else if (succ) {  // BF: the first success in par_list order commits (A-21)
+              cut = __ffs(succ);  // partners 0 .. cut-1 were tried
+              const int e0 = cut - 1;
+              best = g.shfl(Qe, e0);
+              best_m = g.shfl(got, e0);
+              best_uh = g.shfl(uh, e0);
             }
-            // (groups of 8 lanes hold <= 8 tasks: every merge is lane-parallel, the
-            // group-cooperative fallback is compiled out -- smaller code, fewer I-cache misses)
-            for (int r = 0; G > 8 && r < len && !done_round; ++r) {
-              const int Q = scr.bord[r];
-              if (!((elig >> Q) & 1u)) continue;
-              const uint32_t pmQ = g.shfl(pm, Q);
-              const int32_t szQ = g.shfl(psz, Q);
-              const uint32_t S = pmP | pmQ;
-              // Algorithm 2: m < |P1| + |P2| (Def. 3), warp-cooperative tests
-              auto wtest = [&](int32_t m) -> bool {
-                ++st_exec;
-                return warp_pdc(g, t, S, m, H, st_tasks, st_events);
-              };
-              const int32_t got = alg2_search<kGen>(z, max(szP, szQ), szP + szQ - 1, wtest, tests);
-              if (!got) {  // add_to_forbidden_moves(P, Q)
-                if (lane == P) pex |= 1u << Q;
-                if (lane == Q) pex |= 1u << P;
-                continue;
-              }
-              const int32_t uh = warp_uh(g, t, S, got);
-              if (sms) {  // Def. 4 order >>: smallest size, then U*H, then min id
-                if (best < 0 || got < best_m || (got == best_m && (uh < best_uh ||
-                                                                    (uh == best_uh && Q < best)))) {
-                  best = Q;
-                  best_m = got;
-                  best_uh = uh;
-                }
-              } else {  // BF: first success in > order commits
-                best = Q;
-                best_m = got;
-                best_uh = uh;
-                break;
-              }
-            }
-            g.sync();
+            tests += g.sum_i64(lane < cut ? my_tests : 0);
+            const bool failed = lane < cut && lane < E && got == 0;
+            const uint32_t failQ = g.or_u32(failed ? (1u << Qe) : 0u);
+            if (lane == P) pex |= failQ;                 // add_to_forbidden_moves(P, Q)
+            if ((failQ >> lane) & 1u) pex |= 1u << P;
             if (best >= 0) {  // commit: P u Q replaces P and Q in par_list
               const int Q = best;
               const int32_t szQ = g.shfl(psz, Q);
-              const uint32_t pmQ = g.shfl(pm, Q);
+              const uint32_t pmP = g.shfl(pm, P), pmQ = g.shfl(pm, Q);
               const int keep = min(P, Q), drop = max(P, Q);
               Pi -= szP + szQ - best_m;
               if (lane == keep) {
@@ -597,6 +554,49 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               }
               pex &= ~((1u << keep) | (1u << drop));
               dirty = true;
+              scr.pmS[lane] = pm;
+              scr.szS[lane] = psz;
+              g.sync();
+              if (Pi > M) {
+                // the new partition against every live one (lane = the other slot)
+                const uint32_t pk = pm_bcast(g, pm, keep);
+                // ACT never tries a partner holding a task forbidden with one of the new
+                // partition's tasks: no entry needed for those pairs
+                const uint32_t Fk = act ? g.or_u32(((pk >> lane) & 1u) ? forb_row : 0u) : 0u;
+                const bool mine = pm != 0 && lane != keep && !(pm & Fk);
+                const uint32_t S2 = pk | pm;
+                const int c2 = mine ? __popc(S2) : 0;
+                const int maxc = (int)g.reduce_max((unsigned)c2);
+                int32_t got2 = 0, uh2 = 0;
+                int64_t cnt2 = 0;
+                const int32_t lo2 = max(best_m, psz), hi2 = best_m + psz - 1;
+                if (mine && c2 <= 8) {
+                  if (kAllocNs4 && maxc <= 4)
+                    got2 = serial_merge<4, kGen>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec);
+                  else
+                    got2 = serial_merge<8, kGen>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec);
+                  pt_tab[pt_index(min(keep, lane), max(keep, lane), n)] = pt_pack(got2, cnt2, uh2);
+                }
+                // (groups of 8 lanes hold <= 8 tasks: the group-cooperative path for merged
+                // partitions of more than 8 tasks is compiled out -- smaller code)
+                uint32_t big = G > 8 ? g.ballot(mine && c2 > 8) : 0u;
+                while (G > 8 && big) {
+                  const int s2 = __ffs(big) - 1;
+                  big &= big - 1u;
+                  const uint32_t S3 = pk | g.shfl(pm, s2);
+                  const int32_t sz2 = g.shfl(psz, s2);
+                  int64_t cnt3 = 0;
+                  auto wtest = [&](int32_t m) -> bool {
+                    ++st_exec;
+                    return warp_pdc(g, t, S3, m, H, st_tasks, st_events);
+                  };
+                  const int32_t got3 =
+                      alg2_search<kGen>(z, max(best_m, sz2), best_m + sz2 - 1, wtest, cnt3);
+                  const int32_t uh3 = got3 ? warp_uh(g, t, S3, got3) : 0;
+                  if (lane == 0) pt_tab[pt_index(min(keep, s2), max(keep, s2), n)] = pt_pack(got3, cnt3, uh3);
+                }
+                g.sync();
+              }
             }
           }
         }
@@ -729,9 +729,13 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   const bool gen = vo.flags != 0 || vo.masked;
   size_t smem = tab;
   if (gen && vo.masked) smem = ((tab + 15) & ~(size_t)15) + sizeof(SizeTables);
+  // the groups' pair tables (Algorithm 2 outcomes of partition pairs): n(n-1)/2 x 8 B each
+  const size_t pt_off = (smem + 15) & ~(size_t)15;
+  smem = pt_off + (size_t)(256 / G) * (ts->n_tasks * (ts->n_tasks - 1) / 2) * sizeof(uint64_t);
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
-              efficiency, stats, stats_ext ? 1 : 0, use_tab ? 1 : 0, nullptr, vo};
+              efficiency, stats, stats_ext ? 1 : 0, use_tab ? 1 : 0, (uint32_t)pt_off, nullptr,
+              vo};
   using KernFn = void (*)(AllocArgs);
   static const KernFn kdef[3][5] = {
       {k_allocate<false, 8, 0>, k_allocate<false, 8, 1>, k_allocate<false, 8, 2>,
@@ -745,7 +749,14 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
                              : G == 16 ? k_allocate<true, 16, -1> : k_allocate<true, 32, -1>)
                           : kdef[gi][(int)v];
   // dynamic + static shared memory may pass 48 KB (e.g. 16-lane groups: 16 scratches + tables)
-  if (smem > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // opt in to more than 48 KB (static + dynamic) only when needed: setting a function
+  // attribute per call was measured to stall the stream (C3 step +1.4 ms)
+  {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kern);
+    if (fa.sharedSizeBytes + smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   // persistent grid: one wave of resident CTAs; the set counter lives in a stream-ordered
   // 8-byte allocation from the default pool
   int dev = 0, sms = 148, occ = 1;

@@ -100,16 +100,25 @@ GP_DEV int32_t search_sizes(const SizeSpace &z, int32_t lo, int32_t hi, F &&test
 template <class F>
 GP_DEV int32_t first_fit_size(int32_t lo, int32_t hi, F &&test, int64_t &counted) {
   if (hi < lo) return 0;
-  int32_t got = 0;
-  if (test(hi)) {
-    int32_t a = lo, b = hi;  // test(b) holds; the answer lies in [a, b]
-    while (a < b) {
-      const int32_t mid = (a + b) >> 1;
-      if (test(mid)) b = mid;
-      else a = mid + 1;
+  // one call site of test() (it is inlined: a second site would double the code the
+  // divergent groups of a warp must keep in the instruction cache)
+  int32_t a = lo, b = hi, m = hi;
+  bool probed = false, any = false;
+  for (;;) {
+    const bool ok = test(m);
+    if (!probed) {  // the probe at hi: nothing below is schedulable if it fails
+      probed = true;
+      any = ok;
+      if (!ok) break;
+    } else if (ok) {
+      b = m;  // test(b) holds; the answer lies in [a, b]
+    } else {
+      a = m + 1;
     }
-    got = a;  // the last successful test was at b == a (callers record U*H there)
+    if (a >= b) break;
+    m = (a + b) >> 1;
   }
+  const int32_t got = any ? a : 0;  // the last success was at b == a (U*H recorded there)
   counted += got ? got - lo + 1 : hi - lo + 1;
   return got;
 }
