@@ -95,16 +95,11 @@ struct Grp {
   GP_DEV int32_t sum_i32(int32_t v) const { return sum<int32_t>(v); }
   GP_DEV int64_t sum_i64(int64_t v) const { return sum<int64_t>(v); }
   GP_DEV uint64_t sum_u64(uint64_t v) const { return sum<uint64_t>(v); }
-  GP_DEV int32_t min_i32(int32_t v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v = min(v, shfl_xor(v, o));
-    return v;
-  }
-  GP_DEV uint32_t or_u32(uint32_t v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v |= shfl_xor(v, o);
-    return v;
-  }
+  // single-instruction group reductions (redux.sync)
+  GP_DEV int32_t min_i32(int32_t v) const { return __reduce_min_sync(gmask, v); }
+  GP_DEV uint32_t min_u32(uint32_t v) const { return __reduce_min_sync(gmask, v); }
+  GP_DEV uint32_t or_u32(uint32_t v) const { return __reduce_or_sync(gmask, v); }
+  GP_DEV uint32_t add_u32(uint32_t v) const { return __reduce_add_sync(gmask, v); }
 };
 
 // ceil(B_i / m) from the warp's per-set table (uint16, built once per set)
@@ -435,49 +430,40 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               }
             }
           }
-          if (act) tests += g.sum_i64(my_tests);  // the prefill's tests (INA: speculative)
+          if (act) tests += g.add_u32((uint32_t)my_tests);  // the prefill's tests (INA: speculative)
           g.sync();
           const uint32_t forb_row = act ? scr.forb[lane] : 0u;
-          // Algorithm 1 main loop.  par_list order and the ACT exclusions depend
-          // only on the partitions, so they are recomputed after commits only.
-          bool dirty = true;
-          int rank = 0, len = 0;
-          bool live = false;
-          uint32_t livemask = 0, forb_slots = 0;
+          // Algorithm 1 main loop.  par_list order (rank: position of my slot) and the
+          // ACT exclusions depend only on the partitions: built once here, then updated
+          // incrementally at each commit (two partitions leave, one enters).
+          // par_list order: (U*H desc, slot asc), or U*H asc (f4 increasing); best-fit
+          // partner order (brank): always U*H desc (A-21)
+          bool live = pm != 0;
+          uint32_t livemask = g.ballot(live);
+          int rank = 0, brank = 0;
+          for (int s2 = 0; s2 < n; ++s2) {
+            const int32_t u2 = g.shfl(puh, s2);
+            const bool lv = (livemask >> s2) & 1u;
+            brank += lv && (u2 > puh || (u2 == puh && s2 < lane));
+            if (kGen && incr) rank += lv && (u2 < puh || (u2 == puh && s2 < lane));
+          }
+          if (!(kGen && incr)) rank = brank;
+          int len = __popc(livemask);
+          // ACT: F = tasks forbidden with a task of my partition; forb_slots = the slots
+          // holding such a task
+          uint32_t F = forb_row, forb_slots = 0;
+          if (act)
+            for (int s2 = 0; s2 < n; ++s2)
+              if (g.shfl(pm, s2) & F) forb_slots |= 1u << s2;
+          bool rebuild = true;
           for (;;) {
-            if (dirty) {
-              // par_list order: (U*H desc, slot asc), or U*H asc (f4 increasing);
-              // best-fit partner order: always U*H desc (A-21)
-              live = pm != 0;
-              livemask = g.ballot(live);
-              rank = 0;
-              int brank = 0;
-              for (int s2 = 0; s2 < n; ++s2) {
-                const int32_t u2 = g.shfl(puh, s2);
-                const bool lv = (livemask >> s2) & 1u;
-                brank += lv && (u2 > puh || (u2 == puh && s2 < lane));
-                if (kGen && incr) rank += lv && (u2 < puh || (u2 == puh && s2 < lane));
-              }
-              if (!(kGen && incr)) rank = brank;
+            if (rebuild) {
               if (live) {
                 scr.ord[rank] = lane;
                 scr.bord[brank] = lane;
               }
               g.sync();
-              len = __popc(livemask);
-              uint32_t F = 0;  // tasks forbidden with a task of my partition (ACT)
-              if (act)
-                for (int a2 = 0; a2 < n; ++a2) {
-                  const uint32_t fr = g.shfl(forb_row, a2);
-                  if ((pm >> a2) & 1u) F |= fr;
-                }
-              forb_slots = 0;
-              if (act)
-                for (int s2 = 0; s2 < n; ++s2) {
-                  const uint32_t m2 = g.shfl(pm, s2);
-                  if (m2 & F) forb_slots |= 1u << s2;
-                }
-              dirty = false;
+              rebuild = false;
             }
             if (Pi <= M) {
               ok = true;
@@ -510,18 +496,14 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             const uint32_t succ = g.ballot(lane < E && got > 0);
             int cut = E;  // partners whose tests the sequential order performs
             if (sms) {  // Def. 4 order >>: smallest size, then U*H, then min id (A-20, A-22)
-              uint64_t key = (lane < E && got > 0)
-                                 ? ((uint64_t)got << 40) | ((uint64_t)(uint32_t)uh << 8) | (uint64_t)Qe
-                                 : ~0ull;
-#pragma unroll
-              for (int o = G / 2; o > 0; o >>= 1) {
-                const uint64_t k2 = g.shfl_xor(key, o);
-                key = k2 < key ? k2 : key;
-              }
-              if (key != ~0ull) {
-                best = (int)(key & 0xFF);
-                best_m = (int32_t)(key >> 40);
-                best_uh = (int32_t)((key >> 8) & 0xFFFFFFFFu);
+              const uint32_t k1 = (lane < E && got > 0) ? (uint32_t)got : ~0u;
+              const uint32_t m1 = g.min_u32(k1);
+              if (m1 != ~0u) {
+                const uint32_t k2 = k1 == m1 ? (uint32_t)uh : ~0u;  // U*H >= 0
+                const uint32_t m2 = g.min_u32(k2);
+                best = (int)g.min_u32(k2 == m2 && k1 == m1 ? (uint32_t)Qe : ~0u);
+                best_m = (int32_t)m1;
+                best_uh = (int32_t)m2;
               }
             } else if (succ) {  // BF: the first success in par_list order commits (A-21)
               cut = __ffs(succ);  // partners 0 .. cut-1 were tried
@@ -530,7 +512,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               best_m = g.shfl(got, e0);
               best_uh = g.shfl(uh, e0);
             }
-            tests += g.sum_i64(lane < cut ? my_tests : 0);
+            tests += g.add_u32(lane < cut ? (uint32_t)my_tests : 0u);
             const bool failed = lane < cut && lane < E && got == 0;
             const uint32_t failQ = g.or_u32(failed ? (1u << Qe) : 0u);
             if (lane == P) pex |= failQ;                 // add_to_forbidden_moves(P, Q)
@@ -539,21 +521,59 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               const int Q = best;
               const int32_t szQ = g.shfl(psz, Q);
               const uint32_t pmP = g.shfl(pm, P), pmQ = g.shfl(pm, Q);
+              const int32_t uP = g.shfl(puh, P), uQ = g.shfl(puh, Q);
+              const uint32_t FP = g.shfl(F, P), FQ = g.shfl(F, Q);
               const int keep = min(P, Q), drop = max(P, Q);
               Pi -= szP + szQ - best_m;
+              // incremental par_list / best-fit ranks: P and Q leave, (P u Q) enters at keep
+              {
+                auto before_d = [&](int32_t ux, int x) {  // slot x precedes me (U*H desc)
+                  return ux > puh || (ux == puh && x < lane);
+                };
+                auto before_i = [&](int32_t ux, int x) {  // (U*H asc, f4 increasing)
+                  return ux < puh || (ux == puh && x < lane);
+                };
+                if (lane != keep && lane != drop) {
+                  brank += (int)before_d(best_uh, keep) - (int)before_d(uP, P) - (int)before_d(uQ, Q);
+                  if (kGen && incr)
+                    rank += (int)before_i(best_uh, keep) - (int)before_i(uP, P) - (int)before_i(uQ, Q);
+                }
+                // the new partition's ranks: live slots (other than P, Q) before it
+                const bool other = live && lane != P && lane != Q;
+                const uint32_t bd = g.ballot(other && (puh > best_uh || (puh == best_uh && lane < keep)));
+                const uint32_t bi = (kGen && incr)
+                                        ? g.ballot(other && (puh < best_uh || (puh == best_uh && lane < keep)))
+                                        : 0u;
+                if (lane == keep) {
+                  brank = __popc(bd);
+                  rank = (kGen && incr) ? __popc(bi) : brank;
+                }
+                if (!(kGen && incr)) rank = brank;
+              }
               if (lane == keep) {
                 pm = pmP | pmQ;
                 psz = best_m;
                 puh = best_uh;
                 pex = 0;
+                F = FP | FQ;
               } else if (lane == drop) {
                 pm = 0;
                 psz = 0;
                 puh = 0;
                 pex = 0;
+                F = 0;
               }
               pex &= ~((1u << keep) | (1u << drop));
-              dirty = true;
+              live = pm != 0;
+              livemask &= ~(1u << drop);
+              len -= 1;
+              if (act) {  // exclusions against the changed slots
+                forb_slots &= ~((1u << keep) | (1u << drop));
+                if (live && lane != keep && ((pmP | pmQ) & F)) forb_slots |= 1u << keep;
+                const uint32_t fk = g.ballot(live && (pm & (FP | FQ)));
+                if (lane == keep) forb_slots = fk;
+              }
+              rebuild = true;
               scr.pmS[lane] = pm;
               scr.szS[lane] = psz;
               g.sync();
@@ -562,7 +582,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
                 const uint32_t pk = pm_bcast(g, pm, keep);
                 // ACT never tries a partner holding a task forbidden with one of the new
                 // partition's tasks: no entry needed for those pairs
-                const uint32_t Fk = act ? g.or_u32(((pk >> lane) & 1u) ? forb_row : 0u) : 0u;
+                const uint32_t Fk = act ? g.shfl(F, keep) : 0u;
                 const bool mine = pm != 0 && lane != keep && !(pm & Fk);
                 const uint32_t S2 = pk | pm;
                 const int c2 = mine ? __popc(S2) : 0;
