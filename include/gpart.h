@@ -294,10 +294,13 @@ typedef struct {
                                  deadline points examined, tasks in tested blocks}
                                  (THRESHOLD: {sets, threshold tests, deadline points,
                                  schedulable candidates enumerated for the hash});
-                                 [6] with GP_EX_STATS_EXT: [4] += (set, run) pairs the
-                                 bit-sliced evaluator walked, [5] += those with a non-zero
-                                 verdict word (a run = the candidates of one allocation that
-                                 differ in the last part only); 0 for the other evaluators  */
+                                 [8] with GP_EX_STATS_EXT: [4] += (set, run) pairs the
+                                 bit-sliced evaluator walked one by one, [5] += those with a
+                                 non-zero verdict word (a run = the candidates of one
+                                 allocation that differ in the last part only), [6] += (set,
+                                 sweep) pairs it resolved in closed form (a sweep = the runs
+                                 that differ in the second-to-last part only), [7] += the
+                                 live runs inside them; 0 for the other evaluators          */
   uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0);
                                  GP_EX_PER_CANDIDATE (EXHAUSTIVE): force the per-candidate
                                  evaluator; GP_EX_STATS_EXT: stats has 6 slots (above);

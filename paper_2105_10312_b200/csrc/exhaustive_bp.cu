@@ -269,6 +269,104 @@ __global__ void __launch_bounds__(kScanBlock) k_hash_scan_add(uint64_t *P, uint6
   if (r < n_ranks) P[r + 1] += btot[blockIdx.x];
 }
 
+// ---- run-prefix hash table: R[a0][g] = sum over the runs g' < g (global rank order) of
+// the verdict-hash contribution a run makes when its schedulable candidates are exactly
+// last parts a0 + 1 .. len (the run's top range): c_a0(g') = P[end(g')] - P[start(g') + a0]
+// if a0 < len(g'), else 0 (mod 2^64).  With it, a whole sweep's consecutive live runs
+// [lo, hi) of one set -- when that set's words make them exactly top ranges from a0 --
+// add R[a0][hi] - R[a0][lo]: two reads per (set, sweep) instead of two per (set, run).
+// Runs of an allocation with k blocks <-> (k-1)-subsets {c_0 < ... < c_{k-2}} of
+// {1..M-1} in lexicographic order (prefix sums of the first k-1 parts); the run's first
+// candidate has the s-index of the k-subset {c_0, ..., c_{k-2}, c_{k-2} + 1} of {1..M}.
+GP_DEV uint32_t subset_lex_rank(const int32_t *c, int k, int M) {
+  // rank of the k-subset c (ascending) among k-subsets of {1..M} in lexicographic order
+  uint32_t r = 0;
+  int prev = 0;
+  for (int j = 0; j < k; ++j) {
+    for (int v = prev + 1; v < c[j]; ++v) {  // subsets with a smaller j-th element
+      uint64_t b = 1;  // C(M - v, k - 1 - j)
+      const int nn = M - v, kk = k - 1 - j;
+      for (int i = 1; i <= kk; ++i) b = b * (uint64_t)(nn - kk + i) / (uint64_t)i;
+      r += (uint32_t)b;
+    }
+    prev = c[j];
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_run_contrib(const ExhArgs a, const uint64_t *P,
+                                                     uint64_t *R, uint64_t total_runs) {
+  const int M = a.M;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total_runs;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    int k = 1;
+    while (k < a.L.kmax && g >= a.run_base[k + 1]) ++k;
+    const uint64_t loc = g - a.run_base[k];
+    const uint32_t nr = a.L.n_runs[k];
+    const uint64_t p = loc / nr;
+    uint32_t rho = (uint32_t)(loc - p * nr);
+    // unrank rho -> (k-1)-subset of {1..M-1}, lexicographic
+    int32_t c[kBpMaxN + 1];
+    int prev = 0;
+    for (int j = 0; j < k - 1; ++j) {
+      int v = prev + 1;
+      for (;;) {
+        uint64_t b = 1;  // subsets with c_j = v: C(M - 1 - v, k - 2 - j)
+        const int nn = M - 1 - v, kk = k - 2 - j;
+        for (int i = 1; i <= kk; ++i) b = b * (uint64_t)(nn - kk + i) / (uint64_t)i;
+        if (rho < b) break;
+        rho -= (uint32_t)b;
+        ++v;
+      }
+      c[j] = v;
+      prev = v;
+    }
+    const int last = k >= 2 ? c[k - 2] : 0;
+    c[k - 1] = last + 1;
+    const uint32_t len = (uint32_t)(M - last);
+    const uint64_t start = a.L.k_base[k] + p * a.L.per_pi[k] + subset_lex_rank(c, k, M);
+    const uint64_t pe = P[start + len];
+    for (int a0 = 0; a0 < M; ++a0)
+      R[(uint64_t)a0 * a.r_stride + g + 1] = (uint32_t)a0 < len ? pe - P[start + a0] : 0ull;
+  }
+}
+
+// in-place inclusive scan of each row R[a0][1 .. total] (row a0 = blockIdx.y), R[a0][0] = 0
+__global__ void __launch_bounds__(kScanBlock) k_rows_scan_local(uint64_t *R, uint64_t stride,
+                                                                uint64_t total, uint64_t *btot,
+                                                                uint32_t nb) {
+  __shared__ uint64_t wsum[32];
+  uint64_t *row = R + (uint64_t)blockIdx.y * stride;
+  const uint64_t r = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  const uint64_t v = r < total ? row[r + 1] : 0ull;
+  const uint64_t incl = block_incl_scan_u64(v, wsum);
+  if (r < total) row[r + 1] = incl;
+  if (threadIdx.x == kScanBlock - 1) btot[(uint64_t)blockIdx.y * nb + blockIdx.x] = incl;
+  if (blockIdx.x == 0 && threadIdx.x == 0) row[0] = 0ull;
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_rows_scan_blocks(uint64_t *btot, uint32_t nb) {
+  __shared__ uint64_t wsum[32];
+  uint64_t *bt = btot + (uint64_t)blockIdx.x * nb;
+  uint64_t carry = 0;
+  for (uint32_t b0 = 0; b0 < nb; b0 += kScanBlock) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint64_t v = b < nb ? bt[b] : 0ull;
+    const uint64_t incl = block_incl_scan_u64(v, wsum);
+    if (b < nb) bt[b] = carry + incl - v;
+    __syncthreads();
+    carry += wsum[31];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_rows_scan_add(uint64_t *R, uint64_t stride,
+                                                              uint64_t total, const uint64_t *btot,
+                                                              uint32_t nb) {
+  const uint64_t r = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  if (r < total) R[(uint64_t)blockIdx.y * stride + r + 1] += btot[(uint64_t)blockIdx.y * nb + blockIdx.x];
+}
+
 // ---- per-subset lane order: for every subset S, the sets ordered by (utilisation group,
 // first size at which S passes): sets of one group have similar loads in every subset,
 // and within it the lanes of a warp share the upper end of their live run ranges.  A
@@ -406,6 +504,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
   uint32_t acc_n = 0;
   int32_t acc_pi = INT32_MAX;
   uint64_t acc_first = ~0ull, acc_hash = 0, st_cand = 0, st_runs = 0, st_live = 0;
+  uint64_t st_sweeps = 0, st_live_closed = 0;
   int64_t cur_g = -1, set = -1;
   bool lane_ok = false;
   auto flush = [&]() {
@@ -509,10 +608,38 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     // lanes where w1 != 0), s_{k-2} = 1 + i for runs i = 0 .. steps-1, run i with
     // last part 1 .. len0 - i.  w1 bit i: block k-2 passes at size 1 + i.
     // `off` = s-index (within pi) of the sweep's first candidate.
-    auto sweep = [&](int len0, int steps, uint32_t w1, uint32_t off) {
+    auto sweep = [&](int len0, int steps, uint32_t w1, uint32_t off, uint32_t roff) {
       // runs [i_lo, i_hi) can hold schedulable candidates of some lane's set
       const int lo_l = w1 ? __ffs(w1) - 1 : steps;
       const int hi_l = w1 ? min(steps, len0 - a0) : 0;
+      if constexpr (!kWin && kHash == 1 && !kBits) {
+        // the whole sweep at once: when in every lane the live runs are exactly
+        // [lo_l, hi_l) (block k-2's word has every bit of that range) and each live run's
+        // schedulable candidates are its top range a0+1 .. len (`top`), the lane's
+        // count, pi*, first rank and hash follow in closed form, the hash from two reads
+        // of the run-prefix table R (checked per sweep, never assumed; otherwise the runs
+        // are walked one by one below)
+        const int span = hi_l - lo_l;
+        const bool fits = span <= 0 || ((w1 >> lo_l) & ((span >= 32 ? 0u : 1u << span) - 1u)) ==
+                                           ((span >= 32 ? 0u : 1u << span) - 1u);
+        if (top && a.R && __all_sync(GP_FULL, fits)) {
+          if (span > 0) {
+            if constexpr (kStats) {
+              ++st_sweeps;
+              st_live_closed += (uint64_t)span;
+            }
+            // run i holds len0 - i - a0 schedulable candidates (last part a0+1 .. len0-i)
+            acc_n += (uint32_t)(span * (len0 - a0) - (lo_l + hi_l - 1) * span / 2);
+            acc_pi = min(acc_pi, M - len0 + 1 + lo_l + a0);
+            first_off = min(first_off, off + (uint32_t)(lo_l * len0 - lo_l * (lo_l - 1) / 2 + a0));
+            const uint64_t rr = a.run_base[k] + (uint64_t)p * a.L.n_runs[k] + roff;
+            const uint64_t *Ra = a.R + (uint64_t)a0 * a.r_stride + rr;
+            acc_hash += __ldg(reinterpret_cast<const unsigned long long *>(Ra + hi_l)) -
+                        __ldg(reinterpret_cast<const unsigned long long *>(Ra + lo_l));
+          }
+          return;
+        }
+      }
       const int i_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)lo_l);
       const int i_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(hi_l, 0));
       if (i_lo >= i_hi) return;
@@ -609,9 +736,9 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       }
     };
     if (kp == 0) {  // k = 1: one run, the single block at 1 .. M
-      sweep(M, 1, dead ? 0u : 1u, 0u);
+      sweep(M, 1, dead ? 0u : 1u, 0u, 0u);
     } else if (kp == 1) {  // k = 2: one sweep over s_0
-      sweep(M - 1, M - 1, dead ? 0u : Vr[1], 0u);
+      sweep(M - 1, M - 1, dead ? 0u : Vr[1], 0u, 0u);
     } else {
       // k >= 3: the outer parts s_0 .. s_{k-4} (reversed: q[0] = s_{k-4}) in
       // lexicographic order (sum <= M - 3 leaves room for s_{k-3}, s_{k-2}, s_{k-1});
@@ -624,7 +751,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
 #pragma unroll
       for (int t = 0; t < kBpMaxN; ++t) q[t] = 1;
       int qsum = k2;
-      uint32_t off2 = 0;
+      uint32_t off2 = 0, roff2 = 0;  // s-index / run index of the outer prefix's first candidate
       for (;;) {
         uint32_t rh = dead ? 0u : 1u;  // outer blocks pass at q
 #pragma unroll
@@ -637,12 +764,15 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         const int v_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)vlo_l);
         const int v_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(vhi_l, 0));
         const uint32_t tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);
+        const uint32_t tri1 = (uint32_t)(L1 * (L1 + 1) / 2);  // runs of the outer prefix
         for (int v = v_lo; v <= v_hi; ++v) {
           const int len0 = L1 - v + 1;
           const uint32_t offv = off2 + tet1 - (uint32_t)(len0 * (len0 + 1) * (len0 + 2) / 6);
-          sweep(len0, len0, ((w2 >> (v - 1)) & 1u) ? Vr[1] : 0u, offv);
+          const uint32_t roffv = roff2 + tri1 - (uint32_t)(len0 * (len0 + 1) / 2);
+          sweep(len0, len0, ((w2 >> (v - 1)) & 1u) ? Vr[1] : 0u, offv, roffv);
         }
         off2 += tet1;
+        roff2 += tri1;
         // lexicographic successor of the outer parts (sum <= M - 3)
         if (k2 == 0) break;
         if (qsum < M - 3) {
@@ -672,11 +802,14 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
   if constexpr (kStats) {
     const uint64_t c0 = warp_sum_u64(st_cand);
     const uint64_t c4 = warp_sum_u64(st_runs), c5 = warp_sum_u64(st_live);
+    const uint64_t c6 = warp_sum_u64(st_sweeps), c7 = warp_sum_u64(st_live_closed);
     if (lane == 0) {
       atomicAdd(a.stats + 0, c0);
       if (a.flags & GP_EX_STATS_EXT) {
         atomicAdd(a.stats + 4, c4);
         atomicAdd(a.stats + 5, c5);
+        atomicAdd(a.stats + 6, c6);
+        atomicAdd(a.stats + 7, c7);
       }
     }
   }
@@ -711,11 +844,11 @@ namespace gp {
 // stream-ordered temporary): memo words [n_sets][2^n], RGS labels, the per-subset
 // lane order (slots, histograms, load levels) and the hash prefix table.
 struct BpLayout {
-  size_t memo_words, sp_words, sp_total, words32, bytes;
-  uint64_t n_rgs, n_ranks;
-  uint32_t nb;
+  size_t memo_words, sp_words, sp_total, words32, bytes, r_off;
+  uint64_t n_rgs, n_ranks, total_runs, r_stride;
+  uint32_t nb, r_nb;
   int sp_keys;
-  bool use_sp, use_P;
+  bool use_sp, use_P, use_R;
 };
 
 static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_groups,
@@ -737,6 +870,19 @@ static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_
   // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
   // entries past a run's end in lanes whose verdict word is zero there; never summed)
   b.bytes = b.words32 * 4 + (b.use_P ? (b.n_ranks + 1 + kPpad + b.nb) * 8 : 0);
+  // run-prefix table R [M][total runs + 1] (+ block totals), with the hash table, while it
+  // stays within 64 Mi entries (C3: 20 x 148,734)
+  b.total_runs = 0;
+  for (int k = 1; k <= L.kmax; ++k) {
+    uint64_t c = 1;
+    for (int i = 0; i < k - 1; ++i) c = c * (uint64_t)(L.M - 1 - i) / (uint64_t)(i + 1);
+    b.total_runs += L.n_pi[k] * c;
+  }
+  b.r_stride = b.total_runs + 1;
+  b.use_R = b.use_P && (uint64_t)L.M * b.r_stride <= ((uint64_t)1 << 26);
+  b.r_nb = (uint32_t)((b.total_runs + kScanBlock - 1) / kScanBlock);
+  b.r_off = b.bytes;
+  if (b.use_R) b.bytes += ((uint64_t)L.M * b.r_stride + (uint64_t)L.M * b.r_nb) * 8;
   return b;
 }
 }  // namespace gp
@@ -808,11 +954,27 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = ((enum_table_words(M, n) + 3) & ~(size_t)3) * 4;
   k_exh_rgs_table<<<1, 256, smem, st>>>(a, rgs);
-  // runs per allocation: C(M-1, k-1) prefixes
+  // runs per allocation: C(M-1, k-1) prefixes; global run index of the first run of k
+  uint64_t runs = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
     uint64_t c = 1;
     for (int i = 0; i < k - 1; ++i) c = c * (uint64_t)(M - 1 - i) / (uint64_t)(i + 1);
     a.L.n_runs[k] = (uint32_t)c;
+    a.run_base[k] = runs;
+    runs += a.L.n_pi[k] * c;
+  }
+  a.R = nullptr;
+  if (b.use_R) {
+    uint64_t *R = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.r_off);
+    uint64_t *rbt = R + (uint64_t)M * b.r_stride;
+    a.r_stride = b.r_stride;
+    int64_t gk = ((int64_t)b.total_runs + 255) / 256;
+    if (gk > (int64_t)sms * 16) gk = (int64_t)sms * 16;
+    k_run_contrib<<<(unsigned)gk, 256, 0, st>>>(a, P, R, b.total_runs);
+    k_rows_scan_local<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
+    k_rows_scan_blocks<<<M, kScanBlock, 0, st>>>(rbt, b.r_nb);
+    k_rows_scan_add<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
+    a.R = R;
   }
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;

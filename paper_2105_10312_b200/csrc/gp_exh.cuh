@@ -27,6 +27,9 @@ struct ExhArgs {
   uint32_t flags;  // gp_exhaustive_opts.flags
   int32_t force_ranges;  // bit-sliced evaluator: walk okb range by range (env GP_EXH_RANGES, tests)
   const uint32_t *sperm;  // bit-sliced evaluator: [subset][slot] -> set, sets by that subset's first passing size
+  const uint64_t *R;      // bit-sliced evaluator: run-prefix hash table [a0][run + 1] (or null)
+  uint64_t r_stride;      // entries per row of R (total runs + 1)
+  uint64_t run_base[kEnumMaxTasks + 2];  // first global run index of the allocations with k blocks
   uint32_t rgs_base[kEnumMaxTasks + 2];  // bit-sliced evaluator: first RGS index with k blocks
   uint64_t items_per_set, total_items;
   uint64_t item_base[kEnumMaxTasks + 2];

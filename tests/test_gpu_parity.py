@@ -191,8 +191,8 @@ def test_exhaustive_c2_bitmaps(G, ev):
     # the bench's launch configuration: no verdict bits, no stats
     per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
     assert (per2 == ref).all()
-    if ev == 0:  # GP_EX_STATS_EXT: 6 counters, + (set, run) pairs walked and live runs
-        st6 = torch.zeros(6, dtype=torch.int64, device="cuda")
+    if ev == 0:  # GP_EX_STATS_EXT: 8 counters, + runs walked / live, closed-form sweeps / runs
+        st6 = torch.zeros(8, dtype=torch.int64, device="cuda")
         per3 = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
         G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per3,
                          work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"), stats=st6)
@@ -200,10 +200,12 @@ def test_exhaustive_c2_bitmaps(G, ev):
         s6 = st6.cpu().numpy()
         assert (per3.cpu().numpy() == ref).all()
         assert s6[0] == 1000 * 11334 and s6[1] == 1000 * 63 * 8  # candidates, memo tests
-        # every run holding a schedulable candidate is live; live runs <= runs walked
+        # every run holding a schedulable candidate is live, walked one by one ([4], [5]) or
+        # inside a sweep resolved in closed form ([6] sweeps, [7] their live runs)
         n_runs = 1000 * sum(W_stirling(6, k) * comb(7, k - 1) for k in range(1, 7))
-        assert 0 < s6[5] <= s6[4] <= n_runs
-        assert s6[5] >= (ref[:, 0] > 0).sum()
+        assert s6[5] <= s6[4] and s6[4] + s6[7] <= n_runs and s6[6] <= s6[7]
+        assert s6[5] + s6[7] >= (ref[:, 0] > 0).sum()
+        assert s6[6] > 0  # generated sets have up-closed verdict words: the closed form runs
 
 
 @EVALUATORS
