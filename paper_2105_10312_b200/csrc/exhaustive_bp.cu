@@ -601,6 +601,12 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     // kPpad entries of slack for lanes whose a0 runs past a run's end)
     const uint64_t pu_addr = reinterpret_cast<uint64_t>(P) + 8ull * rank_pi;
     const uint64_t pl_addr = pu_addr + 8ull * (uint32_t)(a0 & 31);
+    // this lane's row of the run-prefix table at pi's first run (closed-form sweeps)
+    const uint64_t r_addr =
+        (!kWin && kHash == 1 && !kBits && a.R)
+            ? reinterpret_cast<uint64_t>(a.R) +
+                  8ull * ((uint64_t)(a0 & 31) * a.r_stride + a.run_base[k] + (uint64_t)p * a.L.n_runs[k])
+            : 0ull;
     uint32_t *bits = nullptr;
     if constexpr (kBits) bits = lane_ok ? a.bits + set * a.words : nullptr;
     uint32_t first_off = UINT32_MAX;  // s-index of pi's first schedulable candidate
@@ -629,13 +635,12 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
               st_live_closed += (uint64_t)span;
             }
             // run i holds len0 - i - a0 schedulable candidates (last part a0+1 .. len0-i)
-            acc_n += (uint32_t)(span * (len0 - a0) - (lo_l + hi_l - 1) * span / 2);
+            acc_n += (uint32_t)(span * (len0 - a0) - (((lo_l + hi_l - 1) * span) >> 1));
             acc_pi = min(acc_pi, M - len0 + 1 + lo_l + a0);
-            first_off = min(first_off, off + (uint32_t)(lo_l * len0 - lo_l * (lo_l - 1) / 2 + a0));
-            const uint64_t rr = a.run_base[k] + (uint64_t)p * a.L.n_runs[k] + roff;
-            const uint64_t *Ra = a.R + (uint64_t)a0 * a.r_stride + rr;
-            acc_hash += __ldg(reinterpret_cast<const unsigned long long *>(Ra + hi_l)) -
-                        __ldg(reinterpret_cast<const unsigned long long *>(Ra + lo_l));
+            // sweeps are visited in rank order: the lane's first live one holds its first rank
+            if (first_off == UINT32_MAX)
+              first_off = off + (uint32_t)(lo_l * len0 - ((lo_l * (lo_l - 1)) >> 1) + a0);
+            acc_hash += ld_u64(r_addr, roff + (uint32_t)hi_l) - ld_u64(r_addr, roff + (uint32_t)lo_l);
           }
           return;
         }
