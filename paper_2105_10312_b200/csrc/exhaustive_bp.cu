@@ -752,6 +752,19 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       // sweeps' candidates are counted in closed form: a sweep of len0 = L holds
       // L(L+1)/2 candidates, consecutive sweeps L, L-1, ... sum to tetrahedral numbers)
       const int k2 = kp - 2;
+      // closed items: the closed-form sweep applies to every sweep of every lane -- block
+      // k-2's word is one bit range from lo1 reaching the largest size a run can need
+      // (bit M-2), and the last block's words are top ranges (checked per item)
+      int lo1 = 0;
+      bool c1 = true;
+      if (!dead && Vr[1]) {
+        lo1 = __ffs(Vr[1]) - 1;
+        const int need = M - 1 - lo1;  // bits lo1 .. M-2
+        const uint32_t mk = need >= 32 ? ~0u : (need <= 0 ? 0u : (1u << need) - 1u);
+        c1 = ((Vr[1] >> lo1) & mk) == mk;
+      }
+      const bool closed = (!kWin && kHash == 1 && !kBits) && top && a.R != nullptr &&
+                          !a.force_ranges && __all_sync(GP_FULL, c1);
       int32_t q[kBpMaxN];
 #pragma unroll
       for (int t = 0; t < kBpMaxN; ++t) q[t] = 1;
@@ -765,16 +778,46 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         const int L1 = M - qsum - 2;  // len0 of the sweep with s_{k-3} = 1; s_{k-3} <= L1
         const uint32_t w2 = (rh & 1u) ? Vr[2] : 0u;  // bit v-1: block k-3 passes at v
         const int vlo_l = w2 ? __ffs(w2) : 99;
-        const int vhi_l = w2 ? min(L1, L1 - a0) : 0;
+        // sweep v's live runs need len0 - a0 > lo1 (closed items) / > 0 (run walk)
+        const int vhi_l = w2 ? min(L1, L1 - a0 - (closed ? lo1 : 0)) : 0;
         const int v_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)vlo_l);
         const int v_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(vhi_l, 0));
         const uint32_t tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);
         const uint32_t tri1 = (uint32_t)(L1 * (L1 + 1) / 2);  // runs of the outer prefix
-        for (int v = v_lo; v <= v_hi; ++v) {
-          const int len0 = L1 - v + 1;
-          const uint32_t offv = off2 + tet1 - (uint32_t)(len0 * (len0 + 1) * (len0 + 2) / 6);
-          const uint32_t roffv = roff2 + tri1 - (uint32_t)(len0 * (len0 + 1) / 2);
-          sweep(len0, len0, ((w2 >> (v - 1)) & 1u) ? Vr[1] : 0u, offv, roffv);
+        if (closed) {
+          // every lane's live runs of sweep v are exactly lo1 .. len0 - a0 - 1 (top ranges
+          // from a0): count, pi*, first rank in closed form, the hash from two reads of R;
+          // offsets of consecutive sweeps advance by their candidates / runs
+          if (v_lo <= v_hi) {
+            int len0 = L1 - v_lo + 1;
+            uint32_t offv = off2 + tet1 - (uint32_t)(len0 * (len0 + 1) * (len0 + 2) / 6);
+            uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
+            for (int v = v_lo; v <= v_hi; ++v) {
+              const int span = len0 - a0 - lo1;
+              if (((w2 >> (v - 1)) & 1u) && span > 0) {
+                if constexpr (kStats) {
+                  ++st_sweeps;
+                  st_live_closed += (uint64_t)span;
+                }
+                acc_n += (uint32_t)(span * (len0 - a0) - (((2 * lo1 + span - 1) * span) >> 1));
+                acc_pi = min(acc_pi, M - len0 + 1 + lo1 + a0);
+                if (first_off == UINT32_MAX)
+                  first_off = offv + (uint32_t)(lo1 * len0 - ((lo1 * (lo1 - 1)) >> 1) + a0);
+                acc_hash += ld_u64(r_addr, roffv + (uint32_t)(lo1 + span)) -
+                            ld_u64(r_addr, roffv + (uint32_t)lo1);
+              }
+              offv += (uint32_t)((len0 * (len0 + 1)) >> 1);
+              roffv += (uint32_t)len0;
+              --len0;
+            }
+          }
+        } else {
+          for (int v = v_lo; v <= v_hi; ++v) {
+            const int len0 = L1 - v + 1;
+            const uint32_t offv = off2 + tet1 - (uint32_t)(len0 * (len0 + 1) * (len0 + 2) / 6);
+            const uint32_t roffv = roff2 + tri1 - (uint32_t)(len0 * (len0 + 1) / 2);
+            sweep(len0, len0, ((w2 >> (v - 1)) & 1u) ? Vr[1] : 0u, offv, roffv);
+          }
         }
         off2 += tet1;
         roff2 += tri1;
