@@ -84,6 +84,7 @@ def _declare(L):
     L.gpref_enumerate.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int64, P, P]
     L.gpref_unrank.argtypes = [C.c_int32, C.c_int32, C.c_uint64, P, P]
     L.gpref_exhaustive.argtypes = [P, C.c_uint64, C.c_uint64, P, P, C.c_int64, C.c_int32]
+    L.gpref_exhaustive_ex.argtypes = [P, C.c_uint64, C.c_uint64, P, P, P, C.c_int64, C.c_int32]
     L.gpref_allocate.argtypes = [P, C.c_int32, P, P, P, P, P, P, C.c_int32]
     L.gpref_allocate_ex.argtypes = [P, C.c_int32, P, P, P, P, P, P, P, C.c_int32]
     L.gpref_sched_ratio.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P]
@@ -297,8 +298,20 @@ def unrank(M, n, r):
     return bot, bs
 
 
-def exhaustive(sets: Sets, rank_lo=0, rank_hi=None, bits=False, threads=None):
-    """per_set [n_sets][4] = (n_sched, pi_star, first_rank, hash as int64); bits optional."""
+def _admissible(M, sizes):
+    if sizes is None:
+        return None
+    adm = np.zeros(M + 1, np.uint8)
+    for m in sizes:
+        assert 1 <= m <= M, "admissible sizes lie in 1..M"
+        adm[m] = 1
+    return adm
+
+
+def exhaustive(sets: Sets, rank_lo=0, rank_hi=None, bits=False, threads=None, sizes=None):
+    """per_set [n_sets][4] = (n_sched, pi_star, first_rank, hash as int64); bits optional.
+    ``sizes``: admissible partition sizes (f4, reading B-9; None = every size) --
+    a candidate using another size counts as unschedulable."""
     total = count_candidates(sets.M, sets.n_tasks)
     if rank_hi is None:
         rank_hi = total
@@ -307,8 +320,10 @@ def exhaustive(sets: Sets, rank_lo=0, rank_hi=None, bits=False, threads=None):
     vb = np.zeros((sets.n_sets, words), np.uint32) if bits else None
     cs = sets._c()
     th = threads or os.cpu_count() or 1
-    _check(lib().gpref_exhaustive(C.byref(cs), rank_lo, rank_hi, _p(per),
-                                  _p(vb) if bits else None, words, th), "exhaustive")
+    adm = _admissible(sets.M, sizes)
+    _check(lib().gpref_exhaustive_ex(C.byref(cs), rank_lo, rank_hi,
+                                     None if adm is None else _p(adm), _p(per),
+                                     _p(vb) if bits else None, words, th), "exhaustive")
     return (per, vb) if bits else per
 
 
@@ -334,12 +349,7 @@ def allocate(sets: Sets, variant, threads=None, flags=0, sizes=None):
     nt = np.zeros(S, np.int64)
     cs = sets._c()
     th = threads or os.cpu_count() or 1
-    adm = None
-    if sizes is not None:
-        adm = np.zeros(sets.M + 1, np.uint8)
-        for m in sizes:
-            assert 1 <= m <= sets.M, "admissible sizes lie in 1..M"
-            adm[m] = 1
+    adm = _admissible(sets.M, sizes)
     opts = _AllocOpts(int(flags), None if adm is None else adm.ctypes.data)
     _check(lib().gpref_allocate_ex(C.byref(cs), v, C.byref(opts), _p(ok), _p(bot), _p(bs), _p(pi),
                                    _p(k), _p(nt), th), "allocate")

@@ -467,6 +467,7 @@ typedef struct {
   int64_t n_sched, pi_star, first_rank;
   uint64_t hash;
   uint32_t *bits;
+  const uint8_t *admissible; /* [M+1] or NULL (f4, reading B-9) */
 } exh_ctx;
 
 static int exh_visit(void *vctx, uint64_t rank, int32_t k, const int8_t *rgs,
@@ -482,6 +483,8 @@ static int exh_visit(void *vctx, uint64_t rank, int32_t k, const int8_t *rgs,
     for (int32_t i = 0; i < n; ++i)
       if (rgs[i] == j) mask |= 1u << i;
     sum_s += sizes[j];
+    /* f4 (reading B-9): a block on an inadmissible size is not deployable */
+    if (c->admissible && !c->admissible[sizes[j]]) ok = 0;
     if (ok && !block_schedulable(c->s, c->set, mask, sizes[j])) ok = 0;
   }
   if (ok) {
@@ -503,6 +506,7 @@ typedef struct {
   int64_t *per_set;
   uint32_t *bits;
   int64_t words;
+  const uint8_t *admissible;
   int32_t next; /* shared work counter */
   pthread_mutex_t mu;
 } exh_job;
@@ -511,6 +515,7 @@ static void exhaustive_one(exh_job *j, int32_t set) {
   exh_ctx c;
   memset(&c, 0, sizeof(c));
   c.s = j->s; c.set = set; c.lo = j->lo; c.hi = j->hi; c.first_rank = -1;
+  c.admissible = j->admissible;
   c.bits = j->bits ? j->bits + (int64_t)set * j->words : NULL;
   if (c.bits) memset(c.bits, 0, sizeof(uint32_t) * (size_t)j->words);
   for_each_candidate(j->s->M, j->s->n_tasks, exh_visit, &c);
@@ -534,6 +539,13 @@ static void *exh_worker(void *arg) {
 int gpref_exhaustive(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
                      int64_t *per_set, uint32_t *verdict_bits, int64_t words_per_set,
                      int32_t n_threads) {
+  return gpref_exhaustive_ex(s, rank_lo, rank_hi, NULL, per_set, verdict_bits, words_per_set,
+                             n_threads);
+}
+
+int gpref_exhaustive_ex(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
+                        const uint8_t *admissible, int64_t *per_set, uint32_t *verdict_bits,
+                        int64_t words_per_set, int32_t n_threads) {
   uint64_t total;
   int rc = gpref_count_candidates(s->M, s->n_tasks, &total);
   if (rc) return rc;
@@ -544,6 +556,7 @@ int gpref_exhaustive(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
   memset(&j, 0, sizeof(j));
   j.s = s; j.lo = rank_lo; j.hi = rank_hi; j.per_set = per_set; j.bits = verdict_bits;
   j.words = words_per_set;
+  j.admissible = admissible;
   pthread_mutex_init(&j.mu, NULL);
   if (n_threads < 1) n_threads = 1;
   pthread_t th[256];

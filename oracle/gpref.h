@@ -84,6 +84,14 @@ int gpref_unrank(int32_t M, int32_t n, uint64_t rank, int8_t *block_of_task,
 int gpref_exhaustive(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
                      int64_t *per_set /*[n_sets][4]*/, uint32_t *verdict_bits,
                      int64_t words_per_set, int32_t n_threads);
+/* f4 on the exhaustive path (SURVEY §8(f) f4, P:1136-1140 MIG-style slices;
+ * reading B-9 of DESIGN.md): admissible = [M+1] flags (admissible[m] != 0 ->
+ * partitions of m SMs may be formed) or NULL (every size).  A candidate that
+ * uses an inadmissible size is not a deployable configuration and is counted
+ * unschedulable; the rank space, N_c and the ranks are unchanged.          */
+int gpref_exhaustive_ex(const gpref_sets *s, uint64_t rank_lo, uint64_t rank_hi,
+                        const uint8_t *admissible, int64_t *per_set, uint32_t *verdict_bits,
+                        int64_t words_per_set, int32_t n_threads);
 
 /* ---- A5: heuristics, Alg. 1-3 + 1G ---- */
 enum { GPREF_1G = 0, GPREF_SMS_ACT = 1, GPREF_SMS_INA = 2, GPREF_BF_ACT = 3, GPREF_BF_INA = 4 };

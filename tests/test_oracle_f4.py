@@ -182,3 +182,59 @@ def test_certificates_with_masks(c4_small, v, flags):
                 c, f = (s.cc[g, i], s.fc[g, i]) if conflict else (s.cn[g, i], s.fn[g, i])
                 C.append(oracle.wcet(int(s.B[g, i]), int(c), int(f), szs[j]))
             assert oracle.edf_pdc(C, [int(s.D[g, i]) for i in mem], [int(s.T[g, i]) for i in mem])[0]
+
+
+# ---------------------------------------------------------------- masks on the exhaustive path
+# Reading B-9: with admissible sizes A a candidate (pi, s)
+# is deployable only if every s_j is in A; an inadmissible one counts as
+# unschedulable, and the rank space (C.1.6) is unchanged.  Pinned by
+# composition with separately pinned pieces: the unmasked verdict bits
+# (test_oracle_exhaustive.py) and the enumeration (test_oracle_enum.py).
+MASK64 = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def c2_masked_sample():
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    s = oracle.generate(gen, W.SEED, 0, 3)  # 3 reps x 10 bins
+    per, bits = oracle.exhaustive(s, bits=True)
+    bot, bs = oracle.enumerate_candidates(s.M, s.n_tasks)
+    return s, per, bits, bs
+
+
+@pytest.mark.parametrize("sizes", [[1, 2, 4, 8], [3, 5, 6], [2, 4, 6, 8], [7]])
+def test_exhaustive_mask_is_unmasked_bits_filtered(c2_masked_sample, sizes):
+    s, per, bits, bs = c2_masked_sample
+    per_m, bits_m = oracle.exhaustive(s, bits=True, sizes=sizes)
+    adm = np.zeros(s.M + 1, bool)
+    adm[sizes] = True
+    deploy = np.all(adm[bs.astype(np.int64)] | (bs == 0), axis=1)  # every used size admissible
+    n_c = len(bs)
+    for g in range(s.n_sets):
+        v = np.array([(int(bits[g, r // 32]) >> (r % 32)) & 1 for r in range(n_c)], bool)
+        ranks = np.nonzero(v & deploy)[0]
+        vm = np.array([(int(bits_m[g, r // 32]) >> (r % 32)) & 1 for r in range(n_c)], bool)
+        assert (vm == (v & deploy)).all()
+        assert per_m[g, 0] == len(ranks)
+        assert per_m[g, 2] == (ranks[0] if len(ranks) else -1)
+        assert per_m[g, 1] == (int(bs[ranks].sum(axis=1).min()) if len(ranks) else 0)
+        h = sum(oracle.splitmix64(int(r)) for r in ranks) & MASK64
+        assert int(np.int64(per_m[g, 3]).view(np.uint64)) == h
+    assert per_m[:, 0].sum() < per[:, 0].sum()
+
+
+def test_exhaustive_mask_every_size_is_unmasked(c2_masked_sample):
+    s, per, _, _ = c2_masked_sample
+    assert (oracle.exhaustive(s, sizes=list(range(1, s.M + 1))) == per).all()
+
+
+def test_exhaustive_only_M_is_1G(c2_masked_sample):
+    """Only size M admissible: the one deployable candidate is all tasks in one
+    partition of M SMs (rank N(M,n) of k = 1 is s = M, rank M - 1), so the set is
+    schedulable iff 1G schedules it, at pi* = M."""
+    s, _, _, _ = c2_masked_sample
+    per = oracle.exhaustive(s, sizes=[s.M])
+    g1 = oracle.allocate(s, "1G")["ok"]
+    assert (per[:, 0] == g1).all()
+    assert (per[g1 == 1, 1] == s.M).all() and (per[g1 == 1, 2] == s.M - 1).all()
+    assert 0 < g1.sum() < s.n_sets
