@@ -317,6 +317,15 @@ typedef struct {
                                  and flags, owned by the caller; NULL: a stream-ordered
                                  temporary of that size is allocated and released on `stream` */
   uint64_t workspace_bytes;   /* size of `workspace` (GP_EINVAL if too small)                  */
+  const uint32_t *size_mask;  /* EXHAUSTIVE / THRESHOLD: NULL, or
+                                 ceil(M/32) HOST words in gp_alloc_opts' layout -- bit (m-1) % 32
+                                 of word (m-1) / 32 set = partitions of m SMs are admissible
+                                 (MIG-style slices).  Reading B-9: a candidate that
+                                 uses an inadmissible size is not deployable and counts as
+                                 unschedulable; the rank space, N_c and the ranks are unchanged,
+                                 so per_set, verdict bits and windows keep their meaning.  No
+                                 admissible size in 1..M -> GP_EINVAL.  THRESHOLD: the count and
+                                 hash walk the schedulable runs (cost grows with n_sched)      */
 } gp_exhaustive_opts;
 #define GP_EX_NO_HASH 1u
 #define GP_EX_PER_CANDIDATE 2u

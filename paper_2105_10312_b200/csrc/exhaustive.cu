@@ -99,7 +99,8 @@ GP_DEV void exh_load_set(const ExhArgs &a, WarpSmem &w, int32_t *Wt, int64_t set
     for (int e = lane; e < 2 * n * M; e += 32) {
       const int i = e / (2 * M), x = (e / M) & 1, s = e % M + 1;
       const int64_t o = set * n + i;
-      Wt[e] = x ? wcet_sat(a.B[o], a.cc[o], a.fc[o], s) : wcet_sat(a.B[o], a.cn[o], a.fn[o], s);
+      Wt[e] = x ? wcet_adm(a.adm, a.B[o], a.cc[o], a.fc[o], s)
+                : wcet_adm(a.adm, a.B[o], a.cn[o], a.fn[o], s);
     }
   }
   __syncwarp();
@@ -176,7 +177,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_exhaustive(const ExhArgs a) 
           for (int e = lane; e < 2 * n * M; e += 32) {
             const int i = e / (2 * M), x = (e / M) & 1, s = e % M + 1;
             const int64_t o = set * n + i;
-            Wt[e] = x ? wcet_sat(a.B[o], a.cc[o], a.fc[o], s) : wcet_sat(a.B[o], a.cn[o], a.fn[o], s);
+            Wt[e] = x ? wcet_adm(a.adm, a.B[o], a.cc[o], a.fc[o], s)
+                      : wcet_adm(a.adm, a.B[o], a.cn[o], a.fn[o], s);
           }
         }
         __syncwarp();
@@ -823,6 +825,8 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
                               GP_EX_FORCE_RANGES | GP_EX_NATURAL_ORDER | GP_EX_GENERIC))
     return gp_fail(GP_EINVAL, "EXHAUSTIVE: unknown flags 0x%x", ex->flags);
   a.flags = ex->flags;
+  s = load_size_mask(ex->size_mask, M, a.adm, "EXHAUSTIVE");
+  if (s != GP_OK) return s;
   uint64_t items = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
     // balanced chunks of at most 32 * kMaxL size vectors of one allocation

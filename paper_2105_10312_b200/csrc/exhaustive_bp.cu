@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
       const int64_t o = set * n + i;
       const int32_t Bi = a.B[o], cni = a.cn[o], cci = a.cc[o], fni = a.fn[o], fci = a.fc[o];
       if (lane < M) {
-        w.wt[(i * 2) * kBpMaxM + lane] = wcet_sat(Bi, cni, fni, lane + 1);
-        w.wt[(i * 2 + 1) * kBpMaxM + lane] = wcet_sat(Bi, cci, fci, lane + 1);
+        w.wt[(i * 2) * kBpMaxM + lane] = wcet_adm(a.adm, Bi, cni, fni, lane + 1);
+        w.wt[(i * 2 + 1) * kBpMaxM + lane] = wcet_adm(a.adm, Bi, cci, fci, lane + 1);
       }
     }
     uint32_t mem = 0;  // type mask (memory-intensive tasks)

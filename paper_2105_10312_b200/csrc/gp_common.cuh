@@ -130,3 +130,24 @@ GP_DEV uint64_t splitmix64(uint64_t x) {
 gp_status gp_fail(gp_status st, const char *fmt, ...);
 gp_status gp_cuda_check(const char *what);
 gp_status gp_ok(void);  // clears gp_last_error() (host-only calls: no CUDA API touched)
+
+namespace gp {
+// Host: gp_exhaustive_opts.size_mask -> adm words (NULL -> every size).
+inline gp_status load_size_mask(const uint32_t *mask, int M, uint32_t (&adm)[8], const char *who) {
+  for (int w = 0; w < 8; ++w) adm[w] = ~0u;
+  if (!mask) return GP_OK;
+  bool any = false;
+  for (int w = 0; w < 8; ++w) {
+    const int lo = 32 * w + 1;  // sizes lo .. lo + 31
+    uint32_t keep = 0u;
+    if (lo <= M) {
+      const uint32_t m = mask[w];
+      keep = M - lo + 1 >= 32 ? m : m & ((1u << (M - lo + 1)) - 1u);
+    }
+    adm[w] = keep;
+    any |= keep != 0u;
+  }
+  if (!any) return gp_fail(GP_EINVAL, "%s: size_mask admits no size in 1..M", who);
+  return GP_OK;
+}
+}  // namespace gp

@@ -35,7 +35,20 @@ struct ExhArgs {
   uint64_t item_base[kEnumMaxTasks + 2];
   uint32_t chunks[kEnumMaxTasks + 2];
   int32_t lane_L[kEnumMaxTasks + 2];
+  uint32_t adm[8];  // f4 admissible sizes: bit (m-1) % 32 of word (m-1) / 32 (all ones: every size)
 };
+
+// f4 on the exhaustive path (reading B-9): a partition of an inadmissible size is
+// not deployable, so every candidate using one is unschedulable.  The W tables carry that
+// verdict: W = INT32_MAX at an inadmissible size fails every block at its first deadline
+// (C > D, gp_edf.cuh shortcut 1), so the evaluators themselves are unchanged.
+GP_DEV bool size_admissible(const uint32_t (&adm)[8], int m) {
+  return (adm[(m - 1) >> 5] >> ((m - 1) & 31)) & 1u;
+}
+GP_DEV int32_t wcet_adm(const uint32_t (&adm)[8], int32_t B, int32_t c, int32_t f, int32_t m) {
+  return size_admissible(adm, m) ? wcet_sat(B, c, f, m) : INT32_MAX;
+}
+
 
 // Per-set input contract (gpart.h): returns H = lcm(T) or -1.
 GP_DEV int64_t set_contract(const ExhArgs &a, int64_t set) {

@@ -35,7 +35,16 @@ struct ThrArgs {
   int64_t *counts;
   int32_t slot0, n_slots, setting, want_hash;
   unsigned long long *stats;  // += {sets, threshold tests, deadlines examined, schedulable enumerated}
+  int32_t masked;             // f4 size mask given (reading B-9)
+  uint32_t adm[8];            // admissible sizes, bit (m-1) % 32 of word (m-1) / 32
 };
+
+// f4 (reading B-9): first admissible size >= x, M + 1 if none.
+GP_DEV int next_admissible(const ThrArgs &a, int x) {
+  for (; x <= a.M; ++x)
+    if ((a.adm[(x - 1) >> 5] >> ((x - 1) & 31)) & 1u) return x;
+  return a.M + 1;
+}
 
 GP_DEV int64_t thr_contract(const ThrArgs &a, int64_t set) {
   const int n = a.n;
@@ -97,6 +106,78 @@ GP_DEV uint32_t lexrank_sizes(const EnumTables &t, int M, int k, const int32_t (
     }
   }
   return r;
+}
+
+// Phase 2 of one allocation under an admissible-size mask (f4, reading B-9).
+// Block j is schedulable at s iff s >= m*_j (monotonicity, on the unmasked W) and
+// s is admissible, so the schedulable vectors are prod_j A_j with A_j = {s in A :
+// s >= m*_j}, sum <= M.  lo_j = min A_j: pi* = sum lo_j, the lexicographically first
+// vector is lo.  The rest is walked run by run (a run: fixed s_0..s_{k-2}, last
+// part v = lo_{k-1} .. M - prefix; candidate rank = rank(prefix, 1) + v - 1):
+// the count adds the admissible v of each run, the hash their splitmix64.
+template <int NT>
+GP_DEV void thr_masked_alloc(const ThrArgs &a, const EnumTables &tab, int k, uint64_t rank_pi,
+                             const int32_t (&m)[NT], uint64_t &n_sched, int32_t &pi_star,
+                             uint64_t &first, uint64_t &hash, uint64_t &st_sched) {
+  const int M = a.M;
+  int32_t lo[NT], s[NT];
+  int sum_lo = 0;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    lo[j] = j < k ? next_admissible(a, m[j]) : 0;
+    if (j < k) sum_lo += lo[j];
+    s[j] = lo[j];
+  }
+  if (sum_lo > M) return;  // also covers an empty A_j (lo_j = M + 1)
+  pi_star = min(pi_star, sum_lo);
+  const uint64_t r_first = rank_pi + lexrank_sizes(tab, M, k, lo);
+  first = r_first < first ? r_first : first;
+  int lo_last = 0;
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+    if (j == k - 1) lo_last = lo[j];
+  for (;;) {
+    int prefix = 0;  // s_0 + ... + s_{k-2}
+    int32_t s1[NT];  // (prefix, 1): rank base of the run
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j < k - 1) prefix += s[j];
+      s1[j] = j == k - 1 ? 1 : s[j];
+    }
+    const uint64_t base = rank_pi + lexrank_sizes(tab, M, k, s1);
+    uint64_t cnt = 0;
+    for (int v = lo_last; v <= M - prefix; ++v) {
+      if (!((a.adm[(v - 1) >> 5] >> ((v - 1) & 31)) & 1u)) continue;
+      ++cnt;
+      if (a.want_hash) hash += splitmix64(base + (uint64_t)(v - 1));
+    }
+    n_sched += cnt;
+    if (a.want_hash) st_sched += cnt;
+    // next prefix: the rightmost part j <= k-2 that can move to its next admissible
+    // size with the parts after it reset to their minima
+    int pick = -1, nxt = 0, before = 0;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j < k - 1) {
+        int after = lo_last;  // minima of the parts after j
+#pragma unroll
+        for (int i = j + 1; i < NT; ++i)
+          if (i < k - 1) after += lo[i];
+        const int x = next_admissible(a, s[j] + 1);
+        if (before + x + after <= M) {
+          pick = j;
+          nxt = x;
+        }
+        before += s[j];
+      }
+    }
+    if (pick < 0) break;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j == pick) s[j] = nxt;
+      else if (j > pick && j < k - 1) s[j] = lo[j];
+    }
+  }
 }
 
 __host__ __device__ inline size_t thr_warp_words(int n, int M) {
@@ -183,11 +264,15 @@ __global__ void __launch_bounds__(kThrWarps * 32) k_threshold(const ThrArgs a) {
           }
         }
         if (!feasible || sum_m > M) continue;
+        const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
+        if (a.masked) {
+          thr_masked_alloc<NT>(a, tab, k, rank_pi, m, n_sched, pi_star, first, hash, st_sched);
+          continue;
+        }
         const int R = M - (sum_m - k);  // M - sum(m*_j - 1)
         const uint32_t cnt = tab.C(R, k);
         n_sched += cnt;
         pi_star = min(pi_star, sum_m);
-        const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
         const uint64_t r_first = rank_pi + lexrank_sizes(tab, M, k, m);
         first = r_first < first ? r_first : first;
         if (a.want_hash) {
@@ -325,6 +410,13 @@ gp_status gp_threshold_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_sl
   a.n_sets = ts->n_sets; a.n = n; a.M = M; a.n_groups = ts->n_groups;
   a.per_set = ex->per_set; a.counts = counts; a.slot0 = slot0; a.n_slots = n_slots;
   a.setting = setting; a.want_hash = (ex->flags & GP_EX_NO_HASH) ? 0 : 1; a.stats = ex->stats;
+  a.masked = ex->size_mask != nullptr;
+  {
+    uint32_t adm[8];
+    s = load_size_mask(ex->size_mask, M, adm, "THRESHOLD");
+    if (s != GP_OK) return s;
+    for (int w = 0; w < 8; ++w) a.adm[w] = adm[w];
+  }
   if (ts->n_sets == 0) return gp_cuda_check("THRESHOLD");
   const size_t per_warp = thr_warp_words(n, M);
   const size_t smem = (((enum_table_words(M, n) + 3) & ~(size_t)3) + per_warp * kThrWarps) * 4;

@@ -64,7 +64,8 @@ class _ExOptsC(C.Structure):
     _fields_ = [("rank_lo", C.c_uint64), ("rank_hi", C.c_uint64), ("per_set", C.c_void_p),
                 ("verdict_bits", C.c_void_p), ("words_per_set", C.c_int64),
                 ("work_counter", C.c_void_p), ("stats", C.c_void_p), ("flags", C.c_uint32),
-                ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64)]
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
+                ("size_mask", C.c_void_p)]
 
 
 _P = C.c_void_p
@@ -248,6 +249,18 @@ class AllocOut:
         return d
 
 
+def _size_mask(M, sizes):
+    """Admissible partition sizes (f4) -> ceil(M/32) host words (None -> None)."""
+    if sizes is None:
+        return None
+    mask = (C.c_uint32 * ((M + 31) // 32))()
+    for m in sizes:
+        if not 1 <= int(m) <= M:
+            raise GpError(GP_EINVAL, f"admissible size {m} outside 1..M")
+        mask[(int(m) - 1) // 32] |= 1 << ((int(m) - 1) % 32)
+    return mask
+
+
 class _AllocOptsC(C.Structure):
     _fields_ = [("flags", C.c_uint32), ("size_mask", C.c_void_p)]
 
@@ -269,13 +282,8 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
     if stats is not None and stats.numel() >= 8:
         flags |= GP_AL_STATS_EXT
     if flags or sizes is not None:
-        mask = (C.c_uint32 * ((ts.M + 31) // 32))()
-        if sizes is not None:
-            for m in sizes:
-                if not 1 <= int(m) <= ts.M:
-                    raise GpError(GP_EINVAL, f"admissible size {m} outside 1..M")
-                mask[(int(m) - 1) // 32] |= 1 << ((int(m) - 1) % 32)
-        opts = _AllocOptsC(int(flags), C.cast(mask, C.c_void_p) if sizes is not None else None)
+        mask = _size_mask(ts.M, sizes)
+        opts = _AllocOptsC(int(flags), C.cast(mask, C.c_void_p) if mask is not None else None)
         opts._keep = mask
     _check(_lib.gp_allocate(C.byref(s), v, C.byref(opts) if opts is not None else None,
                             _ptr(out.ok), _ptr(out.block_of_task),
@@ -287,13 +295,14 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
 def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=None, setting=0,
                    per_set=None, verdict_bits=None, words_per_set=0, work_counter=None,
                    stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None, flags=0,
-                   workspace=None):
+                   workspace=None, sizes=None):
     """FROM_VERDICTS: verdicts uint8 [n_rows][n_sets]; EXHAUSTIVE: per_set int64 [n_sets][4]
     (+ work_counter int64 [>=1], optional verdict_bits int32/uint32 [n_sets][words], stats
     int64 [4], or [6] for the bit-sliced evaluator's run counters; optional workspace: a
     uint8 device tensor of >= gp_exhaustive_workspace_size() bytes, else the call makes a
     stream-ordered temporary).  counts int64 [n_settings][n_groups][n_slots][3] is
-    accumulated."""
+    accumulated.  ``sizes``: admissible partition sizes for EXHAUSTIVE / THRESHOLD (f4,
+    reading B-9; None = every size)."""
     s = ts.struct()
     if stats is not None and stats.numel() >= 8 and mode == GP_EXHAUSTIVE:
         flags |= GP_EX_STATS_EXT
@@ -302,6 +311,10 @@ def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=N
         ex = _ExOptsC(rank_lo, rank_hi, _ptr(per_set), _ptr(verdict_bits), words_per_set,
                       _ptr(work_counter), _ptr(stats), flags, _ptr(workspace),
                       0 if workspace is None else workspace.numel() * workspace.element_size())
+        mask = _size_mask(ts.M, sizes)
+        if mask is not None:
+            ex.size_mask = C.cast(mask, C.c_void_p)
+            ex._keep = mask
         exp = C.byref(ex)
         vp = None
     else:

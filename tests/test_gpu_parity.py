@@ -147,7 +147,7 @@ EVALUATORS = pytest.mark.parametrize("ev", [0, 2], ids=["bitsliced", "per_candid
 
 
 def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1, flags=0,
-                   with_stats=True, workspace=False):
+                   with_stats=True, workspace=False, sizes=None):
     S = ts.n_sets
     total = G.gp_count_candidates(ts.M, ts.n_tasks)
     hi_ = total if hi is None else hi
@@ -159,7 +159,8 @@ def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slo
     G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, counts, slot0=slot0, n_slots=n_slots, per_set=per,
                      verdict_bits=vb, words_per_set=words if bits else 0, work_counter=work,
                      stats=stats if with_stats else None, rank_lo=lo, rank_hi=G.UINT64_MAX if hi is None else hi,
-                     flags=flags, workspace=G.exhaustive_workspace(ts, flags=flags) if workspace else None)
+                     flags=flags, workspace=G.exhaustive_workspace(ts, flags=flags) if workspace else None,
+                     sizes=sizes)
     torch.cuda.synchronize()
     out = per.cpu().numpy()
     if bits:
@@ -511,11 +512,11 @@ def test_pipeline_step_c2_matches_oracle(G):
 
 
 # ------------------------------------------------------------------ f3: subset thresholds
-def run_threshold(G, ts, counts=None, n_slots=1, no_hash=False):
+def run_threshold(G, ts, counts=None, n_slots=1, no_hash=False, sizes=None):
     per = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     G.gp_sched_ratio(ts, G.GP_THRESHOLD, counts, slot0=0, n_slots=n_slots, per_set=per,
-                     stats=stats, flags=G.GP_EX_NO_HASH if no_hash else 0)
+                     stats=stats, flags=G.GP_EX_NO_HASH if no_hash else 0, sizes=sizes)
     torch.cuda.synchronize()
     return per.cpu().numpy(), stats.cpu().numpy()
 
@@ -893,3 +894,94 @@ def test_allocate_f1_200_at_load(G):
     # the load points separate the heuristics (not all sets trivially (un)schedulable)
     oks = g["SMS_INA_ok"]
     assert 0 < oks.sum() < len(oks)
+
+
+# ------------------------------------------------------------------ f4 masks on the exhaustive path
+# Reading B-9: a candidate using an inadmissible partition size counts as
+# unschedulable; ranks unchanged.  Every exhaustive evaluator (bit-sliced,
+# per-candidate shaped / generic, subset-threshold) vs gpref_exhaustive_ex.
+MASK_KINDS = ["mig", "sparse", "only_M", "all"]
+
+
+def _mask_sizes(kind, M):
+    if kind == "only_M":
+        return [M]
+    if kind == "all":
+        return list(range(1, M + 1))
+    return _f4_sizes(kind, M)
+
+
+@pytest.mark.parametrize("kind", MASK_KINDS)
+def test_exhaustive_f4_masks_c2(G, kind):
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10 * 100, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 100, ts)
+    host = to_oracle(ts)
+    sizes = _mask_sizes(kind, 8)
+    ref, rbits = oracle.exhaustive(host, bits=True, sizes=sizes)
+    for ev in (0, G.GP_EX_PER_CANDIDATE, G.GP_EX_GENERIC, G.GP_EX_FORCE_RANGES):
+        per, vb, _ = run_exhaustive(G, ts, bits=True, flags=ev, sizes=sizes)
+        assert (per == ref).all() and (vb == rbits).all(), ev
+        per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False, sizes=sizes)
+        assert (per2 == ref).all(), ev
+    thr, _ = run_threshold(G, ts, sizes=sizes)
+    assert (thr == ref).all()
+    thr2, _ = run_threshold(G, ts, sizes=sizes, no_hash=True)
+    assert (thr2[:, :3] == ref[:, :3]).all()
+    for lo, hi in [(5, 37), (100, 4100), (11000, 11334)]:
+        per, vb, _ = run_exhaustive(G, ts, bits=True, lo=lo, hi=hi, sizes=sizes)
+        r2, b2 = oracle.exhaustive(host, lo, hi, bits=True, sizes=sizes)
+        assert (per == r2).all() and (vb == b2).all(), (lo, hi)
+    if kind == "all":
+        assert (ref == oracle.exhaustive(host)).all()
+
+
+@pytest.mark.parametrize("seed,n,M", [(61, 1, 1), (62, 3, 4), (63, 5, 7), (64, 6, 9), (65, 8, 12),
+                                      (66, 4, 32), (67, 3, 40), (68, 2, 31), (69, 7, 5)])
+def test_exhaustive_f4_masks_random(G, seed, n, M):
+    rng = np.random.default_rng(seed)
+    d = W.random_sets(rng, 31, n, M, periods=(4, 6, 8, 12, 24), b_max=2 * M + 3, cost_max=3)
+    ts = gpu_sets(G, d)
+    host = oracle.Sets.from_dict(d)
+    for kind in ("mig", "sparse", "only_M"):
+        sizes = _mask_sizes(kind, M) if M > 1 else [1]
+        ref, rbits = oracle.exhaustive(host, bits=True, sizes=sizes)
+        for ev in (0, G.GP_EX_PER_CANDIDATE):
+            per, vb, _ = run_exhaustive(G, ts, bits=True, flags=ev, sizes=sizes)
+            assert (per == ref).all() and (vb == rbits).all(), (kind, ev)
+        thr, _ = run_threshold(G, ts, sizes=sizes)
+        assert (thr == ref).all(), kind
+
+
+def test_exhaustive_f4_mask_c3_parity_size(G):
+    """C3 at its parity size (10^4 sets, 6.95e9 candidates) under MIG-style
+    slices: bit-sliced = per-candidate = threshold on every set, counts included,
+    and the oracle on a sample of sets."""
+    gen = W.WORKLOADS["c3"]["gen"](R=1000)
+    ts = G.TaskSets(10 * 1000, 6, 20, 10)
+    G.gp_generate(gen, W.SEED, 0, 1000, ts)
+    sizes = _mask_sizes("mig", 20)
+    c1 = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
+    c2 = torch.zeros((1, 10, 1, 3), dtype=torch.int64, device="cuda")
+    bp, _, _ = run_exhaustive(G, ts, counts=c1, sizes=sizes, with_stats=False)
+    pc, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_PER_CANDIDATE, sizes=sizes, with_stats=False)
+    thr, _ = run_threshold(G, ts, counts=c2, sizes=sizes)
+    assert (bp == pc).all() and (bp == thr).all()
+    assert (c1.cpu().numpy() == c2.cpu().numpy()).all()
+    unmasked, _, _ = run_exhaustive(G, ts, with_stats=False)
+    assert (bp[:, 0] <= unmasked[:, 0]).all() and bp[:, 0].sum() < unmasked[:, 0].sum()
+    assert (bp[:, 0] > 0).sum() > 0
+    sample = [0, 17, 2500, 5001, 7777, 9999]
+    assert (bp[sample] == oracle.exhaustive(to_oracle(ts).subset(sample), sizes=sizes)).all()
+
+
+def test_exhaustive_f4_mask_validation(G):
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    ts = G.TaskSets(10, 6, 8, 10)
+    G.gp_generate(gen, W.SEED, 0, 1, ts)
+    with pytest.raises(G.GpError):
+        run_exhaustive(G, ts, sizes=[9])  # outside 1..M (binding)
+    per = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
+    with pytest.raises(G.GpError):  # a mask with no admissible size in 1..M (library)
+        G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per, sizes=[],
+                         work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"))
