@@ -255,7 +255,8 @@ gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *
  *   the EDF processor-demand test of every block (A4); candidate verdict =
  *   AND over its blocks (C.1.8).  For n_tasks <= 8 and M <= 32 the block
  *   verdicts are memoised per (task subset, size) -- 2^n - 1 subsets x M
- *   sizes, every one tested -- and each candidate's verdict is the AND of its
+ *   sizes, each tested unless a subset S - {i} already fails at that size (S
+ *   then fails too: fewer tasks, no more conflicts) -- and each candidate's verdict is the AND of its
  *   blocks' memoised verdicts, evaluated 32 candidates per word along runs of
  *   the last part (workspace: gp_exhaustive_opts.workspace, or a stream-ordered
  *   temporary, see gp_exhaustive_workspace_size); GP_EX_PER_CANDIDATE forces the

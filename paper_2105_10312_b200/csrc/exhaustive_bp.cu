@@ -6,9 +6,10 @@
 // depends only on (S_j, s_j) within a set, so it is computed ONCE per
 // (subset, size) instead of once per (candidate, block):
 //   k_exh_memo: per set, V[S] = bitmask over sizes (bit m-1 = S schedulable on
-//   m SMs) for all 2^n - 1 task subsets S -- C3: 63 x 20 = 1,260 EDF tests per
-//   set where the per-candidate evaluator runs ~2.3 million.  Every (S, m) is
-//   tested; no monotonicity in m is assumed (that is f3's GP_THRESHOLD).
+//   m SMs) for all 2^n - 1 task subsets S -- C3: at most 63 x 20 = 1,260 EDF tests
+//   per set where the per-candidate evaluator runs ~2.3 million.  A pair (S, m) is
+//   skipped only when some S - {i} fails at m (then S fails: fewer tasks, no more
+//   conflicts); no monotonicity in m is assumed (that is f3's GP_THRESHOLD).
 //   k_sp_*: per subset, the sets ordered by (utilisation group, first passing
 //   size, load level): the lane order of the main pass (below).
 //   k_exh_bp: items = (32 sets, allocation pi), candidates in the rank order of
@@ -38,6 +39,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_MEMO_MINB
 #define GP_MEMO_MINB 4  // memo-pass CTAs per SM the register budget targets (A/B)
 #endif
+#ifndef GP_MEMO_PRUNE
+#define GP_MEMO_PRUNE 1  // memo: skip (S, m) when a subset S - {i} fails at m (exact, see k_exh_memo)
+#endif
 #ifndef GP_BP_MINB
 #define GP_BP_MINB 4  // main-pass CTAs per SM the register budget targets (A/B: -DGP_BP_MINB=n)
 #endif
@@ -52,12 +56,13 @@ GP_DEV uint64_t ld_u64(uint64_t base, uint32_t idx) {
 }
 
 // ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
-// The (subset, size) pairs of a set are spread over the lanes (C3: 63 x 20 =
-// 1,260 pairs, 40 per lane; lane pairs pq = lane + 32j).  Subsets are taken in
-// order of increasing size (a per-CTA table), so consecutive pairs -- the 32 of
-// one warp step -- mostly test subsets of the same size, and each test runs on
-// its c tasks only (compacted, templated on c) instead of NT padded slots.  The
-// verdict bits meet in a shared-memory word per subset and are written out once.
+// Subsets are taken level by level in order of increasing size c (a per-CTA table).
+// At level c only the pairs (S, m) whose subsets S - {i} all pass at m are tested
+// (the others fail exactly, see the kernel): they are compacted per chunk of 32
+// subsets by a warp scan and spread over the lanes, so every warp step tests
+// subsets of one size c on their c tasks only (templated on c; no divergence
+// between task counts).  C3: 54 % of the 1,260 pairs per set are decided this way.
+// The verdict bits meet in a shared-memory word per subset and are written out once.
 // The set's WCETs W_i(m, x) (C.1.3) are tabulated once per set in shared memory
 // (n x 2 x M entries), so a test reads its tasks' WCETs instead of recomputing
 // ceil(B/m) per (pair, task).
@@ -65,6 +70,9 @@ struct MemoWarp {
   uint32_t vs[1 << kBpMaxN];          // verdict word per subset
   int32_t wt[kBpMaxN * 2 * kBpMaxM];  // W_i(m, x) at [(i*2 + x)*32 + m-1], x = 1: conflict
   int32_t T[kBpMaxN], D[kBpMaxN], q[kBpMaxN];
+#if GP_MEMO_PRUNE
+  uint16_t list[32 * kBpMaxM];        // compacted (subset, size) pairs of one chunk of a level
+#endif
 };
 
 // EDF-PDC of the c tasks of S at size m (gp_edf.cuh shortcuts), lane-serial.
@@ -143,18 +151,77 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
     }
     mem = __ballot_sync(GP_FULL, lane < n && a.type[set * n + min(lane, n - 1)] == 1);
     __syncwarp();
+#if GP_MEMO_PRUNE
+    // Levels of increasing subset size c.  Level 1: a single task passes iff C <= D (no
+    // conflict).  Level c >= 2 tests (S, m) only if every S - {i} passes at m:
+    // a block's subset S' fails whenever S fails -- S' has fewer tasks and no more
+    // conflicts (x_i(S') <= x_i(S)) and W_i(m, 1) >= W_i(m, 0) (cc >= cn, fc >= fn:
+    // the input contract), so dbf_{S'} <= dbf_S pointwise at the deadlines of S' -- hence
+    // a failing S - {i} decides V[S] bit m = 0 exactly (no monotonicity in m is used).
+    // The surviving pairs of a chunk of up to 32 subsets are compacted (warp scan) and
+    // tested 32 at a time with c uniform across the warp.
+    const uint32_t Mmask = M >= 32 ? ~0u : (1u << M) - 1u;
+    for (int e = lane; e < n * M; e += 32) {
+      const int i = e / M, m = e - i * M + 1;
+      ++st_tests;
+      ++st_tasks;
+      if (w.wt[(i * 2) * kBpMaxM + m - 1] <= w.D[i]) atomicOr(&w.vs[1u << i], 1u << (m - 1));
+    }
+    __syncwarp();
+    int lv0 = 0, nlv = n;  // first sorder index of the level, subsets in it (C(n, c))
+    for (int c = 2; c <= n; ++c) {
+      lv0 += nlv;
+      nlv = nlv * (n - c + 1) / c;
+      for (int ch = 0; ch < nlv; ch += 32) {
+        const bool hs = ch + lane < nlv;
+        const uint32_t S = hs ? sorder[lv0 + ch + lane] : 0u;
+        uint32_t A = hs ? Mmask : 0u;
+        for (uint32_t b = S; b; b &= b - 1u) A &= w.vs[S & ~(b & (0u - b))];
+        const int cntA = __popc(A);
+        int incl = cntA;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(GP_FULL, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(GP_FULL, incl, 31);
+        int p = incl - cntA;
+        for (uint32_t b = A; b; b &= b - 1u) w.list[p++] = (uint16_t)(S | ((uint32_t)(__ffs(b) - 1) << 8));
+        __syncwarp();
+        for (int e = lane; e < total; e += 32) {
+          const uint32_t ent = w.list[e];
+          const uint32_t S2 = ent & 255u;
+          const int m = (int)(ent >> 8) + 1;
+          ++st_tests;
+          st_tasks += c;
+          bool ok;
+          switch (c) {
+            case 2: ok = memo_test<2>(w, S2, m, mem, H32, st_events); break;
+            case 3: ok = memo_test<3>(w, S2, m, mem, H32, st_events); break;
+            case 4: ok = memo_test<4>(w, S2, m, mem, H32, st_events); break;
+            case 5: ok = memo_test<(NT >= 5 ? 5 : 2)>(w, S2, m, mem, H32, st_events); break;
+            case 6: ok = memo_test<(NT >= 6 ? 6 : 2)>(w, S2, m, mem, H32, st_events); break;
+            case 7: ok = memo_test<(NT >= 7 ? 7 : 2)>(w, S2, m, mem, H32, st_events); break;
+            default: ok = memo_test<(NT >= 8 ? 8 : 2)>(w, S2, m, mem, H32, st_events); break;
+          }
+          if (ok) atomicOr(&w.vs[S2], 1u << (m - 1));
+        }
+        __syncwarp();
+      }
+    }
+#else
     int idx = 0, m = lane + 1;  // pair pq = idx * M + (m - 1), pq = lane + 32 j
     while (m > M) {
       m -= M;
       ++idx;
     }
-    for (int pq = lane; pq < npairs; pq += 32) {
-      const uint32_t S = sorder[idx];
+    for (int pq0 = 0; pq0 < npairs; pq0 += 32) {
+      const bool in = pq0 + lane < npairs;
+      const uint32_t S = in ? sorder[idx] : 0u;
       const int cnt = __popc(S);
-      ++st_tests;
-      st_tasks += cnt;
-      bool ok;
-      if (cnt == 1) {
+      bool ok = false;
+      if (!in) {
+      } else if (cnt == 1) {
         const int i = __ffs(S) - 1;  // a single task: C <= D decides (no conflict)
         ok = w.wt[(i * 2) * kBpMaxM + m - 1] <= w.D[i];
       } else {
@@ -168,6 +235,10 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
           default: ok = memo_test<(NT >= 8 ? 8 : 2)>(w, S, m, mem, H32, st_events); break;
         }
       }
+      if (in) {
+        ++st_tests;
+        st_tasks += cnt;
+      }
       if (ok) atomicOr(&w.vs[S], 1u << (m - 1));
       m += 32;  // next pair of this lane
       while (m > M) {
@@ -175,6 +246,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
         ++idx;
       }
     }
+#endif
     __syncwarp();
     for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
     __syncwarp();

@@ -4,7 +4,7 @@ cd $GRAFT_REPO_ROOT
 TAG=${1:-quick}; K=${2:-exhaustive}; shift 2
 mkdir -p gpurun_out
 python -c "import oracle; oracle.build()" > /dev/null
-timeout 900 python -m pytest tests -m gpu -x -q -k "$K" > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_$TAG.log
+timeout ${PYTEST_TIMEOUT:-900} python -m pytest tests -m gpu -x -q -k "$K" > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_$TAG.log
 tail -3 gpurun_out/pytest_$TAG.log
 timeout 600 python bench.py --no-cpu-baseline "$@" > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 python - gpurun_out/bench_$TAG.json <<'PY'
