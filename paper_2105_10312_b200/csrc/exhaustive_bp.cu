@@ -842,27 +842,42 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       for (int t = 0; t < kBpMaxN; ++t) q[t] = 1;
       int qsum = k2;
       uint32_t off2 = 0, roff2 = 0;  // s-index / run index of the outer prefix's first candidate
-      for (;;) {
-        uint32_t rh = dead ? 0u : 1u;  // outer blocks pass at q
+      // the outer blocks' verdict bit at q: the blocks of q[1..] change only when the
+      // odometer carries (rare), q[0]'s at every step
+      auto outer_hi = [&]() {
+        uint32_t r = dead ? 0u : 1u;
 #pragma unroll
-        for (int t = 0; t < kBpMaxN - 3; ++t)
-          if (t < k2) rh &= Vr[t + 3] >> (q[t] - 1);
-        const int L1 = M - qsum - 2;  // len0 of the sweep with s_{k-3} = 1; s_{k-3} <= L1
+        for (int t = 1; t < kBpMaxN - 3; ++t)
+          if (t < k2) r &= Vr[t + 3] >> (q[t] - 1);
+        return r;
+      };
+      uint32_t rh_hi = outer_hi();
+      int L1 = M - qsum - 2;  // len0 of the sweep with s_{k-3} = 1; s_{k-3} <= L1
+      uint32_t tri1 = (uint32_t)(L1 * (L1 + 1) / 2);             // runs of the outer prefix
+      uint32_t tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);  // its candidates
+      for (;;) {
+        const uint32_t rh = k2 > 0 ? rh_hi & (Vr[3] >> (q[0] - 1)) : rh_hi;  // outer blocks pass
         const uint32_t w2 = (rh & 1u) ? Vr[2] : 0u;  // bit v-1: block k-3 passes at v
         const int vlo_l = w2 ? __ffs(w2) : 99;
         // sweep v's live runs need len0 - a0 > lo1 (closed items) / > 0 (run walk)
         const int vhi_l = w2 ? min(L1, L1 - a0 - (closed ? lo1 : 0)) : 0;
         const int v_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)vlo_l);
         const int v_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(vhi_l, 0));
-        const uint32_t tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);
-        const uint32_t tri1 = (uint32_t)(L1 * (L1 + 1) / 2);  // runs of the outer prefix
         if (closed) {
           // every lane's live runs of sweep v are exactly lo1 .. len0 - a0 - 1 (top ranges
-          // from a0): count, pi*, first rank in closed form, the hash from two reads of R;
-          // offsets of consecutive sweeps advance by their candidates / runs
+          // from a0): span = len0 - a0 - lo1 live runs holding span (span + 1) / 2
+          // candidates; the hash from two reads of R.  pi* and the first rank come from
+          // the lane's first live sweep (the largest len0; sweeps are visited in rank
+          // order), outside the loop.
           if (v_lo <= v_hi) {
+            if (vlo_l <= vhi_l) {
+              const int len0f = L1 - vlo_l + 1;
+              acc_pi = min(acc_pi, M - len0f + 1 + lo1 + a0);
+              if (first_off == UINT32_MAX)
+                first_off = off2 + tet1 - (uint32_t)(len0f * (len0f + 1) * (len0f + 2) / 6) +
+                            (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
+            }
             int len0 = L1 - v_lo + 1;
-            uint32_t offv = off2 + tet1 - (uint32_t)(len0 * (len0 + 1) * (len0 + 2) / 6);
             uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
             for (int v = v_lo; v <= v_hi; ++v) {
               const int span = len0 - a0 - lo1;
@@ -871,14 +886,10 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
                   ++st_sweeps;
                   st_live_closed += (uint64_t)span;
                 }
-                acc_n += (uint32_t)(span * (len0 - a0) - (((2 * lo1 + span - 1) * span) >> 1));
-                acc_pi = min(acc_pi, M - len0 + 1 + lo1 + a0);
-                if (first_off == UINT32_MAX)
-                  first_off = offv + (uint32_t)(lo1 * len0 - ((lo1 * (lo1 - 1)) >> 1) + a0);
-                acc_hash += ld_u64(r_addr, roffv + (uint32_t)(lo1 + span)) -
+                acc_n += (uint32_t)((span * (span + 1)) >> 1);
+                acc_hash += ld_u64(r_addr, roffv + (uint32_t)(len0 - a0)) -
                             ld_u64(r_addr, roffv + (uint32_t)lo1);
               }
-              offv += (uint32_t)((len0 * (len0 + 1)) >> 1);
               roffv += (uint32_t)len0;
               --len0;
             }
@@ -898,6 +909,9 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         if (qsum < M - 3) {
           q[0] += 1;
           qsum += 1;
+          tet1 -= tri1;  // tet(L - 1) = tet(L) - tri(L), tri(L - 1) = tri(L) - L
+          tri1 -= (uint32_t)L1;
+          --L1;
         } else {
           int prefix = 0, pick = -1;
 #pragma unroll
@@ -913,6 +927,10 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             ns += t < k2 ? q[t] : 0;
           }
           qsum = ns;
+          rh_hi = outer_hi();
+          L1 = M - qsum - 2;
+          tri1 = (uint32_t)(L1 * (L1 + 1) / 2);
+          tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);
         }
       }
     }
