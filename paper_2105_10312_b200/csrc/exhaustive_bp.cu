@@ -48,7 +48,11 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_UNROLL
 #define GP_BP_UNROLL 2
 #endif
-constexpr int kBpUnroll = GP_BP_UNROLL;  // run loop unroll (A/B builds: -DGP_BP_UNROLL=n)
+#ifndef GP_BP_SWEEP_UNROLL
+#define GP_BP_SWEEP_UNROLL 2  // closed-sweep loop unroll (A/B: 1, 2, 4 -> 2 by 1.3 %)
+#endif
+constexpr int kBpUnroll = GP_BP_UNROLL;
+constexpr int kBpSweepUnroll = GP_BP_SWEEP_UNROLL;  // run loop unroll (A/B builds: -DGP_BP_UNROLL=n)
 
 // 64-bit table entry at byte address base + 8 * idx (one IMAD.WIDE + one load)
 GP_DEV uint64_t ld_u64(uint64_t base, uint32_t idx) {
@@ -111,7 +115,9 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
   MemoWarp &w = mw_all[wid];
   const int n = a.n, M = a.M;
   const int nsub = 1 << n;
+#if !GP_MEMO_PRUNE
   const int npairs = (nsub - 1) * M;
+#endif
   for (int S = threadIdx.x + 1; S < nsub; S += blockDim.x) {  // rank of S in the order
     const int c = __popc((unsigned)S);
     int r = 0;
@@ -879,6 +885,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             }
             int len0 = L1 - v_lo + 1;
             uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
+#pragma unroll kBpSweepUnroll
             for (int v = v_lo; v <= v_hi; ++v) {
               const int span = len0 - a0 - lo1;
               if (((w2 >> (v - 1)) & 1u) && span > 0) {
