@@ -39,6 +39,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_MEMO_MINB
 #define GP_MEMO_MINB 4  // memo-pass CTAs per SM the register budget targets (A/B)
 #endif
+#ifndef GP_MEMO_DENSITY
+#define GP_MEMO_DENSITY 1  // memo tests: density <= 1 passes without the demand walk (exact)
+#endif
 #ifndef GP_MEMO_PRUNE
 #define GP_MEMO_PRUNE 1  // memo: skip (S, m) when a subset S - {i} fails at m (exact, see k_exh_memo)
 #endif
@@ -74,6 +77,7 @@ struct MemoWarp {
   uint32_t vs[1 << kBpMaxN];          // verdict word per subset
   int32_t wt[kBpMaxN * 2 * kBpMaxM];  // W_i(m, x) at [(i*2 + x)*32 + m-1], x = 1: conflict
   int32_t T[kBpMaxN], D[kBpMaxN], q[kBpMaxN];
+  float invD[kBpMaxN];                // 1 / D_i (the density shortcut of memo_test)
 #if GP_MEMO_PRUNE
   uint16_t list[32 * kBpMaxM];        // compacted (subset, size) pairs of one chunk of a level
 #endif
@@ -83,13 +87,14 @@ struct MemoWarp {
 template <int c>
 GP_DEV bool memo_test(const MemoWarp &w, uint32_t S, int m, uint32_t mem, int32_t H,
                       uint32_t &events) {
-  int32_t C[c], D[c], T[c], q[c];
+  int32_t C[c], D[c], T[c], q[c], id[c];
   uint32_t bits = S;
   bool bad = false;
 #pragma unroll
   for (int a = 0; a < c; ++a) {
     const int i = __ffs(bits) - 1;
     bits &= bits - 1u;
+    id[a] = i;
     const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
     const int x = __popc(S & same) > 1 ? 1 : 0;  // conflict
     C[a] = w.wt[(i * 2 + x) * kBpMaxM + m - 1];
@@ -103,6 +108,16 @@ GP_DEV bool memo_test(const MemoWarp &w, uint32_t S, int m, uint32_t mem, int32_
 #pragma unroll
   for (int a = 0; a < c; ++a) UH += C[a] * q[a];
   if (UH > H) return false;
+#if GP_MEMO_DENSITY
+  // density test (exact sufficient condition): for t >= D_i, floor((t - D_i)/T_i) + 1 <=
+  // t / D_i because D_i <= T_i, so dbf(t) <= t * sum_i C_i / D_i <= t when the density is
+  // <= 1.  Evaluated in float against 1 - 1e-5 (the float sum's relative error is below
+  // 2^-20 for <= 8 terms), so a pass here is always a pass of the definition.
+  float dens = 0.f;
+#pragma unroll
+  for (int a = 0; a < c; ++a) dens = fmaf((float)C[a], w.invD[id[a]], dens);
+  if (dens <= 0.99999f) return true;
+#endif
   const int32_t lcut = pdc_cutoff<c>(C, D, T, q, H, UH);
   return pdc_walk<c>(C, D, T, lcut, events);
 }
@@ -154,6 +169,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
       w.T[lane] = a.T[o];
       w.D[lane] = a.D[o];
       w.q[lane] = (int32_t)(H / a.T[o]);
+      w.invD[lane] = __frcp_rn((float)a.D[o]);
     }
     mem = __ballot_sync(GP_FULL, lane < n && a.type[set * n + min(lane, n - 1)] == 1);
     __syncwarp();
