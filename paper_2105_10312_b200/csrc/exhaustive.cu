@@ -57,6 +57,9 @@ GP_DEV bool eval_block(const WarpSmem &w, const int32_t *__restrict__ Wt, int st
 #pragma unroll
   for (int a = 0; a < SZ; ++a) UH += C[a] * q[a];
   if (UH > H) return false;  // utilisation > 1
+  if constexpr (SZ <= 8) {
+    if (pdc_density_ok<SZ>(C, D)) return true;
+  }
   const int32_t lcut = pdc_cutoff<SZ>(C, D, T, q, H, UH);
   return pdc_walk<SZ>(C, D, T, lcut, events);
 }
@@ -392,6 +395,9 @@ GP_DEV bool eval_multi(const int32_t *__restrict__ Wt, const TaskRegs<N> &r, int
 #pragma unroll
   for (int a = 0; a < L; ++a) UH += C[a] * q[a];
   if (UH > H) return false;
+  if constexpr (L <= 8) {
+    if (pdc_density_ok<L>(C, D)) return true;
+  }
   const int32_t lcut = pdc_cutoff<L>(C, D, T, q, H, UH);
   return pdc_walk<L>(C, D, T, lcut, ev);
 }

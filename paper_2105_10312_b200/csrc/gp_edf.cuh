@@ -51,6 +51,22 @@ GP_DEV bool pdc_walk(const int32_t (&C)[SZ], const int32_t (&D)[SZ], const int32
   }
 }
 
+// Density test, an exact SUFFICIENT condition: for t >= D_i, floor((t - D_i)/T_i) + 1 <= t/D_i
+// since D_i <= T_i, so dbf(t) <= t * sum_i C_i/D_i <= t whenever the density is <= 1.  Float
+// with a 1e-5 margin (<= 8 terms of relative error < 2^-21 each), so true means the block
+// passes the definition; false decides nothing (the walk follows).  Padded slots: C = 0.
+#ifndef GP_DENSITY
+#define GP_DENSITY 1
+#endif
+template <int SZ>
+GP_DEV bool pdc_density_ok(const int32_t (&C)[SZ], const int32_t (&D)[SZ]) {
+  static_assert(SZ <= 8, "the 1e-5 margin covers at most 8 terms");
+  float d = 0.f;
+#pragma unroll
+  for (int a = 0; a < SZ; ++a) d += __fdividef((float)C[a], (float)D[a]);
+  return GP_DENSITY && d <= 0.99999f;
+}
+
 // Upper bound on the walk: H when U == 1, else min(H, over-estimate of L_a).
 template <int SZ>
 GP_DEV int32_t pdc_cutoff(const int32_t (&C)[SZ], const int32_t (&D)[SZ], const int32_t (&T)[SZ],
