@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--strong", action="store_true", help="alias of --split sets")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="issue every launch of the timed steps from the host instead of "
+                         "replaying the step's CUDA graphs")
     ap.add_argument("--no-direct", action="store_true",
                     help="skip timing the per-candidate (direct) evaluator beside the headline")
     ap.add_argument("--f3", action="store_true",
@@ -365,6 +368,29 @@ def main():
                          rank_hi=pipe.rank_hi)
         torch.cuda.synchronize()
         direct_stats = pst.cpu().numpy().tolist()
+    # the timed step as CUDA graphs (the same launches, replayed with a few graph launches
+    # per step, so host-side launch latency cannot starve the GPU); the dominant segments are
+    # bracketed by events between graph launches
+    graphs = None
+    if not args.no_graph and args.split != "ranks":
+        graphs = pipe.capture(mode=exh_mode, flags=exh_flags)
+        for _ in range(2):  # warm replays
+            for g in graphs:
+                g.replay()
+        torch.cuda.synchronize()
+
+    def graph_step():
+        for i, g in enumerate(graphs):
+            if i % 2 == 1:  # a dominant segment
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                dom_ev.append((e0, e1))
+            else:
+                g.replay()
+        allreduce_counts(pipe.counts)
+
     pipe.reset_counts()
     if world > 1:
         dist.barrier()
@@ -375,7 +401,10 @@ def main():
         flush.zero_()  # L2 flush between steps, outside the events
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        step(True)
+        if graphs is not None:
+            graph_step()
+        else:
+            step(True)
         s1.record(stream)
         evs.append((s0, s1))
     torch.cuda.synchronize()
@@ -519,6 +548,8 @@ def main():
                    "parallelism": f"dp{world}" + ("" if args.split != "ranks"
                                                   else " (candidate-rank windows)"),
                    "l2": "flushed between steps (256 MiB memset outside the events)",
+                   "launch": ("CUDA graphs: %d segments per step, dominant segments bracketed "
+                              "by events" % len(graphs)) if graphs is not None else "eager",
                    "seed": W.SEED},
         "roofline": roof,
         "gpu_launches": launches_per_step(pipe, args) * args.steps,
@@ -613,15 +644,41 @@ def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
             for f, t in host.items():
                 getattr(dev, f).copy_(t, non_blocking=True)
 
-    def compute(dev, with_stats=False):
-        """The step's ABI calls on `stream`, then the D2H of its results."""
-        with torch.cuda.stream(stream):
+    def compute_on(dev, s, with_stats=False, collectives=True):
+        """The step's ABI calls on stream `s`, then the D2H of its results."""
+        with torch.cuda.stream(s):
             pipe.counts.zero_()
-        pipe.run(stream, mode=exh_mode, flags=exh_flags,
-                 alloc_stats=stats if with_stats else None, ts=dev)
-        with torch.cuda.stream(stream):
+        pipe.run(s, mode=exh_mode, flags=exh_flags,
+                 alloc_stats=stats if with_stats else None, ts=dev, collectives=collectives)
+        with torch.cuda.stream(s):
             for h, d in zip(host_out, outs):
                 h.copy_(d, non_blocking=True)
+
+    # the compute of a step on either input buffer as a CUDA graph (as in the device-only
+    # timed loop); the counts all-reduce and the copies on the copy stream stay outside
+    egraphs = None
+    if not args.no_graph and pipe.split != "ranks":
+        compute_on(devs[0], stream)  # warm (lazy module loading, workspaces)
+        torch.cuda.synchronize()
+        egraphs = []
+        for dev in devs:
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                g.capture_begin()
+                compute_on(dev, side, collectives=False)
+                g.capture_end()
+            stream.wait_stream(side)
+            egraphs.append(g)
+
+    def compute(dev, with_stats=False):
+        if egraphs is not None and not with_stats:
+            egraphs[devs.index(dev)].replay()
+            from paper_2105_10312_b200.pipeline import allreduce_counts
+            allreduce_counts(pipe.counts)
+        else:
+            compute_on(dev, stream, with_stats)
 
     def run(k_steps, with_stats=False):
         """k_steps pipelined steps; returns (start, end) events on `stream`."""
@@ -669,7 +726,9 @@ def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.steps,
             "path": "pinned host task sets -> H2D (double-buffered on a copy stream) -> "
                     "gp_sched_ratio(EXHAUSTIVE) + gp_allocate x5 + gp_sched_ratio -> D2H counts, "
-                    "verdicts, per-set results (one setting), every step inside the timed region"}
+                    "verdicts, per-set results (one setting), every step inside the timed region"
+                    + ("; the compute and D2H replayed as one CUDA graph per input buffer"
+                       if egraphs is not None else "")}
 
 
 if __name__ == "__main__":

@@ -110,7 +110,7 @@ class Pipeline:
         return g
 
     def run(self, stream=None, mode=G.GP_EXHAUSTIVE, flags=0, stats=False, alloc_stats=None,
-            on_dominant=None, ts=None):
+            on_dominant=None, ts=None, collectives=True):
         """Enqueue one full step (no host synchronisation except the collectives of the
         "ranks" split).  ``on_dominant(phase)`` is called with "begin"/"end" around the
         exhaustive call (or around the heuristics when there is none): bench.py records its
@@ -151,7 +151,33 @@ class Pipeline:
                 G.gp_sched_ratio(ts_h, G.GP_FROM_VERDICTS, self.counts,
                                  verdicts=self.verdicts, slot0=1 if self.exhaustive else 0,
                                  n_slots=self.n_slots, setting=si, stream=stream)
-        allreduce_counts(self.counts)
+        if collectives:
+            allreduce_counts(self.counts)
+
+    def capture(self, mode=G.GP_EXHAUSTIVE, flags=0):
+        """One step as CUDA graphs: the launches between the ``on_dominant`` hooks become
+        alternating segments [other, dominant, other, ...] (several for C5's settings), so
+        a caller can replay the step with a handful of graph launches and still bracket
+        the dominant launches with CUDA events between segments.  The counts all-reduce
+        stays outside (call allreduce_counts after a replay).  Not for the "ranks" split,
+        whose per-set merge is a host-driven collective.  Returns the list of graphs."""
+        if self.split == "ranks":
+            raise ValueError("capture: the ranks split merges windows on the host")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        graphs = [torch.cuda.CUDAGraph()]
+
+        def hook(phase):
+            graphs[-1].capture_end()
+            graphs.append(torch.cuda.CUDAGraph())
+            graphs[-1].capture_begin()
+
+        with torch.cuda.stream(side):
+            graphs[0].capture_begin()
+            self.run(side, mode=mode, flags=flags, on_dominant=hook, collectives=False)
+            graphs[-1].capture_end()
+        torch.cuda.current_stream().wait_stream(side)
+        return graphs
 
     def candidates_per_step(self) -> int:
         """Exhaustive candidate evaluations per step on this rank (the metric's unit)."""
