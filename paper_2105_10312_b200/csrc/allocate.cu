@@ -59,11 +59,14 @@ struct AllocArgs {
 };
 
 #ifndef GP_ALLOC_NS4
-#define GP_ALLOC_NS4 1
+#define GP_ALLOC_NS4 8  // widest group that gets the <= 4-task lane-serial merge (0: none)
 #endif
-// lane-serial merge instantiation for <= 4 tasks besides <= 8 (more code for the
-// instruction cache, which the divergent groups of a warp already stress: A/B-measured)
-constexpr bool kAllocNs4 = GP_ALLOC_NS4;
+// lane-serial merge instantiation for <= 4 tasks besides <= 8: more code for the instruction
+// cache, which the divergent groups of a warp already stress (no_instructions is the top stall
+// of the heuristics kernels).  A/B-measured: it pays in 8-lane groups (C3: 4.72 vs 4.89 ms per
+// step) and costs in 16- and 32-lane groups (C5 88 -> 85 ms, C4 124 -> 118 ms without it).
+template <int G>
+constexpr bool kAllocNs4 = G <= GP_ALLOC_NS4;
 
 // A group of G lanes of one warp works on one task set (G = 8, 16 or 32: the
 // smallest power of two >= n), so small sets share a warp.  Every collective is
@@ -591,7 +594,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
                 int64_t cnt2 = 0;
                 const int32_t lo2 = max(best_m, psz), hi2 = best_m + psz - 1;
                 if (mine && c2 <= 8) {
-                  if (kAllocNs4 && maxc <= 4)
+                  if (kAllocNs4<G> && maxc <= 4)
                     got2 = serial_merge<4, kGen>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec);
                   else
                     got2 = serial_merge<8, kGen>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec);
@@ -689,10 +692,12 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
 
 }  // namespace gp
 
-// per-CTA wave-table budget (compile-time A/B switch -DGP_ALLOC_TAB_KB=n, default 40 KB:
-// 3 CTAs per SM stay resident next to the groups' scratch)
+// per-CTA wave-table budget (compile-time A/B switch -DGP_ALLOC_TAB_KB=n).  Default 0 (no
+// table): since the pair tables, building the n x M table of ceil(B_i/m) per set costs more
+// than the divisions it saves (A/B: C3 4.72 -> 4.68 ms per step, C5 99.9 -> 91.4 ms; C4's
+// table never fit the 40 KB budget)
 #ifndef GP_ALLOC_TAB_KB
-#define GP_ALLOC_TAB_KB 40
+#define GP_ALLOC_TAB_KB 0
 #endif
 // minimum group width (compile-time A/B switch -DGP_ALLOC_MIN_G=8|16|32, default 8)
 #ifndef GP_ALLOC_MIN_G
