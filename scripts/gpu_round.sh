@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round measurement (profiles/r01): gpu tests, smoke, bench lines (c3 default + per-candidate A/B,
+# Round measurement (profiles/rNN, collected by scripts/collect_profiles.sh): gpu tests, smoke, bench lines (c3 default + per-candidate A/B,
 # c2, c4, c5, reference arm), launch lists (c3, c4), ncu --set full of the dominant kernels.
 cd $GRAFT_REPO_ROOT
 T=${1:-r1d}
@@ -14,10 +14,11 @@ timeout 900 python bench.py --config c2 > $O/bench_c2.json 2> $O/bench_c2.err; e
 timeout 900 python bench.py --config c4 > $O/bench_c4.json 2> $O/bench_c4.err; echo "c4 rc=$?"
 timeout 900 python bench.py --config c5 > $O/bench_c5.json 2> $O/bench_c5.err; echo "c5 rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference_c3.json 2> $O/bench_ref.err; echo "ref rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches c3 rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c4.csv python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches c4 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_exh_(memo|bp)" -c 2 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_exhaustive" -c 1 -o $O/full_c3_pc python bench.py --per-candidate --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_c3_pc.log 2>&1; echo "ncu c3 pc rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:k_allocate" -c 5 -o $O/full_c4_alloc python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_c4a.log 2>&1; echo "ncu c4 alloc rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_generate" -c 1 -o $O/full_c4_gen python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_c4g.log 2>&1; echo "ncu c4 gen rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1; echo "launches c3 rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c4.csv python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1; echo "launches c4 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_exh_(memo|bp)" -c 2 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > $O/ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_exhaustive" -c 1 -o $O/full_c3_pc python bench.py --per-candidate --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > $O/ncu_c3_pc.log 2>&1; echo "ncu c3 pc rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:k_allocate" -c 5 -o $O/full_c4_alloc python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > $O/ncu_c4a.log 2>&1; echo "ncu c4 alloc rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_generate" -c 1 -o $O/full_c4_gen python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > $O/ncu_c4g.log 2>&1; echo "ncu c4 gen rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_allocate" -c 5 -o $O/full_c3_alloc python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph --no-direct > $O/ncu_c3a.log 2>&1; echo "ncu c3 alloc rc=$?"
 ls $O
