@@ -42,6 +42,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_MEMO_DENSITY
 #define GP_MEMO_DENSITY 1  // memo tests: density <= 1 passes without the demand walk (exact)
 #endif
+#ifndef GP_MEMO_RANK_ORDER
+#define GP_MEMO_RANK_ORDER 1  // memo: compacted tests ordered by their rank within the subset
+#endif
 #ifndef GP_MEMO_PRUNE
 #define GP_MEMO_PRUNE 1  // memo: skip (S, m) when a subset S - {i} fails at m (exact, see k_exh_memo)
 #endif
@@ -199,6 +202,25 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
         const uint32_t S = hs ? sorder[lv0 + ch + lane] : 0u;
         uint32_t A = hs ? Mmask : 0u;
         for (uint32_t b = S; b; b &= b - 1u) A &= w.vs[S & ~(b & (0u - b))];
+#if GP_MEMO_RANK_ORDER
+        // list order: every subset's smallest surviving size first (the tests at a subset's
+        // schedulability boundary, where U is near 1 and the demand walks are long), then
+        // every subset's second, ...: a warp step's 32 walks are of similar length
+        int total = 0;
+        {
+          uint32_t b = A;
+          const uint32_t lt = (1u << lane) - 1u;
+          for (;;) {
+            const uint32_t has = __ballot_sync(GP_FULL, b != 0u);
+            if (!has) break;
+            if (b) {
+              w.list[total + __popc(has & lt)] = (uint16_t)(S | ((uint32_t)(__ffs(b) - 1) << 8));
+              b &= b - 1u;
+            }
+            total += __popc(has);
+          }
+        }
+#else
         const int cntA = __popc(A);
         int incl = cntA;
 #pragma unroll
@@ -209,6 +231,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
         const int total = __shfl_sync(GP_FULL, incl, 31);
         int p = incl - cntA;
         for (uint32_t b = A; b; b &= b - 1u) w.list[p++] = (uint16_t)(S | ((uint32_t)(__ffs(b) - 1) << 8));
+#endif
         __syncwarp();
         for (int e = lane; e < total; e += 32) {
           const uint32_t ent = w.list[e];

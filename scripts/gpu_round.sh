@@ -21,4 +21,20 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_e
 timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:k_allocate" -c 5 -o $O/full_c4_alloc python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > $O/ncu_c4a.log 2>&1; echo "ncu c4 alloc rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_generate" -c 1 -o $O/full_c4_gen python bench.py --config c4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > $O/ncu_c4g.log 2>&1; echo "ncu c4 gen rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_allocate" -c 5 -o $O/full_c3_alloc python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph --no-direct > $O/ncu_c3a.log 2>&1; echo "ncu c3 alloc rc=$?"
-ls $O
+# summarise the ncu reports here and drop them (gpurun returns at most 64 MiB)
+for r in full_c3:ncu_full_bitsliced_c3:c3_exhaustive_20sm:69475500000 \
+         full_c3_alloc:ncu_full_k_allocate_c3:c3_exhaustive_20sm_allocate: \
+         full_c3_pc:ncu_full_per_candidate_c3:c3_exhaustive_20sm_per_candidate:69475500000 \
+         full_c4_alloc:ncu_full_k_allocate_c4:c4_b200_148sm_allocate: \
+         full_c4_gen:ncu_full_k_generate_c4:c4_b200_148sm_generate: ; do
+  IFS=: read rep txt key cand <<< "$r"
+  [ -f $O/$rep.ncu-rep ] || continue
+  python scripts/ncu_summary.py $O/$rep.ncu-rep --top 14 > $O/$txt.txt
+  python scripts/ncu_metrics.py $O/$rep.ncu-rep $key --out $O/ncu_metrics.json ${cand:+--candidates $cand} \
+    --note "ncu --set full --clock-control none at the bench's launch configuration (scripts/gpu_round.sh $T); dram_bytes per call, cold L2" > /dev/null
+done
+[ "$KEEP_REPORTS" = "c3" ] && mv $O/full_c3.ncu-rep $O/keep_full_c3.ncu-rep
+rm -f $O/*.ncu-rep
+[ -f $O/keep_full_c3.ncu-rep ] && mv $O/keep_full_c3.ncu-rep $O/full_c3.ncu-rep
+bash scripts/gpu_sanitize.sh $T
+ls $O; du -sh $O
