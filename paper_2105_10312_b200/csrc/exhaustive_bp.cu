@@ -54,6 +54,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_UNROLL
 #define GP_BP_UNROLL 2
 #endif
+#ifndef GP_BP_LANE_V
+#define GP_BP_LANE_V 1  // closed sweeps: per-lane v ranges instead of the warp union (A/B: 3.69 -> 3.54 ms)
+#endif
 #ifndef GP_BP_SWEEP_UNROLL
 #define GP_BP_SWEEP_UNROLL 2  // closed-sweep loop unroll (A/B: 1, 2, 4 -> 2 by 1.3 %)
 #endif
@@ -922,10 +925,16 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
                 first_off = off2 + tet1 - (uint32_t)(len0f * (len0f + 1) * (len0f + 2) / 6) +
                             (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
             }
-            int len0 = L1 - v_lo + 1;
+#if GP_BP_LANE_V
+            // each lane walks its own live range [vlo_l, vhi_l] (the warp runs the longest)
+            const int v_first = vlo_l, v_last = vhi_l;
+#else
+            const int v_first = v_lo, v_last = v_hi;
+#endif
+            int len0 = L1 - v_first + 1;
             uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
 #pragma unroll kBpSweepUnroll
-            for (int v = v_lo; v <= v_hi; ++v) {
+            for (int v = v_first; v <= v_last; ++v) {
               const int span = len0 - a0 - lo1;
               if (((w2 >> (v - 1)) & 1u) && span > 0) {
                 if constexpr (kStats) {
