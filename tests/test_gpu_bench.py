@@ -52,3 +52,30 @@ def test_bench_reference_arm():
     d = run_bench("--impl", "reference", "--reps", "20", "--steps", "1", "--warmup", "1")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.parametrize("split", ["weak", "sets", "ranks"])
+def test_bench_two_ranks(split):
+    """The N > 1 launch the driver uses (torchrun, one process per rank, max-over-ranks
+    timing), with both ranks sharing the test box's one GPU over gloo: one JSON line from
+    rank 0 with n_gpus = 2; graph-mode replay for the set splits, eager for the rank
+    windows (whose per-set merge is a host-driven collective)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, GP_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--config", "c3", "--reps", "64", "--split", split,
+                          "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-direct"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["scaling"] == ("weak" if split == "weak" else "strong")
+    launch = d["config"]["launch"]
+    assert launch.startswith("CUDA graphs") if split != "ranks" else launch == "eager"
