@@ -681,18 +681,15 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     }
     // block task masks of pi (warp-uniform ballots) -> this lane's set's
     // verdict words, reversed: Vr[jj] = V[set][S_{k-1-jj}]
+    // (compile-time index jj, runtime block k-1-jj: no register-array indexing)
     uint32_t Vr[kBpMaxN];
 #pragma unroll
-    for (int q = 0; q < kBpMaxN; ++q) Vr[q] = 0;
-#pragma unroll
-    for (int j = 0; j < kBpMaxN; ++j) {
-      const uint32_t bm = __ballot_sync(GP_FULL, myb == j);
-      const int jj = k - 1 - j;
-      uint32_t v = 0;
-      if (j < k && lane_ok) v = memo[set * nsub + bm];
-#pragma unroll
-      for (int q = 0; q < kBpMaxN; ++q)
-        if (q == jj) Vr[q] = v;
+    for (int jj = 0; jj < kBpMaxN; ++jj) {
+      Vr[jj] = 0u;
+      if (jj < k) {  // warp-uniform
+        const uint32_t bm = __ballot_sync(GP_FULL, myb == k - 1 - jj);
+        if (lane_ok) Vr[jj] = memo[set * nsub + bm];
+      }
     }
     if (!__any_sync(GP_FULL, lane_ok)) continue;
     const int kp = k - 1;
@@ -912,15 +909,19 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         const int vlo_l = w2 ? __ffs(w2) : 99;
         // sweep v's live runs need len0 - a0 > lo1 (closed items) / > 0 (run walk)
         const int vhi_l = w2 ? min(L1, L1 - a0 - (closed ? lo1 : 0)) : 0;
-        const int v_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)vlo_l);
-        const int v_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(vhi_l, 0));
+        // the warp's union of the lanes' sweep ranges (closed items walk per lane instead)
+        int v_lo = 0, v_hi = -1;
+        if (!(closed && GP_BP_LANE_V)) {
+          v_lo = (int)__reduce_min_sync(GP_FULL, (unsigned)vlo_l);
+          v_hi = (int)__reduce_max_sync(GP_FULL, (unsigned)max(vhi_l, 0));
+        }
         if (closed) {
           // every lane's live runs of sweep v are exactly lo1 .. len0 - a0 - 1 (top ranges
           // from a0): span = len0 - a0 - lo1 live runs holding span (span + 1) / 2
           // candidates; the hash from two reads of R.  pi* and the first rank come from
           // the lane's first live sweep (the largest len0; sweeps are visited in rank
           // order), outside the loop.
-          if (v_lo <= v_hi) {
+          if (GP_BP_LANE_V ? vlo_l <= vhi_l : v_lo <= v_hi) {
             if (vlo_l <= vhi_l) {
               const int len0f = L1 - vlo_l + 1;
               acc_pi = min(acc_pi, M - len0f + 1 + lo1 + a0);
