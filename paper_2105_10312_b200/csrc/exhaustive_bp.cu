@@ -57,6 +57,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_LANE_V
 #define GP_BP_LANE_V 1  // closed sweeps: per-lane v ranges instead of the warp union (A/B: 3.69 -> 3.54 ms)
 #endif
+#ifndef GP_BP_CLOSED2
+#define GP_BP_CLOSED2 1  // closed items whose block k-3 words are top ranges too (A/B)
+#endif
 #ifndef GP_BP_EAGER_LOADS
 #define GP_BP_EAGER_LOADS 1  // closed sweeps: R reads before the bit test (A/B: 3.53 -> 3.45 ms)
 #endif
@@ -885,6 +888,19 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       }
       const bool closed = (!kWin && kHash == 1 && !kBits) && top && a.R != nullptr &&
                           !a.force_ranges && __all_sync(GP_FULL, c1);
+      // closed2: block k-3's word is also one bit range from lo2 reaching the largest
+      // size a sweep can need (bit M-3) in every lane, so a lane's live sweeps of an outer
+      // prefix are exactly v = lo2+1 .. L1 - a0 - lo1 with spans span_hi .. 1: the count
+      // is tetrahedral and only the hash reads remain per sweep (checked per item)
+      int lo2 = 0;
+      bool c2 = true;
+      if (GP_BP_CLOSED2 && !dead && Vr[2]) {
+        lo2 = __ffs(Vr[2]) - 1;
+        const int need = M - 2 - lo2;  // bits lo2 .. M-3
+        const uint32_t mk = need >= 32 ? ~0u : (need <= 0 ? 0u : (1u << need) - 1u);
+        c2 = ((Vr[2] >> lo2) & mk) == mk;
+      }
+      const bool closed2 = GP_BP_CLOSED2 && closed && GP_BP_LANE_V && __all_sync(GP_FULL, c2);
       int32_t q[kBpMaxN];
 #pragma unroll
       for (int t = 0; t < kBpMaxN; ++t) q[t] = 1;
@@ -905,6 +921,31 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       uint32_t tet1 = (uint32_t)(L1 * (L1 + 1) * (L1 + 2) / 6);  // its candidates
       for (;;) {
         const uint32_t rh = k2 > 0 ? rh_hi & (Vr[3] >> (q[0] - 1)) : rh_hi;  // outer blocks pass
+        if (closed2) {
+          const int span_hi = L1 - lo2 - a0 - lo1;  // span of the lane's first sweep v = lo2+1
+          if ((rh & 1u) && Vr[2] && span_hi >= 1) {
+            const int len0f = L1 - lo2;
+            if constexpr (kStats) {
+              st_sweeps += (uint64_t)span_hi;
+              st_live_closed += (uint64_t)((span_hi * (span_hi + 1)) >> 1);
+            }
+            acc_n += (uint32_t)(span_hi * (span_hi + 1) * (span_hi + 2) / 6);
+            acc_pi = min(acc_pi, M - len0f + 1 + lo1 + a0);
+            if (first_off == UINT32_MAX)
+              first_off = off2 + tet1 - (uint32_t)(len0f * (len0f + 1) * (len0f + 2) / 6) +
+                          (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
+            int len0 = len0f;
+            uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
+            uint64_t hsum = 0;
+#pragma unroll kBpSweepUnroll
+            for (int sp = span_hi; sp >= 1; --sp) {
+              hsum += ld_u64(r_addr, roffv + (uint32_t)(len0 - a0)) - ld_u64(r_addr, roffv + (uint32_t)lo1);
+              roffv += (uint32_t)len0;
+              --len0;
+            }
+            acc_hash += hsum;
+          }
+        } else {
         const uint32_t w2 = (rh & 1u) ? Vr[2] : 0u;  // bit v-1: block k-3 passes at v
         const int vlo_l = w2 ? __ffs(w2) : 99;
         // sweep v's live runs need len0 - a0 > lo1 (closed items) / > 0 (run walk)
@@ -977,6 +1018,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             sweep(len0, len0, ((w2 >> (v - 1)) & 1u) ? Vr[1] : 0u, offv, roffv);
           }
         }
+        }  // !closed2
         off2 += tet1;
         roff2 += tri1;
         // lexicographic successor of the outer parts (sum <= M - 3)
