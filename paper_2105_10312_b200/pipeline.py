@@ -46,7 +46,8 @@ INT64_MAX = (1 << 63) - 1
 class Pipeline:
     def __init__(self, key: str, reps: int = None, rank: int = 0, world: int = 1,
                  device="cuda", exhaustive: bool = None, variants=None, settings=None,
-                 seed: int = W.SEED, stats: bool = True, split: str = "weak"):
+                 seed: int = W.SEED, stats: bool = True, split: str = "weak",
+                 memo_heuristics: bool = True):
         if split not in SPLITS:
             raise ValueError(f"split must be one of {SPLITS}")
         wl = W.WORKLOADS[key]
@@ -100,6 +101,10 @@ class Pipeline:
         else:
             self.n_cand = 0
             self.workspace = None
+        # the bit-sliced evaluator's memo words (the workspace's first n_sets * 2^n words)
+        # serve the heuristics of the same step (gpart.h gp_alloc_opts.memo)
+        self.memo_ok = (self.workspace is not None and self.n <= 8 and self.M <= 32
+                        and memo_heuristics)
 
     def _gen(self, kc, km, R):
         wl = self.wl
@@ -143,8 +148,14 @@ class Pipeline:
                                          per_set=self.per_set, stream=stream)
             if not self.exhaustive:
                 hook("begin")
+            # the bit-sliced exhaustive pass just memoised every (subset, size) verdict of
+            # these sets in its workspace: the heuristics look their EDF tests up there
+            memo = None
+            if (self.exhaustive and si == 0 and mode == G.GP_EXHAUSTIVE and self.memo_ok
+                    and not flags & (G.GP_EX_PER_CANDIDATE | G.GP_EX_GENERIC)):
+                memo = self.workspace.data_ptr() + self.h_lo * (4 << self.n)
             for vi, v in enumerate(self.variants):
-                G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats)
+                G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats, memo=memo)
             if not self.exhaustive:
                 hook("end")
             if self.variants and ts_h.n_sets > 0:

@@ -988,3 +988,59 @@ def test_exhaustive_f4_mask_validation(G):
     with pytest.raises(G.GpError):  # a mask with no admissible size in 1..M (library)
         G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per, sizes=[],
                          work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"))
+
+
+# ------------------------------------------------------------------ heuristics on memoised verdicts
+# gp_alloc_opts.memo: the heuristics look up the bit-sliced evaluator's (subset, size)
+# verdicts of the same sets instead of running their EDF tests; every output (n_tests
+# included) must be unchanged.
+def _exhaustive_with_workspace(G, ts):
+    ws = G.exhaustive_workspace(ts)
+    per = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
+    G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per, workspace=ws,
+                     work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"))
+    return ws
+
+
+@pytest.mark.parametrize("key,R,reps", [("c2", 10000, 1000), ("c3", 1000, 1000)])
+def test_allocate_with_memo_equals_tests(G, key, R, reps):
+    gen = W.WORKLOADS[key]["gen"](R=R)
+    wl = W.WORKLOADS[key]
+    ts = G.TaskSets(10 * reps, wl["n"], wl["M"], 10)
+    G.gp_generate(gen, W.SEED, 0, reps, ts)
+    ws = _exhaustive_with_workspace(G, ts)
+    host = to_oracle(ts)
+    sample = list(range(0, ts.n_sets, max(1, ts.n_sets // 300)))
+    for v in VARIANTS:
+        plain = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks)).to_host()
+        memo = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, ts.n_tasks), memo=ws).to_host()
+        for k in ALLOC_KEYS:
+            assert (plain[k] == memo[k]).all(), (v, k)
+        ref = oracle.allocate(host.subset(sample), v)
+        for k in ALLOC_KEYS:
+            assert (memo[k][sample] == ref[k]).all(), (v, k)
+
+
+@pytest.mark.parametrize("seed,n,M", [(71, 3, 4), (72, 6, 9), (73, 8, 12), (74, 5, 32), (75, 1, 1)])
+def test_allocate_with_memo_random_and_f4(G, seed, n, M):
+    d = W.random_sets(np.random.default_rng(seed), 41, n, M, periods=(4, 6, 8, 12, 24),
+                      b_max=2 * M + 3, cost_max=3)
+    d["D"][7, 0] = d["T"][7, 0] + 1  # a contract violation (its memo words are never read)
+    ts = gpu_sets(G, d)
+    ws = _exhaustive_with_workspace(G, ts)
+    sizes = _mask_sizes("sparse", M) if M > 1 else None
+    for v in VARIANTS:
+        for flags, sz in [(0, None), (G.GP_AL_BINARY_MERGE | G.GP_AL_INCREASING, None), (0, sizes)]:
+            plain = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, n), flags=flags, sizes=sz).to_host()
+            memo = G.gp_allocate(ts, v, G.AllocOut(ts.n_sets, n), flags=flags, sizes=sz,
+                                 memo=ws).to_host()
+            for k in ALLOC_KEYS:
+                assert (plain[k] == memo[k]).all(), (v, flags, k)
+
+
+def test_allocate_memo_shape_validation(G):
+    d = W.random_sets(np.random.default_rng(76), 5, 9, 4)
+    ts = gpu_sets(G, d)
+    with pytest.raises(G.GpError):
+        G.gp_allocate(ts, "SMS_ACT", G.AllocOut(5, 9), memo=torch.zeros(5 << 9, dtype=torch.int32,
+                                                                       device="cuda"))
