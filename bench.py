@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--no-memo-heuristics", action="store_true",
                     help="the heuristics run their own EDF tests instead of looking up the "
                          "bit-sliced evaluator's memoised block verdicts (A/B)")
+    ap.add_argument("--serial-variants", action="store_true",
+                    help="launch the heuristic variants one after the other on one stream "
+                         "(default: parallel streams for sets of <= 8 tasks)")
     ap.add_argument("--no-graph", action="store_true",
                     help="issue every launch of the timed steps from the host instead of "
                          "replaying the step's CUDA graphs")
@@ -322,7 +325,8 @@ def main():
             dist.init_process_group(backend)
     wl = W.WORKLOADS[args.config]
     pipe = Pipeline(args.config, reps=args.reps, rank=rank, world=world, split=args.split,
-                    memo_heuristics=not args.no_memo_heuristics)
+                    memo_heuristics=not args.no_memo_heuristics,
+                    parallel_variants=False if args.serial_variants else None)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     alloc_stats = torch.zeros(8, dtype=torch.int64, device="cuda")  # GP_AL_STATS_EXT layout

@@ -207,7 +207,7 @@ struct WarpScratch {
 // U*H there.  `counted` += the tests the paper's linear scan performs
 // (alg2_search: one probe at hi + binary search instead of the scan, exact by
 // monotonicity); `st_exec` += the tests actually run.
-template <int NS, bool kGen, class WS>
+template <int NS, bool kGen, bool kMemo, class WS>
 GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, uint32_t S,
                             int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &counted,
                             uint64_t &st_tasks, uint32_t &st_events, uint32_t &st_exec,
@@ -233,7 +233,7 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
   // of a search is its answer)
   auto test = [&](int32_t m) -> bool {
     ++st_exec;
-    if (vm && m <= M) {
+    if (kMemo && vm && m <= M) {
       // the block verdict memoised by the EXHAUSTIVE pass on the same sets (the same
       // EDF-PDC of S at m); only U*H at m is computed, for the partition orders
       if (!((vm[S] >> (m - 1)) & 1u)) return false;
@@ -291,6 +291,9 @@ template <bool kGen, int G, int kV>
 // measured -- the small-set kernels gain occupancy, the larger ones lose more to spills
 __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArgs a) {
   const int variant = kV >= 0 ? kV : a.variant;
+  // memoised verdicts exist for n <= 8 only, i.e. in 8-lane groups: the wider kernels keep
+  // the plain tests (no extra code or registers)
+  constexpr bool kMemo = G == 8;
   __shared__ WarpScratch<G> scr_all[256 / G];
   extern __shared__ __align__(16) uint16_t wtab_all[];
   const Grp<G> g;
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
     g.sync();
 
     // memoised block verdicts of this set (n <= 8: 2^n words), when the caller passes them
-    const uint32_t *vm = (a.memo && contract) ? a.memo + ((size_t)set << n) : nullptr;
+    const uint32_t *vm = (kMemo && a.memo && contract) ? a.memo + ((size_t)set << n) : nullptr;
     int64_t tests = 0;
     bool ok = false;
     int stage = 0;  // 0: rejected before partitions exist, 1: partitions to report
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
       tests = 1;
       ++st_exec;
       const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
-      ok = (vm && m1 <= M) ? ((vm[all] >> (m1 - 1)) & 1u) != 0
+      ok = (kMemo && vm && m1 <= M) ? ((vm[all] >> (m1 - 1)) & 1u) != 0
                            : warp_pdc(g, t, all, m1, H, st_tasks, st_events);
       pm = lane == 0 ? all : 0;
       psz = lane == 0 ? m1 : 0;
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
             if (idx < np) {
               int32_t uh = 0;
               int64_t cnt = 0;
-              const int32_t got = serial_merge<2, kGen>(
+              const int32_t got = serial_merge<2, kGen, kMemo>(
                   scr, t.wv, z, (1u << i) | (1u << j), max(scr.szS[i], scr.szS[j]),
                   scr.szS[i] + scr.szS[j] - 1, H, uh, cnt, st_pair_tasks, st_pair_events,
                   st_pair_exec, vm, M);
@@ -611,9 +614,9 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
                 const int32_t lo2 = max(best_m, psz), hi2 = best_m + psz - 1;
                 if (mine && c2 <= 8) {
                   if (kAllocNs4<G> && maxc <= 4)
-                    got2 = serial_merge<4, kGen>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, M);
+                    got2 = serial_merge<4, kGen, kMemo>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, M);
                   else
-                    got2 = serial_merge<8, kGen>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, M);
+                    got2 = serial_merge<8, kGen, kMemo>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, M);
                   pt_tab[pt_index(min(keep, lane), max(keep, lane), n)] = pt_pack(got2, cnt2, uh2);
                 }
                 // (groups of 8 lanes hold <= 8 tasks: the group-cooperative path for merged

@@ -47,7 +47,7 @@ class Pipeline:
     def __init__(self, key: str, reps: int = None, rank: int = 0, world: int = 1,
                  device="cuda", exhaustive: bool = None, variants=None, settings=None,
                  seed: int = W.SEED, stats: bool = True, split: str = "weak",
-                 memo_heuristics: bool = True):
+                 memo_heuristics: bool = True, parallel_variants: bool = None):
         if split not in SPLITS:
             raise ValueError(f"split must be one of {SPLITS}")
         wl = W.WORKLOADS[key]
@@ -105,6 +105,12 @@ class Pipeline:
         # serve the heuristics of the same step (gpart.h gp_alloc_opts.memo)
         self.memo_ok = (self.workspace is not None and self.n <= 8 and self.M <= 32
                         and memo_heuristics)
+        # small sets (8-lane groups): the variants' kernels are short and their tails matter,
+        # so they run on parallel streams; larger sets fill the GPU alone (A/B: C2/C3 -2-3 %,
+        # C4 +8 %)
+        self.parallel_variants = (self.n <= 8 if parallel_variants is None
+                                  else parallel_variants)
+        self._vstreams = None
 
     def _gen(self, kc, km, R):
         wl = self.wl
@@ -154,8 +160,26 @@ class Pipeline:
             if (self.exhaustive and si == 0 and mode == G.GP_EXHAUSTIVE and self.memo_ok
                     and not flags & (G.GP_EX_PER_CANDIDATE | G.GP_EX_GENERIC)):
                 memo = self.workspace.data_ptr() + self.h_lo * (4 << self.n)
-            for vi, v in enumerate(self.variants):
-                G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats, memo=memo)
+            if self.parallel_variants and stream is not None and len(self.variants) > 1:
+                # the variants are independent: one stream each (fork / join by events; in
+                # a captured graph, parallel branches), so their persistent grids' tails overlap
+                if self._vstreams is None:
+                    self._vstreams = [torch.cuda.Stream() for _ in self.variants]
+                fork = torch.cuda.Event()
+                fork.record(stream)
+                joins = []
+                for vi, v in enumerate(self.variants):
+                    vs = self._vstreams[vi]
+                    vs.wait_event(fork)
+                    G.gp_allocate(ts_h, v, self.alloc[vi], vs, stats=alloc_stats, memo=memo)
+                    e = torch.cuda.Event()
+                    e.record(vs)
+                    joins.append(e)
+                for e in joins:
+                    stream.wait_event(e)
+            else:
+                for vi, v in enumerate(self.variants):
+                    G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats, memo=memo)
             if not self.exhaustive:
                 hook("end")
             if self.variants and ts_h.n_sets > 0:
