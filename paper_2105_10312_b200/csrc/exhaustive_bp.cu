@@ -45,9 +45,6 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_MEMO_RANK_ORDER
 #define GP_MEMO_RANK_ORDER 1  // memo: compacted tests ordered by their rank within the subset
 #endif
-#ifndef GP_MEMO_PRUNE
-#define GP_MEMO_PRUNE 1  // memo: skip (S, m) when a subset S - {i} fails at m (exact, see k_exh_memo)
-#endif
 #ifndef GP_BP_MINB
 #define GP_BP_MINB 4  // main-pass CTAs per SM the register budget targets (A/B: -DGP_BP_MINB=n)
 #endif
@@ -85,34 +82,36 @@ GP_DEV uint64_t ld_u64(uint64_t base, uint32_t idx) {
 // The set's WCETs W_i(m, x) (C.1.3) are tabulated once per set in shared memory
 // (n x 2 x M entries), so a test reads its tasks' WCETs instead of recomputing
 // ceil(B/m) per (pair, task).
+struct MemoTask {  // one task of the set: one 16-byte shared-memory load per use
+  int32_t D, T, q;  // deadline, period, H / T
+  float invD;       // 1 / D (the density shortcut of memo_test)
+};
+
 struct MemoWarp {
   uint32_t vs[1 << kBpMaxN];          // verdict word per subset
   int32_t wt[kBpMaxN * 2 * kBpMaxM];  // W_i(m, x) at [(i*2 + x)*32 + m-1], x = 1: conflict
-  int32_t T[kBpMaxN], D[kBpMaxN], q[kBpMaxN];
-  float invD[kBpMaxN];                // 1 / D_i (the density shortcut of memo_test)
-#if GP_MEMO_PRUNE
-  uint16_t list[32 * kBpMaxM];        // compacted (subset, size) pairs of one chunk of a level
-#endif
+  MemoTask tk[kBpMaxN];
+  uint32_t cs[32], cd[32];            // the chunk's subsets and their W-column descriptors
+  uint16_t list[32 * kBpMaxM];        // compacted (chunk position, size) pairs of one chunk
 };
 
-// EDF-PDC of the c tasks of S at size m (gp_edf.cuh shortcuts), lane-serial.
+// EDF-PDC of the c tasks of a subset at size m (gp_edf.cuh shortcuts), lane-serial.
+// dsc: the subset's tasks as W columns (i*2 + x_i, 4 bits each; x_i = another task of i's
+// type in the subset).
 template <int c>
-GP_DEV bool memo_test(const MemoWarp &w, uint32_t S, int m, uint32_t mem, int32_t H,
-                      uint32_t &events) {
-  int32_t C[c], D[c], T[c], q[c], id[c];
-  uint32_t bits = S;
+GP_DEV bool memo_test(const MemoWarp &w, uint32_t dsc, int m, int32_t H, uint32_t &events) {
+  int32_t C[c], D[c], T[c], q[c];
+  float iD[c];
   bool bad = false;
 #pragma unroll
   for (int a = 0; a < c; ++a) {
-    const int i = __ffs(bits) - 1;
-    bits &= bits - 1u;
-    id[a] = i;
-    const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
-    const int x = __popc(S & same) > 1 ? 1 : 0;  // conflict
-    C[a] = w.wt[(i * 2 + x) * kBpMaxM + m - 1];
-    D[a] = w.D[i];
-    T[a] = w.T[i];
-    q[a] = w.q[i];
+    const uint32_t col = (dsc >> (4 * a)) & 15u;
+    const MemoTask tk = w.tk[col >> 1];
+    C[a] = w.wt[col * kBpMaxM + m - 1];
+    D[a] = tk.D;
+    T[a] = tk.T;
+    q[a] = tk.q;
+    iD[a] = tk.invD;
     bad |= C[a] > D[a];
   }
   if (bad) return false;
@@ -127,7 +126,7 @@ GP_DEV bool memo_test(const MemoWarp &w, uint32_t S, int m, uint32_t mem, int32_
   // 2^-20 for <= 8 terms), so a pass here is always a pass of the definition.
   float dens = 0.f;
 #pragma unroll
-  for (int a = 0; a < c; ++a) dens = fmaf((float)C[a], w.invD[id[a]], dens);
+  for (int a = 0; a < c; ++a) dens = fmaf((float)C[a], iD[a], dens);
   if (dens <= 0.99999f) return true;
 #endif
   const int32_t lcut = pdc_cutoff<c>(C, D, T, q, H, UH);
@@ -142,9 +141,6 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
   MemoWarp &w = mw_all[wid];
   const int n = a.n, M = a.M;
   const int nsub = 1 << n;
-#if !GP_MEMO_PRUNE
-  const int npairs = (nsub - 1) * M;
-#endif
   for (int S = threadIdx.x + 1; S < nsub; S += blockDim.x) {  // rank of S in the order
     const int c = __popc((unsigned)S);
     int r = 0;
@@ -157,6 +153,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
   __syncthreads();
   uint64_t st_tests = 0, st_tasks = 0;
   uint32_t st_events = 0;
+  const uint32_t Mmask = M >= 32 ? ~0u : (1u << M) - 1u;
   for (int64_t set = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < a.n_sets;
        set += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t H = set_contract(a, set);
@@ -175,31 +172,26 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
         w.wt[(i * 2 + 1) * kBpMaxM + lane] = wcet_adm(a.adm, Bi, cci, fci, lane + 1);
       }
     }
-    uint32_t mem = 0;  // type mask (memory-intensive tasks)
     if (lane < n) {
       const int64_t o = set * n + lane;
-      w.T[lane] = a.T[o];
-      w.D[lane] = a.D[o];
-      w.q[lane] = (int32_t)(H / a.T[o]);
-      w.invD[lane] = __frcp_rn((float)a.D[o]);
+      const int32_t Dl = a.D[o], Tl = a.T[o];
+      w.tk[lane] = MemoTask{Dl, Tl, (int32_t)(H / Tl), __frcp_rn((float)Dl)};
     }
-    mem = __ballot_sync(GP_FULL, lane < n && a.type[set * n + min(lane, n - 1)] == 1);
+    const uint32_t mem = __ballot_sync(GP_FULL, lane < n && a.type[set * n + min(lane, n - 1)] == 1);
     __syncwarp();
-#if GP_MEMO_PRUNE
     // Levels of increasing subset size c.  Level 1: a single task passes iff C <= D (no
     // conflict).  Level c >= 2 tests (S, m) only if every S - {i} passes at m:
     // a block's subset S' fails whenever S fails -- S' has fewer tasks and no more
     // conflicts (x_i(S') <= x_i(S)) and W_i(m, 1) >= W_i(m, 0) (cc >= cn, fc >= fn:
     // the input contract), so dbf_{S'} <= dbf_S pointwise at the deadlines of S' -- hence
     // a failing S - {i} decides V[S] bit m = 0 exactly (no monotonicity in m is used).
-    // The surviving pairs of a chunk of up to 32 subsets are compacted (warp scan) and
-    // tested 32 at a time with c uniform across the warp.
-    const uint32_t Mmask = M >= 32 ? ~0u : (1u << M) - 1u;
+    // The surviving pairs of a chunk of up to 32 subsets are compacted and tested 32 at a
+    // time with c uniform across the warp.
     for (int e = lane; e < n * M; e += 32) {
       const int i = e / M, m = e - i * M + 1;
       ++st_tests;
       ++st_tasks;
-      if (w.wt[(i * 2) * kBpMaxM + m - 1] <= w.D[i]) atomicOr(&w.vs[1u << i], 1u << (m - 1));
+      if (w.wt[(i * 2) * kBpMaxM + m - 1] <= w.tk[i].D) atomicOr(&w.vs[1u << i], 1u << (m - 1));
     }
     __syncwarp();
     int lv0 = 0, nlv = n;  // first sorder index of the level, subsets in it (C(n, c))
@@ -211,11 +203,24 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
         const uint32_t S = hs ? sorder[lv0 + ch + lane] : 0u;
         uint32_t A = hs ? Mmask : 0u;
         for (uint32_t b = S; b; b &= b - 1u) A &= w.vs[S & ~(b & (0u - b))];
+        // the subset's tasks as W columns (conflict flags resolved once per subset)
+        uint32_t dsc = 0u;
+        {
+          uint32_t bits = S;
+          for (int q4 = 0; bits; q4 += 4) {
+            const int i = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            const uint32_t same = ((mem >> i) & 1u) ? mem : ~mem;
+            dsc |= ((uint32_t)(i * 2) + (__popc(S & same) > 1 ? 1u : 0u)) << q4;
+          }
+        }
+        w.cs[lane] = S;
+        w.cd[lane] = dsc;
+        int total = 0;
 #if GP_MEMO_RANK_ORDER
         // list order: every subset's smallest surviving size first (the tests at a subset's
         // schedulability boundary, where U is near 1 and the demand walks are long), then
         // every subset's second, ...: a warp step's 32 walks are of similar length
-        int total = 0;
         {
           uint32_t b = A;
           const uint32_t lt = (1u << lane) - 1u;
@@ -223,84 +228,49 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
             const uint32_t has = __ballot_sync(GP_FULL, b != 0u);
             if (!has) break;
             if (b) {
-              w.list[total + __popc(has & lt)] = (uint16_t)(S | ((uint32_t)(__ffs(b) - 1) << 8));
+              w.list[total + __popc(has & lt)] = (uint16_t)(lane | ((__ffs(b) - 1) << 5));
               b &= b - 1u;
             }
             total += __popc(has);
           }
         }
 #else
-        const int cntA = __popc(A);
-        int incl = cntA;
+        {
+          const int cntA = __popc(A);
+          int incl = cntA;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(GP_FULL, incl, o);
-          if (lane >= o) incl += v;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(GP_FULL, incl, o);
+            if (lane >= o) incl += v;
+          }
+          total = __shfl_sync(GP_FULL, incl, 31);
+          int p = incl - cntA;
+          for (uint32_t b = A; b; b &= b - 1u) w.list[p++] = (uint16_t)(lane | ((__ffs(b) - 1) << 5));
         }
-        const int total = __shfl_sync(GP_FULL, incl, 31);
-        int p = incl - cntA;
-        for (uint32_t b = A; b; b &= b - 1u) w.list[p++] = (uint16_t)(S | ((uint32_t)(__ffs(b) - 1) << 8));
 #endif
         __syncwarp();
         for (int e = lane; e < total; e += 32) {
           const uint32_t ent = w.list[e];
-          const uint32_t S2 = ent & 255u;
-          const int m = (int)(ent >> 8) + 1;
+          const uint32_t pos = ent & 31u;
+          const int m = (int)(ent >> 5) + 1;
+          const uint32_t d2 = w.cd[pos];
           ++st_tests;
           st_tasks += c;
           bool ok;
           switch (c) {
-            case 2: ok = memo_test<2>(w, S2, m, mem, H32, st_events); break;
-            case 3: ok = memo_test<3>(w, S2, m, mem, H32, st_events); break;
-            case 4: ok = memo_test<4>(w, S2, m, mem, H32, st_events); break;
-            case 5: ok = memo_test<(NT >= 5 ? 5 : 2)>(w, S2, m, mem, H32, st_events); break;
-            case 6: ok = memo_test<(NT >= 6 ? 6 : 2)>(w, S2, m, mem, H32, st_events); break;
-            case 7: ok = memo_test<(NT >= 7 ? 7 : 2)>(w, S2, m, mem, H32, st_events); break;
-            default: ok = memo_test<(NT >= 8 ? 8 : 2)>(w, S2, m, mem, H32, st_events); break;
+            case 2: ok = memo_test<2>(w, d2, m, H32, st_events); break;
+            case 3: ok = memo_test<3>(w, d2, m, H32, st_events); break;
+            case 4: ok = memo_test<4>(w, d2, m, H32, st_events); break;
+            case 5: ok = memo_test<(NT >= 5 ? 5 : 2)>(w, d2, m, H32, st_events); break;
+            case 6: ok = memo_test<(NT >= 6 ? 6 : 2)>(w, d2, m, H32, st_events); break;
+            case 7: ok = memo_test<(NT >= 7 ? 7 : 2)>(w, d2, m, H32, st_events); break;
+            default: ok = memo_test<(NT >= 8 ? 8 : 2)>(w, d2, m, H32, st_events); break;
           }
-          if (ok) atomicOr(&w.vs[S2], 1u << (m - 1));
+          if (ok) atomicOr(&w.vs[w.cs[pos]], 1u << (m - 1));
         }
         __syncwarp();
       }
     }
-#else
-    int idx = 0, m = lane + 1;  // pair pq = idx * M + (m - 1), pq = lane + 32 j
-    while (m > M) {
-      m -= M;
-      ++idx;
-    }
-    for (int pq0 = 0; pq0 < npairs; pq0 += 32) {
-      const bool in = pq0 + lane < npairs;
-      const uint32_t S = in ? sorder[idx] : 0u;
-      const int cnt = __popc(S);
-      bool ok = false;
-      if (!in) {
-      } else if (cnt == 1) {
-        const int i = __ffs(S) - 1;  // a single task: C <= D decides (no conflict)
-        ok = w.wt[(i * 2) * kBpMaxM + m - 1] <= w.D[i];
-      } else {
-        switch (cnt) {
-          case 2: ok = memo_test<2>(w, S, m, mem, H32, st_events); break;
-          case 3: ok = memo_test<3>(w, S, m, mem, H32, st_events); break;
-          case 4: ok = memo_test<4>(w, S, m, mem, H32, st_events); break;
-          case 5: ok = memo_test<(NT >= 5 ? 5 : 2)>(w, S, m, mem, H32, st_events); break;
-          case 6: ok = memo_test<(NT >= 6 ? 6 : 2)>(w, S, m, mem, H32, st_events); break;
-          case 7: ok = memo_test<(NT >= 7 ? 7 : 2)>(w, S, m, mem, H32, st_events); break;
-          default: ok = memo_test<(NT >= 8 ? 8 : 2)>(w, S, m, mem, H32, st_events); break;
-        }
-      }
-      if (in) {
-        ++st_tests;
-        st_tasks += cnt;
-      }
-      if (ok) atomicOr(&w.vs[S], 1u << (m - 1));
-      m += 32;  // next pair of this lane
-      while (m > M) {
-        m -= M;
-        ++idx;
-      }
-    }
-#endif
     __syncwarp();
     for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
     __syncwarp();
