@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-memo-heuristics", action="store_true",
                     help="the heuristics run their own EDF tests instead of looking up the "
                          "bit-sliced evaluator's memoised block verdicts (A/B)")
+    ap.add_argument("--exh-flags", type=int, default=0,
+                    help="extra gp_exhaustive_opts flags for the timed call (A/B of test hooks)")
     ap.add_argument("--serial-variants", action="store_true",
                     help="launch the heuristic variants one after the other on one stream "
                          "(default: parallel streams for sets of <= 8 tasks)")
@@ -334,6 +336,7 @@ def main():
     exh_flags = G.GP_EX_NO_HASH if (args.f3 and not args.f3_hash) else 0
     if args.per_candidate:
         exh_flags |= G.GP_EX_PER_CANDIDATE
+    exh_flags |= args.exh_flags
     if args.f3 and not pipe.exhaustive:
         raise SystemExit("--f3 needs an exhaustive config (c2, c3)")
     if args.f3 and args.split == "ranks":
