@@ -6,7 +6,8 @@ set -e
 T=$1; O=profiles/$2; I=gpurun_out/$T
 mkdir -p $O
 for f in bench_c2.json bench_c3.json bench_c3_per_candidate.json bench_c4.json bench_c5.json \
-         bench_reference_c3.json pytest_gpu.log smoke.log launches_c3.csv launches_c4.csv; do
+         bench_c3_f3.json bench_reference_c3.json pytest_gpu.log smoke.log launches_c3.csv \
+         launches_c4.csv f1_sweep.json f1_sweep.log; do
   [ -f $I/$f ] && cp $I/$f $O/
 done
 for l in c3 c4; do

@@ -13,6 +13,8 @@ timeout 900 python bench.py --per-candidate --no-cpu-baseline > $O/bench_c3_per_
 timeout 900 python bench.py --config c2 > $O/bench_c2.json 2> $O/bench_c2.err; echo "c2 rc=$?"
 timeout 900 python bench.py --config c4 > $O/bench_c4.json 2> $O/bench_c4.err; echo "c4 rc=$?"
 timeout 900 python bench.py --config c5 > $O/bench_c5.json 2> $O/bench_c5.err; echo "c5 rc=$?"
+timeout 900 python bench.py --f3 > $O/bench_c3_f3.json 2> $O/bench_c3_f3.err; echo "c3 f3 rc=$?"
+timeout 900 python scripts/f1_sweep.py --f4 --out $O/f1_sweep.json > $O/f1_sweep.log 2>&1; echo "f1 rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference_c3.json 2> $O/bench_ref.err; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1; echo "launches c3 rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches_c4.csv python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1; echo "launches c4 rc=$?"
