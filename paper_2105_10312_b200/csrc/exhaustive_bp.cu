@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       // runs [i_lo, i_hi) can hold schedulable candidates of some lane's set
       const int lo_l = w1 ? __ffs(w1) - 1 : steps;
       const int hi_l = w1 ? min(steps, len0 - a0) : 0;
-      if constexpr (!kWin && kHash == 1 && !kBits) {
+      if constexpr (!kWin && kHash != 2 && !kBits) {
         // the whole sweep at once: when in every lane the live runs are exactly
         // [lo_l, hi_l) (block k-2's word has every bit of that range) and each live run's
         // schedulable candidates are its top range a0+1 .. len (`top`), the lane's
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         const int span = hi_l - lo_l;
         const bool fits = span <= 0 || ((w1 >> lo_l) & ((span >= 32 ? 0u : 1u << span) - 1u)) ==
                                            ((span >= 32 ? 0u : 1u << span) - 1u);
-        if (top && a.R && __all_sync(GP_FULL, fits)) {
+        if (top && (kHash == 0 || a.R) && __all_sync(GP_FULL, fits)) {
           if (span > 0) {
             if constexpr (kStats) {
               ++st_sweeps;
@@ -733,7 +733,8 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             // sweeps are visited in rank order: the lane's first live one holds its first rank
             if (first_off == UINT32_MAX)
               first_off = off + (uint32_t)(lo_l * len0 - ((lo_l * (lo_l - 1)) >> 1) + a0);
-            acc_hash += ld_u64(r_addr, roff + (uint32_t)hi_l) - ld_u64(r_addr, roff + (uint32_t)lo_l);
+            if constexpr (kHash == 1)
+              acc_hash += ld_u64(r_addr, roff + (uint32_t)hi_l) - ld_u64(r_addr, roff + (uint32_t)lo_l);
           }
           return;
         }
@@ -747,7 +748,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       uint32_t lmask = len >= 32 ? ~0u : (1u << len) - 1u;
       w1 >>= i_lo;
       const int psb = M - len0 + 1;  // (sum of the prefix parts but s_{k-2}) + 1 + 1
-      if constexpr (!kWin && kHash == 1) {
+      if constexpr (!kWin && kHash != 2) {
         if (top) {
           // per live run: n += len - a0, hash += P[next run start] - P[run start + a0]
 #pragma unroll kBpUnroll
@@ -759,7 +760,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
               acc_n += (uint32_t)(len - a0);
               acc_pi = min(acc_pi, psb + i + a0);
               first_off = min(first_off, o2 + (uint32_t)a0);
-              acc_hash += ld_u64(pu_addr, o2n) - ld_u64(pl_addr, o2);
+              if constexpr (kHash == 1) acc_hash += ld_u64(pu_addr, o2n) - ld_u64(pl_addr, o2);
               if constexpr (kBits) {
                 const uint64_t ob = rank_pi + o2 + (uint64_t)a0;
                 const uint32_t w2 = okb >> a0;
@@ -856,7 +857,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         const uint32_t mk = need >= 32 ? ~0u : (need <= 0 ? 0u : (1u << need) - 1u);
         c1 = ((Vr[1] >> lo1) & mk) == mk;
       }
-      const bool closed = (!kWin && kHash == 1 && !kBits) && top && a.R != nullptr &&
+      const bool closed = (!kWin && kHash != 2 && !kBits) && top && (kHash == 0 || a.R != nullptr) &&
                           !a.force_ranges && __all_sync(GP_FULL, c1);
       // closed2: block k-3's word is also one bit range from lo2 reaching the largest
       // size a sweep can need (bit M-3) in every lane, so a lane's live sweeps of an outer
@@ -906,14 +907,16 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
                           (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
             int len0 = len0f;
             uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
-            uint64_t hsum = 0;
+            if constexpr (kHash == 1) {  // (without the hash the outer prefix is O(1))
+              uint64_t hsum = 0;
 #pragma unroll kBpSweepUnroll
-            for (int sp = span_hi; sp >= 1; --sp) {
-              hsum += ld_u64(r_addr, roffv + (uint32_t)(len0 - a0)) - ld_u64(r_addr, roffv + (uint32_t)lo1);
-              roffv += (uint32_t)len0;
-              --len0;
+              for (int sp = span_hi; sp >= 1; --sp) {
+                hsum += ld_u64(r_addr, roffv + (uint32_t)(len0 - a0)) - ld_u64(r_addr, roffv + (uint32_t)lo1);
+                roffv += (uint32_t)len0;
+                --len0;
+              }
+              acc_hash += hsum;
             }
-            acc_hash += hsum;
           }
         } else {
         const uint32_t w2 = (rh & 1u) ? Vr[2] : 0u;  // bit v-1: block k-3 passes at v
@@ -955,15 +958,18 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
               // inside the lane's own range span >= 1, so both indices lie in the
               // allocation's runs: read unconditionally (the unrolled iterations' loads
               // overlap), add when block k-3 passes at v
-              const uint64_t he = ld_u64(r_addr, roffv + (uint32_t)(len0 - a0));
-              const uint64_t hs = ld_u64(r_addr, roffv + (uint32_t)lo1);
+              uint64_t he = 0, hs = 0;
+              if constexpr (kHash == 1) {
+                he = ld_u64(r_addr, roffv + (uint32_t)(len0 - a0));
+                hs = ld_u64(r_addr, roffv + (uint32_t)lo1);
+              }
               if ((w2 >> (v - 1)) & 1u) {
                 if constexpr (kStats) {
                   ++st_sweeps;
                   st_live_closed += (uint64_t)span;
                 }
                 acc_n += (uint32_t)((span * (span + 1)) >> 1);
-                acc_hash += he - hs;
+                if constexpr (kHash == 1) acc_hash += he - hs;
               }
 #else
               if (((w2 >> (v - 1)) & 1u) && span > 0) {
@@ -972,8 +978,9 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
                   st_live_closed += (uint64_t)span;
                 }
                 acc_n += (uint32_t)((span * (span + 1)) >> 1);
-                acc_hash += ld_u64(r_addr, roffv + (uint32_t)(len0 - a0)) -
-                            ld_u64(r_addr, roffv + (uint32_t)lo1);
+                if constexpr (kHash == 1)
+                  acc_hash += ld_u64(r_addr, roffv + (uint32_t)(len0 - a0)) -
+                              ld_u64(r_addr, roffv + (uint32_t)lo1);
               }
 #endif
               roffv += (uint32_t)len0;

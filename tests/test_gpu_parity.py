@@ -1044,3 +1044,25 @@ def test_allocate_memo_shape_validation(G):
     with pytest.raises(G.GpError):
         G.gp_allocate(ts, "SMS_ACT", G.AllocOut(5, 9), memo=torch.zeros(5 << 9, dtype=torch.int32,
                                                                        device="cuda"))
+
+
+def test_exhaustive_no_hash_closed_paths(G):
+    """GP_EX_NO_HASH takes the closed-form sweep / item paths without the hash tables:
+    n_sched, pi* and first rank equal the hash-mode call's on the C3 parity size (10^4
+    sets, the timed instantiation), on random shapes and under a size mask."""
+    gen = W.WORKLOADS["c3"]["gen"](R=1000)
+    ts = G.TaskSets(10 * 1000, 6, 20, 10)
+    G.gp_generate(gen, W.SEED, 0, 1000, ts)
+    full, _, _ = run_exhaustive(G, ts, with_stats=False)
+    nh, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NO_HASH, with_stats=False)
+    assert (nh[:, :3] == full[:, :3]).all() and (nh[:, 3] == 0).all()
+    sizes = _mask_sizes("mig", 20)
+    fm, _, _ = run_exhaustive(G, ts, with_stats=False, sizes=sizes)
+    nm, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NO_HASH, with_stats=False, sizes=sizes)
+    assert (nm[:, :3] == fm[:, :3]).all()
+    for seed, n, M in [(81, 4, 7), (82, 6, 12), (83, 8, 9), (84, 3, 32)]:
+        d = W.random_sets(np.random.default_rng(seed), 37, n, M, periods=(4, 6, 8, 12, 24),
+                          b_max=2 * M + 3, cost_max=3)
+        ref = oracle.exhaustive(oracle.Sets.from_dict(d))
+        got, _, _ = run_exhaustive(G, gpu_sets(G, d), flags=G.GP_EX_NO_HASH, with_stats=False)
+        assert (got[:, :3] == ref[:, :3]).all(), (seed, n, M)
