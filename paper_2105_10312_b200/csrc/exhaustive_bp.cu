@@ -133,7 +133,7 @@ GP_DEV bool memo_test(const MemoWarp &w, uint32_t dsc, int m, int32_t H, uint32_
   return pdc_walk<c>(C, D, T, lcut, events);
 }
 
-template <int NT>
+template <int NT, bool kStats>
 __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a, uint32_t *memo) {
   __shared__ MemoWarp mw_all[8];
   __shared__ uint8_t sorder[1 << kBpMaxN];  // subsets 1 .. 2^n - 1 by (size, value)
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
     for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
     __syncwarp();
   }
-  if (a.stats) {
+  if constexpr (kStats) {  // (the timed instantiation carries no counters)
     const uint64_t t0 = warp_sum_u64(st_tests), t1 = warp_sum_u64(st_tasks);
     const uint64_t t2 = warp_sum_u64((uint64_t)st_events);
     if (lane == 0) {
@@ -1212,9 +1212,15 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
     const unsigned g = (unsigned)(blocks > 0 ? blocks : 1);
-    if (n <= 4) k_exh_memo<4><<<g, 256, 0, st>>>(a, memo);
-    else if (n <= 6) k_exh_memo<6><<<g, 256, 0, st>>>(a, memo);
-    else k_exh_memo<8><<<g, 256, 0, st>>>(a, memo);
+    if (a.stats) {
+      if (n <= 4) k_exh_memo<4, true><<<g, 256, 0, st>>>(a, memo);
+      else if (n <= 6) k_exh_memo<6, true><<<g, 256, 0, st>>>(a, memo);
+      else k_exh_memo<8, true><<<g, 256, 0, st>>>(a, memo);
+    } else {
+      if (n <= 4) k_exh_memo<4, false><<<g, 256, 0, st>>>(a, memo);
+      else if (n <= 6) k_exh_memo<6, false><<<g, 256, 0, st>>>(a, memo);
+      else k_exh_memo<8, false><<<g, 256, 0, st>>>(a, memo);
+    }
   }
   a.sperm = nullptr;
   if (use_sp) {
