@@ -286,7 +286,7 @@ GP_DEV uint32_t pm_bcast(const Grp<G> &g, uint32_t pm, int src) { return g.shfl(
 // kV >= 0: the variant is a compile-time constant (one kernel per variant: each carries only
 // its own code, e.g. no ACT prefill in INA, which keeps the instruction working set small);
 // kV = -1: runtime variant (the f4 kGen kernels)
-template <bool kGen, int G, int kV>
+template <bool kGen, int G, int kV, bool kStats>
 // register budget: 4 CTAs per SM for 8-lane groups (64 registers), 3 otherwise (80): A/B
 // measured -- the small-set kernels gain occupancy, the larger ones lose more to spills
 __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArgs a) {
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
     }
     g.sync();
   }
-  if (a.stats) {
+  if constexpr (kStats) {  // (the timed instantiation carries no counters: fewer registers)
     const uint64_t pt = g.sum_u64(st_pair_tasks), pe = g.sum_u64(st_pair_events);
     const uint64_t px = g.sum_u64(st_pair_exec);
     if (lane == 0) {
@@ -784,17 +784,27 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
               efficiency, stats, stats_ext ? 1 : 0, use_tab ? 1 : 0, (uint32_t)pt_off, nullptr,
               vo, memo};
   using KernFn = void (*)(AllocArgs);
-  static const KernFn kdef[3][5] = {
-      {k_allocate<false, 8, 0>, k_allocate<false, 8, 1>, k_allocate<false, 8, 2>,
-       k_allocate<false, 8, 3>, k_allocate<false, 8, 4>},
-      {k_allocate<false, 16, 0>, k_allocate<false, 16, 1>, k_allocate<false, 16, 2>,
-       k_allocate<false, 16, 3>, k_allocate<false, 16, 4>},
-      {k_allocate<false, 32, 0>, k_allocate<false, 32, 1>, k_allocate<false, 32, 2>,
-       k_allocate<false, 32, 3>, k_allocate<false, 32, 4>}};
+  static const KernFn kdef[2][3][5] = {
+      {{k_allocate<false, 8, 0, false>, k_allocate<false, 8, 1, false>, k_allocate<false, 8, 2, false>,
+        k_allocate<false, 8, 3, false>, k_allocate<false, 8, 4, false>},
+       {k_allocate<false, 16, 0, false>, k_allocate<false, 16, 1, false>, k_allocate<false, 16, 2, false>,
+        k_allocate<false, 16, 3, false>, k_allocate<false, 16, 4, false>},
+       {k_allocate<false, 32, 0, false>, k_allocate<false, 32, 1, false>, k_allocate<false, 32, 2, false>,
+        k_allocate<false, 32, 3, false>, k_allocate<false, 32, 4, false>}},
+      {{k_allocate<false, 8, 0, true>, k_allocate<false, 8, 1, true>, k_allocate<false, 8, 2, true>,
+        k_allocate<false, 8, 3, true>, k_allocate<false, 8, 4, true>},
+       {k_allocate<false, 16, 0, true>, k_allocate<false, 16, 1, true>, k_allocate<false, 16, 2, true>,
+        k_allocate<false, 16, 3, true>, k_allocate<false, 16, 4, true>},
+       {k_allocate<false, 32, 0, true>, k_allocate<false, 32, 1, true>, k_allocate<false, 32, 2, true>,
+        k_allocate<false, 32, 3, true>, k_allocate<false, 32, 4, true>}}};
   const int gi = G == 8 ? 0 : (G == 16 ? 1 : 2);
-  const KernFn kern = gen ? (G == 8 ? k_allocate<true, 8, -1>
-                             : G == 16 ? k_allocate<true, 16, -1> : k_allocate<true, 32, -1>)
-                          : kdef[gi][(int)v];
+  const bool st_on = stats != nullptr;
+  const KernFn kern =
+      gen ? (st_on ? (G == 8 ? k_allocate<true, 8, -1, true>
+                             : G == 16 ? k_allocate<true, 16, -1, true> : k_allocate<true, 32, -1, true>)
+                   : (G == 8 ? k_allocate<true, 8, -1, false>
+                             : G == 16 ? k_allocate<true, 16, -1, false> : k_allocate<true, 32, -1, false>))
+          : kdef[st_on ? 1 : 0][gi][(int)v];
   // dynamic + static shared memory may pass 48 KB (e.g. 16-lane groups: 16 scratches + tables)
   // opt in to more than 48 KB (static + dynamic) only when needed: setting a function
   // attribute per call was measured to stall the stream (C3 step +1.4 ms)
