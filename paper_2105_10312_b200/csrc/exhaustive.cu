@@ -109,7 +109,7 @@ GP_DEV void exh_load_set(const ExhArgs &a, WarpSmem &w, int32_t *Wt, int64_t set
   __syncwarp();
 }
 
-template <int NT>
+template <int NT, bool kStats>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_exhaustive(const ExhArgs a) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int n = a.n, M = a.M;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_exhaustive(const ExhArgs a) 
   const size_t per_warp = ((sizeof(WarpSmem) / 4 + wt_words) + 3) & ~(size_t)3;
   WarpSmem &w = *reinterpret_cast<WarpSmem *>(smem + off + per_warp * warp);
   int32_t *Wt = reinterpret_cast<int32_t *>(&w + 1);
-  const bool stats = a.stats != nullptr;
+  const bool stats = kStats && a.stats != nullptr;
 
   LaneAcc acc;
   int64_t cur = -1;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_exhaustive(const ExhArgs a) 
     }
   }
   flush();
-  if (stats) {
+  if (kStats && stats) {
     const uint64_t c0 = warp_sum_u64(acc.st_cand), c1 = warp_sum_u64(acc.st_blocks);
     const uint64_t c2 = warp_sum_u64(acc.st_events), c3 = warp_sum_u64(acc.st_tasks);
     if (lane == 0) {
@@ -523,7 +523,7 @@ GP_DEV void shape_dispatch(unsigned cuts, const ShapeItem &c, LaneAcc &acc) {
   }
 }
 
-template <int N>
+template <int N, bool kStats>
 __global__ void __launch_bounds__(kWarps * 32, 3)
     k_exhaustive_shaped(const ExhArgs a, const ShapeTable sh) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
   const size_t per_warp = ((sizeof(WarpSmem) / 4 + (size_t)2 * n * M) + 3) & ~(size_t)3;
   WarpSmem &w = *reinterpret_cast<WarpSmem *>(smem + off + per_warp * warp);
   int32_t *Wt = reinterpret_cast<int32_t *>(&w + 1);
-  const bool stats = a.stats != nullptr;
+  const bool stats = kStats && a.stats != nullptr;
   LaneAcc acc;
   int64_t cur = -1;
   int shape = 0;
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
     }
   }
   exh_flush(a, acc, cur, lane);
-  exh_stats_flush(a, acc, lane);
+  if constexpr (kStats) exh_stats_flush(a, acc, lane);  // (the timed instantiation: no counters)
 }
 
 __global__ void k_exh_init(int64_t *per_set, int32_t n_sets) {
@@ -674,10 +674,11 @@ __global__ void k_exh_finalize(const ExhArgs a) {
 // thread-safe; microseconds against a launch of milliseconds).
 template <int NT>
 static gp_status launch_exh(ExhArgs &a, size_t smem, cudaStream_t st) {
+  auto kern = a.stats ? k_exhaustive<NT, true> : k_exhaustive<NT, false>;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_exhaustive<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exhaustive<NT>, kWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, smem);
   if (occ < 1) occ = 1;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -685,7 +686,7 @@ static gp_status launch_exh(ExhArgs &a, size_t smem, cudaStream_t st) {
   uint64_t want = (a.total_items + kGrab * kWarps - 1) / (kGrab * kWarps);
   uint64_t grid = (uint64_t)sms * occ;
   if (want < grid) grid = want > 0 ? want : 1;
-  k_exhaustive<NT><<<(unsigned)grid, kWarps * 32, smem, st>>>(a);
+  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(a);
   return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) main kernel");
 }
 
@@ -759,11 +760,11 @@ static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
   build_shape_table(N, a, sh);
   if (sh.item_base[sh.n_shapes] != a.total_items)
     return gp_fail(GP_EINVAL, "EXHAUSTIVE: shape table does not cover the candidate space");
+  auto kern = a.stats ? k_exhaustive_shaped<N, true> : k_exhaustive_shaped<N, false>;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_exhaustive_shaped<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exhaustive_shaped<N>, kWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, smem);
   if (occ < 1) occ = 1;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -771,7 +772,7 @@ static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
   uint64_t want = (a.total_items + kGrab * kWarps - 1) / (kGrab * kWarps);
   uint64_t grid = (uint64_t)sms * occ;
   if (want < grid) grid = want > 0 ? want : 1;
-  k_exhaustive_shaped<N><<<(unsigned)grid, kWarps * 32, smem, st>>>(a, sh);
+  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(a, sh);
   return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) shaped kernel");
 }
 
