@@ -60,6 +60,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_EAGER_LOADS
 #define GP_BP_EAGER_LOADS 1  // closed sweeps: R reads before the bit test (A/B: 3.53 -> 3.45 ms)
 #endif
+#ifndef GP_BP_CORNER
+#define GP_BP_CORNER 1  // closed2 blocks: one corner-table read instead of the sweep loop (A/B)
+#endif
 #ifndef GP_BP_SWEEP_UNROLL
 #define GP_BP_SWEEP_UNROLL 2  // closed-sweep loop unroll (A/B: 1, 2, 4 -> 2 by 1.3 %)
 #endif
@@ -86,6 +89,17 @@ struct MemoTask {  // one task of the set: one 16-byte shared-memory load per us
   int32_t D, T, q;  // deadline, period, H / T
   float invD;       // 1 / D (the density shortcut of memo_test)
 };
+
+#ifndef GP_SP_LEVELS
+#define GP_SP_LEVELS 4
+#endif
+constexpr int kSpLevels = GP_SP_LEVELS;  // load levels inside a (group, first size) key of the lane order
+
+// the set's load level: its number of schedulable (subset, size) pairs, quantised
+GP_DEV uint8_t sp_level(uint32_t npass, int nsub, int M) {
+  const uint32_t cap = (uint32_t)(nsub - 1) * (uint32_t)M + 1u;
+  return (uint8_t)(npass * (uint32_t)kSpLevels / cap);
+}
 
 struct MemoWarp {
   uint32_t vs[1 << kBpMaxN];          // verdict word per subset
@@ -272,7 +286,16 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
       }
     }
     __syncwarp();
-    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
+    uint32_t npass = 0;  // schedulable (subset, size) pairs: the set's load level (lane order)
+    for (int S2 = lane; S2 < nsub; S2 += 32) {
+      const uint32_t v = w.vs[S2];
+      V[S2] = S2 == 0 ? 1u : v;
+      npass += S2 == 0 ? 0u : (uint32_t)__popc(v & Mmask);
+    }
+    if (a.sp_lvl) {
+      npass = __reduce_add_sync(GP_FULL, npass);
+      if (lane == 0) a.sp_lvl[set] = sp_level(npass, nsub, M);
+    }
     __syncwarp();
   }
   if constexpr (kStats) {  // (the timed instantiation carries no counters)
@@ -463,6 +486,67 @@ __global__ void __launch_bounds__(kScanBlock) k_rows_scan_add(uint64_t *R, uint6
   if (r < total) R[(uint64_t)blockIdx.y * stride + r + 1] += btot[(uint64_t)blockIdx.y * nb + blockIdx.x];
 }
 
+// ---- corner table: CT[r] for every candidate r of an allocation with k >= 3 blocks.  Fix
+// the outer parts s_0 .. s_{k-4} of r's allocation pi (a BLOCK of candidates: the last
+// three parts (v, s_{k-2}, s_{k-1}) range over v + s_{k-2} + s_{k-1} <= N = M - sum(outer)).
+// CT[r] = the verdict-hash sum of the candidates of r's block that dominate r in all three
+// last parts (v' >= v, s'_{k-2} >= s_{k-2}, s'_{k-1} >= s_{k-1}): a corner of the block.
+// When a set's verdict words make its schedulable candidates of a block exactly such a
+// corner (the main pass's closed2 items: blocks k-3, k-2, k-1 pass exactly from sizes
+// lo2+1, lo1+1, a0+1 up), the block adds CT at the corner's apex -- one read per (set,
+// block) instead of two per (set, sweep).  Each entry is built from R exactly as the
+// closed2 sweep loop sums it (the sweeps v = x+1 .. of the corner, their live runs
+// [y, len0 - z) as R[z] differences), so the two give the same sum mod 2^64.
+__global__ void __launch_bounds__(256) k_corner_table(const ExhArgs a, const uint64_t *R,
+                                                      uint64_t *CT) {
+  const int M = a.M;
+  if (a.L.kmax < 3) return;
+  const uint64_t r0 = a.L.k_base[3], r1 = a.L.total;
+  for (uint64_t r = r0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    int k = 3;
+    while (k < a.L.kmax && r >= a.L.k_base[k + 1]) ++k;
+    const uint64_t loc = r - a.L.k_base[k];
+    const uint64_t p = loc / a.L.per_pi[k];
+    uint32_t rho = (uint32_t)(loc - p * a.L.per_pi[k]);
+    // unrank rho -> the k-subset c of {1..M} (prefix sums of the parts), lexicographic
+    int32_t c[kBpMaxN + 1];
+    int prev = 0;
+    for (int j = 0; j < k; ++j) {
+      int v = prev + 1;
+      for (;;) {
+        uint64_t b = 1;  // subsets with c_j = v: C(M - v, k - 1 - j)
+        const int nn = M - v, kk = k - 1 - j;
+        for (int i = 1; i <= kk; ++i) b = b * (uint64_t)(nn - kk + i) / (uint64_t)i;
+        if (rho < b) break;
+        rho -= (uint32_t)b;
+        ++v;
+      }
+      c[j] = v;
+      prev = v;
+    }
+    const int qsum = k >= 4 ? c[k - 4] : 0;                      // outer parts
+    const int x = c[k - 3] - qsum - 1, y = c[k - 2] - c[k - 3] - 1, z = c[k - 1] - c[k - 2] - 1;
+    const int L1 = M - qsum - 2;
+    // run offset (within pi) of sweep v = x + 1's first run: the (k-1)-subset
+    // {c_0 .. c_{k-4}, qsum + v, qsum + v + 1} of {1..M-1}
+    int32_t cc[kBpMaxN + 1];
+    for (int j = 0; j < k - 3; ++j) cc[j] = c[j];
+    cc[k - 3] = qsum + x + 1;
+    cc[k - 2] = qsum + x + 2;
+    uint32_t roff = subset_lex_rank(cc, k - 1, M - 1);
+    const uint64_t *row = R + (uint64_t)z * a.r_stride + a.run_base[k] + p * a.L.n_runs[k];
+    int len0 = L1 - x;
+    uint64_t h = 0;
+    for (int sp = len0 - z - y; sp >= 1; --sp) {
+      h += row[roff + (uint32_t)(len0 - z)] - row[roff + (uint32_t)y];
+      roff += (uint32_t)len0;
+      --len0;
+    }
+    CT[r] = h;
+  }
+}
+
 // ---- per-subset lane order: for every subset S, the sets ordered by (utilisation group,
 // first size at which S passes): sets of one group have similar loads in every subset,
 // and within it the lanes of a warp share the upper end of their live run ranges.  A
@@ -473,54 +557,62 @@ constexpr int kThrBins = kBpMaxM + 1;
 
 GP_DEV int first_pass(uint32_t v) { return v ? __ffs(v) - 1 : kBpMaxM; }
 
-#ifndef GP_SP_LEVELS
-#define GP_SP_LEVELS 4
-#endif
-constexpr int kSpLevels = GP_SP_LEVELS;  // load levels inside a (group, first size) key
-
-// key = (group, first passing size of S, load level of the set); load level = the set's
-// number of schedulable (subset, size) pairs, quantised
-GP_DEV int sp_key(const ExhArgs &a, const uint32_t *V, int64_t set, int S, const uint8_t *lvl) {
-  if (V[0] == 0u) return a.n_groups * kThrBins * kSpLevels;  // contract violated: last
-  const int g = a.group[set];
-  return ((g >= 0 && g < a.n_groups ? g : 0) * kThrBins + first_pass(V[S])) * kSpLevels + lvl[set];
+// key = (group, first passing size of S, load level of the set); the load level (the
+// set's number of schedulable (subset, size) pairs, quantised: sp_level) is written by the
+// memo pass
+GP_DEV int sp_key(const ExhArgs &a, uint32_t V0, uint32_t VS, int g, uint8_t lvl) {
+  if (V0 == 0u) return a.n_groups * kThrBins * kSpLevels;  // contract violated: last
+  return ((g >= 0 && g < a.n_groups ? g : 0) * kThrBins + first_pass(VS)) * kSpLevels + lvl;
 }
 
-__global__ void k_sp_level(const ExhArgs a, const uint32_t *memo, int nsub, uint8_t *lvl) {
-  const uint32_t mmask = a.M >= 32 ? ~0u : (1u << a.M) - 1u;
-  const uint32_t cap = (uint32_t)(nsub - 1) * (uint32_t)a.M + 1u;
-  for (int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; set < a.n_sets;
-       set += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t *V = memo + set * nsub;
-    uint32_t c = 0;
-    for (int S = 1; S < nsub; ++S) c += __popc(V[S] & mmask);
-    lvl[set] = (uint8_t)(c * (uint32_t)kSpLevels / cap);
-  }
-}
+// Only the subsets that can be an allocation's LAST block need an order: the last block
+// carries the highest RGS label, so it holds task 0 (label 0) only when k = 1, i.e. when
+// it is the whole set.  The other subsets holding task 0 are skipped (half of them).
+GP_DEV bool sp_used(int S, int nsub) { return (S & 1) == 0 || S == nsub - 1; }
 
-// thread = (subset, set), sets fastest: the 32 sets of a warp mostly share a key (same
-// group, similar first passing size), so each warp adds once per distinct key
-// (warp-aggregated atomics via __match_any_sync).  The grid-stride loop keeps whole warps
-// in step (total is rounded up to a multiple of 32; lanes past the end carry no key).
-GP_DEV uint32_t sp_slot(const ExhArgs &a, const uint32_t *memo, int nsub, int nkeys, int64_t e,
-                        const uint8_t *lvl, int64_t &set, int &S) {
-  S = (int)(e / a.n_sets) + 1;
-  set = e - (int64_t)(S - 1) * a.n_sets;
-  return (uint32_t)S * (uint32_t)nkeys + (uint32_t)sp_key(a, memo + set * nsub, set, S, lvl);
-}
-
-__global__ void __launch_bounds__(256) k_sp_hist(const ExhArgs a, const uint32_t *memo, int nsub,
-                                                 int nkeys, uint32_t *hist, const uint8_t *lvl) {
-  const int64_t total = a.n_sets * (int64_t)(nsub - 1);
-  const int64_t total32 = (total + 31) & ~(int64_t)31;
-  const int lane = threadIdx.x & 31;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total32;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t set;
-    int S;
-    const uint32_t slot = e < total ? sp_slot(a, memo, nsub, nkeys, e, lvl, set, S) : ~0u;
-    const uint32_t peers = __match_any_sync(GP_FULL, slot);
-    if (slot != ~0u && lane == __ffs(peers) - 1) atomicAdd(&hist[slot], (uint32_t)__popc(peers));
+// One CTA per tile of 32 consecutive sets: the tile's verdict words are staged in shared
+// memory by coalesced loads (a set's words are contiguous), then warp w keys subsets
+// S = w+1, w+9, ... with lane = set, so the 32 sets of a warp mostly share a key (same
+// group, similar first passing size) and each warp adds once per distinct key
+// (warp-aggregated atomics via __match_any_sync).  kScatter = false: histogram;
+// true: scatter into the scanned offsets.
+constexpr int kSpTile = 32;
+template <bool kScatter>
+__global__ void __launch_bounds__(256) k_sp_tile(const ExhArgs a, const uint32_t *memo, int nsub,
+                                                 int nkeys, uint32_t *hist, uint32_t *sperm) {
+  __shared__ uint32_t tv[kSpTile * ((1 << kBpMaxN) + 1)];  // row stride nsub + 1: no bank conflicts
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int rs = nsub + 1;
+  const int64_t n_tiles = ((int64_t)a.n_sets + kSpTile - 1) / kSpTile;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t s0 = tile * kSpTile;
+    const int nt = (int)min((int64_t)kSpTile, (int64_t)a.n_sets - s0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * nsub; i += blockDim.x) {
+      const int r = i / nsub;
+      tv[r * rs + (i - r * nsub)] = memo[s0 * nsub + i];
+    }
+    __syncthreads();
+    const int64_t set = s0 + lane;
+    const bool has = lane < nt;
+    const int g = has ? a.group[set] : 0;
+    const uint8_t lvl = has ? a.sp_lvl[set] : 0;
+    const uint32_t V0 = has ? tv[lane * rs] : 0u;
+    for (int S = wid + 1; S < nsub; S += 8) {
+      if (!sp_used(S, nsub)) continue;  // warp-uniform
+      const uint32_t slot =
+          has ? (uint32_t)S * (uint32_t)nkeys + (uint32_t)sp_key(a, V0, tv[lane * rs + S], g, lvl) : ~0u;
+      const uint32_t peers = __match_any_sync(GP_FULL, slot);
+      const int leader = __ffs(peers) - 1;
+      if constexpr (!kScatter) {
+        if (has && lane == leader) atomicAdd(&hist[slot], (uint32_t)__popc(peers));
+      } else {
+        uint32_t base = 0;
+        if (has && lane == leader) base = atomicAdd(&hist[slot], (uint32_t)__popc(peers));
+        base = __shfl_sync(GP_FULL, base, leader);
+        if (has) sperm[(size_t)S * a.n_sets + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)set;
+      }
+    }
   }
 }
 
@@ -541,27 +633,6 @@ __global__ void __launch_bounds__(32) k_sp_scan(uint32_t *hist, int nkeys) {
     const uint32_t c = h[b];
     h[b] = run;
     run += c;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_sp_scatter(const ExhArgs a, const uint32_t *memo, int nsub,
-                                                    int nkeys, uint32_t *offs, uint32_t *sperm,
-                                                    const uint8_t *lvl) {
-  const int64_t total = a.n_sets * (int64_t)(nsub - 1);
-  const int64_t total32 = (total + 31) & ~(int64_t)31;
-  const int lane = threadIdx.x & 31;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total32;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t set = 0;
-    int S = 0;
-    const uint32_t slot = e < total ? sp_slot(a, memo, nsub, nkeys, e, lvl, set, S) : ~0u;
-    const uint32_t peers = __match_any_sync(GP_FULL, slot);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (slot != ~0u && lane == leader) base = atomicAdd(&offs[slot], (uint32_t)__popc(peers));
-    base = __shfl_sync(GP_FULL, base, leader);
-    if (slot != ~0u)
-      sperm[(size_t)S * a.n_sets + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)set;
   }
 }
 
@@ -700,6 +771,10 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             ? reinterpret_cast<uint64_t>(a.R) +
                   8ull * ((uint64_t)(a0 & 31) * a.r_stride + a.run_base[k] + (uint64_t)p * a.L.n_runs[k])
             : 0ull;
+    // the corner table at pi's first rank (closed2 blocks)
+    const uint64_t ct_addr =
+        (GP_BP_CORNER && !kWin && kHash == 1 && !kBits && a.CT) ? reinterpret_cast<uint64_t>(a.CT) + 8ull * rank_pi
+                                                                : 0ull;
     uint32_t *bits = nullptr;
     if constexpr (kBits) bits = lane_ok ? a.bits + set * a.words : nullptr;
     uint32_t first_off = UINT32_MAX;  // s-index of pi's first schedulable candidate
@@ -871,7 +946,8 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         const uint32_t mk = need >= 32 ? ~0u : (need <= 0 ? 0u : (1u << need) - 1u);
         c2 = ((Vr[2] >> lo2) & mk) == mk;
       }
-      const bool closed2 = GP_BP_CLOSED2 && closed && GP_BP_LANE_V && __all_sync(GP_FULL, c2);
+      const bool closed2 = GP_BP_CLOSED2 && closed && GP_BP_LANE_V &&
+                           (!GP_BP_CORNER || kHash != 1 || a.CT != nullptr) && __all_sync(GP_FULL, c2);
       int32_t q[kBpMaxN];
 #pragma unroll
       for (int t = 0; t < kBpMaxN; ++t) q[t] = 1;
@@ -905,9 +981,16 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             if (first_off == UINT32_MAX)
               first_off = off2 + tet1 - (uint32_t)(len0f * (len0f + 1) * (len0f + 2) / 6) +
                           (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
-            int len0 = len0f;
-            uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
             if constexpr (kHash == 1) {  // (without the hash the outer prefix is O(1))
+#if GP_BP_CORNER
+              // the lane's schedulable candidates of this block are the corner with apex
+              // (lo2+1, lo1+1, a0+1): its hash is one corner-table read at the apex rank
+              const uint32_t apex = off2 + tet1 - (uint32_t)(len0f * (len0f + 1) * (len0f + 2) / 6) +
+                                    (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
+              acc_hash += ld_u64(ct_addr, apex);
+#else
+              int len0 = len0f;
+              uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
               uint64_t hsum = 0;
 #pragma unroll kBpSweepUnroll
               for (int sp = span_hi; sp >= 1; --sp) {
@@ -916,6 +999,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
                 --len0;
               }
               acc_hash += hsum;
+#endif
             }
           }
         } else {
@@ -1076,11 +1160,11 @@ namespace gp {
 // stream-ordered temporary): memo words [n_sets][2^n], RGS labels, the per-subset
 // lane order (slots, histograms, load levels) and the hash prefix table.
 struct BpLayout {
-  size_t memo_words, sp_words, sp_total, words32, bytes, r_off;
+  size_t memo_words, sp_words, sp_total, words32, bytes, r_off, ct_off;
   uint64_t n_rgs, n_ranks, total_runs, r_stride;
   uint32_t nb, r_nb;
   int sp_keys;
-  bool use_sp, use_P, use_R;
+  bool use_sp, use_P, use_R, use_CT;
 };
 
 static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_groups,
@@ -1115,6 +1199,10 @@ static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_
   b.r_nb = (uint32_t)((b.total_runs + kScanBlock - 1) / kScanBlock);
   b.r_off = b.bytes;
   if (b.use_R) b.bytes += ((uint64_t)L.M * b.r_stride + (uint64_t)L.M * b.r_nb) * 8;
+  // corner table CT[rank] (allocations of k >= 3 blocks) next to R: 8 B per rank
+  b.use_CT = GP_BP_CORNER && b.use_R && L.kmax >= 3;
+  b.ct_off = b.bytes;
+  if (b.use_CT) b.bytes += (uint64_t)L.total * 8;
   return b;
 }
 }  // namespace gp
@@ -1196,6 +1284,7 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     runs += a.L.n_pi[k] * c;
   }
   a.R = nullptr;
+  a.CT = nullptr;
   if (b.use_R) {
     uint64_t *R = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.r_off);
     uint64_t *rbt = R + (uint64_t)M * b.r_stride;
@@ -1207,7 +1296,16 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     k_rows_scan_blocks<<<M, kScanBlock, 0, st>>>(rbt, b.r_nb);
     k_rows_scan_add<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
     a.R = R;
+    if (b.use_CT) {
+      uint64_t *CT = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.ct_off);
+      int64_t gc = ((int64_t)(a.L.total - a.L.k_base[3]) + 255) / 256;
+      if (gc > (int64_t)sms * 16) gc = (int64_t)sms * 16;
+      k_corner_table<<<(unsigned)(gc > 0 ? gc : 1), 256, 0, st>>>(a, R, CT);
+      a.CT = CT;
+    }
   }
+  // the lane order's per-set load levels (after its histograms), written by the memo pass
+  a.sp_lvl = use_sp ? reinterpret_cast<uint8_t *>(sphist + (size_t)(1 << n) * sp_keys) : nullptr;
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
@@ -1226,13 +1324,11 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   if (use_sp) {
     const int nsub = 1 << n;
     cudaMemsetAsync(sphist, 0, (size_t)nsub * sp_keys * 4, st);
-    int64_t gk = ((int64_t)a.n_sets * (nsub - 1) + 255) / 256;
+    int64_t gk = ((int64_t)a.n_sets + kSpTile - 1) / kSpTile;
     if (gk > (int64_t)sms * 8) gk = (int64_t)sms * 8;
-    uint8_t *lvl = reinterpret_cast<uint8_t *>(sphist + (size_t)nsub * sp_keys);
-    k_sp_level<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, lvl);
-    k_sp_hist<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, lvl);
+    k_sp_tile<false><<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, nullptr);
     k_sp_scan<<<nsub - 1, 32, 0, st>>>(sphist, sp_keys);
-    k_sp_scatter<<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm, lvl);
+    k_sp_tile<true><<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm);
     a.sperm = sperm;
   }
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
