@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
   uint32_t acc_n = 0;
   int32_t acc_pi = INT32_MAX;
   uint64_t acc_first = ~0ull, acc_hash = 0, st_cand = 0, st_runs = 0, st_live = 0;
-  uint64_t st_sweeps = 0, st_live_closed = 0;
+  uint64_t st_sweeps = 0, st_live_closed = 0, st_ct_blocks = 0, st_ct_sweeps = 0;
   int64_t cur_g = -1, set = -1;
   bool lane_ok = false;
   auto flush = [&]() {
@@ -988,6 +988,10 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
               const uint32_t apex = off2 + tet1 - (uint32_t)(len0f * (len0f + 1) * (len0f + 2) / 6) +
                                     (uint32_t)(lo1 * len0f - ((lo1 * (lo1 - 1)) >> 1) + a0);
               acc_hash += ld_u64(ct_addr, apex);
+              if constexpr (kStats) {
+                ++st_ct_blocks;
+                st_ct_sweeps += (uint64_t)span_hi;
+              }
 #else
               int len0 = len0f;
               uint32_t roffv = roff2 + tri1 - (uint32_t)((len0 * (len0 + 1)) >> 1);
@@ -1119,6 +1123,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     const uint64_t c0 = warp_sum_u64(st_cand);
     const uint64_t c4 = warp_sum_u64(st_runs), c5 = warp_sum_u64(st_live);
     const uint64_t c6 = warp_sum_u64(st_sweeps), c7 = warp_sum_u64(st_live_closed);
+    const uint64_t c8 = warp_sum_u64(st_ct_blocks), c9 = warp_sum_u64(st_ct_sweeps);
     if (lane == 0) {
       atomicAdd(a.stats + 0, c0);
       if (a.flags & GP_EX_STATS_EXT) {
@@ -1126,6 +1131,8 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         atomicAdd(a.stats + 5, c5);
         atomicAdd(a.stats + 6, c6);
         atomicAdd(a.stats + 7, c7);
+        atomicAdd(a.stats + 8, c8);
+        atomicAdd(a.stats + 9, c9);
       }
     }
   }

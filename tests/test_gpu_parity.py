@@ -192,8 +192,9 @@ def test_exhaustive_c2_bitmaps(G, ev):
     # the bench's launch configuration: no verdict bits, no stats
     per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
     assert (per2 == ref).all()
-    if ev == 0:  # GP_EX_STATS_EXT: 8 counters, + runs walked / live, closed-form sweeps / runs
-        st6 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    if ev == 0:  # GP_EX_STATS_EXT: 10 counters, + runs walked / live, closed-form sweeps / runs,
+        # corner-table blocks / their sweeps
+        st6 = torch.zeros(10, dtype=torch.int64, device="cuda")
         per3 = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
         G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per3,
                          work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"), stats=st6)
@@ -210,6 +211,7 @@ def test_exhaustive_c2_bitmaps(G, ev):
         assert s6[5] <= s6[4] and s6[4] + s6[7] <= n_runs and s6[6] <= s6[7]
         assert s6[5] + s6[7] >= (ref[:, 0] > 0).sum()
         assert s6[6] > 0  # generated sets have up-closed verdict words: the closed form runs
+        assert s6[8] <= s6[9] <= s6[6]  # corner-table blocks hold >= 1 sweep each
 
 
 @EVALUATORS
