@@ -365,7 +365,7 @@ def main():
     alloc_stats.zero_()
     step(False, stats=True)
     torch.cuda.synchronize()
-    exh_stats = pipe.stats.cpu().numpy().tolist() if pipe.exhaustive else [0] * 10
+    exh_stats = pipe.stats.cpu().numpy().tolist() if pipe.exhaustive else [0] * 12
     al_stats = alloc_stats.cpu().numpy().tolist()
     # §8(d)'s per-candidate work (the direct evaluation's W lookups, utilisation
     # passes and demand-walk events), counted by the per-candidate evaluator on
@@ -482,18 +482,23 @@ def main():
             runs = pipe.ts.n_sets * sum(stirling2(pipe.n, k) * math.comb(pipe.M - 1, k - 1)
                                         for k in range(1, min(pipe.n, pipe.M) + 1))
             ops = (3 * exh_stats[3] + 4 * exh_stats[2] + 2 * exh_stats[4] + 6 * exh_stats[5]
-                   + 12 * (exh_stats[6] - exh_stats[9]) + 12 * exh_stats[8])
+                   + 12 * (exh_stats[6] - exh_stats[9]) + 12 * exh_stats[8]
+                   + 5 * exh_stats[10] + 7 * exh_stats[11])
             ops_basis = ("the bit-sliced evaluator's own essential work, counted by its kernels: "
                          "memo-pass EDF tests (3/task + 4/deadline) + 2 per (set, run) walked + "
                          "6 per live run walked + 12 per (set, sweep) resolved in closed form "
                          "(count, pi*, first rank: 10 int ops; hash: 2 table reads) + 12 per "
-                         "(set, block) resolved by one corner-table read (its sweeps not counted)")
+                         "(set, block) resolved by one corner-table read (its sweeps not counted) + "
+                         "per (set, allocation) resolved as one full corner 5 (count, pi*, first "
+                         "rank, hash read and add) + 7 per block (first size, range check, prefix "
+                         "sum, rank term)")
         per_unit = ops / max(pipe.candidates_per_step(), 1)
         extra = {"ops_basis": ops_basis, "candidates_per_launch": pipe.candidates_per_step(),
                  "memo_edf_tests": exh_stats[1], "memo_deadlines": exh_stats[2],
                  "runs_total": runs, "runs_walked": exh_stats[4], "live_runs": exh_stats[5],
                  "closed_sweeps": exh_stats[6], "closed_live_runs": exh_stats[7],
                  "corner_blocks": exh_stats[8], "corner_block_sweeps": exh_stats[9],
+                 "full_corner_allocations": exh_stats[10], "full_corner_blocks": exh_stats[11],
                  "direct_ops_per_step": float(direct_ops),
                  "direct_events_per_candidate": st[2] / max(st[0], 1)}
     else:

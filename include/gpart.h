@@ -306,7 +306,7 @@ typedef struct {
                                  deadline points examined, tasks in tested blocks}
                                  (THRESHOLD: {sets, threshold tests, deadline points,
                                  schedulable candidates enumerated for the hash});
-                                 [10] with GP_EX_STATS_EXT: [4] += (set, run) pairs the
+                                 [12] with GP_EX_STATS_EXT: [4] += (set, run) pairs the
                                  bit-sliced evaluator walked one by one, [5] += those with a
                                  non-zero verdict word (a run = the candidates of one
                                  allocation that differ in the last part only), [6] += (set,
@@ -315,11 +315,13 @@ typedef struct {
                                  live runs inside them, [8] += (set, block) pairs whose hash
                                  was one corner-table read (a block = the candidates of one
                                  allocation that differ in the last three parts only), [9] +=
-                                 the sweeps inside them (also counted in [6]); 0 for the
-                                 other evaluators                                           */
+                                 the sweeps inside them (also counted in [6]), [10] +=
+                                 (set, allocation) pairs resolved as one full corner (every
+                                 block word one bit range; closed form, one table read),
+                                 [11] += their blocks; 0 for the other evaluators           */
   uint32_t flags;             /* GP_EX_NO_HASH: skip the verdict hash (per_set[3] = 0);
                                  GP_EX_PER_CANDIDATE (EXHAUSTIVE): force the per-candidate
-                                 evaluator; GP_EX_STATS_EXT: stats has 10 slots (above);
+                                 evaluator; GP_EX_STATS_EXT: stats has 12 slots (above);
                                  test hooks (same outputs, other code paths):
                                  GP_EX_FORCE_RANGES: the bit-sliced evaluator walks every
                                  verdict word range by range (no contiguous fast path);

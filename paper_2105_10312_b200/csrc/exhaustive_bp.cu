@@ -63,6 +63,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_CORNER
 #define GP_BP_CORNER 1  // closed2 blocks: one corner-table read instead of the sweep loop (A/B)
 #endif
+#ifndef GP_BP_FULLCORNER
+#define GP_BP_FULLCORNER 1  // (set, allocation) pairs whose every block word is a top range: closed form (A/B)
+#endif
 #ifndef GP_BP_SWEEP_UNROLL
 #define GP_BP_SWEEP_UNROLL 2  // closed-sweep loop unroll (A/B: 1, 2, 4 -> 2 by 1.3 %)
 #endif
@@ -547,6 +550,82 @@ __global__ void __launch_bounds__(256) k_corner_table(const ExhArgs a, const uin
   }
 }
 
+// ---- full corner table: FCT[r] = the verdict-hash sum of the candidates of r's allocation pi
+// that dominate r in EVERY part (s' >= s componentwise, sum(s') <= M).  When a set's verdict
+// word of every block of pi is one bit range from its first passing size lo_j up to the
+// largest size a part can take (M - k + 1) -- checked per (set, allocation) in the main pass,
+// never assumed -- the set's schedulable candidates of pi are exactly that corner with apex
+// s_j = lo_j + 1: n_sched = C(M - sum lo, k), pi* = sum(lo) + k, the first rank is the apex's
+// and the hash is FCT at the apex -- one read per (set, allocation).
+// Built as k suffix scans over pi's simplex: level 0 = splitmix64(r); pass j (= 1 .. kmax)
+// scans dimension i = k - j of every allocation with k >= j, one thread per CHAIN (the
+// candidates that differ in part i only), walking part i downwards and summing in place.
+// The candidate ranks come from the lex rank of the prefix-sum k-subset c of {1..M}:
+// rank(c) = C(M, k) - 1 - sum_j C(M - c_j, k - j).
+struct Binom {  // C(a, b), 0 <= a <= kBpMaxM, 0 <= b <= kBpMaxN (shared memory)
+  uint32_t t[(kBpMaxM + 1) * (kBpMaxN + 1)];
+  GP_DEV void build() {
+    for (int e = threadIdx.x; e < (kBpMaxM + 1) * (kBpMaxN + 1); e += blockDim.x) {
+      const int aa = e / (kBpMaxN + 1), bb = e - aa * (kBpMaxN + 1);
+      uint64_t c = 1;
+      for (int i = 1; i <= bb; ++i) c = c * (uint64_t)(aa - bb + i) / (uint64_t)i;
+      t[e] = bb > aa ? 0u : (uint32_t)c;
+    }
+  }
+  GP_DEV uint32_t operator()(int aa, int bb) const {
+    return (aa < 0 || bb > aa) ? 0u : t[aa * (kBpMaxN + 1) + bb];
+  }
+};
+
+__global__ void __launch_bounds__(256) k_fct_init(uint64_t *F, uint64_t n_ranks) {
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranks;
+       r += (uint64_t)gridDim.x * blockDim.x)
+    F[r] = splitmix64(r);
+}
+
+__global__ void __launch_bounds__(256) k_fct_pass(const ExhArgs a, uint64_t *F, int j) {
+  __shared__ Binom C;
+  C.build();
+  __syncthreads();
+  const int M = a.M;
+  const uint64_t g0 = a.run_base[j], total = a.run_base[a.L.kmax + 1];
+  for (uint64_t g = g0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    int k = j;
+    while (k < a.L.kmax && g >= a.run_base[k + 1]) ++k;
+    const uint64_t loc = g - a.run_base[k];
+    const uint32_t nr = a.L.n_runs[k];
+    const uint64_t p = loc / nr;
+    uint32_t rho = (uint32_t)(loc - p * nr);
+    // the chain's other parts: the (k-1)-subset d of {1..M-1} (their prefix sums), lex
+    int32_t d[kBpMaxN + 1];
+    int prev = 0;
+    for (int m = 0; m < k - 1; ++m) {
+      int v = prev + 1;
+      while (rho >= C(M - 1 - v, k - 2 - m)) {
+        rho -= C(M - 1 - v, k - 2 - m);
+        ++v;
+      }
+      d[m] = v;
+      prev = v;
+    }
+    const int i = k - j;                          // the scanned part
+    const int dtot = k >= 2 ? d[k - 2] : 0;       // sum of the other parts
+    const int dpre = i > 0 ? d[i - 1] : 0;        // sum of the parts before i
+    // the part of the rank that does not depend on part i's value t
+    uint32_t fixed = C(M, k) - 1u;
+    for (int m = 0; m < i; ++m) fixed -= C(M - d[m], k - m);
+    const uint64_t base = a.L.k_base[k] + p * (uint64_t)a.L.per_pi[k];
+    uint64_t acc = 0;
+    for (int t = M - dtot; t >= 1; --t) {
+      uint32_t rk = fixed - C(M - (dpre + t), k - i);
+      for (int m = i + 1; m < k; ++m) rk -= C(M - (d[m - 1] + t), k - m);
+      acc += F[base + rk];
+      F[base + rk] = acc;
+    }
+  }
+}
+
 // ---- per-subset lane order: for every subset S, the sets ordered by (utilisation group,
 // first size at which S passes): sets of one group have similar loads in every subset,
 // and within it the lanes of a warp share the upper end of their live run ranges.  A
@@ -672,6 +751,11 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
   int32_t acc_pi = INT32_MAX;
   uint64_t acc_first = ~0ull, acc_hash = 0, st_cand = 0, st_runs = 0, st_live = 0;
   uint64_t st_sweeps = 0, st_live_closed = 0, st_ct_blocks = 0, st_ct_sweeps = 0;
+  uint64_t st_fc_items = 0, st_fc_blocks = 0;
+  __shared__ Binom binom_s;  // C(a, b) for the full-corner closed forms
+  binom_s.build();
+  __syncthreads();
+  auto bn = [&](int aa, int bb) -> uint32_t { return binom_s(aa, bb); };
   int64_t cur_g = -1, set = -1;
   bool lane_ok = false;
   auto flush = [&]() {
@@ -718,6 +802,10 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     }
     const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
     const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
+    // the full corner table at pi's first rank
+    const uint64_t fct_addr =
+        (GP_BP_FULLCORNER && !kWin && kHash == 1 && !kBits && a.FCT) ? reinterpret_cast<uint64_t>(a.FCT) + 8ull * rank_pi
+                                                                     : 0ull;
     bool full = true;
     if constexpr (kWin) {
       if (rank_pi >= a.hi || rank_pi + per_pi <= a.lo) continue;
@@ -752,6 +840,47 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     for (int jj = 0; jj < kBpMaxN; ++jj)
       if (jj < k) dead |= Vr[jj] == 0u;
     if (__all_sync(GP_FULL, dead)) continue;
+#if GP_BP_FULLCORNER
+    if constexpr (!kWin && !kBits && kHash != 2) {
+      if ((kHash == 0 || a.FCT) && !a.force_ranges) {
+        // full corner: when every block's word is one bit range from its first passing size
+        // lo_j + 1 through the largest size a part can take (M - k + 1) -- checked here per
+        // (set, allocation) -- the set's schedulable candidates of pi are the corner with apex
+        // s_j = lo_j + 1 of pi's simplex: count, pi*, first rank in closed form, the hash one
+        // read of the full corner table at the apex (lanes done here skip the rest)
+        bool corner = !dead;
+        int csum = 0;      // prefix sums of the apex parts, block order j = 0 .. k-1
+        uint32_t sub = 0;  // sum_j C(M - c_j, k - j): the apex's lex rank complement
+#pragma unroll
+        for (int jj = kBpMaxN - 1; jj >= 0; --jj) {
+          if (jj < k) {  // warp-uniform; block j = k - 1 - jj
+            const uint32_t V = Vr[jj];
+            const int lo = V ? __ffs(V) - 1 : 0;
+            const int nb = M - k + 1 - lo;
+            const uint32_t mk = nb >= 32 ? ~0u : (nb <= 0 ? 0u : (1u << nb) - 1u);
+            corner &= ((V >> lo) & mk) == mk;
+            csum += lo + 1;
+            sub += bn(M - csum, jj + 1);
+          }
+        }
+        if (corner) {
+          if (csum <= M) {  // the apex fits: C(M - sum lo, k) candidates
+            acc_n += bn(M - csum + k, k);
+            acc_pi = min(acc_pi, csum);
+            const uint32_t off = bn(M, k) - 1u - sub;
+            acc_first = min(acc_first, rank_pi + off);
+            if constexpr (kHash == 1) acc_hash += ld_u64(fct_addr, off);
+            if constexpr (kStats) {
+              ++st_fc_items;
+              st_fc_blocks += (uint64_t)k;
+            }
+          }
+          dead = true;
+        }
+        if (__all_sync(GP_FULL, dead)) continue;
+      }
+    }
+#endif
     const uint32_t V0 = dead ? 0u : Vr[0];
     // lowest size index of the last block that can pass; contiguity of its word
     const int a0 = V0 ? __ffs(V0) - 1 : 32;
@@ -1124,6 +1253,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     const uint64_t c4 = warp_sum_u64(st_runs), c5 = warp_sum_u64(st_live);
     const uint64_t c6 = warp_sum_u64(st_sweeps), c7 = warp_sum_u64(st_live_closed);
     const uint64_t c8 = warp_sum_u64(st_ct_blocks), c9 = warp_sum_u64(st_ct_sweeps);
+    const uint64_t c10 = warp_sum_u64(st_fc_items), c11 = warp_sum_u64(st_fc_blocks);
     if (lane == 0) {
       atomicAdd(a.stats + 0, c0);
       if (a.flags & GP_EX_STATS_EXT) {
@@ -1133,6 +1263,8 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
         atomicAdd(a.stats + 7, c7);
         atomicAdd(a.stats + 8, c8);
         atomicAdd(a.stats + 9, c9);
+        atomicAdd(a.stats + 10, c10);
+        atomicAdd(a.stats + 11, c11);
       }
     }
   }
@@ -1167,11 +1299,11 @@ namespace gp {
 // stream-ordered temporary): memo words [n_sets][2^n], RGS labels, the per-subset
 // lane order (slots, histograms, load levels) and the hash prefix table.
 struct BpLayout {
-  size_t memo_words, sp_words, sp_total, words32, bytes, r_off, ct_off;
+  size_t memo_words, sp_words, sp_total, words32, bytes, r_off, ct_off, fct_off;
   uint64_t n_rgs, n_ranks, total_runs, r_stride;
   uint32_t nb, r_nb;
   int sp_keys;
-  bool use_sp, use_P, use_R, use_CT;
+  bool use_sp, use_P, use_R, use_CT, use_FCT;
 };
 
 static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_groups,
@@ -1210,6 +1342,10 @@ static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_
   b.use_CT = GP_BP_CORNER && b.use_R && L.kmax >= 3;
   b.ct_off = b.bytes;
   if (b.use_CT) b.bytes += (uint64_t)L.total * 8;
+  // full corner table FCT[rank]: 8 B per rank, with the hash prefix table
+  b.use_FCT = GP_BP_FULLCORNER && b.use_P;
+  b.fct_off = b.bytes;
+  if (b.use_FCT) b.bytes += (uint64_t)L.total * 8;
   return b;
 }
 }  // namespace gp
@@ -1290,8 +1426,22 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     a.run_base[k] = runs;
     runs += a.L.n_pi[k] * c;
   }
+  a.run_base[a.L.kmax + 1] = runs;
   a.R = nullptr;
   a.CT = nullptr;
+  a.FCT = nullptr;
+  if (b.use_FCT) {
+    uint64_t *F = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.fct_off);
+    int64_t gi = ((int64_t)a.L.total + 255) / 256;
+    if (gi > (int64_t)sms * 16) gi = (int64_t)sms * 16;
+    k_fct_init<<<(unsigned)(gi > 0 ? gi : 1), 256, 0, st>>>(F, a.L.total);
+    for (int j = 1; j <= a.L.kmax; ++j) {
+      int64_t gj = ((int64_t)(runs - a.run_base[j]) + 255) / 256;
+      if (gj > (int64_t)sms * 16) gj = (int64_t)sms * 16;
+      k_fct_pass<<<(unsigned)(gj > 0 ? gj : 1), 256, 0, st>>>(a, F, j);
+    }
+    a.FCT = F;
+  }
   if (b.use_R) {
     uint64_t *R = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.r_off);
     uint64_t *rbt = R + (uint64_t)M * b.r_stride;

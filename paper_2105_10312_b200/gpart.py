@@ -23,8 +23,8 @@ VARIANTS = {"1G": GP_1G, "SMS_ACT": GP_SMS_ACT, "SMS_INA": GP_SMS_INA, "BF_ACT":
 GP_FROM_VERDICTS, GP_EXHAUSTIVE, GP_THRESHOLD, GP_FROM_PER_SET = 0, 1, 2, 3
 GP_EX_NO_HASH = 1
 GP_EX_PER_CANDIDATE = 2  # force the per-candidate EXHAUSTIVE evaluator
-GP_EX_STATS_EXT = 4  # stats has 10 slots: + runs walked / live, closed-form sweeps / their runs,
-                     # corner-table blocks / their sweeps
+GP_EX_STATS_EXT = 4  # stats has 12 slots: + runs walked / live, closed-form sweeps / their runs,
+                     # corner-table blocks / their sweeps, full-corner allocations / their blocks
 GP_EX_FORCE_RANGES = 8  # test hook: bit-sliced evaluator walks verdict words range by range
 GP_EX_NATURAL_ORDER = 16  # test hook: bit-sliced evaluator without the per-subset lane order
 GP_EX_GENERIC = 32  # test hook: per-candidate evaluator without shape specialisation
@@ -303,13 +303,13 @@ def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=N
                    workspace=None, sizes=None):
     """FROM_VERDICTS: verdicts uint8 [n_rows][n_sets]; EXHAUSTIVE: per_set int64 [n_sets][4]
     (+ work_counter int64 [>=1], optional verdict_bits int32/uint32 [n_sets][words], stats
-    int64 [4], or [10] for the bit-sliced evaluator's run counters; optional workspace: a
+    int64 [4], or [12] for the bit-sliced evaluator's run counters; optional workspace: a
     uint8 device tensor of >= gp_exhaustive_workspace_size() bytes, else the call makes a
     stream-ordered temporary).  counts int64 [n_settings][n_groups][n_slots][3] is
     accumulated.  ``sizes``: admissible partition sizes for EXHAUSTIVE / THRESHOLD (f4,
     reading B-9; None = every size)."""
     s = ts.struct()
-    if stats is not None and stats.numel() >= 10 and mode == GP_EXHAUSTIVE:
+    if stats is not None and stats.numel() >= 12 and mode == GP_EXHAUSTIVE:
         flags |= GP_EX_STATS_EXT
     if mode in (GP_EXHAUSTIVE, GP_THRESHOLD, GP_FROM_PER_SET):
         n_rows = 1

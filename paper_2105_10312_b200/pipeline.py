@@ -95,7 +95,7 @@ class Pipeline:
                                           if split == "ranks" else (0, self.n_cand))
             self.per_set = torch.zeros((S, 4), dtype=torch.int64, device=device)
             self.work = torch.zeros(1, dtype=torch.int64, device=device)
-            self.stats = torch.zeros(10, dtype=torch.int64, device=device) if stats else None
+            self.stats = torch.zeros(12, dtype=torch.int64, device=device) if stats else None
             # caller-owned evaluator workspace (gpart.h: no hidden persistent allocations)
             self.workspace = G.exhaustive_workspace(self.ts, device=device)
         else:

@@ -192,9 +192,9 @@ def test_exhaustive_c2_bitmaps(G, ev):
     # the bench's launch configuration: no verdict bits, no stats
     per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)
     assert (per2 == ref).all()
-    if ev == 0:  # GP_EX_STATS_EXT: 10 counters, + runs walked / live, closed-form sweeps / runs,
-        # corner-table blocks / their sweeps
-        st6 = torch.zeros(10, dtype=torch.int64, device="cuda")
+    if ev == 0:  # GP_EX_STATS_EXT: 12 counters, + runs walked / live, closed-form sweeps / runs,
+        # corner-table blocks / their sweeps, full-corner allocations / their blocks
+        st6 = torch.zeros(12, dtype=torch.int64, device="cuda")
         per3 = torch.empty((ts.n_sets, 4), dtype=torch.int64, device="cuda")
         G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per3,
                          work_counter=torch.zeros(1, dtype=torch.int64, device="cuda"), stats=st6)
@@ -208,10 +208,13 @@ def test_exhaustive_c2_bitmaps(G, ev):
         # every run holding a schedulable candidate is live, walked one by one ([4], [5]) or
         # inside a sweep resolved in closed form ([6] sweeps, [7] their live runs)
         n_runs = 1000 * sum(W_stirling(6, k) * comb(7, k - 1) for k in range(1, 7))
+        # or inside an allocation resolved as one full corner ([10] allocations, [11] blocks)
         assert s6[5] <= s6[4] and s6[4] + s6[7] <= n_runs and s6[6] <= s6[7]
-        assert s6[5] + s6[7] >= (ref[:, 0] > 0).sum()
-        assert s6[6] > 0  # generated sets have up-closed verdict words: the closed form runs
+        assert s6[5] + s6[7] + s6[10] >= (ref[:, 0] > 0).sum()
+        # generated sets have up-closed verdict words: the closed forms run
+        assert s6[6] + s6[10] > 0
         assert s6[8] <= s6[9] <= s6[6]  # corner-table blocks hold >= 1 sweep each
+        assert s6[10] <= s6[11] <= 6 * s6[10]  # 1..n blocks per allocation
 
 
 @EVALUATORS
