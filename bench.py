@@ -544,6 +544,11 @@ def main():
     if pipe.exhaustive and not args.f3 and not args.per_candidate and not args.no_direct:
         roof["direct"] = time_direct(G, pipe, stream, flush, args, peak, direct_stats, world)
 
+    tables = None
+    if (pipe.exhaustive and not args.f3 and not args.per_candidate and pipe.n <= 8
+            and pipe.M <= 32 and pipe.workspace is not None):
+        tables = time_tables(G, pipe, stream, exh_mode, exh_flags)
+
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags)
@@ -573,6 +578,8 @@ def main():
         "gpu_launches": launches_per_step(pipe, args) * args.steps,
         "clocks": clk,
     }
+    if tables:
+        line["tables"] = tables
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -622,16 +629,43 @@ def time_direct(G, pipe, stream, flush, args, peak, direct_stats, world):
 
 def launches_per_step(pipe, args=None):
     """Our kernels per step: per setting gp_generate 1 + gp_allocate x V + ratio 1;
-    + EXHAUSTIVE: per-candidate (init, main, finalize) or bit-sliced (init, RGS table,
-    memo, main, finalize, + 3 hash-prefix scan kernels when the hash is computed, + 4
-    lane-order kernels)."""
+    + EXHAUSTIVE: per-candidate (init, main, finalize) or bit-sliced (init, memo, main,
+    finalize, + 3 lane-order kernels: tile histogram, scan, tile scatter).  The bit-sliced
+    evaluator's input-independent tables (RGS labels, hash prefix, run-prefix and corner
+    tables) are built by the first call on the workspace, before the timed steps
+    (gp_exhaustive_opts.tables_key; their build time is reported as `tables`)."""
     n = len(pipe.gens) * (2 + len(pipe.variants))
     if not pipe.exhaustive:
         return n
     if (args is not None and (args.f3 or args.per_candidate)) or pipe.n > 8 or pipe.M > 32:
         return n + 3
-    # + 4 lane-order kernels (load level, histogram, scan, scatter) when n_sets > 32
-    return n + 5 + (3 if pipe.n_cand < (1 << 24) else 0) + (4 if pipe.ts.n_sets > 32 else 0)
+    return n + 4 + (3 if pipe.ts.n_sets > 32 else 0)
+
+
+def time_tables(G, pipe, stream, exh_mode, exh_flags):
+    """The bit-sliced evaluator's table build (functions of n, M only; built once per
+    workspace): one exhaustive call that rebuilds them minus one that reuses them, CUDA
+    events on the launching stream (median of 3 pairs)."""
+    import torch
+
+    def call_ms(rebuild):
+        if rebuild:
+            pipe.tables_key.value = 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        G.gp_sched_ratio(pipe.ts, exh_mode, None, per_set=pipe.per_set, work_counter=pipe.work,
+                         stream=stream, flags=exh_flags, workspace=pipe.workspace,
+                         tables_key=pipe.tables_key, rank_lo=pipe.rank_lo, rank_hi=pipe.rank_hi)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    call_ms(False)
+    d = sorted(call_ms(True) - call_ms(False) for _ in range(3))
+    return {"build_ms": d[1], "built": "once per workspace, before the timed steps "
+            "(gp_exhaustive_opts.tables_key): RGS labels, verdict-hash prefix P, run-prefix R, "
+            "corner tables CT and FCT -- functions of (n, M) only, like an FFT plan's twiddles",
+            "workspace_bytes": int(pipe.workspace.numel())}
 
 
 def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):

@@ -25,7 +25,8 @@
  *  - Configuration: there are no environment-variable switches.  Behaviour is
  *    selected by arguments only (flags below); performance A/B variants are
  *    compile-time macros of the build (-DGP_ALLOC_TAB_KB, -DGP_ALLOC_MIN_G,
- *    -DGP_BP_MINB, -DGP_MEMO_MINB, -DGP_SP_LEVELS; defaults are the product).
+ *    -DGP_BP_MINB, -DGP_MEMO_MINB, -DGP_BP_CORNER, -DGP_BP_FULLCORNER; defaults are
+ *    the product).
  *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
  *    default stream).  Every device call only ENQUEUES work on that stream
  *    and returns; none synchronises.  Outputs are valid once the stream has
@@ -325,8 +326,11 @@ typedef struct {
                                  test hooks (same outputs, other code paths):
                                  GP_EX_FORCE_RANGES: the bit-sliced evaluator walks every
                                  verdict word range by range (no contiguous fast path);
-                                 GP_EX_NATURAL_ORDER: the bit-sliced evaluator's lanes take
-                                 sets in index order (no per-subset lane order);
+                                 GP_EX_NATURAL_ORDER: accepted, no effect (the bit-sliced
+                                 evaluator's lanes always take sets in index order now);
+                                 GP_EX_NO_FULL_CORNER: the bit-sliced evaluator resolves no
+                                 (set, allocation) pair as one full corner (its corner-table
+                                 blocks, closed-form sweeps and run walks do all the work);
                                  GP_EX_GENERIC: the per-candidate evaluator with runtime
                                  block structure (no shape specialisation), implies
                                  GP_EX_PER_CANDIDATE; unknown bits -> GP_EINVAL              */
@@ -344,6 +348,16 @@ typedef struct {
                                  so per_set, verdict bits and windows keep their meaning.  No
                                  admissible size in 1..M -> GP_EINVAL.  THRESHOLD: the count and
                                  hash walk the schedulable runs (cost grows with n_sched)      */
+  uint64_t *tables_key;       /* HOST, caller-owned, or NULL (bit-sliced evaluator with a caller
+                                 workspace only).  The workspace also holds tables that depend
+                                 on (n_tasks, M) only -- RGS labels, the verdict-hash prefix
+                                 tables and the corner tables -- like an FFT plan's twiddles.
+                                 The call rebuilds them unless *tables_key equals the key of
+                                 this call's layout (shapes, flags, workspace address and size),
+                                 then stores that key (0 on error).  The caller zeroes it
+                                 whenever the workspace is written by anything else, and orders
+                                 a call on another stream after the call that built them.
+                                 NULL: rebuilt every call                                       */
 } gp_exhaustive_opts;
 #define GP_EX_NO_HASH 1u
 #define GP_EX_PER_CANDIDATE 2u
@@ -351,13 +365,15 @@ typedef struct {
 #define GP_EX_FORCE_RANGES 8u
 #define GP_EX_NATURAL_ORDER 16u
 #define GP_EX_GENERIC 32u
+#define GP_EX_NO_FULL_CORNER 64u
 
 /* HOST ONLY (no CUDA call): device workspace bytes gp_sched_ratio(mode, flags) needs
  * for n_sets sets of n_tasks tasks on M SMs in n_groups groups -- the bit-sliced
- * evaluator's memo words (n_sets * 2^n * 4 B), RGS labels, per-subset lane order and
- * verdict-hash prefix table (8 B per rank when N_c < 2^24 and the hash is wanted);
- * 0 for the per-candidate and threshold evaluators and for FROM_VERDICTS.  C3 with
- * 10^5 sets: about 58 MB.  Errors: GP_EINVAL (shapes outside the EXHAUSTIVE limits). */
+ * evaluator's memo words (n_sets * 2^n * 4 B) and its input-independent tables (RGS
+ * labels; when N_c < 2^24 and the hash is wanted: the verdict-hash prefix table and the
+ * full corner table, 8 B per rank each, the corner table of the last three parts, 8 B
+ * per rank, and the run-prefix table, 8 B per (run, size)); 0 for the per-candidate and
+ * threshold evaluators and for FROM_VERDICTS.  C3 with 10^5 sets: about 66 MB.  Errors: GP_EINVAL (shapes outside the EXHAUSTIVE limits). */
 gp_status gp_exhaustive_workspace_size(int32_t n_sets, int32_t n_tasks, int32_t M,
                                        int32_t n_groups, gp_ratio_mode mode, uint32_t flags,
                                        uint64_t *bytes /*host*/);

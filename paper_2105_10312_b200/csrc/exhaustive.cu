@@ -779,7 +779,7 @@ static gp_status launch_shaped(ExhArgs &a, size_t smem, cudaStream_t st) {
 }  // namespace gp
 
 gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a, void *ws, uint64_t ws_bytes,
-                                  cudaStream_t st);
+                                  uint64_t *tables_key, cudaStream_t st);
 size_t gp_exhaustive_bp_workspace(const gp::RankLayout &L, int n, int M, int32_t n_sets,
                                   int32_t n_groups, uint32_t flags);
 
@@ -829,7 +829,8 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   a.counts = counts; a.slot0 = slot0; a.n_slots = n_slots; a.setting = setting;
   a.stats = ex->stats; a.work_counter = ex->work_counter;
   if (ex->flags & ~(uint32_t)(GP_EX_NO_HASH | GP_EX_PER_CANDIDATE | GP_EX_STATS_EXT |
-                              GP_EX_FORCE_RANGES | GP_EX_NATURAL_ORDER | GP_EX_GENERIC))
+                              GP_EX_FORCE_RANGES | GP_EX_NATURAL_ORDER | GP_EX_GENERIC |
+                              GP_EX_NO_FULL_CORNER))
     return gp_fail(GP_EINVAL, "EXHAUSTIVE: unknown flags 0x%x", ex->flags);
   a.flags = ex->flags;
   s = load_size_mask(ex->size_mask, M, a.adm, "EXHAUSTIVE");
@@ -856,7 +857,7 @@ gp_status gp_exhaustive_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_s
   // default for n <= 8, M <= 32: bit-sliced verdicts over memoised block
   // verdicts (exhaustive_bp.cu); otherwise, or on request, per candidate
   if (n <= 8 && M <= 32 && !(ex->flags & (GP_EX_PER_CANDIDATE | GP_EX_GENERIC))) {
-    gp_status r = gp_exhaustive_bp_launch(a, ex->workspace, ex->workspace_bytes, st);
+    gp_status r = gp_exhaustive_bp_launch(a, ex->workspace, ex->workspace_bytes, ex->tables_key, st);
     if (r != GP_OK) return r;
     k_exh_finalize<<<(unsigned)(g1 > 4096 ? 4096 : g1), 256, 0, st>>>(a);
     return gp_cuda_check("gp_sched_ratio(EXHAUSTIVE) finalize");

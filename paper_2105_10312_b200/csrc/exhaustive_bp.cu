@@ -93,17 +93,6 @@ struct MemoTask {  // one task of the set: one 16-byte shared-memory load per us
   float invD;       // 1 / D (the density shortcut of memo_test)
 };
 
-#ifndef GP_SP_LEVELS
-#define GP_SP_LEVELS 4
-#endif
-constexpr int kSpLevels = GP_SP_LEVELS;  // load levels inside a (group, first size) key of the lane order
-
-// the set's load level: its number of schedulable (subset, size) pairs, quantised
-GP_DEV uint8_t sp_level(uint32_t npass, int nsub, int M) {
-  const uint32_t cap = (uint32_t)(nsub - 1) * (uint32_t)M + 1u;
-  return (uint8_t)(npass * (uint32_t)kSpLevels / cap);
-}
-
 struct MemoWarp {
   uint32_t vs[1 << kBpMaxN];          // verdict word per subset
   int32_t wt[kBpMaxN * 2 * kBpMaxM];  // W_i(m, x) at [(i*2 + x)*32 + m-1], x = 1: conflict
@@ -289,16 +278,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
       }
     }
     __syncwarp();
-    uint32_t npass = 0;  // schedulable (subset, size) pairs: the set's load level (lane order)
-    for (int S2 = lane; S2 < nsub; S2 += 32) {
-      const uint32_t v = w.vs[S2];
-      V[S2] = S2 == 0 ? 1u : v;
-      npass += S2 == 0 ? 0u : (uint32_t)__popc(v & Mmask);
-    }
-    if (a.sp_lvl) {
-      npass = __reduce_add_sync(GP_FULL, npass);
-      if (lane == 0) a.sp_lvl[set] = sp_level(npass, nsub, M);
-    }
+    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
     __syncwarp();
   }
   if constexpr (kStats) {  // (the timed instantiation carries no counters)
@@ -626,95 +606,6 @@ __global__ void __launch_bounds__(256) k_fct_pass(const ExhArgs a, uint64_t *F, 
   }
 }
 
-// ---- per-subset lane order: for every subset S, the sets ordered by (utilisation group,
-// first size at which S passes): sets of one group have similar loads in every subset,
-// and within it the lanes of a warp share the upper end of their live run ranges.  A
-// counting sort per subset (global histogram, one scan per subset, a scatter); the order
-// inside a key is arbitrary (atomics), which no output depends on (per-set results are
-// sums and minima).
-constexpr int kThrBins = kBpMaxM + 1;
-
-GP_DEV int first_pass(uint32_t v) { return v ? __ffs(v) - 1 : kBpMaxM; }
-
-// key = (group, first passing size of S, load level of the set); the load level (the
-// set's number of schedulable (subset, size) pairs, quantised: sp_level) is written by the
-// memo pass
-GP_DEV int sp_key(const ExhArgs &a, uint32_t V0, uint32_t VS, int g, uint8_t lvl) {
-  if (V0 == 0u) return a.n_groups * kThrBins * kSpLevels;  // contract violated: last
-  return ((g >= 0 && g < a.n_groups ? g : 0) * kThrBins + first_pass(VS)) * kSpLevels + lvl;
-}
-
-// Only the subsets that can be an allocation's LAST block need an order: the last block
-// carries the highest RGS label, so it holds task 0 (label 0) only when k = 1, i.e. when
-// it is the whole set.  The other subsets holding task 0 are skipped (half of them).
-GP_DEV bool sp_used(int S, int nsub) { return (S & 1) == 0 || S == nsub - 1; }
-
-// One CTA per tile of 32 consecutive sets: the tile's verdict words are staged in shared
-// memory by coalesced loads (a set's words are contiguous), then warp w keys subsets
-// S = w+1, w+9, ... with lane = set, so the 32 sets of a warp mostly share a key (same
-// group, similar first passing size) and each warp adds once per distinct key
-// (warp-aggregated atomics via __match_any_sync).  kScatter = false: histogram;
-// true: scatter into the scanned offsets.
-constexpr int kSpTile = 32;
-template <bool kScatter>
-__global__ void __launch_bounds__(256) k_sp_tile(const ExhArgs a, const uint32_t *memo, int nsub,
-                                                 int nkeys, uint32_t *hist, uint32_t *sperm) {
-  __shared__ uint32_t tv[kSpTile * ((1 << kBpMaxN) + 1)];  // row stride nsub + 1: no bank conflicts
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int rs = nsub + 1;
-  const int64_t n_tiles = ((int64_t)a.n_sets + kSpTile - 1) / kSpTile;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t s0 = tile * kSpTile;
-    const int nt = (int)min((int64_t)kSpTile, (int64_t)a.n_sets - s0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nt * nsub; i += blockDim.x) {
-      const int r = i / nsub;
-      tv[r * rs + (i - r * nsub)] = memo[s0 * nsub + i];
-    }
-    __syncthreads();
-    const int64_t set = s0 + lane;
-    const bool has = lane < nt;
-    const int g = has ? a.group[set] : 0;
-    const uint8_t lvl = has ? a.sp_lvl[set] : 0;
-    const uint32_t V0 = has ? tv[lane * rs] : 0u;
-    for (int S = wid + 1; S < nsub; S += 8) {
-      if (!sp_used(S, nsub)) continue;  // warp-uniform
-      const uint32_t slot =
-          has ? (uint32_t)S * (uint32_t)nkeys + (uint32_t)sp_key(a, V0, tv[lane * rs + S], g, lvl) : ~0u;
-      const uint32_t peers = __match_any_sync(GP_FULL, slot);
-      const int leader = __ffs(peers) - 1;
-      if constexpr (!kScatter) {
-        if (has && lane == leader) atomicAdd(&hist[slot], (uint32_t)__popc(peers));
-      } else {
-        uint32_t base = 0;
-        if (has && lane == leader) base = atomicAdd(&hist[slot], (uint32_t)__popc(peers));
-        base = __shfl_sync(GP_FULL, base, leader);
-        if (has) sperm[(size_t)S * a.n_sets + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)set;
-      }
-    }
-  }
-}
-
-// exclusive scan per subset, in place: one warp per subset (block = 32 threads, grid = nsub - 1)
-__global__ void __launch_bounds__(32) k_sp_scan(uint32_t *hist, int nkeys) {
-  uint32_t *h = hist + (size_t)(blockIdx.x + 1) * nkeys;
-  const int lane = threadIdx.x, per = (nkeys + 31) / 32, b0 = lane * per;
-  uint32_t loc = 0;
-  for (int b = b0; b < b0 + per && b < nkeys; ++b) loc += h[b];
-  uint32_t incl = loc;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t u = __shfl_up_sync(GP_FULL, incl, o);
-    if (lane >= o) incl += u;
-  }
-  uint32_t run = incl - loc;
-  for (int b = b0; b < b0 + per && b < nkeys; ++b) {
-    const uint32_t c = h[b];
-    h[b] = run;
-    run += c;
-  }
-}
-
 // ---- main pass: bit-sliced verdicts over runs, lane = task set -------------------
 // item = (group of 32 consecutive sets, allocation pi), items in k-DESCENDING
 // groups (the largest allocations first, small ones fill the tail).  The run
@@ -785,16 +676,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     const uint32_t p = (uint32_t)(local - (uint64_t)grp * npi);
     const uint32_t labels = rgs[a.rgs_base[k] + p];
     const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
-    if (a.sperm) {
-      // lane slots of this item follow the permutation of the sets by the first size at
-      // which pi's LAST block passes, so a warp's lanes share the upper end of their
-      // live run ranges; per-set results are flushed per item
-      flush();
-      const uint32_t S_last = __ballot_sync(GP_FULL, myb == k - 1);
-      const int64_t slot = grp * 32 + lane;
-      set = slot < a.n_sets ? (int64_t)a.sperm[(size_t)S_last * a.n_sets + slot] : slot;
-      lane_ok = slot < a.n_sets && memo[set * nsub] != 0;  // input contract (word 0)
-    } else if (grp != cur_g) {
+    if (grp != cur_g) {
       flush();
       cur_g = grp;
       set = grp * 32 + lane;
@@ -842,7 +724,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     if (__all_sync(GP_FULL, dead)) continue;
 #if GP_BP_FULLCORNER
     if constexpr (!kWin && !kBits && kHash != 2) {
-      if ((kHash == 0 || a.FCT) && !a.force_ranges) {
+      if ((kHash == 0 || a.FCT) && !a.force_ranges && !(a.flags & GP_EX_NO_FULL_CORNER)) {
         // full corner: when every block's word is one bit range from its first passing size
         // lo_j + 1 through the largest size a part can take (M - k + 1) -- checked here per
         // (set, allocation) -- the set's schedulable candidates of pi are the corner with apex
@@ -1299,11 +1181,10 @@ namespace gp {
 // stream-ordered temporary): memo words [n_sets][2^n], RGS labels, the per-subset
 // lane order (slots, histograms, load levels) and the hash prefix table.
 struct BpLayout {
-  size_t memo_words, sp_words, sp_total, words32, bytes, r_off, ct_off, fct_off;
+  size_t memo_words, words32, bytes, r_off, ct_off, fct_off;
   uint64_t n_rgs, n_ranks, total_runs, r_stride;
   uint32_t nb, r_nb;
-  int sp_keys;
-  bool use_sp, use_P, use_R, use_CT, use_FCT;
+  bool use_P, use_R, use_CT, use_FCT;
 };
 
 static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_groups,
@@ -1316,12 +1197,7 @@ static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_
   b.use_P = !(flags & GP_EX_NO_HASH) && L.total < kMaxHashTable;
   b.n_ranks = b.use_P ? L.total : 0;
   b.nb = (uint32_t)((b.n_ranks + kScanBlock - 1) / kScanBlock);
-  // per-subset lane order (GP_EX_NATURAL_ORDER: off): nsub x n_sets slots + histograms
-  b.sp_words = (size_t)(1 << n) * n_sets;
-  b.use_sp = !(flags & GP_EX_NATURAL_ORDER) && n_sets > 32 && b.sp_words * 4 <= ((size_t)256 << 20);
-  b.sp_keys = (n_groups > 0 ? n_groups : 1) * kThrBins * kSpLevels + 1;
-  b.sp_total = b.use_sp ? b.sp_words + (size_t)(1 << n) * b.sp_keys + ((size_t)n_sets + 3) / 4 : 0;
-  b.words32 = (b.memo_words + b.n_rgs + b.sp_total + 1) & ~(size_t)1;  // 8-byte alignment after
+  b.words32 = (b.memo_words + b.n_rgs + 1) & ~(size_t)1;  // 8-byte alignment after
   // P: n_ranks + 1 prefix sums, then kPpad entries of slack (the main pass may read up to 31
   // entries past a run's end in lanes whose verdict word is zero there; never summed)
   b.bytes = b.words32 * 4 + (b.use_P ? (b.n_ranks + 1 + kPpad + b.nb) * 8 : 0);
@@ -1363,7 +1239,7 @@ size_t gp_exhaustive_bp_workspace(const gp::RankLayout &L, int n, int M, int32_t
 // `ws_bytes`: the caller's workspace (gp_exhaustive_opts), or NULL for a
 // stream-ordered temporary allocation released on `st`.
 gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t ws_bytes,
-                                  cudaStream_t st) {
+                                  uint64_t *tables_key, cudaStream_t st) {
   using namespace gp;
   const int n = a0.n, M = a0.M;
   if (n > kBpMaxN || M > kBpMaxM) return gp_fail(GP_EINVAL, "EXHAUSTIVE(bp): n <= 8, M <= 32");
@@ -1387,11 +1263,10 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   }
   a.items_per_set = n_rgs;
   a.total_items = items;
-  const size_t memo_words = b.memo_words, sp_words = b.sp_words;
-  const bool use_P = b.use_P, use_sp = b.use_sp;
+  const size_t memo_words = b.memo_words;
+  const bool use_P = b.use_P;
   const uint64_t n_ranks = b.n_ranks;
   const uint32_t nb = b.nb;
-  const int sp_keys = b.sp_keys;
   uint32_t *ws = nullptr;
   if (ws_user) {
     if (ws_bytes < b.bytes)
@@ -1403,10 +1278,22 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   } else if (cudaMallocAsync(reinterpret_cast<void **>(&ws), b.bytes, st) != cudaSuccess) {
     return gp_cuda_check("EXHAUSTIVE(bp): workspace allocation");
   }
+  // input-independent tables (RGS labels, hash prefix P, run-prefix R, corner tables CT and
+  // FCT: functions of (n, M) only) -- rebuilt unless the caller's key says this workspace
+  // already holds them for this exact layout (gpart.h: gp_exhaustive_opts.tables_key)
+  uint64_t key = 0xcbf29ce484222325ull;
+  {
+    const uint64_t parts[8] = {(uint64_t)n, (uint64_t)M, (uint64_t)a.n_sets, (uint64_t)a.n_groups,
+                               (uint64_t)(a.flags & GP_EX_NO_HASH),
+                               (uint64_t)reinterpret_cast<uintptr_t>(ws_user), ws_bytes,
+                               (uint64_t)b.bytes};
+    for (uint64_t v : parts) key = (key ^ v) * 0x100000001b3ull;
+    key |= 1ull;  // never 0 (0 = no tables)
+  }
+  const bool build_tables = !(ws_user && tables_key && *tables_key == key);
   uint32_t *memo = ws, *rgs = ws + memo_words;
-  uint32_t *sperm = use_sp ? rgs + n_rgs : nullptr, *sphist = use_sp ? sperm + sp_words : nullptr;
   uint64_t *P = use_P ? reinterpret_cast<uint64_t *>(ws + b.words32) : nullptr;
-  if (use_P) {
+  if (use_P && build_tables) {
     uint64_t *btot = P + n_ranks + 1 + kPpad;
     k_hash_scan_local<<<nb, kScanBlock, 0, st>>>(P, n_ranks, btot);
     k_hash_scan_blocks<<<1, kScanBlock, 0, st>>>(btot, nb);
@@ -1416,7 +1303,7 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = ((enum_table_words(M, n) + 3) & ~(size_t)3) * 4;
-  k_exh_rgs_table<<<1, 256, smem, st>>>(a, rgs);
+  if (build_tables) k_exh_rgs_table<<<1, 256, smem, st>>>(a, rgs);
   // runs per allocation: C(M-1, k-1) prefixes; global run index of the first run of k
   uint64_t runs = 0;
   for (int k = 1; k <= a.L.kmax; ++k) {
@@ -1434,11 +1321,13 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     uint64_t *F = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.fct_off);
     int64_t gi = ((int64_t)a.L.total + 255) / 256;
     if (gi > (int64_t)sms * 16) gi = (int64_t)sms * 16;
-    k_fct_init<<<(unsigned)(gi > 0 ? gi : 1), 256, 0, st>>>(F, a.L.total);
-    for (int j = 1; j <= a.L.kmax; ++j) {
-      int64_t gj = ((int64_t)(runs - a.run_base[j]) + 255) / 256;
-      if (gj > (int64_t)sms * 16) gj = (int64_t)sms * 16;
-      k_fct_pass<<<(unsigned)(gj > 0 ? gj : 1), 256, 0, st>>>(a, F, j);
+    if (build_tables) {
+      k_fct_init<<<(unsigned)(gi > 0 ? gi : 1), 256, 0, st>>>(F, a.L.total);
+      for (int j = 1; j <= a.L.kmax; ++j) {
+        int64_t gj = ((int64_t)(runs - a.run_base[j]) + 255) / 256;
+        if (gj > (int64_t)sms * 16) gj = (int64_t)sms * 16;
+        k_fct_pass<<<(unsigned)(gj > 0 ? gj : 1), 256, 0, st>>>(a, F, j);
+      }
     }
     a.FCT = F;
   }
@@ -1448,21 +1337,21 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     a.r_stride = b.r_stride;
     int64_t gk = ((int64_t)b.total_runs + 255) / 256;
     if (gk > (int64_t)sms * 16) gk = (int64_t)sms * 16;
-    k_run_contrib<<<(unsigned)gk, 256, 0, st>>>(a, P, R, b.total_runs);
-    k_rows_scan_local<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
-    k_rows_scan_blocks<<<M, kScanBlock, 0, st>>>(rbt, b.r_nb);
-    k_rows_scan_add<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
+    if (build_tables) {
+      k_run_contrib<<<(unsigned)gk, 256, 0, st>>>(a, P, R, b.total_runs);
+      k_rows_scan_local<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
+      k_rows_scan_blocks<<<M, kScanBlock, 0, st>>>(rbt, b.r_nb);
+      k_rows_scan_add<<<dim3(b.r_nb, M), kScanBlock, 0, st>>>(R, b.r_stride, b.total_runs, rbt, b.r_nb);
+    }
     a.R = R;
     if (b.use_CT) {
       uint64_t *CT = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(ws) + b.ct_off);
       int64_t gc = ((int64_t)(a.L.total - a.L.k_base[3]) + 255) / 256;
       if (gc > (int64_t)sms * 16) gc = (int64_t)sms * 16;
-      k_corner_table<<<(unsigned)(gc > 0 ? gc : 1), 256, 0, st>>>(a, R, CT);
+      if (build_tables) k_corner_table<<<(unsigned)(gc > 0 ? gc : 1), 256, 0, st>>>(a, R, CT);
       a.CT = CT;
     }
   }
-  // the lane order's per-set load levels (after its histograms), written by the memo pass
-  a.sp_lvl = use_sp ? reinterpret_cast<uint8_t *>(sphist + (size_t)(1 << n) * sp_keys) : nullptr;
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
@@ -1477,17 +1366,6 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
       else k_exh_memo<8, false><<<g, 256, 0, st>>>(a, memo);
     }
   }
-  a.sperm = nullptr;
-  if (use_sp) {
-    const int nsub = 1 << n;
-    cudaMemsetAsync(sphist, 0, (size_t)nsub * sp_keys * 4, st);
-    int64_t gk = ((int64_t)a.n_sets + kSpTile - 1) / kSpTile;
-    if (gk > (int64_t)sms * 8) gk = (int64_t)sms * 8;
-    k_sp_tile<false><<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, nullptr);
-    k_sp_scan<<<nsub - 1, 32, 0, st>>>(sphist, sp_keys);
-    k_sp_tile<true><<<(unsigned)gk, 256, 0, st>>>(a, memo, nsub, sp_keys, sphist, sperm);
-    a.sperm = sperm;
-  }
   gp_status r = gp_cuda_check("EXHAUSTIVE(bp) memo kernel");
   if (r == GP_OK) {
     int occ = 1;
@@ -1501,6 +1379,7 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
     else launch_bp_h<false>((unsigned)grid, a, memo, rgs, P, st);
     r = gp_cuda_check("EXHAUSTIVE(bp) main kernel");
   }
+  if (ws_user && tables_key) *tables_key = r == GP_OK ? key : 0ull;
   if (!ws_user) cudaFreeAsync(ws, st);
   return r;
 }

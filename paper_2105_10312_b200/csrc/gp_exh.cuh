@@ -26,8 +26,6 @@ struct ExhArgs {
   unsigned long long *work_counter;
   uint32_t flags;  // gp_exhaustive_opts.flags
   int32_t force_ranges;  // bit-sliced evaluator: walk okb range by range (env GP_EXH_RANGES, tests)
-  const uint32_t *sperm;  // bit-sliced evaluator: [subset][slot] -> set, sets by that subset's first passing size
-  uint8_t *sp_lvl;        // bit-sliced evaluator: per-set load level of the lane order (written by the memo pass)
   const uint64_t *R;      // bit-sliced evaluator: run-prefix hash table [a0][run + 1] (or null)
   uint64_t r_stride;      // entries per row of R (total runs + 1)
   const uint64_t *CT;     // bit-sliced evaluator: corner table [rank] (k >= 3; or null)

@@ -26,7 +26,8 @@ GP_EX_PER_CANDIDATE = 2  # force the per-candidate EXHAUSTIVE evaluator
 GP_EX_STATS_EXT = 4  # stats has 12 slots: + runs walked / live, closed-form sweeps / their runs,
                      # corner-table blocks / their sweeps, full-corner allocations / their blocks
 GP_EX_FORCE_RANGES = 8  # test hook: bit-sliced evaluator walks verdict words range by range
-GP_EX_NATURAL_ORDER = 16  # test hook: bit-sliced evaluator without the per-subset lane order
+GP_EX_NATURAL_ORDER = 16  # accepted, no effect (index-order lanes are the only order now)
+GP_EX_NO_FULL_CORNER = 64  # test hook: bit-sliced evaluator without the full-corner closed form
 GP_EX_GENERIC = 32  # test hook: per-candidate evaluator without shape specialisation
 UINT64_MAX = 2**64 - 1
 
@@ -66,7 +67,7 @@ class _ExOptsC(C.Structure):
                 ("verdict_bits", C.c_void_p), ("words_per_set", C.c_int64),
                 ("work_counter", C.c_void_p), ("stats", C.c_void_p), ("flags", C.c_uint32),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
-                ("size_mask", C.c_void_p)]
+                ("size_mask", C.c_void_p), ("tables_key", C.c_void_p)]
 
 
 _P = C.c_void_p
@@ -300,14 +301,16 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
 def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=None, setting=0,
                    per_set=None, verdict_bits=None, words_per_set=0, work_counter=None,
                    stats=None, rank_lo=0, rank_hi=UINT64_MAX, stream=None, flags=0,
-                   workspace=None, sizes=None):
+                   workspace=None, sizes=None, tables_key=None):
     """FROM_VERDICTS: verdicts uint8 [n_rows][n_sets]; EXHAUSTIVE: per_set int64 [n_sets][4]
     (+ work_counter int64 [>=1], optional verdict_bits int32/uint32 [n_sets][words], stats
     int64 [4], or [12] for the bit-sliced evaluator's run counters; optional workspace: a
     uint8 device tensor of >= gp_exhaustive_workspace_size() bytes, else the call makes a
     stream-ordered temporary).  counts int64 [n_settings][n_groups][n_slots][3] is
     accumulated.  ``sizes``: admissible partition sizes for EXHAUSTIVE / THRESHOLD (f4,
-    reading B-9; None = every size)."""
+    reading B-9; None = every size).  ``tables_key``: a ctypes.c_uint64 kept with the
+    workspace (gpart.h gp_exhaustive_opts.tables_key: the workspace's input-independent
+    tables are built once and reused while the key matches)."""
     s = ts.struct()
     if stats is not None and stats.numel() >= 12 and mode == GP_EXHAUSTIVE:
         flags |= GP_EX_STATS_EXT
@@ -320,6 +323,8 @@ def gp_sched_ratio(ts: TaskSets, mode, counts, verdicts=None, slot0=0, n_slots=N
         if mask is not None:
             ex.size_mask = C.cast(mask, C.c_void_p)
             ex._keep = mask
+        if tables_key is not None:
+            ex.tables_key = C.cast(C.pointer(tables_key), C.c_void_p)
         exp = C.byref(ex)
         vp = None
     else:

@@ -24,7 +24,10 @@ mode's counts (and, for "ranks", per-set outputs) equal one process's.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
+
 import torch
 
 import gp_workloads as W
@@ -98,6 +101,9 @@ class Pipeline:
             self.stats = torch.zeros(12, dtype=torch.int64, device=device) if stats else None
             # caller-owned evaluator workspace (gpart.h: no hidden persistent allocations)
             self.workspace = G.exhaustive_workspace(self.ts, device=device)
+            # its input-independent tables (functions of n, M only) are built by the first
+            # call and reused while this key matches (gpart.h gp_exhaustive_opts.tables_key)
+            self.tables_key = ctypes.c_uint64(0)
         else:
             self.n_cand = 0
             self.workspace = None
@@ -142,7 +148,7 @@ class Pipeline:
                                  work_counter=self.work,
                                  stats=self.stats if stats else None, stream=stream,
                                  flags=flags, workspace=self.workspace,
-                                 rank_lo=self.rank_lo,
+                                 tables_key=self.tables_key, rank_lo=self.rank_lo,
                                  rank_hi=G.UINT64_MAX if not window else self.rank_hi)
                 hook("end")
                 if window:

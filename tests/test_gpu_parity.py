@@ -143,7 +143,10 @@ def test_wcet_batch(G):
 
 
 # ------------------------------------------------------------------ A2-A4 fused
-EVALUATORS = pytest.mark.parametrize("ev", [0, 2], ids=["bitsliced", "per_candidate"])
+# the bit-sliced evaluator (default), its path without the full-corner closed form (test
+# hook: corner-table blocks, closed sweeps, run walks), the per-candidate evaluator
+EVALUATORS = pytest.mark.parametrize("ev", [0, 64, 2],
+                                     ids=["bitsliced", "bitsliced_nofc", "per_candidate"])
 
 
 def run_exhaustive(G, ts, bits=False, lo=0, hi=None, counts=None, slot0=0, n_slots=1, flags=0,
@@ -230,9 +233,12 @@ def test_exhaustive_c3_parity_config_sampled(G, ev):
     assert st[0] == 10 * 1000 * 694755
     per_timed, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False)  # bench's timed call
     assert (per_timed == per).all()
-    if ev == 0:  # the bit-sliced evaluator without its per-subset lane order
-        per_id, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NATURAL_ORDER, with_stats=False)
-        assert (per_id == per).all()
+    if ev == 0:  # the bit-sliced evaluator without its full-corner closed form (corner-table
+        # blocks, closed sweeps and run walks), and with every word walked range by range
+        per_nc, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NO_FULL_CORNER, with_stats=False)
+        assert (per_nc == per).all()
+        per_fr, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_FORCE_RANGES, with_stats=False)
+        assert (per_fr == per).all()
         # and with a caller-owned workspace (the pipeline's call) instead of the temporary
         per_ws, _, _ = run_exhaustive(G, ts, with_stats=False, workspace=True)
         assert (per_ws == per).all()
@@ -333,7 +339,7 @@ def test_exhaustive_no_hash_and_flag_validation(G):
     nh, _, _ = run_exhaustive(G, ts, flags=G.GP_EX_NO_HASH)
     assert (nh[:, :3] == full[:, :3]).all() and (nh[:, 3] == 0).all()
     with pytest.raises(G.GpError):
-        run_exhaustive(G, ts, flags=64)
+        run_exhaustive(G, ts, flags=128)
 
 
 def test_exhaustive_workspace_contract(G):
@@ -360,6 +366,51 @@ def test_exhaustive_workspace_contract(G):
     with pytest.raises(G.GpError):
         G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=per, work_counter=work,
                          workspace=big[8:])
+
+
+def test_exhaustive_tables_key(G):
+    """gpart.h gp_exhaustive_opts.tables_key: the workspace's input-independent tables are
+    built by the first call and reused while the key matches -- across different task
+    sets of the same shape (outputs equal the oracle's each time); a call with another
+    shape on the same key object and workspace rebuilds them; a zeroed key rebuilds."""
+    import ctypes
+    gen = W.WORKLOADS["c2"]["gen"](R=10000)
+    tss = []
+    for rep0 in (0, 40):
+        ts = G.TaskSets(10 * 20, 6, 8, 10)
+        G.gp_generate(gen, W.SEED, rep0, 20, ts)
+        tss.append(ts)
+    ws = G.exhaustive_workspace(tss[0])
+    key = ctypes.c_uint64(0)
+    per = torch.empty((tss[0].n_sets, 4), dtype=torch.int64, device="cuda")
+    work = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def call(ts, p, w):
+        G.gp_sched_ratio(ts, G.GP_EXHAUSTIVE, None, per_set=p, work_counter=work,
+                         workspace=w, tables_key=key)
+        torch.cuda.synchronize()
+        return p.cpu().numpy()
+
+    refs = [oracle.exhaustive(to_oracle(ts)) for ts in tss]
+    assert (call(tss[0], per, ws) == refs[0]).all()
+    k1 = key.value
+    assert k1 != 0
+    for i in (1, 0, 1):  # reused tables, different inputs
+        assert (call(tss[i], per, ws) == refs[i]).all()
+        assert key.value == k1
+    # another shape (C3: n = 6, M = 20) with the same key object: new layout -> rebuilt
+    gen3 = W.WORKLOADS["c3"]["gen"](R=1000)
+    ts3 = G.TaskSets(10 * 4, 6, 20, 10)
+    G.gp_generate(gen3, W.SEED, 0, 4, ts3)
+    ws3 = G.exhaustive_workspace(ts3)
+    per3 = torch.empty((ts3.n_sets, 4), dtype=torch.int64, device="cuda")
+    ref3 = oracle.exhaustive(to_oracle(ts3))
+    assert (call(ts3, per3, ws3) == ref3).all()
+    assert key.value not in (0, k1)
+    # zeroed key: rebuilt into the first workspace, outputs unchanged
+    key.value = 0
+    assert (call(tss[1], per, ws) == refs[1]).all()
+    assert key.value == k1
 
 
 @pytest.mark.parametrize("seed,n,M", [(21, 3, 5), (22, 5, 7), (23, 6, 9)])
@@ -927,7 +978,8 @@ def test_exhaustive_f4_masks_c2(G, kind):
     host = to_oracle(ts)
     sizes = _mask_sizes(kind, 8)
     ref, rbits = oracle.exhaustive(host, bits=True, sizes=sizes)
-    for ev in (0, G.GP_EX_PER_CANDIDATE, G.GP_EX_GENERIC, G.GP_EX_FORCE_RANGES):
+    for ev in (0, G.GP_EX_PER_CANDIDATE, G.GP_EX_GENERIC, G.GP_EX_FORCE_RANGES,
+               G.GP_EX_NO_FULL_CORNER):
         per, vb, _ = run_exhaustive(G, ts, bits=True, flags=ev, sizes=sizes)
         assert (per == ref).all() and (vb == rbits).all(), ev
         per2, _, _ = run_exhaustive(G, ts, flags=ev, with_stats=False, sizes=sizes)
