@@ -232,17 +232,21 @@ typedef enum {
 typedef struct {
   uint32_t flags;            /* gp_alloc_flag bits; unknown bits -> GP_EINVAL */
   const uint32_t *size_mask; /* see above */
-  const uint32_t *memo;      /* NULL, or DEVICE [n_sets][2^n_tasks] block verdict words V[set][S]
-                                (bit m-1 = task subset S passes EDF-PDC on m SMs, C.1.7) of the
-                                SAME task sets: the first n_sets * 2^n_tasks words of the
-                                caller-owned workspace of a gp_sched_ratio(GP_EXHAUSTIVE) call
-                                that ran the bit-sliced evaluator without a size_mask (n_tasks
-                                <= 8, M <= 32, not GP_EX_PER_CANDIDATE), earlier on the stream.
+  const uint32_t *memo;      /* NULL, or DEVICE block verdict words of the SAME task sets,
+                                subset-major: word S of set s at memo[S * memo_stride + s]
+                                (bit m-1 = task subset S passes EDF-PDC on m SMs, C.1.7): the
+                                first 2^n_tasks * N words of the caller-owned workspace of a
+                                gp_sched_ratio(GP_EXHAUSTIVE) call on N sets that ran the
+                                bit-sliced evaluator without a size_mask (n_tasks <= 8, M <=
+                                32, not GP_EX_PER_CANDIDATE), earlier on the stream (memo_stride
+                                = N; sets [h, h + n_sets) of that call: memo + h).
                                 Every EDF test the heuristics run at a size m <= M becomes a
                                 lookup (U*H is still computed for the partition orders); outputs
                                 are identical.  n_tasks > 8 or M > 32 -> GP_EINVAL; a memo of
                                 other sets or of a masked call gives wrong verdicts (the library
                                 cannot check it).                                           */
+  int64_t memo_stride;       /* words between the subsets' rows of memo; 0 = n_sets; < n_sets
+                                -> GP_EINVAL                                                    */
 } gp_alloc_opts;
 
 gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *opts,

@@ -56,7 +56,8 @@ struct AllocArgs {
   uint32_t pt_off;            // byte offset of the groups' pair tables in dynamic shared memory
   unsigned long long *next_set;  // work counter (zeroed per launch)
   AllocVariantOpts vo;        // f4
-  const uint32_t *memo;       // optional [n_sets][2^n] block verdict words of an EXHAUSTIVE call
+  const uint32_t *memo;       // optional [2^n][memo_stride] block verdict words of an EXHAUSTIVE call
+  int64_t memo_stride;        // words between consecutive subsets' rows of memo
 };
 
 #ifndef GP_ALLOC_NS4
@@ -211,7 +212,7 @@ template <int NS, bool kGen, bool kMemo, class WS>
 GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, uint32_t S,
                             int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &counted,
                             uint64_t &st_tasks, uint32_t &st_events, uint32_t &st_exec,
-                            const uint32_t *vm, int32_t M) {
+                            const uint32_t *vm, size_t vst, int32_t M) {
   int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   const int cnt = __popc(S);
   uint32_t bits = S;
@@ -236,7 +237,7 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
     if (kMemo && vm && m <= M) {
       // the block verdict memoised by the EXHAUSTIVE pass on the same sets (the same
       // EDF-PDC of S at m); only U*H at m is computed, for the partition orders
-      if (!((vm[S] >> (m - 1)) & 1u)) return false;
+      if (!((vm[(size_t)S * vst] >> (m - 1)) & 1u)) return false;
       int32_t UH = 0;
 #pragma unroll
       for (int a = 0; a < NS; ++a)
@@ -370,7 +371,9 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
     g.sync();
 
     // memoised block verdicts of this set (n <= 8: 2^n words), when the caller passes them
-    const uint32_t *vm = (kMemo && a.memo && contract) ? a.memo + ((size_t)set << n) : nullptr;
+    // (subset-major: word S of this set at vm[S * vst])
+    const uint32_t *vm = (kMemo && a.memo && contract) ? a.memo + set : nullptr;
+    const size_t vst = (size_t)a.memo_stride;
     int64_t tests = 0;
     bool ok = false;
     int stage = 0;  // 0: rejected before partitions exist, 1: partitions to report
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
       tests = 1;
       ++st_exec;
       const int32_t m1 = z.largest();  // M, or the largest admissible size (f4)
-      ok = (kMemo && vm && m1 <= M) ? ((vm[all] >> (m1 - 1)) & 1u) != 0
+      ok = (kMemo && vm && m1 <= M) ? ((vm[(size_t)all * vst] >> (m1 - 1)) & 1u) != 0
                            : warp_pdc(g, t, all, m1, H, st_tasks, st_events);
       pm = lane == 0 ? all : 0;
       psz = lane == 0 ? m1 : 0;
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
               const int32_t got = serial_merge<2, kGen, kMemo>(
                   scr, t.wv, z, (1u << i) | (1u << j), max(scr.szS[i], scr.szS[j]),
                   scr.szS[i] + scr.szS[j] - 1, H, uh, cnt, st_pair_tasks, st_pair_events,
-                  st_pair_exec, vm, M);
+                  st_pair_exec, vm, vst, M);
               pt_tab[idx] = pt_pack(got, cnt, uh);
               my_tests += cnt;
               if (act && !got) {  // §5.3: the couple is forbidden
@@ -614,9 +617,9 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
                 const int32_t lo2 = max(best_m, psz), hi2 = best_m + psz - 1;
                 if (mine && c2 <= 8) {
                   if (kAllocNs4<G> && maxc <= 4)
-                    got2 = serial_merge<4, kGen, kMemo>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, M);
+                    got2 = serial_merge<4, kGen, kMemo>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, vst, M);
                   else
-                    got2 = serial_merge<8, kGen, kMemo>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, M);
+                    got2 = serial_merge<8, kGen, kMemo>(scr, t.wv, z, S2, lo2, hi2, H, uh2, cnt2, st_pair_tasks, st_pair_events, st_pair_exec, vm, vst, M);
                   pt_tab[pt_index(min(keep, lane), max(keep, lane), n)] = pt_pack(got2, cnt2, uh2);
                 }
                 // (groups of 8 lanes hold <= 8 tasks: the group-cooperative path for merged
@@ -753,6 +756,9 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
     }
   }
   const uint32_t *memo = opts ? opts->memo : nullptr;
+  const int64_t memo_stride = (opts && opts->memo_stride) ? opts->memo_stride : (int64_t)ts->n_sets;
+  if (memo && memo_stride < ts->n_sets)
+    return gp_fail(GP_EINVAL, "gp_allocate: memo_stride %lld < n_sets", (long long)memo_stride);
   if (memo && (ts->n_tasks > 8 || ts->M > 32))
     return gp_fail(GP_EINVAL, "gp_allocate: memo needs n_tasks <= 8 and M <= 32");
   if (ts->n_sets == 0) return gp_cuda_check("gp_allocate");
@@ -782,7 +788,7 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
   AllocArgs a{ts->T, ts->D, ts->B, ts->cn, ts->cc, ts->fn, ts->fc, ts->type, ts->n_sets,
               ts->n_tasks, ts->M, (int32_t)v, ok, block_of_task, block_size, pi, k, n_tests,
               efficiency, stats, stats_ext ? 1 : 0, use_tab ? 1 : 0, (uint32_t)pt_off, nullptr,
-              vo, memo};
+              vo, memo, memo_stride};
   using KernFn = void (*)(AllocArgs);
   static const KernFn kdef[2][3][5] = {
       {{k_allocate<false, 8, 0, false>, k_allocate<false, 8, 1, false>, k_allocate<false, 8, 2, false>,

@@ -69,6 +69,10 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_BP_SWEEP_UNROLL
 #define GP_BP_SWEEP_UNROLL 2  // closed-sweep loop unroll (A/B: 1, 2, 4 -> 2 by 1.3 %)
 #endif
+#ifndef GP_BP_CHUNK
+#define GP_BP_CHUNK 8  // allocations per main-pass work item (A/B)
+#endif
+constexpr uint32_t kBpChunk = GP_BP_CHUNK;
 constexpr int kBpUnroll = GP_BP_UNROLL;
 constexpr int kBpSweepUnroll = GP_BP_SWEEP_UNROLL;  // run loop unroll (A/B builds: -DGP_BP_UNROLL=n)
 
@@ -163,7 +167,8 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
   for (int64_t set = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < a.n_sets;
        set += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t H = set_contract(a, set);
-    uint32_t *V = memo + set * nsub;
+    uint32_t *V = memo + set;  // subset-major: word S of this set at V[S * n_sets]
+    const size_t vstride = (size_t)a.n_sets;
     if (H <= 0) {
       if (lane == 0) V[0] = 0u;  // word 0: the set's input contract
       continue;
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
       }
     }
     __syncwarp();
-    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2] = S2 == 0 ? 1u : w.vs[S2];
+    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2 * vstride] = S2 == 0 ? 1u : w.vs[S2];
     __syncwarp();
   }
   if constexpr (kStats) {  // (the timed instantiation carries no counters)
@@ -672,15 +677,18 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     while (k > 1 && it >= a.item_base[k]) --k;
     const uint64_t local = it - (k == a.L.kmax ? 0 : a.item_base[k + 1]);
     const uint32_t npi = (uint32_t)a.L.n_pi[k];
-    const int64_t grp = (int64_t)(local / npi);
-    const uint32_t p = (uint32_t)(local - (uint64_t)grp * npi);
+    const uint32_t nch = (npi + kBpChunk - 1) / kBpChunk;  // chunks of allocations with k blocks
+    const int64_t grp = (int64_t)(local / nch);
+    const uint32_t p0 = (uint32_t)(local - (uint64_t)grp * nch) * kBpChunk;
+    const uint32_t p1 = min(npi, p0 + kBpChunk);
+    for (uint32_t p = p0; p < p1; ++p) {
     const uint32_t labels = rgs[a.rgs_base[k] + p];
     const int myb = lane < n ? (int)((labels >> (4 * lane)) & 15u) : -1;
     if (grp != cur_g) {
       flush();
       cur_g = grp;
       set = grp * 32 + lane;
-      lane_ok = set < a.n_sets && memo[set * nsub] != 0;  // input contract (word 0)
+      lane_ok = set < a.n_sets && memo[set] != 0;  // input contract (word 0)
     }
     const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
     const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
@@ -702,7 +710,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       Vr[jj] = 0u;
       if (jj < k) {  // warp-uniform
         const uint32_t bm = __ballot_sync(GP_FULL, myb == k - 1 - jj);
-        if (lane_ok) Vr[jj] = memo[set * nsub + bm];
+        if (lane_ok) Vr[jj] = memo[(size_t)bm * a.n_sets + set];  // coalesced: lane = set
       }
     }
     if (!__any_sync(GP_FULL, lane_ok)) continue;
@@ -1128,6 +1136,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       }
     }
     if (first_off != UINT32_MAX) acc_first = min(acc_first, rank_pi + first_off);
+    }  // allocations of the item
   }
   flush();
   if constexpr (kStats) {
@@ -1257,8 +1266,8 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   }
   uint64_t items = 0;
   const uint64_t groups32 = ((uint64_t)a.n_sets + 31) / 32;  // lane = set
-  for (int k = a.L.kmax; k >= 1; --k) {
-    items += a.L.n_pi[k] * groups32;
+  for (int k = a.L.kmax; k >= 1; --k) {  // item = (32 sets, <= kBpChunk allocations of k blocks)
+    items += (a.L.n_pi[k] + kBpChunk - 1) / kBpChunk * groups32;
     a.item_base[k] = items;
   }
   a.items_per_set = n_rgs;

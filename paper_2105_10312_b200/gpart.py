@@ -264,7 +264,8 @@ def _size_mask(M, sizes):
 
 
 class _AllocOptsC(C.Structure):
-    _fields_ = [("flags", C.c_uint32), ("size_mask", C.c_void_p), ("memo", C.c_void_p)]
+    _fields_ = [("flags", C.c_uint32), ("size_mask", C.c_void_p), ("memo", C.c_void_p),
+                ("memo_stride", C.c_int64)]
 
 
 GP_AL_BINARY_MERGE = 1  # f4: Algorithm 2 by binary search
@@ -273,11 +274,12 @@ GP_AL_STATS_EXT = 4     # stats has 8 slots (+ tests run, selections, partitions
 
 
 def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=None, flags=0,
-                sizes=None, memo=None):
+                sizes=None, memo=None, memo_stride=0):
     """A5 heuristics / 1G.  f4: ``flags`` (GP_AL_*) and ``sizes`` = admissible
     partition sizes (iterable of ints; None = every size).  ``memo``: a device pointer (int)
     or tensor holding the block verdict words of an EXHAUSTIVE call on the same sets (its
-    workspace; gpart.h gp_alloc_opts.memo)."""
+    workspace, subset-major; gpart.h gp_alloc_opts.memo), ``memo_stride`` the words between
+    its subsets' rows (0 = n_sets)."""
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     if out is None:
         out = AllocOut(ts.n_sets, ts.n_tasks, ts.T.device)
@@ -289,7 +291,7 @@ def gp_allocate(ts: TaskSets, variant, out: AllocOut = None, stream=None, stats=
         mask = _size_mask(ts.M, sizes)
         mp = None if memo is None else (memo if isinstance(memo, int) else memo.data_ptr())
         opts = _AllocOptsC(int(flags), C.cast(mask, C.c_void_p) if mask is not None else None,
-                           mp)
+                           mp, int(memo_stride))
         opts._keep = mask
     _check(_lib.gp_allocate(C.byref(s), v, C.byref(opts) if opts is not None else None,
                             _ptr(out.ok), _ptr(out.block_of_task),

@@ -165,7 +165,7 @@ class Pipeline:
             memo = None
             if (self.exhaustive and si == 0 and mode == G.GP_EXHAUSTIVE and self.memo_ok
                     and not flags & (G.GP_EX_PER_CANDIDATE | G.GP_EX_GENERIC)):
-                memo = self.workspace.data_ptr() + self.h_lo * (4 << self.n)
+                memo = self.workspace.data_ptr() + self.h_lo * 4  # subset-major rows
             if self.parallel_variants and stream is not None and len(self.variants) > 1:
                 # the variants are independent: one stream each (fork / join by events; in
                 # a captured graph, parallel branches), so their persistent grids' tails overlap
@@ -177,7 +177,8 @@ class Pipeline:
                 for vi, v in enumerate(self.variants):
                     vs = self._vstreams[vi]
                     vs.wait_event(fork)
-                    G.gp_allocate(ts_h, v, self.alloc[vi], vs, stats=alloc_stats, memo=memo)
+                    G.gp_allocate(ts_h, v, self.alloc[vi], vs, stats=alloc_stats, memo=memo,
+                                  memo_stride=ts.n_sets)
                     e = torch.cuda.Event()
                     e.record(vs)
                     joins.append(e)
@@ -185,7 +186,8 @@ class Pipeline:
                     stream.wait_event(e)
             else:
                 for vi, v in enumerate(self.variants):
-                    G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats, memo=memo)
+                    G.gp_allocate(ts_h, v, self.alloc[vi], stream, stats=alloc_stats, memo=memo,
+                                  memo_stride=ts.n_sets)
             if not self.exhaustive:
                 hook("end")
             if self.variants and ts_h.n_sets > 0:
