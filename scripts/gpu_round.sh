@@ -38,5 +38,6 @@ done
 [ "$KEEP_REPORTS" = "c3" ] && mv $O/full_c3.ncu-rep $O/keep_full_c3.ncu-rep
 rm -f $O/*.ncu-rep
 [ -f $O/keep_full_c3.ncu-rep ] && mv $O/keep_full_c3.ncu-rep $O/full_c3.ncu-rep
-bash scripts/gpu_sanitize.sh $T
+# compute-sanitizer is closed on the GPU pool (it left GPUs needing a reset): no sanitizer pass
+# bash scripts/gpu_sanitize.sh $T
 ls $O; du -sh $O
