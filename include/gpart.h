@@ -239,7 +239,9 @@ typedef struct {
                                 gp_sched_ratio(GP_EXHAUSTIVE) call on N sets that ran the
                                 bit-sliced evaluator without a size_mask (n_tasks <= 8, M <=
                                 32, not GP_EX_PER_CANDIDATE), earlier on the stream (memo_stride
-                                = N; sets [h, h + n_sets) of that call: memo + h).
+                                = N; sets [h, h + n_sets) of that call: memo + h).  Row S = 0
+                                holds the set's hyperperiod H (0: input contract violated),
+                                which the heuristics then take instead of recomputing it.
                                 Every EDF test the heuristics run at a size m <= M becomes a
                                 lookup (U*H is still computed for the partition orders); outputs
                                 are identical.  n_tasks > 8 or M > 32 -> GP_EINVAL; a memo of

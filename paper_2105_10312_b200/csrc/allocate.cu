@@ -343,14 +343,24 @@ __global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArg
     // input contract and H = lcm of all periods (capped)
     const bool fields_ok = !t.in || (t.T >= 1 && t.D >= 1 && t.D <= t.T && t.B >= 1 && t.cn >= 1 &&
                                      t.cc >= t.cn && t.fn >= 0 && t.fc >= t.fn);
-    const int64_t cap = ((int64_t)1 << 31) / (n + 1) - 1;
-    int64_t h = (t.in && fields_ok) ? t.T : (t.in ? -1 : 1);
+    int64_t h;
+    bool contract;
+    if (kMemo && a.memo) {
+      // the exhaustive pass checked the same contract on the same sets and left H (the lcm of
+      // the periods; 0 = violated) in its words' row 0
+      const uint32_t hm = a.memo[set];
+      h = hm ? (int64_t)hm : -1;
+      contract = h > 0;
+    } else {
+      const int64_t cap = ((int64_t)1 << 31) / (n + 1) - 1;
+      h = (t.in && fields_ok) ? t.T : (t.in ? -1 : 1);
 #pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) {
-      const int64_t other = g.shfl_xor(h, off);
-      h = (h < 0 || other < 0) ? -1 : lcm_capped(h, other, cap);
+      for (int off = G / 2; off > 0; off >>= 1) {
+        const int64_t other = g.shfl_xor(h, off);
+        h = (h < 0 || other < 0) ? -1 : lcm_capped(h, other, cap);
+      }
+      contract = g.all(fields_ok) && h > 0;
     }
-    const bool contract = g.all(fields_ok) && h > 0;
     const int32_t H = contract ? (int32_t)h : 1;
     t.q = (contract && t.in) ? H / t.T : 0;
     scr.T[lane] = t.T; scr.D[lane] = t.D; scr.B[lane] = t.B; scr.cn[lane] = t.cn;

@@ -42,6 +42,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_MEMO_DENSITY
 #define GP_MEMO_DENSITY 1  // memo tests: density <= 1 passes without the demand walk (exact)
 #endif
+#ifndef GP_MEMO_DYNAMIC
+#define GP_MEMO_DYNAMIC 1  // memo pass: persistent grid, sets from a counter (0: static stride)
+#endif
 #ifndef GP_MEMO_RANK_ORDER
 #define GP_MEMO_RANK_ORDER 1  // memo: compacted tests ordered by their rank within the subset
 #endif
@@ -164,8 +167,18 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
   uint64_t st_tests = 0, st_tasks = 0;
   uint32_t st_events = 0;
   const uint32_t Mmask = M >= 32 ? ~0u : (1u << M) - 1u;
-  for (int64_t set = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; set < a.n_sets;
-       set += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+  // sets: dynamic (a warp grabs its next set from a counter: sets differ widely in work)
+  // or a static grid stride
+  auto next_set = [&](int64_t cur) -> int64_t {
+    if (GP_MEMO_DYNAMIC && a.memo_counter) {
+      unsigned long long s0 = 0;
+      if (lane == 0) s0 = atomicAdd(a.memo_counter, 1ull);
+      return (int64_t)__shfl_sync(GP_FULL, s0, 0);
+    }
+    return cur < 0 ? ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5
+                   : cur + (((int64_t)gridDim.x * blockDim.x) >> 5);
+  };
+  for (int64_t set = next_set(-1); set < a.n_sets; set = next_set(set)) {
     const int64_t H = set_contract(a, set);
     uint32_t *V = memo + set;  // subset-major: word S of this set at V[S * n_sets]
     const size_t vstride = (size_t)a.n_sets;
@@ -283,7 +296,9 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
       }
     }
     __syncwarp();
-    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2 * vstride] = S2 == 0 ? 1u : w.vs[S2];
+    // row 0: the set's H (lcm of the periods, > 0: contract kept; 0: violated), which the
+    // heuristics reuse (gpart.h gp_alloc_opts.memo)
+    for (int S2 = lane; S2 < nsub; S2 += 32) V[S2 * vstride] = S2 == 0 ? (uint32_t)H32 : w.vs[S2];
     __syncwarp();
   }
   if constexpr (kStats) {  // (the timed instantiation carries no counters)
@@ -1191,7 +1206,7 @@ namespace gp {
 // lane order (slots, histograms, load levels) and the hash prefix table.
 struct BpLayout {
   size_t memo_words, words32, bytes, r_off, ct_off, fct_off;
-  uint64_t n_rgs, n_ranks, total_runs, r_stride;
+  uint64_t n_rgs, n_ranks, total_runs, r_stride, mc_off;
   uint32_t nb, r_nb;
   bool use_P, use_R, use_CT, use_FCT;
 };
@@ -1231,6 +1246,8 @@ static BpLayout bp_layout(const RankLayout &L, int n, int32_t n_sets, int32_t n_
   b.use_FCT = GP_BP_FULLCORNER && b.use_P;
   b.fct_off = b.bytes;
   if (b.use_FCT) b.bytes += (uint64_t)L.total * 8;
+  b.mc_off = b.bytes;  // the memo pass's set counter
+  b.bytes += 8;
   return b;
 }
 }  // namespace gp
@@ -1364,6 +1381,12 @@ gp_status gp_exhaustive_bp_launch(const gp::ExhArgs &a0, void *ws_user, uint64_t
   {
     int64_t blocks = ((int64_t)a.n_sets + 7) / 8;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    a.memo_counter = nullptr;
+    if (GP_MEMO_DYNAMIC) {  // one wave of resident CTAs, sets from the counter
+      a.memo_counter = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(ws) + b.mc_off);
+      cudaMemsetAsync(a.memo_counter, 0, 8, st);
+      if (blocks > (int64_t)sms * GP_MEMO_MINB) blocks = (int64_t)sms * GP_MEMO_MINB;
+    }
     const unsigned g = (unsigned)(blocks > 0 ? blocks : 1);
     if (a.stats) {
       if (n <= 4) k_exh_memo<4, true><<<g, 256, 0, st>>>(a, memo);

@@ -30,6 +30,7 @@ struct ExhArgs {
   uint64_t r_stride;      // entries per row of R (total runs + 1)
   const uint64_t *CT;     // bit-sliced evaluator: corner table [rank] (k >= 3; or null)
   const uint64_t *FCT;    // bit-sliced evaluator: full corner table [rank] (or null)
+  unsigned long long *memo_counter;  // bit-sliced memo pass: next set (or null: static stride)
   uint64_t run_base[kEnumMaxTasks + 2];  // first global run index of the allocations with k blocks
   uint32_t rgs_base[kEnumMaxTasks + 2];  // bit-sliced evaluator: first RGS index with k blocks
   uint64_t items_per_set, total_items;
