@@ -671,72 +671,93 @@ def time_tables(G, pipe, stream, exh_mode, exh_flags):
 def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
     """Host task sets (pinned) -> H2D -> evaluation -> D2H, through the C ABI.
     The host inputs are the first setting's task sets of this rank.  Every step copies
-    its inputs H2D and its results D2H inside the timed region; the inputs of step k+1
-    are copied on a second stream into a second device buffer while step k computes
-    (double buffering), so the copies overlap the evaluation.  The evaluation is
-    Pipeline.run on the uploaded sets (same calls and collectives as the device-only
-    step, minus gp_generate)."""
+    its inputs H2D and its results D2H inside the timed region.  Two slots, each with its
+    own device inputs, device outputs and pinned host outputs: the H2D of step k+1 (copy
+    stream) and the D2H of step k-1 (a second copy stream) overlap the evaluation of step
+    k; a slot is reused only after its D2H finished.  The evaluation is Pipeline.run on the
+    uploaded sets (same calls and collectives as the device-only step, minus gp_generate)."""
     import torch
     fields = ("T", "D", "B", "cn", "cc", "fn", "fc", "type", "valid", "group")
     G.gp_generate(pipe.gens[0], pipe.seed, pipe.rep_begin, pipe.reps, pipe.ts, stream)
     host = {f: getattr(pipe.ts, f).cpu().pin_memory() for f in fields}
     devs = [G.TaskSets(pipe.ts.n_sets, pipe.ts.n_tasks, pipe.ts.M, pipe.ts.n_groups)
             for _ in range(2)]
-    outs = [pipe.counts, pipe.verdicts] + ([pipe.per_set] if pipe.exhaustive else [])
-    host_out = [torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for t in outs]
-    h2d = sum(t.numel() * t.element_size() for t in host.values())
-    d2h = sum(t.numel() * t.element_size() for t in host_out)
-    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
-    copy_stream = torch.cuda.Stream()
     settings = pipe.settings
     pipe.settings = settings[:1]  # the host inputs are one setting's task sets
+    # per-slot device outputs (the pipeline's own tensors for slot 0, copies for slot 1)
+    orig = (pipe.counts, pipe.verdicts, pipe.per_set if pipe.exhaustive else None)
+
+    def make_outs(first):
+        if first:
+            return orig
+        return tuple(None if t is None else torch.zeros_like(t) for t in orig)
+
+    slot_outs = [make_outs(True), make_outs(False)]
+
+    def use_slot(b):
+        """Point the pipeline's output tensors at slot b's (graphs capture the pointers)."""
+        counts, verdicts, per_set = slot_outs[b]
+        pipe.counts, pipe.verdicts = counts, verdicts
+        for vi, out in enumerate(pipe.alloc):
+            out.ok = verdicts[vi]
+        if per_set is not None:
+            pipe.per_set = per_set
+
+    def out_list(b):
+        return [t for t in slot_outs[b] if t is not None]
+
+    host_out = [[torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for t in out_list(b)]
+                for b in range(2)]
+    h2d = sum(t.numel() * t.element_size() for t in host.values())
+    d2h = sum(t.numel() * t.element_size() for t in host_out[0])
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    copy_stream, d2h_stream = torch.cuda.Stream(), torch.cuda.Stream()
 
     def upload(dev, s):
         with torch.cuda.stream(s):
             for f, t in host.items():
                 getattr(dev, f).copy_(t, non_blocking=True)
 
-    def compute_on(dev, s, with_stats=False, collectives=True):
-        """The step's ABI calls on stream `s`, then the D2H of its results."""
+    def compute_on(b, s, with_stats=False, collectives=True):
+        """The step's ABI calls on stream `s` into slot b's outputs."""
+        use_slot(b)
         with torch.cuda.stream(s):
             pipe.counts.zero_()
         pipe.run(s, mode=exh_mode, flags=exh_flags,
-                 alloc_stats=stats if with_stats else None, ts=dev, collectives=collectives)
-        with torch.cuda.stream(s):
-            for h, d in zip(host_out, outs):
-                h.copy_(d, non_blocking=True)
+                 alloc_stats=stats if with_stats else None, ts=devs[b], collectives=collectives)
 
-    # the compute of a step on either input buffer as a CUDA graph (as in the device-only
-    # timed loop); the counts all-reduce and the copies on the copy stream stay outside
+    # the compute of a step in either slot as a CUDA graph (as in the device-only timed
+    # loop); the counts all-reduce and the copies stay outside
     egraphs = None
     if not args.no_graph and pipe.split != "ranks":
-        compute_on(devs[0], stream)  # warm (lazy module loading, workspaces)
+        compute_on(0, stream)  # warm (lazy module loading, workspaces)
         torch.cuda.synchronize()
         egraphs = []
-        for dev in devs:
+        for b in range(2):
             side = torch.cuda.Stream()
             side.wait_stream(stream)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(side):
                 g.capture_begin()
-                compute_on(dev, side, collectives=False)
+                compute_on(b, side, collectives=False)
                 g.capture_end()
             stream.wait_stream(side)
             egraphs.append(g)
 
-    def compute(dev, with_stats=False):
+    def compute(b, with_stats=False):
         if egraphs is not None and not with_stats:
-            egraphs[devs.index(dev)].replay()
+            egraphs[b].replay()
             from paper_2105_10312_b200.pipeline import allreduce_counts
-            allreduce_counts(pipe.counts)
+            allreduce_counts(slot_outs[b][0])
         else:
-            compute_on(dev, stream, with_stats)
+            compute_on(b, stream, with_stats)
 
     def run(k_steps, with_stats=False):
         """k_steps pipelined steps; returns (start, end) events on `stream`."""
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         copied = [torch.cuda.Event(), torch.cuda.Event()]
-        freed = [None, None]
+        freed = [None, None]    # slot's inputs consumed (its compute finished)
+        fetched = [None, None]  # slot's outputs copied to the host
         start.record(stream)
         copy_stream.wait_event(start)
         upload(devs[0], copy_stream)
@@ -744,14 +765,25 @@ def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
         for k in range(k_steps):
             cur, nxt = k % 2, 1 - k % 2
             stream.wait_event(copied[cur])
-            if k + 1 < k_steps:  # next step's inputs, once its buffer's last user is done
+            if fetched[cur] is not None:  # its outputs of step k-2 are on the host
+                stream.wait_event(fetched[cur])
+            if k + 1 < k_steps:  # next step's inputs, once its slot's last compute is done
                 if freed[nxt] is not None:
                     copy_stream.wait_event(freed[nxt])
                 upload(devs[nxt], copy_stream)
                 copied[nxt].record(copy_stream)
-            compute(devs[cur], with_stats)
+            compute(cur, with_stats)
             freed[cur] = torch.cuda.Event()
             freed[cur].record(stream)
+            d2h_stream.wait_event(freed[cur])
+            with torch.cuda.stream(d2h_stream):
+                for h, d in zip(host_out[cur], out_list(cur)):
+                    h.copy_(d, non_blocking=True)
+            fetched[cur] = torch.cuda.Event()
+            fetched[cur].record(d2h_stream)
+        for e in fetched:
+            if e is not None:
+                stream.wait_event(e)
         end.record(stream)
         return start, end
 
@@ -767,6 +799,7 @@ def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
     torch.cuda.synchronize()
     a, b = run(args.steps)
     torch.cuda.synchronize()
+    use_slot(0)
     pipe.settings = settings
     ms = a.elapsed_time(b)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -776,10 +809,11 @@ def run_e2e(G, pipe, stream, args, world, exh_mode, exh_flags):
     ms = float(t.item())
     return {"value": evals * args.steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.steps,
-            "path": "pinned host task sets -> H2D (double-buffered on a copy stream) -> "
-                    "gp_sched_ratio(EXHAUSTIVE) + gp_allocate x5 + gp_sched_ratio -> D2H counts, "
-                    "verdicts, per-set results (one setting), every step inside the timed region"
-                    + ("; the compute and D2H replayed as one CUDA graph per input buffer"
+            "path": "pinned host task sets -> H2D (copy stream) -> gp_sched_ratio(EXHAUSTIVE) + "
+                    "gp_allocate x5 + gp_sched_ratio -> D2H counts, verdicts, per-set results "
+                    "(second copy stream), every step inside the timed region; two slots of "
+                    "inputs and outputs, so step k+1's H2D and step k-1's D2H overlap step k"
+                    + ("; the compute replayed as one CUDA graph per slot"
                        if egraphs is not None else "")}
 
 

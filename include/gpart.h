@@ -301,7 +301,7 @@ gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_alloc_opts *
  *   n_sched = sum_pi C(M - sum(m* - 1), k), pi_star = min sum(m*), first_rank =
  *   rank(pi, m*); the hash enumerates the schedulable vectors only (skipped with
  *   GP_EX_NO_HASH).  Full rank window only; verdict_bits must be NULL;
- *   work_counter unused.
+ *   work_counter optional (when given: the sets' work queue).
  * ------------------------------------------------------------------------- */
 typedef struct {
   uint64_t rank_lo, rank_hi;  /* window [lo, hi) of candidate ranks; hi = UINT64_MAX -> N_c  */

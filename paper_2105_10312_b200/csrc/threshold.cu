@@ -37,6 +37,7 @@ struct ThrArgs {
   unsigned long long *stats;  // += {sets, threshold tests, deadlines examined, schedulable enumerated}
   int32_t masked;             // f4 size mask given (reading B-9)
   uint32_t adm[8];            // admissible sizes, bit (m-1) % 32 of word (m-1) / 32
+  unsigned long long *next;   // set counter (persistent warps take sets dynamically) or null
 };
 
 // f4 (reading B-9): first admissible size >= x, M + 1 if none.
@@ -201,8 +202,16 @@ __global__ void __launch_bounds__(kThrWarps * 32) k_threshold(const ThrArgs a) {
   uint64_t st_tests = 0, st_sched = 0;
   uint32_t st_events = 0;
   uint64_t st_sets = 0;
-  for (int64_t set = (int64_t)blockIdx.x * kThrWarps + warp; set < a.n_sets;
-       set += (int64_t)gridDim.x * kThrWarps) {
+  // sets from a counter (they differ widely in work) or, without one, a static stride
+  auto next_set = [&](int64_t cur) -> int64_t {
+    if (a.next) {
+      unsigned long long s0 = 0;
+      if (lane == 0) s0 = atomicAdd(a.next, 1ull);
+      return (int64_t)__shfl_sync(GP_FULL, s0, 0);
+    }
+    return cur < 0 ? (int64_t)blockIdx.x * kThrWarps + warp : cur + (int64_t)gridDim.x * kThrWarps;
+  };
+  for (int64_t set = next_set(-1); set < a.n_sets; set = next_set(set)) {
     const int64_t H64 = thr_contract(a, set);
     int64_t *ps = a.per_set + set * 4;
     if (H64 <= 0) {
@@ -411,6 +420,7 @@ gp_status gp_threshold_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_sl
   a.per_set = ex->per_set; a.counts = counts; a.slot0 = slot0; a.n_slots = n_slots;
   a.setting = setting; a.want_hash = (ex->flags & GP_EX_NO_HASH) ? 0 : 1; a.stats = ex->stats;
   a.masked = ex->size_mask != nullptr;
+  a.next = ex->work_counter;  // optional here: dynamic set scheduling when given
   {
     uint32_t adm[8];
     s = load_size_mask(ex->size_mask, M, adm, "THRESHOLD");
@@ -418,6 +428,7 @@ gp_status gp_threshold_launch(const gp_tasksets *ts, int32_t slot0, int32_t n_sl
     for (int w = 0; w < 8; ++w) a.adm[w] = adm[w];
   }
   if (ts->n_sets == 0) return gp_cuda_check("THRESHOLD");
+  if (a.next) cudaMemsetAsync(a.next, 0, 8, st);
   const size_t per_warp = thr_warp_words(n, M);
   const size_t smem = (((enum_table_words(M, n) + 3) & ~(size_t)3) + per_warp * kThrWarps) * 4;
   if (smem > 227 * 1024) return gp_fail(GP_EINVAL, "THRESHOLD: shared memory need %zu B", smem);
