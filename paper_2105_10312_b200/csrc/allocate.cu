@@ -60,6 +60,9 @@ struct AllocArgs {
   int64_t memo_stride;        // words between consecutive subsets' rows of memo
 };
 
+#ifndef GP_ALLOC_MINB8
+#define GP_ALLOC_MINB8 5  // CTAs per SM the 8-lane-group kernels' register budget targets (A/B: 3, 4, 5, 6 -> 5)
+#endif
 #ifndef GP_ALLOC_NS4
 #define GP_ALLOC_NS4 8  // widest group that gets the <= 4-task lane-serial merge (0: none)
 #endif
@@ -213,8 +216,55 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
                             int32_t lo, int32_t hi, int32_t H, int32_t &uh_out, int64_t &counted,
                             uint64_t &st_tasks, uint32_t &st_events, uint32_t &st_exec,
                             const uint32_t *vm, size_t vst, int32_t M) {
-  int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   const int cnt = __popc(S);
+  if constexpr (kMemo) {
+    // memo kernels: a test at m <= M is a lookup plus U*H, both from shared memory; the task
+    // records are gathered into registers only for the (rare) full test at m > M, so they
+    // hold no registers across the search (8-lane groups: more resident CTAs)
+    auto test = [&](int32_t m) -> bool {
+      ++st_exec;
+      if (vm && m <= M) {
+        if (!((vm[(size_t)S * vst] >> (m - 1)) & 1u)) return false;
+        int32_t UH = 0;
+        for (uint32_t b = S; b; b &= b - 1u) {
+          const int i = __ffs(b) - 1;
+          const bool x = __popc(S & w.same[i]) > 1;  // conflict
+          UH += w_from_waves(wv(i, w.B[i], m), x ? w.cc[i] : w.cn[i], x ? w.fc[i] : w.fn[i]) * w.q[i];
+        }
+        uh_out = UH;
+        return true;
+      }
+      st_tasks += cnt;
+      int32_t C[NS], D[NS], T[NS], q[NS];
+      uint32_t bits = S;
+      bool bad = false;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        const bool v = bits != 0;
+        const int i = v ? __ffs(bits) - 1 : 0;
+        bits &= bits - 1u;
+        const bool x = __popc(S & w.same[i]) > 1;
+        T[a] = v ? w.T[i] : INT32_MAX;
+        D[a] = v ? w.D[i] : INT32_MAX;
+        q[a] = v ? w.q[i] : 0;
+        C[a] = v ? w_from_waves(wv(i, w.B[i], m), x ? w.cc[i] : w.cn[i], x ? w.fc[i] : w.fn[i]) : 0;
+        bad |= C[a] > D[a];
+      }
+      if (bad) return false;
+      int32_t UH = 0;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) UH += C[a] * q[a];
+      if (UH > H) return false;
+      if (cnt > 1) {
+        const int32_t lcut = pdc_cutoff<NS>(C, D, T, q, H, UH);
+        if (!pdc_walk<NS>(C, D, T, lcut, st_events)) return false;
+      }
+      uh_out = UH;
+      return true;
+    };
+    return alg2_search<kGen>(z, lo, hi, test, counted);
+  }
+  int32_t T[NS], D[NS], B[NS], c[NS], f[NS], q[NS], id[NS];
   uint32_t bits = S;
 #pragma unroll
   for (int a = 0; a < NS; ++a) {
@@ -234,17 +284,6 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
   // of a search is its answer)
   auto test = [&](int32_t m) -> bool {
     ++st_exec;
-    if (kMemo && vm && m <= M) {
-      // the block verdict memoised by the EXHAUSTIVE pass on the same sets (the same
-      // EDF-PDC of S at m); only U*H at m is computed, for the partition orders
-      if (!((vm[(size_t)S * vst] >> (m - 1)) & 1u)) return false;
-      int32_t UH = 0;
-#pragma unroll
-      for (int a = 0; a < NS; ++a)
-        UH += (c[a] ? w_from_waves(wv(id[a], B[a], m), c[a], f[a]) : 0) * q[a];
-      uh_out = UH;
-      return true;
-    }
     st_tasks += cnt;
     int32_t C[NS];
     bool bad = false;
@@ -290,7 +329,7 @@ GP_DEV uint32_t pm_bcast(const Grp<G> &g, uint32_t pm, int src) { return g.shfl(
 template <bool kGen, int G, int kV, bool kStats>
 // register budget: 4 CTAs per SM for 8-lane groups (64 registers), 3 otherwise (80): A/B
 // measured -- the small-set kernels gain occupancy, the larger ones lose more to spills
-__global__ void __launch_bounds__(256, G == 8 ? 4 : 3) k_allocate(const AllocArgs a) {
+__global__ void __launch_bounds__(256, G == 8 ? GP_ALLOC_MINB8 : 3) k_allocate(const AllocArgs a) {
   const int variant = kV >= 0 ? kV : a.variant;
   // memoised verdicts exist for n <= 8 only, i.e. in 8-lane groups: the wider kernels keep
   // the plain tests (no extra code or registers)
