@@ -63,6 +63,12 @@ struct AllocArgs {
 #ifndef GP_ALLOC_MINB8
 #define GP_ALLOC_MINB8 5  // CTAs per SM the 8-lane-group kernels' register budget targets (A/B: 3, 4, 5, 6 -> 5)
 #endif
+#ifndef GP_ALLOC_MINB32
+#define GP_ALLOC_MINB32 4  // the same for the 16- and 32-lane-group kernels (A/B: 3, 4 -> 4)
+#endif
+#ifndef GP_ALLOC_GATHER_PER_TEST
+#define GP_ALLOC_GATHER_PER_TEST 1  // 16/32-lane groups: task records gathered per test (A/B: C4 -2 %, C5 -11 % with 4 CTAs)
+#endif
 #ifndef GP_ALLOC_NS4
 #define GP_ALLOC_NS4 8  // widest group that gets the <= 4-task lane-serial merge (0: none)
 #endif
@@ -217,10 +223,10 @@ GP_DEV int32_t serial_merge(const WS &w, const Waves &wv, const SizeSpace &z, ui
                             uint64_t &st_tasks, uint32_t &st_events, uint32_t &st_exec,
                             const uint32_t *vm, size_t vst, int32_t M) {
   const int cnt = __popc(S);
-  if constexpr (kMemo) {
-    // memo kernels: a test at m <= M is a lookup plus U*H, both from shared memory; the task
-    // records are gathered into registers only for the (rare) full test at m > M, so they
-    // hold no registers across the search (8-lane groups: more resident CTAs)
+  if constexpr (kMemo || GP_ALLOC_GATHER_PER_TEST) {
+    // a test at m <= M with memo words is a lookup plus U*H, both from shared memory; the
+    // task records are gathered into registers only for a full test (with memo words the
+    // rare m > M), so they hold no registers across the search (more resident CTAs)
     auto test = [&](int32_t m) -> bool {
       ++st_exec;
       if (vm && m <= M) {
@@ -327,9 +333,10 @@ GP_DEV uint32_t pm_bcast(const Grp<G> &g, uint32_t pm, int src) { return g.shfl(
 // its own code, e.g. no ACT prefill in INA, which keeps the instruction working set small);
 // kV = -1: runtime variant (the f4 kGen kernels)
 template <bool kGen, int G, int kV, bool kStats>
-// register budget: 4 CTAs per SM for 8-lane groups (64 registers), 3 otherwise (80): A/B
-// measured -- the small-set kernels gain occupancy, the larger ones lose more to spills
-__global__ void __launch_bounds__(256, G == 8 ? GP_ALLOC_MINB8 : 3) k_allocate(const AllocArgs a) {
+// register budget: 5 CTAs per SM for 8-lane groups (48 registers), 4 otherwise (64): A/B
+// measured, with the task records of a lane-serial merge gathered per test (no registers
+// held across the size search)
+__global__ void __launch_bounds__(256, G == 8 ? GP_ALLOC_MINB8 : GP_ALLOC_MINB32) k_allocate(const AllocArgs a) {
   const int variant = kV >= 0 ? kV : a.variant;
   // memoised verdicts exist for n <= 8 only, i.e. in 8-lane groups: the wider kernels keep
   // the plain tests (no extra code or registers)
