@@ -575,6 +575,9 @@ struct Binom {  // C(a, b), 0 <= a <= kBpMaxM, 0 <= b <= kBpMaxN (shared memory)
   GP_DEV uint32_t operator()(int aa, int bb) const {
     return (aa < 0 || bb > aa) ? 0u : t[aa * (kBpMaxN + 1) + bb];
   }
+  // 0 <= bb <= kBpMaxN, aa <= kBpMaxM: the table holds C(aa, bb) = 0 for bb > aa, and a
+  // negative aa reads C(0, bb) (0 for bb >= 1; callers pass bb >= 1 there)
+  GP_DEV uint32_t at(int aa, int bb) const { return t[max(aa, 0) * (kBpMaxN + 1) + bb]; }
 };
 
 __global__ void __launch_bounds__(256) k_fct_init(uint64_t *F, uint64_t n_ranks) {
@@ -668,6 +671,8 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
   __syncthreads();
   auto bn = [&](int aa, int bb) -> uint32_t { return binom_s(aa, bb); };
   int64_t cur_g = -1, set = -1;
+  const uint32_t *memo_set = memo;             // this lane's set's column of the memo words
+  const size_t memo_stride = (size_t)a.n_sets;  // words between subsets' rows
   bool lane_ok = false;
   auto flush = [&]() {
     if (lane_ok && acc_n > 0) {
@@ -704,6 +709,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       cur_g = grp;
       set = grp * 32 + lane;
       lane_ok = set < a.n_sets && memo[set] != 0;  // input contract (word 0)
+      memo_set = memo + (lane_ok ? set : 0);
     }
     const uint32_t per_pi = (uint32_t)a.L.per_pi[k];
     const uint64_t rank_pi = a.L.k_base[k] + (uint64_t)p * per_pi;
@@ -725,7 +731,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
       Vr[jj] = 0u;
       if (jj < k) {  // warp-uniform
         const uint32_t bm = __ballot_sync(GP_FULL, myb == k - 1 - jj);
-        if (lane_ok) Vr[jj] = memo[(size_t)bm * a.n_sets + set];  // coalesced: lane = set
+        if (lane_ok) Vr[jj] = memo_set[bm * memo_stride];  // coalesced: lane = set
       }
     }
     if (!__any_sync(GP_FULL, lane_ok)) continue;
@@ -765,7 +771,7 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
             const uint32_t mk = nb >= 32 ? ~0u : (nb <= 0 ? 0u : (1u << nb) - 1u);
             corner &= ((V >> lo) & mk) == mk;
             csum += lo + 1;
-            sub += bn(M - csum, jj + 1);
+            sub += binom_s.at(M - csum, jj + 1);  // (csum > M: unused, see below)
           }
         }
         if (corner) {
