@@ -630,16 +630,18 @@ def time_direct(G, pipe, stream, flush, args, peak, direct_stats, world):
 def launches_per_step(pipe, args=None):
     """Our kernels per step: per setting gp_generate 1 + gp_allocate x V + ratio 1;
     + EXHAUSTIVE: per-candidate (init, main, finalize) or bit-sliced (init, memo, main,
-    finalize, + 3 lane-order kernels: tile histogram, scan, tile scatter).  The bit-sliced
-    evaluator's input-independent tables (RGS labels, hash prefix, run-prefix and corner
+    finalize); THRESHOLD (threshold, violations).  The bit-sliced evaluator's
+    input-independent tables (RGS labels, hash prefix, run-prefix and corner
     tables) are built by the first call on the workspace, before the timed steps
     (gp_exhaustive_opts.tables_key; their build time is reported as `tables`)."""
     n = len(pipe.gens) * (2 + len(pipe.variants))
     if not pipe.exhaustive:
         return n
-    if (args is not None and (args.f3 or args.per_candidate)) or pipe.n > 8 or pipe.M > 32:
+    if args is not None and args.f3:
+        return n + 2  # k_threshold, k_thr_violations
+    if (args is not None and args.per_candidate) or pipe.n > 8 or pipe.M > 32:
         return n + 3
-    return n + 4 + (3 if pipe.ts.n_sets > 32 else 0)
+    return n + 4
 
 
 def time_tables(G, pipe, stream, exh_mode, exh_flags):
