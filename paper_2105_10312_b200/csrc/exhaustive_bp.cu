@@ -45,6 +45,9 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #ifndef GP_MEMO_DYNAMIC
 #define GP_MEMO_DYNAMIC 1  // memo pass: persistent grid, sets from a counter (0: static stride)
 #endif
+#ifndef GP_MEMO_PAIRS_PER_ROUND
+#define GP_MEMO_PAIRS_PER_ROUND 1  // rank-order lists: two sizes per subset and round (A/B: -0.4 %)
+#endif
 #ifndef GP_MEMO_RANK_ORDER
 #define GP_MEMO_RANK_ORDER 1  // memo: compacted tests ordered by their rank within the subset
 #endif
@@ -248,6 +251,25 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
         {
           uint32_t b = A;
           const uint32_t lt = (1u << lane) - 1u;
+#if GP_MEMO_PAIRS_PER_ROUND
+          // two sizes per subset and round (half the ballot rounds; a round's entries are
+          // each subset's next two surviving sizes)
+          for (;;) {
+            const uint32_t has = __ballot_sync(GP_FULL, b != 0u);
+            if (!has) break;
+            const uint32_t has2 = __ballot_sync(GP_FULL, (b & (b - 1u)) != 0u);
+            if (b) {
+              const int pos = total + __popc(has & lt) + __popc(has2 & lt);
+              w.list[pos] = (uint16_t)(lane | ((__ffs(b) - 1) << 5));
+              b &= b - 1u;
+              if (b) {
+                w.list[pos + 1] = (uint16_t)(lane | ((__ffs(b) - 1) << 5));
+                b &= b - 1u;
+              }
+            }
+            total += __popc(has) + __popc(has2);
+          }
+#else
           for (;;) {
             const uint32_t has = __ballot_sync(GP_FULL, b != 0u);
             if (!has) break;
@@ -257,6 +279,7 @@ __global__ void __launch_bounds__(256, GP_MEMO_MINB) k_exh_memo(const ExhArgs a,
             }
             total += __popc(has);
           }
+#endif
         }
 #else
         {
