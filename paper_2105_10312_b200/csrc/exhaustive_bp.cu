@@ -10,10 +10,13 @@
 //   per set where the per-candidate evaluator runs ~2.3 million.  A pair (S, m) is
 //   skipped only when some S - {i} fails at m (then S fails: fewer tasks, no more
 //   conflicts); no monotonicity in m is assumed (that is f3's GP_THRESHOLD).
-//   k_sp_*: per subset, the sets ordered by (utilisation group, first passing
-//   size, load level): the lane order of the main pass (below).
-//   k_exh_bp: items = (32 sets, allocation pi), candidates in the rank order of
-//   C.1.6.  Candidates of pi that differ in the last part only form a RUN
+//   The words are stored subset-major (V[S][set]; row 0 = the set's H).
+//   k_exh_bp: items = (32 sets, up to 8 allocations pi), candidates in the rank
+//   order of C.1.6.  FULL CORNER: when every block word of pi is one bit range from
+//   its first passing size lo_j + 1 through M - k + 1 (checked per (set, pi)), the
+//   schedulable candidates of pi are the corner s >= lo + 1 of pi's simplex: count,
+//   pi*, first rank in closed form, the hash one read of the full corner table FCT.
+//   Otherwise: candidates of pi that differ in the last part only form a RUN
 //   (last part 1 .. len); its verdicts are one word V_last & len_mask when the
 //   other blocks pass, i.e. up to 32 candidate verdicts per word operation.
 //   The warp walks pi's runs in lockstep -- outer parts by a successor, the
@@ -21,8 +24,10 @@
 //   second-to-last likewise per run -- visiting only the runs some lane's set
 //   can pass, and records the set bits: count by popcount (or range length),
 //   pi* and the first rank from the lowest bit, the verdict hash from a prefix
-//   table of splitmix64 over the rank space, verdict bits with word-level
-//   atomics (tests).
+//   table of splitmix64 over the rank space (whole sweeps and blocks in closed
+//   form from the run-prefix table R and the corner table CT), verdict bits with
+//   word-level atomics (tests).  The tables depend on (n, M) only and are built
+//   once per caller workspace (gp_exhaustive_opts.tables_key).
 // Outputs are byte-identical to the per-candidate evaluator (GP_EX_PER_CANDIDATE
 // selects that one, for A/B runs and parity).
 #include <stdlib.h>
@@ -87,7 +92,7 @@ GP_DEV uint64_t ld_u64(uint64_t base, uint32_t idx) {
   return __ldg(reinterpret_cast<const unsigned long long *>(base + 8ull * idx));
 }
 
-// ---- pre-pass: V[set][S] for every subset S, one warp per set --------------------
+// ---- pre-pass: V[S][set] for every subset S, one warp per set --------------------
 // Subsets are taken level by level in order of increasing size c (a per-CTA table).
 // At level c only the pairs (S, m) whose subsets S - {i} all pass at m are tested
 // (the others fail exactly, see the kernel): they are compacted per chunk of 32
@@ -1231,8 +1236,9 @@ static void launch_bp_h(unsigned grid, const ExhArgs &a, const uint32_t *memo,
 
 namespace gp {
 // Workspace of one bit-sliced call, carved from one buffer (caller-provided or a
-// stream-ordered temporary): memo words [n_sets][2^n], RGS labels, the per-subset
-// lane order (slots, histograms, load levels) and the hash prefix table.
+// stream-ordered temporary): memo words [2^n][n_sets], RGS labels, the hash prefix
+// table P, the run-prefix table R, the corner tables CT / FCT and the memo pass's set
+// counter.
 struct BpLayout {
   size_t memo_words, words32, bytes, r_off, ct_off, fct_off;
   uint64_t n_rgs, n_ranks, total_runs, r_stride, mc_off;
