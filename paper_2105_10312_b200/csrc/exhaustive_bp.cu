@@ -32,6 +32,8 @@
 // selects that one, for A/B runs and parity).
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "gp_common.cuh"
 #include "gp_edf.cuh"
 #include "gp_enum.cuh"
@@ -754,72 +756,89 @@ __global__ void __launch_bounds__(kWarps * 32, GP_BP_MINB)
     // verdict words, reversed: Vr[jj] = V[set][S_{k-1-jj}]
     // (compile-time index jj, runtime block k-1-jj: no register-array indexing)
     uint32_t Vr[kBpMaxN];
+    bool dead = true;
+    // the verdict words, the dead check and the full corner, specialised on k (compile-time
+    // loop bounds); returns true when no lane has anything left in this item
+    auto front = [&](auto kc) -> bool {
+      constexpr int K = decltype(kc)::value;
 #pragma unroll
-    for (int jj = 0; jj < kBpMaxN; ++jj) {
-      Vr[jj] = 0u;
-      if (jj < k) {  // warp-uniform
-        const uint32_t bm = __ballot_sync(GP_FULL, myb == k - 1 - jj);
-        if (lane_ok) Vr[jj] = memo_set[bm * memo_stride];  // coalesced: lane = set
+      for (int jj = 0; jj < kBpMaxN; ++jj) {
+        Vr[jj] = 0u;
+        if (jj < K) {
+          const uint32_t bm = __ballot_sync(GP_FULL, myb == K - 1 - jj);
+          if (lane_ok) Vr[jj] = memo_set[bm * memo_stride];  // coalesced: lane = set
+        }
       }
-    }
-    if (!__any_sync(GP_FULL, lane_ok)) continue;
-    const int kp = k - 1;
-    // candidates of pi inside the rank window (all evaluated, bit-sliced)
-    if (lane_ok) {
-      if constexpr (kWin) {
-        const uint64_t w_lo = max(a.lo, rank_pi), w_hi = min(a.hi, rank_pi + per_pi);
-        st_cand += w_hi > w_lo ? w_hi - w_lo : 0;
-      } else {
-        st_cand += per_pi;
+      if (!__any_sync(GP_FULL, lane_ok)) return true;
+      // candidates of pi inside the rank window (all evaluated, bit-sliced)
+      if (lane_ok) {
+        if constexpr (kWin) {
+          const uint64_t w_lo = max(a.lo, rank_pi), w_hi = min(a.hi, rank_pi + per_pi);
+          st_cand += w_hi > w_lo ? w_hi - w_lo : 0;
+        } else {
+          st_cand += per_pi;
+        }
       }
-    }
-    // a block never schedulable at any size: every candidate of pi fails
-    bool dead = !lane_ok;
+      // a block never schedulable at any size: every candidate of pi fails
+      dead = !lane_ok;
 #pragma unroll
-    for (int jj = 0; jj < kBpMaxN; ++jj)
-      if (jj < k) dead |= Vr[jj] == 0u;
-    if (__all_sync(GP_FULL, dead)) continue;
+      for (int jj = 0; jj < K; ++jj) dead |= Vr[jj] == 0u;
+      if (__all_sync(GP_FULL, dead)) return true;
 #if GP_BP_FULLCORNER
-    if constexpr (!kWin && !kBits && kHash != 2) {
-      if ((kHash == 0 || a.FCT) && !a.force_ranges && !(a.flags & GP_EX_NO_FULL_CORNER)) {
-        // full corner: when every block's word is one bit range from its first passing size
-        // lo_j + 1 through the largest size a part can take (M - k + 1) -- checked here per
-        // (set, allocation) -- the set's schedulable candidates of pi are the corner with apex
-        // s_j = lo_j + 1 of pi's simplex: count, pi*, first rank in closed form, the hash one
-        // read of the full corner table at the apex (lanes done here skip the rest)
-        bool corner = !dead;
-        int csum = 0;      // prefix sums of the apex parts, block order j = 0 .. k-1
-        uint32_t sub = 0;  // sum_j C(M - c_j, k - j): the apex's lex rank complement
+      if constexpr (!kWin && !kBits && kHash != 2) {
+        if ((kHash == 0 || a.FCT) && !a.force_ranges && !(a.flags & GP_EX_NO_FULL_CORNER)) {
+          // full corner: when every block's word is one bit range from its first passing
+          // size lo_j + 1 through the largest size a part can take (M - k + 1) -- checked
+          // here per (set, allocation) -- the set's schedulable candidates of pi are the
+          // corner with apex s_j = lo_j + 1 of pi's simplex: count, pi*, first rank in closed
+          // form, the hash one read of the full corner table at the apex (lanes done here
+          // skip the rest)
+          bool corner = !dead;
+          int csum = 0;      // prefix sums of the apex parts, block order j = 0 .. k-1
+          uint32_t sub = 0;  // sum_j C(M - c_j, k - j): the apex's lex rank complement
 #pragma unroll
-        for (int jj = kBpMaxN - 1; jj >= 0; --jj) {
-          if (jj < k) {  // warp-uniform; block j = k - 1 - jj
+          for (int jj = K - 1; jj >= 0; --jj) {  // block j = K - 1 - jj
             const uint32_t V = Vr[jj];
             const int lo = V ? __ffs(V) - 1 : 0;
-            const int nb = M - k + 1 - lo;
+            const int nb = M - K + 1 - lo;
             const uint32_t mk = nb >= 32 ? ~0u : (nb <= 0 ? 0u : (1u << nb) - 1u);
             corner &= ((V >> lo) & mk) == mk;
             csum += lo + 1;
             sub += binom_s.at(M - csum, jj + 1);  // (csum > M: unused, see below)
           }
-        }
-        if (corner) {
-          if (csum <= M) {  // the apex fits: C(M - sum lo, k) candidates
-            acc_n += bn(M - csum + k, k);
-            acc_pi = min(acc_pi, csum);
-            const uint32_t off = bn(M, k) - 1u - sub;
-            acc_first = min(acc_first, rank_pi + off);
-            if constexpr (kHash == 1) acc_hash += ld_u64(fct_addr, off);
-            if constexpr (kStats) {
-              ++st_fc_items;
-              st_fc_blocks += (uint64_t)k;
+          if (corner) {
+            if (csum <= M) {  // the apex fits: C(M - sum lo, k) candidates
+              acc_n += bn(M - csum + K, K);
+              acc_pi = min(acc_pi, csum);
+              const uint32_t off = bn(M, K) - 1u - sub;
+              acc_first = min(acc_first, rank_pi + off);
+              if constexpr (kHash == 1) acc_hash += ld_u64(fct_addr, off);
+              if constexpr (kStats) {
+                ++st_fc_items;
+                st_fc_blocks += (uint64_t)K;
+              }
             }
+            dead = true;
           }
-          dead = true;
+          if (__all_sync(GP_FULL, dead)) return true;
         }
-        if (__all_sync(GP_FULL, dead)) continue;
       }
-    }
 #endif
+      return false;
+    };
+    bool skip;
+    switch (k) {  // warp-uniform
+      case 1: skip = front(std::integral_constant<int, 1>{}); break;
+      case 2: skip = front(std::integral_constant<int, 2>{}); break;
+      case 3: skip = front(std::integral_constant<int, 3>{}); break;
+      case 4: skip = front(std::integral_constant<int, 4>{}); break;
+      case 5: skip = front(std::integral_constant<int, 5>{}); break;
+      case 6: skip = front(std::integral_constant<int, 6>{}); break;
+      case 7: skip = front(std::integral_constant<int, 7>{}); break;
+      default: skip = front(std::integral_constant<int, 8>{}); break;
+    }
+    if (skip) continue;
+    const int kp = k - 1;
     const uint32_t V0 = dead ? 0u : Vr[0];
     // lowest size index of the last block that can pass; contiguity of its word
     const int a0 = V0 ? __ffs(V0) - 1 : 32;
