@@ -69,6 +69,9 @@ struct AllocArgs {
 #ifndef GP_ALLOC_GATHER_PER_TEST
 #define GP_ALLOC_GATHER_PER_TEST 1  // 16/32-lane groups: task records gathered per test (A/B: C4 -2 %, C5 -11 % with 4 CTAs)
 #endif
+#ifndef GP_ALLOC_N6
+#define GP_ALLOC_N6 1  // 8-lane kernels specialised on n = 6 (A/B)
+#endif
 #ifndef GP_ALLOC_NS4
 #define GP_ALLOC_NS4 8  // widest group that gets the <= 4-task lane-serial merge (0: none)
 #endif
@@ -332,7 +335,9 @@ GP_DEV uint32_t pm_bcast(const Grp<G> &g, uint32_t pm, int src) { return g.shfl(
 // kV >= 0: the variant is a compile-time constant (one kernel per variant: each carries only
 // its own code, e.g. no ACT prefill in INA, which keeps the instruction working set small);
 // kV = -1: runtime variant (the f4 kGen kernels)
-template <bool kGen, int G, int kV, bool kStats>
+// kN > 0: the task count as a compile-time constant (the paper-shaped n = 6 sets of C1-C3 scale:
+// every loop over tasks, slots and pairs has a constant trip count); 0: runtime a.n
+template <bool kGen, int G, int kV, bool kStats, int kN = 0>
 // register budget: 5 CTAs per SM for 8-lane groups (48 registers), 4 otherwise (64): A/B
 // measured, with the task records of a lane-serial merge gathered per test (no registers
 // held across the size search)
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(256, G == 8 ? GP_ALLOC_MINB8 : GP_ALLOC_MINB32
   const Grp<G> g;
   const int lane = g.gl, wid = threadIdx.x / G;  // lane within the group, group in the CTA
   WarpScratch<G> &scr = scr_all[wid];
-  const int n = a.n, M = a.M;
+  const int n = kN > 0 ? kN : a.n, M = a.M;
   uint16_t *wtab = a.use_tab ? wtab_all + (size_t)wid * n * M : nullptr;
   // this group's pair table (dynamic shared memory after the wave / size tables)
   uint64_t *pt_tab = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(wtab_all) +
@@ -859,6 +864,11 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
         k_allocate<false, 16, 3, true>, k_allocate<false, 16, 4, true>},
        {k_allocate<false, 32, 0, true>, k_allocate<false, 32, 1, true>, k_allocate<false, 32, 2, true>,
         k_allocate<false, 32, 3, true>, k_allocate<false, 32, 4, true>}}};
+  static const KernFn kdef6[2][5] = {  // n = 6 (C2, C3 shapes), 8-lane groups
+      {k_allocate<false, 8, 0, false, 6>, k_allocate<false, 8, 1, false, 6>, k_allocate<false, 8, 2, false, 6>,
+       k_allocate<false, 8, 3, false, 6>, k_allocate<false, 8, 4, false, 6>},
+      {k_allocate<false, 8, 0, true, 6>, k_allocate<false, 8, 1, true, 6>, k_allocate<false, 8, 2, true, 6>,
+       k_allocate<false, 8, 3, true, 6>, k_allocate<false, 8, 4, true, 6>}};
   const int gi = G == 8 ? 0 : (G == 16 ? 1 : 2);
   const bool st_on = stats != nullptr;
   const KernFn kern =
@@ -866,7 +876,8 @@ extern "C" gp_status gp_allocate(const gp_tasksets *ts, gp_variant v, const gp_a
                              : G == 16 ? k_allocate<true, 16, -1, true> : k_allocate<true, 32, -1, true>)
                    : (G == 8 ? k_allocate<true, 8, -1, false>
                              : G == 16 ? k_allocate<true, 16, -1, false> : k_allocate<true, 32, -1, false>))
-          : kdef[st_on ? 1 : 0][gi][(int)v];
+          : (G == 8 && ts->n_tasks == 6 && GP_ALLOC_N6) ? kdef6[st_on ? 1 : 0][(int)v]
+                                                          : kdef[st_on ? 1 : 0][gi][(int)v];
   // dynamic + static shared memory may pass 48 KB (e.g. 16-lane groups: 16 scratches + tables)
   // opt in to more than 48 KB (static + dynamic) only when needed: setting a function
   // attribute per call was measured to stall the stream (C3 step +1.4 ms)
