@@ -65,6 +65,8 @@ def parse():
                          "bit-sliced evaluator's memoised block verdicts (A/B)")
     ap.add_argument("--exh-flags", type=int, default=0,
                     help="extra gp_exhaustive_opts flags for the timed call (A/B of test hooks)")
+    ap.add_argument("--variants-in-order", action="store_true",
+                    help="A/B: launch the parallel variant kernels in list order, not longest first")
     ap.add_argument("--serial-variants", action="store_true",
                     help="launch the heuristic variants one after the other on one stream "
                          "(default: parallel streams for sets of <= 8 tasks)")
@@ -329,6 +331,7 @@ def main():
     pipe = Pipeline(args.config, reps=args.reps, rank=rank, world=world, split=args.split,
                     memo_heuristics=not args.no_memo_heuristics,
                     parallel_variants=False if args.serial_variants else None)
+    pipe.longest_first = not args.variants_in_order
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     alloc_stats = torch.zeros(8, dtype=torch.int64, device="cuda")  # GP_AL_STATS_EXT layout

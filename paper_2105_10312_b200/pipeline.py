@@ -117,6 +117,7 @@ class Pipeline:
         self.parallel_variants = (self.n <= 8 if parallel_variants is None
                                   else parallel_variants)
         self._vstreams = None
+        self.longest_first = True  # launch order of the parallel variant kernels (A/B)
 
     def _gen(self, kc, km, R):
         wl = self.wl
@@ -174,7 +175,12 @@ class Pipeline:
                 fork = torch.cuda.Event()
                 fork.record(stream)
                 joins = []
-                for vi, v in enumerate(self.variants):
+                # the longest kernels (INA, then ACT) first: they start before the short ones
+                order = list(range(len(self.variants)))
+                if self.longest_first:
+                    order.sort(key=lambda i: -_VARIANT_COST.get(self.variants[i], 0))
+                for vi in order:
+                    v = self.variants[vi]
                     vs = self._vstreams[vi]
                     vs.wait_event(fork)
                     G.gp_allocate(ts_h, v, self.alloc[vi], vs, stats=alloc_stats, memo=memo,
@@ -305,6 +311,11 @@ def merge_window_shards(per_set: torch.Tensor, group=None):
         dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(m, op=dist.ReduceOp.MIN, group=group)
     return unpack_window_shards(s, m, per_set)
+
+
+# relative kernel time of the heuristic variants (C3 launch lists: INA > ACT > 1G), used only
+# to order their launches on parallel streams
+_VARIANT_COST = {"SMS_INA": 4, "BF_INA": 3, "SMS_ACT": 2, "BF_ACT": 1, "1G": 0}
 
 
 def allreduce_counts(counts: torch.Tensor):
