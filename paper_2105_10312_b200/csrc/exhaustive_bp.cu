@@ -11,7 +11,7 @@
 //   skipped only when some S - {i} fails at m (then S fails: fewer tasks, no more
 //   conflicts); no monotonicity in m is assumed (that is f3's GP_THRESHOLD).
 //   The words are stored subset-major (V[S][set]; row 0 = the set's H).
-//   k_exh_bp: items = (32 sets, up to 8 allocations pi), candidates in the rank
+//   k_exh_bp: items = (32 sets, up to 16 allocations pi), candidates in the rank
 //   order of C.1.6.  FULL CORNER: when every block word of pi is one bit range from
 //   its first passing size lo_j + 1 through M - k + 1 (checked per (set, pi)), the
 //   schedulable candidates of pi are the corner s >= lo + 1 of pi's simplex: count,
@@ -83,7 +83,7 @@ constexpr int kBpMaxM = 32;  // sizes per verdict word
 #define GP_BP_SWEEP_UNROLL 2  // closed-sweep loop unroll (A/B: 1, 2, 4 -> 2 by 1.3 %)
 #endif
 #ifndef GP_BP_CHUNK
-#define GP_BP_CHUNK 8  // allocations per main-pass work item (A/B)
+#define GP_BP_CHUNK 16  // allocations per main-pass work item (A/B: 1, 4, 8, 16 -> 16)
 #endif
 constexpr uint32_t kBpChunk = GP_BP_CHUNK;
 constexpr int kBpUnroll = GP_BP_UNROLL;
